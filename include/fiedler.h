@@ -1,0 +1,175 @@
+/*
+ * fiedler.h -- C ABI of the B200-native cascadic-multigrid Fiedler solver
+ * (libfiedler.so, package paper_1602_04386_b200).
+ *
+ * Method: Gandhi, "Improvement of the Cascadic Multigrid Algorithm with a
+ * Gauss Seidel Smoother to Efficiently Compute the Fiedler Vector of a Graph
+ * Laplacian", arXiv 1602.04386.  "PAPER.md:NN" cites a line of the paper text,
+ * "R<k>" a reading of the paper listed in DESIGN.md section 3.
+ *
+ *   fiedler_create   Algorithm 3 Step 1, Setup Phase:
+ *                    repeated heavy edge coarsening (Algorithm 1, PAPER.md:49-74,
+ *                    parallel order R2), aggregate numbering by prefix scan,
+ *                    Galerkin product L^{i+1} = I L^i I^T (order R3),
+ *                    plus the multicolour ordering of every level (R4).
+ *   fiedler_solve    Algorithm 3 Steps 2-3: shifted power
+ *                    iteration on the coarsest level (R5), then per
+ *                    level prolongation y^j = I^T y^{j+1},
+ *                    Gauss-Seidel sweeps (Algorithm 2, R5) and
+ *                    power iteration on c I - L with deflation (R8);
+ *                    finally the Rayleigh quotient.
+ *   fiedler_destroy  frees the handle.
+ *
+ * Conventions (all entry points):
+ *   - Graph input is the weighted ADJACENCY W of an undirected graph in CSR:
+ *     row_ptr[n+1] (int64, row_ptr[0]=0, nondecreasing), col_idx[nnz] (int32,
+ *     strictly increasing within each row, no self loops), weights[nnz]
+ *     (float64, finite, > 0, w_ij == w_ji bit-for-bit).  The Laplacian is
+ *     L = D - W (Definition 2.1).  nnz counts both directions.
+ *   - `mem` arguments say where a pointer lives: FIEDLER_MEM_HOST (pageable or
+ *     pinned host memory) or FIEDLER_MEM_DEVICE (memory of opts->device).
+ *     Input buffers are only read and never retained after the call returns
+ *     (fiedler_create copies what it needs); output buffers are caller-owned.
+ *   - Every call returns FIEDLER_OK (0) or a negative FIEDLER_ERR_* code and
+ *     leaves a human-readable message for fiedler_last_error() (thread-local).
+ *     No call falls back to a CPU path: without a usable sm_100 device every
+ *     call that needs one fails with FIEDLER_ERR_CUDA.
+ *   - Work is issued on opts->stream (a cudaStream_t; NULL = a stream owned by
+ *     the handle) and the calls return after that stream has finished the
+ *     call's work (results are ready on return).
+ */
+#ifndef FIEDLER_H
+#define FIEDLER_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FIEDLER_API __attribute__((visibility("default")))
+#else
+#define FIEDLER_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FIEDLER_OK 0
+#define FIEDLER_ERR_ARG -1           /* invalid argument / option               */
+#define FIEDLER_ERR_GRAPH -2         /* CSR violates the conventions above      */
+#define FIEDLER_ERR_DISCONNECTED -3  /* lambda_2 = 0: Fiedler vector undefined  */
+#define FIEDLER_ERR_CUDA -4          /* CUDA runtime / launch / device failure  */
+#define FIEDLER_ERR_NOMEM -5         /* device allocation failed                */
+#define FIEDLER_ERR_INTERNAL -6      /* an internal invariant failed            */
+#define FIEDLER_ERR_TOO_LARGE -7     /* nnz >= 2^31 (int32 offsets) or n >= 2^31 */
+
+#define FIEDLER_MEM_HOST 0
+#define FIEDLER_MEM_DEVICE 1
+
+/* Options.  Obtain defaults with fiedler_default_opts(). */
+typedef struct fiedler_opts {
+    int32_t device;               /* CUDA device ordinal (default 0)                        */
+    int32_t coarsest_size;        /* stop coarsening when n <= this ("n_i > 25") */
+    int32_t max_levels;           /* hard cap on hierarchy depth (default 50)               */
+    int32_t gs_sweeps;            /* Gauss-Seidel sweeps per level below J (default 2)      */
+    int32_t power_iters;          /* power iterations per level (default 10)                */
+    int32_t coarsest_power_iters; /* power iterations on level J; -1 = power_iters          */
+    int32_t validate;             /* 1 = check the CSR conventions on the device (default 1) */
+    int32_t use_graph;            /* 1 = replay the solve as one CUDA graph (default 1)     */
+    uint64_t seed;                /* counter-based generator seed (R6), default 0           */
+    void *stream;                 /* cudaStream_t to use; NULL = handle-owned stream        */
+} fiedler_opts;
+
+#define FIEDLER_MAX_LEVELS 64
+
+/* Diagnostics filled by fiedler_solve (optional). */
+typedef struct fiedler_info {
+    int32_t num_levels;                     /* J + 1                                    */
+    int32_t launches;                       /* kernels launched by this solve call      */
+    double lambda2;                         /* Rayleigh quotient of the returned vector  */
+    double residual_norm;                   /* || L v - lambda2 v ||_2                   */
+    double setup_ms;                        /* device time of fiedler_create's setup     */
+    double solve_ms;                        /* device time of this solve                 */
+    int64_t level_n[FIEDLER_MAX_LEVELS];    /* vertices per level                        */
+    int64_t level_nnz[FIEDLER_MAX_LEVELS];  /* adjacency nonzeros per level              */
+    int32_t level_colors[FIEDLER_MAX_LEVELS]; /* colours of the multicolour ordering     */
+    int32_t level_match_rounds[FIEDLER_MAX_LEVELS]; /* handshake rounds of the matching  */
+    double level_shift[FIEDLER_MAX_LEVELS]; /* c of c I - L (R8)                          */
+} fiedler_info;
+
+typedef struct fiedler_handle_s *fiedler_handle;
+
+/* Fill *opts with the defaults listed above. */
+FIEDLER_API void fiedler_default_opts(fiedler_opts *opts);
+
+/* Build the multilevel hierarchy of the graph (Setup Phase).
+ *   n, nnz       vertices (n >= 2) and stored adjacency entries.
+ *   row_ptr, col_idx, weights   CSR of W as described above, in `mem`.
+ *   opts         NULL = defaults; device/coarsest_size/max_levels/validate/seed/stream used.
+ *   out          receives the handle on success (NULL on failure).
+ * Errors: ARG (bad sizes/pointers), GRAPH (validation failed: unsorted or
+ * out-of-range columns, self loop, non-positive or non-finite weight,
+ * asymmetric entry), DISCONNECTED (the coarsest level is disconnected, which
+ * holds iff the input is), TOO_LARGE, NOMEM, CUDA. */
+FIEDLER_API int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr,
+                   const int32_t *col_idx, const double *weights, int32_t mem,
+                   const fiedler_opts *opts, fiedler_handle *out);
+
+/* Run the cascadic refinement (Steps 2-3) and the Rayleigh quotient.
+ *   opts            NULL = the options given to fiedler_create; otherwise
+ *                   gs_sweeps/power_iters/coarsest_power_iters/seed/use_graph/stream.
+ *   fiedler_vector  n doubles in `vec_mem` (may be NULL): the unit-norm vector,
+ *                   orthogonal to 1, first nonzero entry positive.
+ *   lambda2         (may be NULL) algebraic connectivity estimate = Rayleigh
+ *                   quotient of the returned vector (Definition 2.2).
+ *   info            (may be NULL) diagnostics.
+ * Errors: ARG, CUDA, INTERNAL. */
+FIEDLER_API int fiedler_solve(fiedler_handle h, const fiedler_opts *opts, double *fiedler_vector,
+                  int32_t vec_mem, double *lambda2, fiedler_info *info);
+
+/* Release every device resource of the handle (NULL is a no-op). */
+FIEDLER_API int fiedler_destroy(fiedler_handle h);
+
+/* Message of the last failing call on this thread ("" if none). */
+FIEDLER_API const char *fiedler_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Introspection and single-operation calls (used by the parity tests; they
+ * run the same kernels as fiedler_create/fiedler_solve on one level).
+ * All vectors here are in the level's NATURAL numbering (the numbering of the
+ * oracle: level 0 = input order, level l+1 = aggregate ids of R2).
+ * ------------------------------------------------------------------------- */
+
+/* Number of levels J+1 of the hierarchy. */
+FIEDLER_API int fiedler_num_levels(fiedler_handle h, int32_t *num_levels);
+
+/* Size of level `level`: vertices, adjacency nonzeros, colours. */
+FIEDLER_API int fiedler_level_size(fiedler_handle h, int32_t level, int64_t *n, int64_t *nnz,
+                       int32_t *colors);
+
+/* Copy level `level` to HOST buffers (any pointer may be NULL):
+ *   row_ptr[n+1] (int64), col_idx[nnz], weights[nnz]: adjacency W^level in
+ *     natural numbering with columns ascending (the Galerkin product of R3);
+ *   agg[n]: aggregate id of every vertex on level+1 (q of Algorithm 1; -1 on J);
+ *   mate[n]: partner in the heavy-edge matching (-1 if unmatched or on J);
+ *   color[n]: colour of the multicolour ordering (R4). */
+FIEDLER_API int fiedler_level_export(fiedler_handle h, int32_t level, int64_t *row_ptr,
+                         int32_t *col_idx, double *weights, int32_t *agg,
+                         int32_t *mate, int32_t *color);
+
+#define FIEDLER_OP_GS_SWEEPS 1   /* x_out = `count` multicolour GS sweeps on L x = 0 from x_in (no deflation) */
+#define FIEDLER_OP_POWER 2       /* x_out = `count` steps of y <- normalise(deflate((cI - L) y)), y0 = x_in */
+#define FIEDLER_OP_PROLONG 3     /* x_out (level) = I^T x_in (level+1): x_out[i] = x_in[q(i)] */
+#define FIEDLER_OP_RAYLEIGH 4    /* scalar_out[0] = x^T L x / x^T x of x_in; x_out unused */
+
+/* Apply one solve-phase operation on level `level`.  x_in/x_out live in
+ * `mem`, natural numbering, sizes n_level (n_{level+1} for x_in of PROLONG).
+ * scalar_out (host, may be NULL) receives {mean, norm} of the result for
+ * GS/POWER/PROLONG and {rayleigh, residual_norm} for RAYLEIGH. */
+FIEDLER_API int fiedler_level_apply(fiedler_handle h, int32_t level, int32_t op, int32_t count,
+                        const double *x_in, double *x_out, int32_t mem,
+                        double *scalar_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIEDLER_H */

@@ -307,7 +307,7 @@ def build_hierarchy(g: Graph, cfg: Config = Config()) -> List[Level]:
             mate = None
         else:
             raise ValueError(cfg.mode)
-        if c > cfg.stall_ratio * L.g.n:
+        if c > cfg.stall_ratio * L.g.n or c < 2:     # stall guard / no 1-vertex level (R9)
             break
         L.q, L.c, L.mate = q, c, mate
         levels.append(Level(galerkin(L.g, q, c)))

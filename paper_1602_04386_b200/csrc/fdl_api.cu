@@ -1,0 +1,375 @@
+// fdl_api.cu -- the extern "C" boundary declared in include/fiedler.h.
+// Argument checking, host<->device staging, CUDA-graph capture/replay of the
+// solve schedule, and error translation.  All numerical work is in
+// fdl_setup.cu / fdl_solve.cu kernels; there is no CPU fallback.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "fdl_internal.h"
+
+namespace fdl {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string &m) { g_last_error = m; }
+
+Handle::~Handle() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+    levels.clear();
+    xa.release(); xb.release(); vnat.release(); scal.release();
+    partials.release(); counter.release(); result.release();
+    if (stream) cudaStreamSynchronize(stream);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32, cudaStream_t st);
+int rowpass_grid();
+
+struct EventTimer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s;
+    explicit EventTimer(cudaStream_t st) : s(st) {
+        FDL_CK(cudaEventCreate(&a));
+        FDL_CK(cudaEventCreate(&b));
+        FDL_CK(cudaEventRecord(a, s));
+    }
+    double stop_ms() {
+        FDL_CK(cudaEventRecord(b, s));
+        FDL_CK(cudaEventSynchronize(b));
+        float ms = 0.f;
+        FDL_CK(cudaEventElapsedTime(&ms, a, b));
+        return ms;
+    }
+    ~EventTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+static void check_device(int dev) {
+    int count = 0;
+    FDL_CK(cudaGetDeviceCount(&count));
+    FDL_REQUIRE(dev >= 0 && dev < count, FIEDLER_ERR_CUDA, "no such CUDA device");
+    FDL_CK(cudaSetDevice(dev));
+    cudaDeviceProp p;
+    FDL_CK(cudaGetDeviceProperties(&p, dev));
+    FDL_REQUIRE(p.major == 10, FIEDLER_ERR_CUDA,
+                "libfiedler is built for sm_100a (B200); device is sm_" + std::to_string(p.major) +
+                    std::to_string(p.minor));
+    static bool pool_done = false;
+    if (!pool_done) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_done = true;
+    }
+}
+
+static SolveCfg cfg_of(const fiedler_opts &o) {
+    SolveCfg c;
+    c.gs = o.gs_sweeps;
+    c.pi = o.power_iters;
+    c.piJ = o.coarsest_power_iters < 0 ? o.power_iters : o.coarsest_power_iters;
+    c.seed = o.seed;
+    return c;
+}
+
+int prepare_solve(Handle &h, const SolveCfg &cfg);
+
+}  // namespace fdl
+
+using namespace fdl;
+
+#define API_BEGIN try {
+#define API_END                                                  \
+    }                                                            \
+    catch (const fdl::Error &e) {                                \
+        fdl::set_error(e.what());                                \
+        return e.code;                                           \
+    }                                                            \
+    catch (const std::bad_alloc &) {                             \
+        fdl::set_error("host allocation failed");                \
+        return FIEDLER_ERR_NOMEM;                                \
+    }                                                            \
+    catch (const std::exception &e) {                            \
+        fdl::set_error(e.what());                                \
+        return FIEDLER_ERR_INTERNAL;                             \
+    }
+
+extern "C" {
+
+void fiedler_default_opts(fiedler_opts *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->device = 0;
+    o->coarsest_size = 25;
+    o->max_levels = 50;
+    o->gs_sweeps = 2;
+    o->power_iters = 10;
+    o->coarsest_power_iters = -1;
+    o->validate = 1;
+    o->use_graph = 1;
+    o->seed = 0;
+    o->stream = nullptr;
+}
+
+const char *fiedler_last_error(void) { return fdl::g_last_error.c_str(); }
+
+int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                   const double *weights, int32_t mem, const fiedler_opts *opts,
+                   fiedler_handle *out) {
+    API_BEGIN
+    fdl::set_error("");
+    FDL_REQUIRE(out != nullptr, FIEDLER_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    fiedler_opts o;
+    if (opts) o = *opts; else fiedler_default_opts(&o);
+    FDL_REQUIRE(n >= 2, FIEDLER_ERR_ARG, "need n >= 2");
+    FDL_REQUIRE(nnz >= 0, FIEDLER_ERR_ARG, "nnz < 0");
+    FDL_REQUIRE(n < (int64_t(1) << 31) - 1 && nnz < (int64_t(1) << 31) - 1, FIEDLER_ERR_TOO_LARGE,
+                "n and nnz must be < 2^31 - 1 (int32 offsets)");
+    FDL_REQUIRE(row_ptr && (nnz == 0 || (col_idx && weights)), FIEDLER_ERR_ARG, "NULL CSR pointer");
+    FDL_REQUIRE(mem == FIEDLER_MEM_HOST || mem == FIEDLER_MEM_DEVICE, FIEDLER_ERR_ARG, "bad mem kind");
+    FDL_REQUIRE(o.coarsest_size >= 2 && o.max_levels >= 1 && o.max_levels <= FIEDLER_MAX_LEVELS &&
+                    o.gs_sweeps >= 0 && o.power_iters >= 0,
+                FIEDLER_ERR_ARG, "invalid options");
+    check_device(o.device);
+
+    std::unique_ptr<Handle> h(new Handle());
+    h->device = o.device;
+    h->opts = o;
+    if (o.stream) {
+        h->stream = (cudaStream_t)o.stream;
+        h->own_stream = false;
+    } else {
+        FDL_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    cudaStream_t st = h->stream;
+    h->row_grid = rowpass_grid();
+    EventTimer timer(st);
+
+    NatGraph g0;
+    g0.n = (int)n;
+    g0.nnz = (int)nnz;
+    g0.own_rp.alloc((size_t)(n + 1) * 4, st);
+    if (mem == FIEDLER_MEM_DEVICE) {
+        convert_row_ptr(row_ptr, n, nnz, g0.own_rp.as<int>(), st);
+        g0.ci = col_idx;
+        g0.w = weights;
+    } else {
+        DBuf rp64((size_t)(n + 1) * 8, st);
+        FDL_CK(cudaMemcpyAsync(rp64.p, row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st));
+        convert_row_ptr(rp64.as<int64_t>(), n, nnz, g0.own_rp.as<int>(), st);
+        g0.own_ci.alloc((size_t)std::max<int64_t>(nnz, 1) * 4, st);
+        g0.own_w.alloc((size_t)std::max<int64_t>(nnz, 1) * 8, st);
+        if (nnz) {
+            FDL_CK(cudaMemcpyAsync(g0.own_ci.p, col_idx, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
+            FDL_CK(cudaMemcpyAsync(g0.own_w.p, weights, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
+        }
+        g0.ci = g0.own_ci.as<int>();
+        g0.w = g0.own_w.as<double>();
+    }
+    g0.rp = g0.own_rp.as<int>();
+    if (o.validate) validate_input(n, nnz, g0.rp, g0.ci, g0.w, st);
+    h->n0 = (int)n;
+    build_hierarchy(*h, std::move(g0));
+    prepare_solve(*h, cfg_of(o));
+    h->setup_ms = timer.stop_ms();
+    *out = reinterpret_cast<fiedler_handle>(h.release());
+    return FIEDLER_OK;
+    API_END
+}
+
+int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int32_t vec_mem,
+                  double *lambda2, fiedler_info *info) {
+    API_BEGIN
+    fdl::set_error("");
+    FDL_REQUIRE(hh != nullptr, FIEDLER_ERR_ARG, "NULL handle");
+    Handle &h = *reinterpret_cast<Handle *>(hh);
+    FDL_REQUIRE(vec_mem == FIEDLER_MEM_HOST || vec_mem == FIEDLER_MEM_DEVICE, FIEDLER_ERR_ARG,
+                "bad mem kind");
+    fiedler_opts o = opts ? *opts : h.opts;
+    FDL_REQUIRE(o.gs_sweeps >= 0 && o.power_iters >= 0, FIEDLER_ERR_ARG, "invalid options");
+    FDL_CK(cudaSetDevice(h.device));
+    if (opts && opts->stream && (cudaStream_t)opts->stream != h.stream) {
+        FDL_CK(cudaStreamSynchronize(h.stream));
+        if (h.own_stream) FDL_CK(cudaStreamDestroy(h.stream));
+        h.stream = (cudaStream_t)opts->stream;
+        h.own_stream = false;
+        if (h.gexec) { cudaGraphExecDestroy(h.gexec); h.gexec = nullptr; }
+    }
+    cudaStream_t st = h.stream;
+    SolveCfg cfg = cfg_of(o);
+    prepare_solve(h, cfg);
+    EventTimer timer(st);
+    int launches = 0;
+    if (o.use_graph) {
+        if (!h.gexec || h.g_gs != cfg.gs || h.g_pi != cfg.pi || h.g_piJ != cfg.piJ ||
+            h.g_seed != cfg.seed) {
+            if (h.gexec) { cudaGraphExecDestroy(h.gexec); h.gexec = nullptr; }
+            cudaGraph_t g = nullptr;
+            FDL_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            try {
+                launches = enqueue_solve(h, cfg);
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            FDL_CK(cudaStreamEndCapture(st, &g));
+            cudaError_t e = cudaGraphInstantiate(&h.gexec, g, 0);
+            cudaGraphDestroy(g);
+            FDL_CK(e);
+            h.g_gs = cfg.gs; h.g_pi = cfg.pi; h.g_piJ = cfg.piJ; h.g_seed = cfg.seed;
+            h.g_launches = launches;
+        }
+        FDL_CK(cudaGraphLaunch(h.gexec, st));
+        launches = h.g_launches;
+    } else {
+        launches = enqueue_solve(h, cfg);
+    }
+    if (vec) {
+        FDL_CK(cudaMemcpyAsync(vec, h.vnat.p, (size_t)h.n0 * 8,
+                               vec_mem == FIEDLER_MEM_HOST ? cudaMemcpyDeviceToHost
+                                                           : cudaMemcpyDeviceToDevice, st));
+    }
+    double res[3] = {0, 0, 0};
+    FDL_CK(cudaMemcpyAsync(res, h.result.p, sizeof(res), cudaMemcpyDeviceToHost, st));
+    double ms = timer.stop_ms();
+    FDL_CK(cudaStreamSynchronize(st));
+    if (lambda2) *lambda2 = res[0];
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->num_levels = (int)h.levels.size();
+        info->launches = launches;
+        info->lambda2 = res[0];
+        info->residual_norm = res[1];
+        info->setup_ms = h.setup_ms;
+        info->solve_ms = ms;
+        for (size_t l = 0; l < h.levels.size() && l < FIEDLER_MAX_LEVELS; l++) {
+            info->level_n[l] = h.levels[l].n;
+            info->level_nnz[l] = h.levels[l].nnz;
+            info->level_colors[l] = h.levels[l].ncolors;
+            info->level_match_rounds[l] = h.levels[l].match_rounds;
+            info->level_shift[l] = h.levels[l].shift;
+        }
+    }
+    return FIEDLER_OK;
+    API_END
+}
+
+int fiedler_destroy(fiedler_handle hh) {
+    API_BEGIN
+    if (!hh) return FIEDLER_OK;
+    Handle *h = reinterpret_cast<Handle *>(hh);
+    cudaSetDevice(h->device);
+    delete h;
+    return FIEDLER_OK;
+    API_END
+}
+
+int fiedler_num_levels(fiedler_handle hh, int32_t *num_levels) {
+    API_BEGIN
+    FDL_REQUIRE(hh && num_levels, FIEDLER_ERR_ARG, "NULL argument");
+    *num_levels = (int)reinterpret_cast<Handle *>(hh)->levels.size();
+    return FIEDLER_OK;
+    API_END
+}
+
+int fiedler_level_size(fiedler_handle hh, int32_t level, int64_t *n, int64_t *nnz, int32_t *colors) {
+    API_BEGIN
+    FDL_REQUIRE(hh, FIEDLER_ERR_ARG, "NULL handle");
+    Handle &h = *reinterpret_cast<Handle *>(hh);
+    FDL_REQUIRE(level >= 0 && level < (int)h.levels.size(), FIEDLER_ERR_ARG, "bad level");
+    const Level &L = h.levels[level];
+    if (n) *n = L.n;
+    if (nnz) *nnz = L.nnz;
+    if (colors) *colors = L.ncolors;
+    return FIEDLER_OK;
+    API_END
+}
+
+int fiedler_level_export(fiedler_handle hh, int32_t level, int64_t *row_ptr, int32_t *col_idx,
+                         double *weights, int32_t *agg, int32_t *mate, int32_t *color) {
+    API_BEGIN
+    FDL_REQUIRE(hh, FIEDLER_ERR_ARG, "NULL handle");
+    Handle &h = *reinterpret_cast<Handle *>(hh);
+    FDL_REQUIRE(level >= 0 && level < (int)h.levels.size(), FIEDLER_ERR_ARG, "bad level");
+    FDL_CK(cudaSetDevice(h.device));
+    const Level &L = h.levels[level];
+    cudaStream_t st = h.stream;
+    const int n = L.n, nnz = L.nnz;
+    std::vector<int> perm(n), inv(n), rp(n + 1), ci(std::max(nnz, 1));
+    std::vector<double> w(std::max(nnz, 1));
+    FDL_CK(cudaMemcpyAsync(perm.data(), L.perm.p, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaMemcpyAsync(inv.data(), L.inv.p, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaMemcpyAsync(rp.data(), L.rp.p, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (nnz) {
+        FDL_CK(cudaMemcpyAsync(ci.data(), L.ci.p, (size_t)nnz * 4, cudaMemcpyDeviceToHost, st));
+        FDL_CK(cudaMemcpyAsync(w.data(), L.w.p, (size_t)nnz * 8, cudaMemcpyDeviceToHost, st));
+    }
+    auto copy_nat = [&](const DBuf &b, int32_t *dst) {
+        if (!dst) return;
+        if (b.p) FDL_CK(cudaMemcpyAsync(dst, b.p, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+        else std::fill(dst, dst + n, -1);
+    };
+    copy_nat(L.q_nat, agg);
+    copy_nat(L.mate_nat, mate);
+    copy_nat(L.color_nat, color);
+    FDL_CK(cudaStreamSynchronize(st));
+    // un-permute (introspection only): natural row v = solve row inv[v]; the
+    // within-row order of the solve layout is the natural ascending order
+    int64_t off = 0;
+    for (int v = 0; v < n; v++) {
+        if (row_ptr) row_ptr[v] = off;
+        int t = inv[v];
+        for (int k = rp[t]; k < rp[t + 1]; k++, off++) {
+            if (col_idx) col_idx[off] = perm[ci[k]];
+            if (weights) weights[off] = w[k];
+        }
+    }
+    if (row_ptr) row_ptr[n] = off;
+    return FIEDLER_OK;
+    API_END
+}
+
+int fiedler_level_apply(fiedler_handle hh, int32_t level, int32_t op, int32_t count,
+                        const double *x_in, double *x_out, int32_t mem, double *scalar_out) {
+    API_BEGIN
+    FDL_REQUIRE(hh && x_in, FIEDLER_ERR_ARG, "NULL argument");
+    Handle &h = *reinterpret_cast<Handle *>(hh);
+    const int nl = (int)h.levels.size();
+    FDL_REQUIRE(level >= 0 && level < nl, FIEDLER_ERR_ARG, "bad level");
+    FDL_REQUIRE(op >= 1 && op <= 4 && count >= 0, FIEDLER_ERR_ARG, "bad op/count");
+    FDL_REQUIRE(op != FIEDLER_OP_PROLONG || level + 1 < nl, FIEDLER_ERR_ARG, "no coarser level");
+    FDL_REQUIRE(op == FIEDLER_OP_RAYLEIGH || x_out, FIEDLER_ERR_ARG, "x_out is NULL");
+    FDL_CK(cudaSetDevice(h.device));
+    cudaStream_t st = h.stream;
+    const int n_out = h.levels[level].n;
+    const int n_in = op == FIEDLER_OP_PROLONG ? h.levels[level + 1].n : n_out;
+    DBuf din, dout;
+    const double *pin = x_in;
+    double *pout = x_out;
+    if (mem == FIEDLER_MEM_HOST) {
+        din.alloc((size_t)n_in * 8, st);
+        dout.alloc((size_t)n_out * 8, st);
+        FDL_CK(cudaMemcpyAsync(din.p, x_in, (size_t)n_in * 8, cudaMemcpyHostToDevice, st));
+        pin = din.as<double>();
+        pout = dout.as<double>();
+    }
+    apply_level_op(h, level, op, count, pin, pout, scalar_out);
+    if (mem == FIEDLER_MEM_HOST && x_out && op != FIEDLER_OP_RAYLEIGH) {
+        FDL_CK(cudaMemcpyAsync(x_out, dout.p, (size_t)n_out * 8, cudaMemcpyDeviceToHost, st));
+        FDL_CK(cudaStreamSynchronize(st));
+    }
+    return FIEDLER_OK;
+    API_END
+}
+
+}  // extern "C"

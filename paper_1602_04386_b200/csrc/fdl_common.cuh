@@ -1,0 +1,127 @@
+// fdl_common.cuh -- internal helpers of libfiedler (product path, sm_100a).
+// Nothing here is shared with oracle/ (task rule 3): the counter-based
+// generator below is this side's own implementation of DESIGN.md reading R6.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/fiedler.h"
+
+namespace fdl {
+
+// ----------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define FDL_CK(call)                                                                      \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            throw ::fdl::Error(e_ == cudaErrorMemoryAllocation ? FIEDLER_ERR_NOMEM        \
+                                                               : FIEDLER_ERR_CUDA,        \
+                               std::string(#call) + ": " + cudaGetErrorString(e_) +       \
+                                   " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
+    } while (0)
+
+#define FDL_LAUNCH_CK() FDL_CK(cudaGetLastError())
+
+#define FDL_REQUIRE(cond, code, msg)                                                      \
+    do {                                                                                  \
+        if (!(cond)) throw ::fdl::Error((code), (msg));                                   \
+    } while (0)
+
+// ----------------------------------------------------------------- memory
+// Stream-ordered device buffer (cudaMallocAsync pool; capture-safe frees are
+// never issued inside a captured region).
+struct DBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(size_t b, cudaStream_t st) { alloc(b, st); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept { *this = std::move(o); }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p; bytes = o.bytes; s = o.s;
+            o.p = nullptr; o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t b, cudaStream_t st) {
+        release();
+        s = st;
+        bytes = b;
+        if (b) FDL_CK(cudaMallocAsync(&p, b, st));
+    }
+    void release() noexcept {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// ----------------------------------------------------------------- generator (R6)
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+constexpr uint64_t kTagMatch = 0x6D61746368000000ULL;  // "match"
+constexpr uint64_t kTagColor = 0x636F6C6F72000000ULL;  // "color"
+constexpr uint64_t kTagRand = 0x72616E6400000000ULL;   // "rand"
+
+__host__ __device__ __forceinline__ uint64_t salt_match(uint64_t seed, int level) {
+    return splitmix64(seed ^ (kTagMatch + (uint64_t)level));
+}
+__host__ __device__ __forceinline__ uint64_t salt_color(uint64_t seed, int level) {
+    return splitmix64(seed ^ (kTagColor + (uint64_t)level));
+}
+// tie-break hash of the undirected edge {a, b} (R2)
+__device__ __forceinline__ uint64_t edge_hash(uint64_t salt, int a, int b) {
+    uint64_t lo = (uint64_t)(unsigned)min(a, b), hi = (uint64_t)(unsigned)max(a, b);
+    return splitmix64(salt ^ ((lo << 32) | hi));
+}
+
+// ----------------------------------------------------------------- launch helpers
+constexpr int kNumSMs = 148;
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+inline int grid_for(int64_t threads, int block = 256, int cap = kNumSMs * 32) {
+    int64_t g = (threads + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// ----------------------------------------------------------------- primitives (fdl_prims.cu)
+// Exclusive prefix sum of int32; `total` (device, may be null) receives the sum.
+void scan_exclusive(const int *in, int *out, int64_t n, int *total, cudaStream_t st);
+// Stable LSD radix sort of (key, value) pairs on bits [0, bits); result in keys/vals.
+void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStream_t st);
+void radix_sort_u64_f64(unsigned long long *keys, double *vals, int64_t n, int bits,
+                        cudaStream_t st);
+// Device-wide max of an int array (n >= 1) into *out (device).
+void reduce_max_i32(const int *in, int64_t n, int *out, cudaStream_t st);
+
+inline int bits_for(int64_t maxval) {  // bits to represent values in [0, maxval]
+    int b = 0;
+    while (b < 63 && (int64_t(1) << b) <= maxval) b++;
+    return b < 1 ? 1 : b;
+}
+
+}  // namespace fdl

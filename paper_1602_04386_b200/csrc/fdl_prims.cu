@@ -1,0 +1,252 @@
+// fdl_prims.cu -- hand-written device primitives: exclusive scan (reduce-then-
+// scan, 4096-element tiles, vectorised int4 traffic) and a stable LSD radix
+// sort (8-bit digits, 8192-element tiles, warp __match_any_sync ranking).
+// Used by the aggregate numbering (prefix scan of leader flags), the Galerkin
+// product (sort of coarse-pair keys) and the multicolour layout.
+#include <climits>
+
+#include "fdl_common.cuh"
+
+namespace fdl {
+
+// =============================================================== scan
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane_id() >= o) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one int per thread; returns the block total.
+__device__ __forceinline__ int block_excl_scan(int v, int &total) {
+    __shared__ int s_warp[32];
+    __shared__ int s_total;
+    int incl = warp_incl_scan(v);
+    int w = threadIdx.x >> 5;
+    if (lane_id() == 31) s_warp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int nw = blockDim.x >> 5;
+        int x = lane_id() < nw ? s_warp[lane_id()] : 0;
+        int xi = warp_incl_scan(x);
+        if (lane_id() < nw) s_warp[lane_id()] = xi - x;
+    }
+    __syncthreads();
+    int res = incl - v + s_warp[w];
+    if (threadIdx.x == blockDim.x - 1) s_total = res + v;
+    __syncthreads();
+    total = s_total;
+    __syncthreads();
+    return res;
+}
+
+__device__ __forceinline__ void load4(const int *in, int64_t n, int64_t i, int x[4]) {
+    if (i + 3 < n && ((reinterpret_cast<uintptr_t>(in + i) & 15) == 0)) {
+        int4 v = *reinterpret_cast<const int4 *>(in + i);
+        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) x[k] = (i + k < n) ? in[i + k] : 0;
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const int *in, int64_t n, int *bsums) {
+    int64_t i = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int x[4];
+    load4(in, n, i, x);
+    int s = x[0] + x[1] + x[2] + x[3];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __shared__ int sw[32];
+    if (lane_id() == 0) sw[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int t = sw[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0) bsums[blockIdx.x] = t;
+    }
+}
+
+// single block: exclusive scan of nb block sums in place; writes total
+__global__ void __launch_bounds__(kScanThreads) k_scan_bsums(int *bsums, int nb, int *total) {
+    int carry = 0;
+    for (int base = 0; base < nb; base += kScanThreads) {
+        int i = base + threadIdx.x;
+        int v = i < nb ? bsums[i] : 0;
+        int tot;
+        int ex = block_excl_scan(v, tot);
+        if (i < nb) bsums[i] = ex + carry;
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_final(const int *in, int *out, int64_t n,
+                                                             const int *bsums) {
+    int64_t i = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int x[4];
+    load4(in, n, i, x);
+    int s = x[0] + x[1] + x[2] + x[3];
+    int tot;
+    int ex = block_excl_scan(s, tot) + bsums[blockIdx.x];
+    int y[4];
+    y[0] = ex;
+    y[1] = ex + x[0];
+    y[2] = y[1] + x[1];
+    y[3] = y[2] + x[2];
+    if (i + 3 < n && ((reinterpret_cast<uintptr_t>(out + i) & 15) == 0)) {
+        *reinterpret_cast<int4 *>(out + i) = make_int4(y[0], y[1], y[2], y[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (i + k < n) out[i + k] = y[k];
+    }
+}
+
+void scan_exclusive(const int *in, int *out, int64_t n, int *total, cudaStream_t st) {
+    if (n <= 0) {
+        if (total) FDL_CK(cudaMemsetAsync(total, 0, sizeof(int), st));
+        return;
+    }
+    int nb = div_up(n, kScanTile);
+    DBuf bs((size_t)nb * sizeof(int), st);
+    k_scan_reduce<<<nb, kScanThreads, 0, st>>>(in, n, bs.as<int>());
+    FDL_LAUNCH_CK();
+    k_scan_bsums<<<1, kScanThreads, 0, st>>>(bs.as<int>(), nb, total);
+    FDL_LAUNCH_CK();
+    k_scan_final<<<nb, kScanThreads, 0, st>>>(in, out, n, bs.as<int>());
+    FDL_LAUNCH_CK();
+}
+
+// =============================================================== radix sort
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsSub = 32;                        // sub-tiles of 256 items per tile
+constexpr int kRsTile = kRsThreads * kRsSub;      // 8192 items per block
+
+template <class K>
+__global__ void __launch_bounds__(kRsThreads) k_rs_hist(const K *keys, int64_t n, int shift,
+                                                        int nb, int *hist) {
+    __shared__ int cnt[256];
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * kRsTile;
+    for (int s = 0; s < kRsSub; s++) {
+        int64_t i = base + (int64_t)s * kRsThreads + threadIdx.x;
+        if (i < n) atomicAdd(&cnt[(unsigned)(keys[i] >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    hist[(int64_t)threadIdx.x * nb + blockIdx.x] = cnt[threadIdx.x];
+}
+
+template <class K, class V>
+__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const K *keys, const V *vals,
+                                                           int64_t n, int shift, int nb,
+                                                           const int *offs, K *keys_out,
+                                                           V *vals_out) {
+    __shared__ int s_run[256];
+    __shared__ int s_cnt[kRsWarps][256];
+    s_run[threadIdx.x] = offs[(int64_t)threadIdx.x * nb + blockIdx.x];
+#pragma unroll
+    for (int w = 0; w < kRsWarps; w++) s_cnt[w][threadIdx.x] = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    int64_t base = (int64_t)blockIdx.x * kRsTile;
+    for (int s = 0; s < kRsSub; s++) {
+        if (base + (int64_t)s * kRsThreads >= n) break;  // block-uniform
+        int64_t i = base + (int64_t)s * kRsThreads + threadIdx.x;
+        bool valid = i < n;
+        K k = valid ? keys[i] : K(0);
+        V v = valid ? vals[i] : V(0);
+        int d = valid ? (int)((unsigned)(k >> shift) & 255u) : 256;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        int rank = __popc(peers & lt);
+        if (valid && rank == 0) s_cnt[warp][d] = __popc(peers);
+        __syncthreads();
+        {   // per-digit exclusive scan over warps, continuing the running offset
+            int t = threadIdx.x;
+            int run = s_run[t];
+#pragma unroll
+            for (int w = 0; w < kRsWarps; w++) {
+                int c = s_cnt[w][t];
+                s_cnt[w][t] = run;
+                run += c;
+            }
+            s_run[t] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            int pos = s_cnt[warp][d] + rank;
+            keys_out[pos] = k;
+            vals_out[pos] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < kRsWarps; w++) s_cnt[w][threadIdx.x] = 0;
+        __syncthreads();
+    }
+}
+
+template <class K, class V>
+static void radix_sort_impl(K *keys, V *vals, int64_t n, int bits, cudaStream_t st) {
+    if (n <= 1 || bits <= 0) return;
+    FDL_REQUIRE(n < (int64_t(1) << 31), FIEDLER_ERR_TOO_LARGE, "radix sort: n >= 2^31");
+    int nb = div_up(n, kRsTile);
+    DBuf hist((size_t)256 * nb * sizeof(int), st);
+    DBuf kalt((size_t)n * sizeof(K), st), valt((size_t)n * sizeof(V), st);
+    K *ka = keys, *kb = kalt.as<K>();
+    V *va = vals, *vb = valt.as<V>();
+    int passes = (bits + 7) / 8;
+    for (int p = 0; p < passes; p++) {
+        int shift = 8 * p;
+        k_rs_hist<K><<<nb, kRsThreads, 0, st>>>(ka, n, shift, nb, hist.as<int>());
+        FDL_LAUNCH_CK();
+        scan_exclusive(hist.as<int>(), hist.as<int>(), (int64_t)256 * nb, nullptr, st);
+        k_rs_scatter<K, V><<<nb, kRsThreads, 0, st>>>(ka, va, n, shift, nb, hist.as<int>(), kb, vb);
+        FDL_LAUNCH_CK();
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    if (ka != keys) {
+        FDL_CK(cudaMemcpyAsync(keys, ka, (size_t)n * sizeof(K), cudaMemcpyDeviceToDevice, st));
+        FDL_CK(cudaMemcpyAsync(vals, va, (size_t)n * sizeof(V), cudaMemcpyDeviceToDevice, st));
+    }
+}
+
+void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStream_t st) {
+    radix_sort_impl<unsigned, int>(keys, vals, n, bits, st);
+}
+void radix_sort_u64_f64(unsigned long long *keys, double *vals, int64_t n, int bits,
+                        cudaStream_t st) {
+    radix_sort_impl<unsigned long long, double>(keys, vals, n, bits, st);
+}
+
+// =============================================================== max
+__global__ void k_max_i32(const int *in, int64_t n, int *out) {
+    int m = INT_MIN;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, in[i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane_id() == 0) atomicMax(out, m);
+}
+
+__global__ void k_set_i32(int *p, int v) { *p = v; }
+
+void reduce_max_i32(const int *in, int64_t n, int *out, cudaStream_t st) {
+    k_set_i32<<<1, 1, 0, st>>>(out, INT_MIN);
+    FDL_LAUNCH_CK();
+    k_max_i32<<<grid_for(n, 256, kNumSMs * 8), 256, 0, st>>>(in, n, out);
+    FDL_LAUNCH_CK();
+}
+
+}  // namespace fdl

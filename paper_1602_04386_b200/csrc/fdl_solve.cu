@@ -1,0 +1,532 @@
+// fdl_solve.cu -- Steps 2-3 of Algorithm 3 and the final
+// Rayleigh quotient, as row-pass kernels over the solve layout.
+//
+// One row-pass kernel serves the three HBM-bound sweeps of the path:
+//   OP_GS  multicolour Gauss-Seidel on L x = 0 (Algorithm 2 line 87 with
+//          b = 0: x_i = sum_j w_ij x_j / d_i, in place, one colour per launch);
+//   OP_PI  one step of power iteration on c I - L with deflation (R5, R8):
+//          z_i = [c (y_i - mu) + sum_j w_ij (y_j - y_i)] / sigma, where (mu, sigma)
+//          are the mean / deflated norm of y from the previous pass (lazy
+//          deflate + normalise: the whole step is ONE pass over the level);
+//   OP_RQ  Rayleigh quotient of v = s (z - mu) / sigma with the edge form
+//          sum_ij w_ij (z_i - z_j)^2 (R7), ||L v||, and v scattered to natural order.
+// d_i = sum_j w_ij is recomputed on the fly from the streamed weights (no
+// degree array is read).  Every pass produces its reductions with a
+// deterministic two-level tree (per-CTA partials, last CTA folds them in
+// fixed order), so results are bit-reproducible run to run.
+//
+// Work decomposition (fdl_internal.h): short rows (<= 32 nnz) in tiles of
+// ~2048 nonzeros whose column/weight streams are staged through shared memory
+// with coalesced loads, medium rows one warp each, long rows one CTA each.
+#include <algorithm>
+#include <cmath>
+
+#include "fdl_internal.h"
+
+namespace fdl {
+
+enum { OP_GS = 0, OP_PI = 1, OP_RQ = 2 };
+constexpr int kRowThreads = 256;
+constexpr int kNumStats = 3;
+
+struct LevelView {
+    int n;
+    const int *rp;
+    const int *ci;
+    const double *w;
+};
+
+struct PassArgs {
+    const double *x;        // input (GS: in/out)
+    double *y;              // output (PI)
+    const double *in_stat;  // slot of the input vector: [2]=mu, [3]=sigma
+    double *out_stat;       // slot receiving S, Q, mu, sigma
+    int stat_mode;          // bit0: first contribution (assign), bit1: last (finalise), bit2: wanted
+    int n;                  // level size (mean)
+    double shift;           // c
+    double *partials;       // [grid][kNumStats]
+    unsigned *counter;
+    const int *perm;        // RQ: solve row -> natural id
+    double *vnat;           // RQ: output vector, natural order
+    const double *sign;     // RQ: +-1
+    double *result;         // RQ: {lambda2, residual}
+};
+
+// ----------------------------------------------------------------- per-row math
+template <int OP> struct RowAcc {
+    double a = 0.0, b = 0.0;  // GS: (sum w x, sum w); PI: (sum w (x_j - y_i), -); RQ: (sum w d^2, sum w d)
+    double own = 0.0;
+    __device__ __forceinline__ void add(double wk, double xj) {
+        if (OP == OP_GS) { a = fma(wk, xj, a); b += wk; }
+        else if (OP == OP_PI) { a = fma(wk, xj - own, a); }
+        else { double d = own - xj; a = fma(wk * d, d, a); b = fma(wk, d, b); }
+    }
+    __device__ __forceinline__ void merge(const RowAcc &o) { a += o.a; b += o.b; }
+};
+
+struct Scal {
+    double mu, inv_sigma, sigma, sign;
+};
+
+// row epilogue: write result, accumulate statistics st[0..2]
+template <int OP>
+__device__ __forceinline__ void row_finish(int r, const RowAcc<OP> &acc, const PassArgs &a,
+                                           const Scal &sc, double st[kNumStats]) {
+    if (OP == OP_GS) {
+        double xn = acc.a / acc.b;
+        const_cast<double *>(a.x)[r] = xn;
+        st[0] += xn;
+        st[1] = fma(xn, xn, st[1]);
+    } else if (OP == OP_PI) {
+        double z = (a.shift * (acc.own - sc.mu) + acc.a) * sc.inv_sigma;
+        a.y[r] = z;
+        st[0] += z;
+        st[1] = fma(z, z, st[1]);
+    } else {
+        double zc = acc.own - sc.mu;
+        a.vnat[a.perm[r]] = sc.sign * zc * sc.inv_sigma;
+        double lv = acc.b * sc.inv_sigma;
+        st[0] += acc.a;
+        st[1] = fma(zc, zc, st[1]);
+        st[2] = fma(lv, lv, st[2]);
+    }
+}
+
+// ----------------------------------------------------------------- reductions
+template <int N>
+__device__ __forceinline__ void block_sum(double v[N], double (*sm)[N]) {
+#pragma unroll
+    for (int k = 0; k < N; k++)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    const int w = threadIdx.x >> 5;
+    if (lane_id() == 0)
+#pragma unroll
+        for (int k = 0; k < N; k++) sm[w][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int k = 0; k < N; k++) {
+            double t = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x][k] : 0.0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            v[k] = t;
+        }
+    }
+    __syncthreads();
+}
+
+// Per-CTA partials -> last CTA folds all partials in a fixed order and runs
+// `fin(total)` on thread 0.  Deterministic for a fixed grid.
+template <class Fin>
+__device__ __forceinline__ void grid_reduce(double st[kNumStats], double *partials,
+                                            unsigned *counter, Fin fin) {
+    __shared__ double sm[32][kNumStats];
+    __shared__ bool s_last;
+    block_sum<kNumStats>(st, sm);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < kNumStats; k++) partials[blockIdx.x * kNumStats + k] = st[k];
+        __threadfence();
+        unsigned t = atomicAdd(counter, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double v[kNumStats] = {0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < kNumStats; k++) v[k] += __ldcg(&partials[b * kNumStats + k]);
+    block_sum<kNumStats>(v, sm);
+    if (threadIdx.x == 0) {
+        fin(v);
+        *counter = 0u;
+    }
+}
+
+__device__ __forceinline__ void finish_stats(const double tot[kNumStats], double *slot, int mode,
+                                             int n) {
+    if (mode & 1) { slot[0] = tot[0]; slot[1] = tot[1]; }
+    else { slot[0] += tot[0]; slot[1] += tot[1]; }
+    if (mode & 2) {
+        double mu = slot[0] / (double)n;
+        double var = slot[1] - (double)n * mu * mu;   // sum (x - mu)^2
+        slot[2] = mu;
+        slot[3] = sqrt(fmax(var, 0.0));
+    }
+}
+
+// ----------------------------------------------------------------- the row pass
+template <int OP>
+__global__ void __launch_bounds__(kRowThreads) k_rowpass(const Item *__restrict__ items, int nitems,
+                                                         LevelView L, PassArgs a) {
+    __shared__ int s_ci[kTileCap];
+    __shared__ double s_w[kTileCap];
+    __shared__ RowAcc<OP> s_red[kRowThreads / 32];
+    const double *__restrict__ x = a.x;
+    Scal sc{0.0, 1.0, 1.0, 1.0};
+    if (OP != OP_GS) {
+        sc.mu = a.in_stat[2];
+        sc.sigma = a.in_stat[3];
+        sc.inv_sigma = 1.0 / sc.sigma;
+        if (OP == OP_RQ) sc.sign = *a.sign;
+    }
+    double st[kNumStats] = {0.0, 0.0, 0.0};
+    const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item item = items[it];
+        if (item.x == 0) {
+            // ---- short rows: stage the tile's column/weight streams in smem
+            const int r0 = item.y, r1 = item.z;
+            const int e0 = L.rp[r0], e1 = L.rp[r1];
+            const int cnt = e1 - e0;
+            for (int k = tid; k < cnt; k += kRowThreads) {
+                s_ci[k] = __ldcs(L.ci + e0 + k);
+                s_w[k] = __ldcs(L.w + e0 + k);
+            }
+            __syncthreads();
+            for (int r = r0 + tid; r < r1; r += kRowThreads) {
+                const int b = L.rp[r] - e0, e = L.rp[r + 1] - e0;
+                RowAcc<OP> acc;
+                if (OP != OP_GS) acc.own = x[r];
+                for (int k = b; k < e; k++) acc.add(s_w[k], __ldg(x + s_ci[k]));
+                row_finish<OP>(r, acc, a, sc, st);
+            }
+            __syncthreads();
+        } else if (item.x == 1) {
+            // ---- medium rows: one warp per row
+            const int r = item.y + warp;
+            if (r < item.z) {
+                const int b = L.rp[r], e = L.rp[r + 1];
+                RowAcc<OP> acc;
+                if (OP != OP_GS) acc.own = x[r];
+                for (int k = b + lane; k < e; k += 32) acc.add(__ldcs(L.w + k), __ldg(x + __ldcs(L.ci + k)));
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    acc.a += __shfl_xor_sync(0xffffffffu, acc.a, o);
+                    acc.b += __shfl_xor_sync(0xffffffffu, acc.b, o);
+                }
+                if (lane == 0) row_finish<OP>(r, acc, a, sc, st);
+            }
+        } else {
+            // ---- long rows: one CTA per row
+            const int r = item.y;
+            const int b = L.rp[r], e = L.rp[r + 1];
+            RowAcc<OP> acc;
+            if (OP != OP_GS) acc.own = x[r];
+            for (int k = b + tid; k < e; k += kRowThreads) acc.add(__ldcs(L.w + k), __ldg(x + __ldcs(L.ci + k)));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                acc.a += __shfl_xor_sync(0xffffffffu, acc.a, o);
+                acc.b += __shfl_xor_sync(0xffffffffu, acc.b, o);
+            }
+            if (lane == 0) s_red[warp] = acc;
+            __syncthreads();
+            if (tid == 0) {
+                RowAcc<OP> t = s_red[0];
+                for (int k = 1; k < kRowThreads / 32; k++) t.merge(s_red[k]);
+                row_finish<OP>(r, t, a, sc, st);
+            }
+            __syncthreads();
+        }
+    }
+    if (OP == OP_GS && !(a.stat_mode & 4)) return;   // uniform: statistics not wanted
+    grid_reduce(st, a.partials, a.counter, [&](const double *tot) {
+        if (OP == OP_RQ) {
+            double lam = 0.5 * tot[0] / tot[1];
+            double vn2 = tot[1] * sc.inv_sigma * sc.inv_sigma;   // ||v||^2
+            double res2 = tot[2] - lam * lam * vn2;
+            a.result[0] = lam;
+            a.result[1] = sqrt(fmax(res2, 0.0));
+            a.result[2] = sqrt(vn2);
+        } else {
+            finish_stats(tot, a.out_stat, a.stat_mode, a.n);
+        }
+    });
+}
+
+// ----------------------------------------------------------------- small kernels
+// prolongation y^j = I^T y^{j+1} + statistics of y^j
+__global__ void __launch_bounds__(256) k_prolong(int n, const int *__restrict__ qp,
+                                                 const double *__restrict__ xc, double *__restrict__ y,
+                                                 double *slot, double *partials, unsigned *counter) {
+    double st[kNumStats] = {0.0, 0.0, 0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double v = __ldg(xc + __ldcs(qp + i));
+        y[i] = v;
+        st[0] += v;
+        st[1] = fma(v, v, st[1]);
+    }
+    grid_reduce(st, partials, counter, [&](const double *tot) { finish_stats(tot, slot, 3, n); });
+}
+
+// rand(n_J) in natural order, counter-based (R6)
+__global__ void __launch_bounds__(256) k_rand(int n, const int *__restrict__ perm, uint64_t seed,
+                                              double *__restrict__ y, double *slot, double *partials,
+                                              unsigned *counter) {
+    const uint64_t s0 = splitmix64(seed ^ kTagRand);
+    double st[kNumStats] = {0.0, 0.0, 0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double v = (double)(splitmix64(s0 + (uint64_t)perm[i]) >> 11) * 0x1.0p-53;
+        y[i] = v;
+        st[0] += v;
+        st[1] = fma(v, v, st[1]);
+    }
+    grid_reduce(st, partials, counter, [&](const double *tot) { finish_stats(tot, slot, 3, n); });
+}
+
+// sign convention: first nonzero entry (natural order) of v = (z - mu)/sigma positive
+__global__ void k_sign(int n, const int *__restrict__ inv, const double *__restrict__ z,
+                       const double *slot, double *sign) {
+    const double mu = slot[2];
+    for (int base = 0; base < n; base += 32) {
+        int i = base + lane_id();
+        double v = i < n ? z[inv[i]] - mu : 0.0;
+        unsigned nz = __ballot_sync(0xffffffffu, v != 0.0);
+        if (nz) {
+            int src = __ffs(nz) - 1;
+            double f = __shfl_sync(0xffffffffu, v, src);
+            if (lane_id() == 0) *sign = f > 0.0 ? 1.0 : -1.0;
+            return;
+        }
+    }
+    if (lane_id() == 0) *sign = 1.0;
+}
+
+__global__ void k_set_slot(double *slot, double mu, double sigma) {
+    slot[0] = 0.0; slot[1] = 0.0; slot[2] = mu; slot[3] = sigma;
+}
+
+__global__ void k_gather_f64(int n, const int *__restrict__ idx, const double *__restrict__ src,
+                             double *__restrict__ dst) {  // dst[i] = src[idx[i]]
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+__global__ void k_scatter_f64(int n, const int *__restrict__ idx, const double *__restrict__ src,
+                              double *__restrict__ dst) {  // dst[idx[i]] = src[i]
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[idx[i]] = src[i];
+}
+// materialise (z - mu)/sigma in place
+__global__ void k_normalise(int n, double *z, const double *slot) {
+    const double mu = slot[2], is = 1.0 / slot[3];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        z[i] = (z[i] - mu) * is;
+}
+
+// ----------------------------------------------------------------- host-side schedule
+struct Enq {
+    Handle &h;
+    cudaStream_t st;
+    int launches = 0;
+    double *slot(int k) { return h.scal.as<double>() + 4 * k; }
+
+    template <int OP>
+    void rowpass(const Level &L, int ib, int ie, PassArgs a) {
+        int ni = ie - ib;
+        if (ni <= 0) return;
+        int grid = std::min(ni, h.row_grid);
+        a.partials = h.partials.as<double>();
+        a.counter = h.counter.as<unsigned>();
+        LevelView v{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()};
+        k_rowpass<OP><<<grid, kRowThreads, 0, st>>>(L.items.as<Item>() + ib, ni, v, a);
+        FDL_LAUNCH_CK();
+        launches++;
+    }
+    void gs(const Level &L, double *x, int sweeps, double *out_slot) {
+        for (int s = 0; s < sweeps; s++)
+            for (int c = 0; c < L.ncolors; c++) {
+                PassArgs a{};
+                a.x = x;
+                a.n = L.n;
+                bool want = (s == sweeps - 1) && out_slot;
+                a.out_stat = out_slot;
+                a.stat_mode = want ? (4 | (c == 0 ? 1 : 0) | (c == L.ncolors - 1 ? 2 : 0)) : 0;
+                rowpass<OP_GS>(L, L.citem[c], L.citem[c + 1], a);
+            }
+    }
+    void pi(const Level &L, const double *x, double *y, const double *in_slot, double *out_slot) {
+        PassArgs a{};
+        a.x = x;
+        a.y = y;
+        a.in_stat = in_slot;
+        a.out_stat = out_slot;
+        a.stat_mode = 7;
+        a.n = L.n;
+        a.shift = L.shift;
+        rowpass<OP_PI>(L, 0, L.nitems, a);
+    }
+    void prolong(const Level &L, const double *xc, double *y, double *out_slot) {
+        k_prolong<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(
+            L.n, L.qp.as<int>(), xc, y, out_slot, h.partials.as<double>(), h.counter.as<unsigned>());
+        FDL_LAUNCH_CK();
+        launches++;
+    }
+};
+
+static void ensure_solve_buffers(Handle &h, int nslots) {
+    cudaStream_t st = h.stream;
+    if (!h.xa.p) {
+        h.xa.alloc((size_t)h.n0 * 8, st);
+        h.xb.alloc((size_t)h.n0 * 8, st);
+        h.vnat.alloc((size_t)h.n0 * 8, st);
+        h.partials.alloc((size_t)h.row_grid * kNumStats * 8, st);
+        h.counter.alloc(64, st);
+        FDL_CK(cudaMemsetAsync(h.counter.p, 0, 64, st));
+        h.result.alloc(8 * 8, st);
+    }
+    if (h.nslots < nslots) {
+        if (h.gexec) { cudaGraphExecDestroy(h.gexec); h.gexec = nullptr; }   // it captured the old slots
+        h.scal.alloc((size_t)nslots * 4 * 8, st);
+        FDL_CK(cudaMemsetAsync(h.scal.p, 0, (size_t)nslots * 4 * 8, st));
+        h.nslots = nslots;
+    }
+}
+
+static int slots_needed(const Handle &h, const SolveCfg &cfg) {
+    const int J = (int)h.levels.size() - 1;
+    // 1 (rand) + piJ + per level (1 prolong + 1 gs + pi) + sign, and >= 8 for level ops
+    return std::max(8, 2 + cfg.piJ + J * (2 + cfg.pi) + 2);
+}
+
+// allocate everything the solve needs (never inside a graph capture)
+int prepare_solve(Handle &h, const SolveCfg &cfg) {
+    ensure_solve_buffers(h, slots_needed(h, cfg));
+    return 0;
+}
+
+int rowpass_grid() {
+    int b0 = 0, b1 = 0, b2 = 0;
+    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_rowpass<OP_GS>, kRowThreads, 0));
+    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_rowpass<OP_PI>, kRowThreads, 0));
+    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_rowpass<OP_RQ>, kRowThreads, 0));
+    int b = std::max(1, std::min(b0, std::min(b1, b2)));
+    int dev = 0, sms = kNumSMs;
+    FDL_CK(cudaGetDevice(&dev));
+    FDL_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return sms * b;
+}
+
+int enqueue_solve(Handle &h, const SolveCfg &cfg) {
+    const int J = (int)h.levels.size() - 1;
+    const int nslots = slots_needed(h, cfg);
+    FDL_REQUIRE(h.nslots >= nslots && h.xa.p, FIEDLER_ERR_INTERNAL, "solve buffers not prepared");
+    Enq e{h, h.stream};
+    int sl = 0;
+    double *xa = h.xa.as<double>(), *xb = h.xb.as<double>();
+    // ---- coarsest level: rand(n_J), deflate + normalise (lazily), power iteration
+    const Level &LJ = h.levels[J];
+    double *cur_slot = e.slot(sl++);
+    k_rand<<<grid_for(LJ.n, 256, h.row_grid), 256, 0, h.stream>>>(
+        LJ.n, LJ.perm.as<int>(), cfg.seed, xa, cur_slot, h.partials.as<double>(), h.counter.as<unsigned>());
+    FDL_LAUNCH_CK();
+    e.launches++;
+    double *cur = xa, *oth = xb;
+    for (int k = 0; k < cfg.piJ; k++) {
+        double *ns = e.slot(sl++);
+        e.pi(LJ, cur, oth, cur_slot, ns);
+        std::swap(cur, oth);
+        cur_slot = ns;
+    }
+    // ---- cascadic refinement
+    for (int ell = J - 1; ell >= 0; ell--) {
+        const Level &L = h.levels[ell];
+        double *ps = e.slot(sl++);
+        e.prolong(L, cur, oth, ps);
+        std::swap(cur, oth);
+        cur_slot = ps;
+        if (cfg.gs > 0) {
+            double *gsl = e.slot(sl++);
+            e.gs(L, cur, cfg.gs, gsl);
+            cur_slot = gsl;
+        }
+        for (int k = 0; k < cfg.pi; k++) {
+            double *ns = e.slot(sl++);
+            e.pi(L, cur, oth, cur_slot, ns);
+            std::swap(cur, oth);
+            cur_slot = ns;
+        }
+    }
+    // ---- Rayleigh quotient on level 0 (+ vector in natural order)
+    const Level &L0 = h.levels[0];
+    double *sgn = e.slot(sl++);
+    k_sign<<<1, 32, 0, h.stream>>>(L0.n, L0.inv.as<int>(), cur, cur_slot, sgn);
+    FDL_LAUNCH_CK();
+    e.launches++;
+    PassArgs a{};
+    a.x = cur;
+    a.in_stat = cur_slot;
+    a.n = L0.n;
+    a.perm = L0.perm.as<int>();
+    a.vnat = h.vnat.as<double>();
+    a.sign = sgn;
+    a.result = h.result.as<double>();
+    e.rowpass<OP_RQ>(L0, 0, L0.nitems, a);
+    FDL_REQUIRE(sl <= nslots, FIEDLER_ERR_INTERNAL, "slot overflow");
+    return e.launches;
+}
+
+// ----------------------------------------------------------------- fiedler_level_apply
+void apply_level_op(Handle &h, int level, int op, int count, const double *x_in, double *x_out,
+                    double *scal_host) {
+    const Level &L = h.levels[level];
+    cudaStream_t st = h.stream;
+    ensure_solve_buffers(h, 8);
+    Enq e{h, st};
+    double *xa = h.xa.as<double>(), *xb = h.xb.as<double>();
+    double *s0 = e.slot(0), *s1 = e.slot(1);
+    double res[4] = {0, 0, 0, 0};
+    if (op == FIEDLER_OP_PROLONG) {
+        const Level &C = h.levels[level + 1];
+        k_gather_f64<<<grid_for(C.n), 256, 0, st>>>(C.n, C.perm.as<int>(), x_in, xa);
+        e.prolong(L, xa, xb, s0);
+        k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), xb, x_out);
+        FDL_LAUNCH_CK();
+        FDL_CK(cudaMemcpyAsync(res, s0, 32, cudaMemcpyDeviceToHost, st));
+        if (scal_host) { scal_host[0] = res[2]; scal_host[1] = res[3]; }
+    } else {
+        k_gather_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), x_in, xa);
+        FDL_LAUNCH_CK();
+        if (op == FIEDLER_OP_GS_SWEEPS) {
+            e.gs(L, xa, count, s0);
+            k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), xa, x_out);
+            FDL_LAUNCH_CK();
+            FDL_CK(cudaMemcpyAsync(res, s0, 32, cudaMemcpyDeviceToHost, st));
+            if (scal_host) { scal_host[0] = res[2]; scal_host[1] = res[3]; }
+        } else if (op == FIEDLER_OP_POWER) {
+            k_set_slot<<<1, 1, 0, st>>>(s0, 0.0, 1.0);
+            double *cur = xa, *oth = xb, *cs = s0, *ns = s1;
+            for (int k = 0; k < count; k++) {
+                e.pi(L, cur, oth, cs, ns);
+                std::swap(cur, oth);
+                std::swap(cs, ns);
+            }
+            if (count > 0) k_normalise<<<grid_for(L.n), 256, 0, st>>>(L.n, cur, cs);
+            k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), cur, x_out);
+            FDL_LAUNCH_CK();
+            FDL_CK(cudaMemcpyAsync(res, cs, 32, cudaMemcpyDeviceToHost, st));
+            if (scal_host) { scal_host[0] = res[2]; scal_host[1] = res[3]; }
+        } else if (op == FIEDLER_OP_RAYLEIGH) {
+            k_set_slot<<<1, 1, 0, st>>>(s0, 0.0, 1.0);
+            k_set_slot<<<1, 1, 0, st>>>(s1, 1.0, 1.0);   // sign = slot1[0]... use [2]
+            PassArgs a{};
+            a.x = xa;
+            a.in_stat = s0;
+            a.n = L.n;
+            a.perm = L.perm.as<int>();
+            a.vnat = xb;     // scratch (natural order)
+            a.sign = s1 + 2;
+            a.result = h.result.as<double>();
+            e.rowpass<OP_RQ>(L, 0, L.nitems, a);
+            FDL_CK(cudaMemcpyAsync(res, h.result.p, 24, cudaMemcpyDeviceToHost, st));
+            if (scal_host) { scal_host[0] = res[0]; scal_host[1] = res[1]; }
+        } else {
+            throw Error(FIEDLER_ERR_ARG, "unknown op");
+        }
+    }
+    FDL_CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace fdl

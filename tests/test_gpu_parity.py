@@ -1,0 +1,213 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle, on
+the same seeded inputs.  Bars:
+  * hierarchy (matching, aggregate ids, coarse CSR pattern AND values, colours):
+    bit-exact;
+  * single operations from identical inputs: GS / power steps rel 1e-12,
+    prolongation exact, Rayleigh quotient rel 1e-12;
+  * full solve with identical iteration counts: |lambda_gpu - lambda_orc| /
+    lambda_orc <= 1e-10 and 1 - |cos(v_gpu, v_orc)| <= 1e-10 (north star).
+"""
+import numpy as np
+import pytest
+
+import graphgen as gg
+
+pytestmark = pytest.mark.gpu
+
+LAM_TOL = 1e-10
+COS_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1602_04386_b200 as fd
+    from paper_1602_04386_b200 import build
+    build.build()
+    return fd
+
+
+def orc_graph(orc, g):
+    return orc.Graph.from_csr(g.n, g.rp, g.ci, g.w)
+
+
+SMALL = {
+    "grid32_unit(config0)": lambda: gg.grid2d(32, "unit"),
+    "grid50x37_uniform": lambda: gg.grid2d(50, "uniform", seed=7, mx=37),
+    "grid3d_12_lognormal": lambda: gg.grid3d(12, "lognormal", seed=3),
+    "rmat12": lambda: gg.rmat(12, 16.0, seed=5),
+    "rand500_int_ties": lambda: gg.random_connected(500, 900, 11, integer_weights=True),
+    "rand300": lambda: gg.random_connected(300, 1500, 12),
+    "path100": lambda: gg.path(100),
+    "star40": lambda: gg.star(40),
+    "complete30": lambda: gg.complete(30),
+    "tiny_p5": lambda: gg.path(5),
+    "tiny_p3": lambda: gg.path(3),   # (P2 is degenerate for the Gershgorin shift: c = lambda_2)
+}
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_hierarchy_bit_exact(fd, orc, name):
+    g = SMALL[name]()
+    levels = orc.build_hierarchy(orc_graph(orc, g), orc.Config())
+    h = fd.fiedler_create(g.n, g.nnz, g.rp, g.ci, g.w)
+    try:
+        assert fd.fiedler_num_levels(h) == len(levels)
+        for ell, L in enumerate(levels):
+            ex = fd.fiedler_level_export(h, ell)
+            assert ex["n"] == L.g.n
+            assert np.array_equal(ex["rp"], L.g.rp), (name, ell)
+            assert np.array_equal(ex["ci"], L.g.ci), (name, ell)
+            assert np.array_equal(ex["w"].view(np.uint64), L.g.w.view(np.uint64)), (name, ell)
+            assert np.array_equal(ex["color"], L.color), (name, ell)
+            if ell < len(levels) - 1:
+                assert np.array_equal(ex["agg"], L.q), (name, ell)
+                assert np.array_equal(ex["mate"], L.mate), (name, ell)
+    finally:
+        fd.fiedler_destroy(h)
+
+
+@pytest.mark.parametrize("name", ["grid32_unit(config0)", "grid3d_12_lognormal", "rmat12", "rand300"])
+def test_single_ops_vs_oracle(fd, orc, name):
+    g = SMALL[name]()
+    levels = orc.build_hierarchy(orc_graph(orc, g), orc.Config())
+    h = fd.fiedler_create(g.n, g.nnz, g.rp, g.ci, g.w)
+    rng = np.random.default_rng(0)
+    try:
+        for ell, L in enumerate(levels):
+            x = rng.standard_normal(L.g.n)
+            # Gauss-Seidel sweeps in the multicolour order
+            for sweeps in (1, 2):
+                out = np.empty_like(x)
+                fd.fiedler_level_apply(h, ell, fd.FIEDLER_OP_GS_SWEEPS, x, out, sweeps)
+                ref = orc.gs_sweeps(L.g, x, sweeps, L.order, L.d)
+                np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-13 * np.abs(ref).max())
+            # power iteration on c I - L with deflation + normalisation
+            for it in (1, 3):
+                out = np.empty_like(x)
+                fd.fiedler_level_apply(h, ell, fd.FIEDLER_OP_POWER, x, out, it)
+                ref = orc.power_iterations(L.g, x, it, L.shift, L.d)
+                np.testing.assert_allclose(out, ref, rtol=1e-11, atol=1e-13)
+            # Rayleigh quotient
+            lam, _ = fd.fiedler_level_apply(h, ell, fd.FIEDLER_OP_RAYLEIGH, x)
+            assert lam == pytest.approx(orc.rayleigh(L.g, x), rel=1e-12)
+            # prolongation from the next level (exact)
+            if ell + 1 < len(levels):
+                yc = rng.standard_normal(levels[ell + 1].g.n)
+                out = np.empty(L.g.n)
+                fd.fiedler_level_apply(h, ell, fd.FIEDLER_OP_PROLONG, yc, out)
+                assert np.array_equal(out, orc.prolongate(L.q, yc))
+    finally:
+        fd.fiedler_destroy(h)
+
+
+def compare_solve(fd, orc, g, cfg_kw=None, device_input=False):
+    cfg_kw = cfg_kw or {}
+    ref = orc.solve(orc_graph(orc, g), orc.Config(**cfg_kw))
+    opts = fd.fiedler_default_opts(**{k: v for k, v in cfg_kw.items()
+                                      if k in ("gs_sweeps", "power_iters", "seed", "coarsest_size")})
+    if device_input:
+        import torch
+        args = [torch.from_numpy(a).cuda() for a in (g.rp, g.ci, g.w)]
+        vec = torch.empty(g.n, dtype=torch.float64, device="cuda")
+    else:
+        args = [g.rp, g.ci, g.w]
+        vec = np.empty(g.n)
+    info = fd.fiedler_info()
+    h = fd.fiedler_create(g.n, g.nnz, *args, opts)
+    try:
+        lam = fd.fiedler_solve(h, vec, None, info)
+    finally:
+        fd.fiedler_destroy(h)
+    v = vec.cpu().numpy() if device_input else vec
+    assert info.num_levels == len(ref.levels)
+    assert abs(lam - ref.lambda2) / ref.lambda2 <= LAM_TOL, (lam, ref.lambda2)
+    cos = abs(float(v @ ref.vector)) / (np.linalg.norm(v) * np.linalg.norm(ref.vector))
+    assert 1 - cos <= COS_TOL, 1 - cos
+    assert np.linalg.norm(v) == pytest.approx(1.0, rel=1e-12)
+    assert abs(v.sum()) <= 1e-9 * np.sqrt(g.n)
+    nz = np.flatnonzero(v)
+    assert v[nz[0]] > 0
+    # the residual is a diagnostic from sqrt(||Lv||^2 - lambda^2 ||v||^2): absolute
+    # accuracy ~ sqrt(eps) * lambda (cancellation when v is an exact eigenvector)
+    assert info.residual_norm == pytest.approx(ref.residual_norm, rel=1e-6, abs=1e-7 * ref.lambda2)
+    return lam, v, info
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_solve_parity_small(fd, orc, name):
+    compare_solve(fd, orc, SMALL[name]())
+
+
+def test_solve_parity_iteration_variants(fd, orc):
+    g = gg.grid2d(40, "uniform", seed=2)
+    for kw in ({"gs_sweeps": 0}, {"power_iters": 0}, {"gs_sweeps": 3, "power_iters": 25},
+               {"seed": 12345}, {"coarsest_size": 100}):
+        compare_solve(fd, orc, g, kw)
+
+
+def test_device_input_equals_host_input(fd, orc):
+    g = gg.grid2d(64, "uniform", seed=9)
+    lam_h, v_h, _ = compare_solve(fd, orc, g)
+    lam_d, v_d, _ = compare_solve(fd, orc, g, device_input=True)
+    assert lam_h == lam_d and np.array_equal(v_h, v_d)
+
+
+def test_repeated_solves_bit_identical(fd):
+    g = gg.rmat(13, 16.0, seed=1)
+    s = fd.FiedlerSolver(g.n, g.rp, g.ci, g.w)
+    a, b = np.empty(g.n), np.empty(g.n)
+    la = s.solve(a)
+    lb = s.solve(b)
+    lc = s.solve(b, use_graph=0)
+    s.close()
+    assert la == lb == lc and np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,make", [
+    ("grid256_uniform(config1_recipe)", lambda: gg.config(1, small=True)),
+    ("rmat14(config2_recipe)", lambda: gg.config(2, small=True)),
+    ("grid3d_40(config3_recipe)", lambda: gg.config(3, small=True)),
+])
+def test_solve_parity_medium(fd, orc, name, make):
+    compare_solve(fd, orc, make())
+
+
+def test_solve_parity_config1_full_size(fd, orc):
+    """BASELINE configs[1] at full size (1024 x 1024, uniform weights):
+    the oracle completes it in seconds, so every output is compared."""
+    compare_solve(fd, orc, gg.config(1))
+
+
+# ------------------------------------------------------------------ error paths
+
+def test_rejects_disconnected(fd):
+    a = gg.grid2d(8)
+    b = gg.grid2d(5)
+    u1, v1, w1 = gg.edges_of(a)
+    u2, v2, w2 = gg.edges_of(b)
+    g = gg.csr_from_edges(a.n + b.n, np.r_[u1, u2 + a.n], np.r_[v1, v2 + a.n], np.r_[w1, w2])
+    with pytest.raises(fd.FiedlerError) as e:
+        fd.fiedler_create(g.n, g.nnz, g.rp, g.ci, g.w)
+    assert e.value.code == fd.FIEDLER_ERR_DISCONNECTED
+
+
+def test_rejects_invalid_csr(fd):
+    g = gg.grid2d(6, "uniform", seed=1)
+    bad = g.w.copy(); bad[3] *= 1.0000001                     # asymmetric
+    with pytest.raises(fd.FiedlerError) as e:
+        fd.fiedler_create(g.n, g.nnz, g.rp, g.ci, bad)
+    assert e.value.code == fd.FIEDLER_ERR_GRAPH
+    bad = g.w.copy(); bad[0] = -1.0
+    with pytest.raises(fd.FiedlerError):
+        fd.fiedler_create(g.n, g.nnz, g.rp, g.ci, bad)
+    ci = g.ci.copy(); ci[0], ci[1] = ci[1], ci[0]            # unsorted row
+    with pytest.raises(fd.FiedlerError):
+        fd.fiedler_create(g.n, g.nnz, g.rp, ci, g.w)
+    rp = g.rp.copy(); rp[3] = rp[4] + 1                      # bad offsets
+    with pytest.raises(fd.FiedlerError):
+        fd.fiedler_create(g.n, g.nnz, rp, g.ci, g.w)
+    with pytest.raises(fd.FiedlerError) as e:
+        fd.fiedler_create(1, 0, np.zeros(2, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    assert e.value.code == fd.FIEDLER_ERR_ARG
