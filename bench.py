@@ -1,0 +1,316 @@
+#!/usr/bin/env python3
+"""bench.py -- Fiedler solve throughput on B200 (driver contract).
+
+One step = the whole hot path on one synthetic graph resident in HBM:
+fiedler_create (Setup Phase: heavy-edge coarsening, prefix-scan numbering,
+Galerkin products, colourings, solve layouts) + fiedler_solve (coarsest power
+iteration, prolongation, multicolour Gauss-Seidel, shifted power iteration,
+Rayleigh quotient) + fiedler_destroy, all through the C ABI.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+Metric: fine-level Laplacian nonzeros (n + adjacency nnz) processed per second
+by complete Fiedler solves, summed over ranks ("nnz/s", higher is better).
+Default workload: BASELINE configs[4], the 8192 x 8192 grid quoted at
+1/2/4/8 B200 (fits one GPU).  Prints ONE JSON line on rank 0.
+
+The reference arm (--impl reference) times the oracle (oracle/, plain C,
+single thread) on the host cores on a bounded sample of the same recipe.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import graphgen as gg  # noqa: E402
+
+METRIC = "fiedler_solve_throughput (Fiedler solve time and SpMV/GS achieved HBM GB/s vs peak)"
+UNIT = "nnz/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--kernel-reps", type=int, default=20)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9
+                          for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_sample_graph(config):
+    """Bounded CPU sample of the same recipe (about 3-5 s of oracle work)."""
+    if config in (1, 4):
+        return gg.grid2d(1024, "uniform", seed=config), "grid2d 1024x1024 uniform[0.5,1.5] (same recipe, 1 solve)"
+    if config == 2:
+        return gg.rmat(17, 16.0, seed=2), "rmat scale 17 deg 16 lcc (same recipe, 1 solve)"
+    if config == 3:
+        return gg.grid3d(64, "lognormal", seed=3), "grid3d 64^3 lognormal(0,0.5) (same recipe, 1 solve)"
+    return gg.grid2d(32, "unit"), "grid2d 32x32 unit (config 0 itself)"
+
+
+def run_oracle_once(g):
+    import oracle
+    G = oracle.Graph.from_csr(g.n, g.rp, g.ci, g.w)
+    t0 = time.perf_counter()
+    r = oracle.solve(G, oracle.Config())
+    dt = time.perf_counter() - t0
+    return dt, r
+
+
+def cpu_baseline(config):
+    g, desc = cpu_sample_graph(config)
+    dt, _ = run_oracle_once(g)
+    return {"value": (g.n + g.nnz) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": desc + ", %.2f s wall" % dt}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the oracle as it stands, on host cores, rank 0 only."""
+    if rank != 0:
+        return
+    g, desc = cpu_sample_graph(args.config)
+    for _ in range(max(args.warmup, 0)):
+        run_oracle_once(g)
+    times = []
+    for _ in range(args.steps):
+        dt, _ = run_oracle_once(g)
+        times.append(dt)
+    tot = sum(times)
+    value = (g.n + g.nnz) * len(times) / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": gg.CONFIG_NAMES[args.config], "sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def traffic_from_profiles():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except ValueError:
+            return None
+    return None
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import paper_1602_04386_b200 as fd
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    g = gg.config(args.config)
+    n, nnz = g.n, g.nnz
+    nnz_L = n + nnz                      # Laplacian nonzeros incl. diagonal
+    dev = torch.device("cuda", local)
+    rp = torch.from_numpy(g.rp).to(dev)
+    ci = torch.from_numpy(g.ci).to(dev)
+    w = torch.from_numpy(g.w).to(dev)
+    vec = torch.empty(n, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    opts = fd.fiedler_default_opts(device=local, validate=0, stream=stream.cuda_stream)
+    # validate the input once (outside the timed region)
+    h = fd.fiedler_create(n, nnz, rp, ci, w, fd.fiedler_default_opts(device=local, validate=1,
+                                                                       stream=stream.cuda_stream))
+    info = fd.fiedler_info()
+    lam = fd.fiedler_solve(h, vec, None, info)
+    fd.fiedler_destroy(h)
+    l2_bytes = 126 * 2 ** 20
+    big = (nnz * 12 + n * 12) > 2 * l2_bytes
+    flush = None if big else torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        hh = fd.fiedler_create(n, nnz, rp, ci, w, opts)
+        fd.fiedler_solve(hh, vec, None, info)
+        fd.fiedler_destroy(hh)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = []
+    launches = 0
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1.0)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        launches += info.launches + info.setup_launches
+    ck = clocks.stop()
+    tot_ms = sum(times)
+    if dist:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = nnz_L * args.steps * world / (tot_ms / 1e3)
+    setup_ms, solve_ms = info.setup_ms, info.solve_ms
+
+    # ---- dominant-kernel roofline: level-0 power-iteration row pass (CUDA events)
+    hh = fd.fiedler_create(n, nnz, rp, ci, w, opts)
+    k_ms, k_bytes = fd.fiedler_level_time(hh, 0, fd.FIEDLER_OP_POWER, args.kernel_reps)
+    gs_ms, gs_bytes = fd.fiedler_level_time(hh, 0, fd.FIEDLER_OP_GS_SWEEPS, args.kernel_reps)
+    rq_ms, rq_bytes = fd.fiedler_level_time(hh, 0, fd.FIEDLER_OP_RAYLEIGH, args.kernel_reps)
+    nlev = fd.fiedler_num_levels(hh)
+    fd.fiedler_destroy(hh)
+    peak, peak_src = load_peaks()
+    achieved = k_bytes / (k_ms / 1e3) / 1e9
+    tr = traffic_from_profiles()
+    traffic = None
+    if tr and tr.get("config") == args.config and tr.get("kernel_bytes_per_launch"):
+        traffic = tr["kernel_bytes_per_launch"]
+
+    # ---- end to end through the public API with HOST buffers (pinned)
+    prp = torch.from_numpy(g.rp).pin_memory()
+    pci = torch.from_numpy(g.ci).pin_memory()
+    pw = torch.from_numpy(g.w).pin_memory()
+    pvec = torch.empty(n, dtype=torch.float64).pin_memory()
+    eo = fd.fiedler_default_opts(device=local, validate=0, stream=stream.cuda_stream)
+
+    def e2e_step():
+        hh2 = fd.fiedler_create(n, nnz, prp, pci, pw, eo)
+        fd.fiedler_solve(hh2, pvec, None, None)
+        fd.fiedler_destroy(hh2)
+
+    e2e_step()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = nnz_L * args.e2e_steps * world / e2e_s
+    h2d = 8 * (n + 1) + 4 * nnz + 8 * nnz
+    d2h = 8 * n + 8
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": gg.CONFIG_NAMES[args.config], "n": n, "adjacency_nnz": nnz,
+                       "laplacian_nnz": nnz_L, "levels": nlev, "gs_sweeps": 2, "power_iters": 10,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": ("inputs larger than L2 (no flush)" if big else "L2 flushed between steps")},
+            "solve_time_ms": tot_ms / args.steps, "setup_ms": setup_ms, "solve_ms": solve_ms,
+            "lambda2": lam,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_rowpass<OP_PI> level 0 (power-iteration step)",
+                         "algorithmic_bytes_per_launch": k_bytes, "launch_ms": k_ms,
+                         "peak_source": peak_src},
+            "kernels": {"gs_sweep_level0": {"ms": gs_ms, "GB/s": gs_bytes / (gs_ms / 1e3) / 1e9,
+                                            "frac": gs_bytes / (gs_ms / 1e3) / 1e9 / peak},
+                        "rayleigh_level0": {"ms": rq_ms, "GB/s": rq_bytes / (rq_ms / 1e3) / 1e9,
+                                            "frac": rq_bytes / (rq_ms / 1e3) / 1e9 / peak}},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -85,6 +85,7 @@ typedef struct fiedler_opts {
 typedef struct fiedler_info {
     int32_t num_levels;                     /* J + 1                                    */
     int32_t launches;                       /* kernels launched by this solve call      */
+    int32_t setup_launches;                 /* kernels launched by fiedler_create        */
     double lambda2;                         /* Rayleigh quotient of the returned vector  */
     double residual_norm;                   /* || L v - lambda2 v ||_2                   */
     double setup_ms;                        /* device time of fiedler_create's setup     */
@@ -168,6 +169,19 @@ FIEDLER_API int fiedler_level_export(fiedler_handle h, int32_t level, int64_t *r
 FIEDLER_API int fiedler_level_apply(fiedler_handle h, int32_t level, int32_t op, int32_t count,
                         const double *x_in, double *x_out, int32_t mem,
                         double *scalar_out);
+
+/* Profiling: time `reps` back-to-back launches of one hot kernel on `level`
+ * with CUDA events on the handle's stream (after one warm-up launch):
+ *   FIEDLER_OP_GS_SWEEPS one full multicolour sweep (all colour launches) per rep,
+ *   FIEDLER_OP_POWER     one power-iteration row pass per rep,
+ *   FIEDLER_OP_RAYLEIGH  one Rayleigh-quotient row pass per rep.
+ * *ms_per_rep = mean device time of one rep; *bytes_per_rep (may be NULL) =
+ * the ALGORITHMIC HBM bytes of one rep (4(n+1) row
+ * offsets + 12 per adjacency nonzero + 8n vector read + 8n vector written,
+ * + 4n + 8n for the Rayleigh pass's natural-order output).  The level's solve
+ * buffers are used as scratch; call between solves, not during one. */
+FIEDLER_API int fiedler_level_time(fiedler_handle h, int32_t level, int32_t op, int32_t reps,
+                                   double *ms_per_rep, double *bytes_per_rep);
 
 #ifdef __cplusplus
 }

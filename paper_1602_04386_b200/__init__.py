@@ -37,7 +37,7 @@ FIEDLER_OP_RAYLEIGH = 4
 
 EXPORTED = ("fiedler_default_opts", "fiedler_create", "fiedler_solve", "fiedler_destroy",
             "fiedler_last_error", "fiedler_num_levels", "fiedler_level_size",
-            "fiedler_level_export", "fiedler_level_apply")
+            "fiedler_level_export", "fiedler_level_apply", "fiedler_level_time")
 
 
 class fiedler_opts(ctypes.Structure):
@@ -50,6 +50,7 @@ class fiedler_opts(ctypes.Structure):
 
 class fiedler_info(ctypes.Structure):
     _fields_ = [("num_levels", ctypes.c_int32), ("launches", ctypes.c_int32),
+                ("setup_launches", ctypes.c_int32),
                 ("lambda2", ctypes.c_double), ("residual_norm", ctypes.c_double),
                 ("setup_ms", ctypes.c_double), ("solve_ms", ctypes.c_double),
                 ("level_n", ctypes.c_int64 * FIEDLER_MAX_LEVELS),
@@ -102,6 +103,9 @@ def _load():
         lib.fiedler_level_size.argtypes = [P, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32)]
         lib.fiedler_level_export.restype = ctypes.c_int
         lib.fiedler_level_export.argtypes = [P, i32, P, P, P, P, P, P]
+        lib.fiedler_level_time.restype = ctypes.c_int
+        lib.fiedler_level_time.argtypes = [P, i32, i32, i32, ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_double)]
         lib.fiedler_level_apply.restype = ctypes.c_int
         lib.fiedler_level_apply.argtypes = [P, i32, i32, i32, P, P, i32, ctypes.POINTER(ctypes.c_double)]
         _lib = lib
@@ -209,6 +213,13 @@ def fiedler_level_apply(handle, level, op, x_in, x_out=None, count=1):
     sc = (ctypes.c_double * 2)()
     _check(_load().fiedler_level_apply(handle, level, op, count, pin, pout, mi, sc))
     return sc[0], sc[1]
+
+
+def fiedler_level_time(handle, level, op, reps=20):
+    """(ms per rep, algorithmic bytes per rep) of one hot kernel (CUDA events)."""
+    ms, by = ctypes.c_double(), ctypes.c_double()
+    _check(_load().fiedler_level_time(handle, level, op, reps, ctypes.byref(ms), ctypes.byref(by)))
+    return ms.value, by.value
 
 
 class FiedlerSolver:

@@ -12,6 +12,7 @@
 namespace fdl {
 
 thread_local std::string g_last_error;
+thread_local long long g_launch_count = 0;
 
 void set_error(const std::string &m) { g_last_error = m; }
 
@@ -178,8 +179,10 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     g0.rp = g0.own_rp.as<int>();
     if (o.validate) validate_input(n, nnz, g0.rp, g0.ci, g0.w, st);
     h->n0 = (int)n;
+    const long long l0 = g_launch_count;
     build_hierarchy(*h, std::move(g0));
     prepare_solve(*h, cfg_of(o));
+    h->setup_launches = (int)(g_launch_count - l0);
     h->setup_ms = timer.stop_ms();
     *out = reinterpret_cast<fiedler_handle>(h.release());
     return FIEDLER_OK;
@@ -248,6 +251,7 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
         std::memset(info, 0, sizeof(*info));
         info->num_levels = (int)h.levels.size();
         info->launches = launches;
+        info->setup_launches = h.setup_launches;
         info->lambda2 = res[0];
         info->residual_norm = res[1];
         info->setup_ms = h.setup_ms;
@@ -335,6 +339,20 @@ int fiedler_level_export(fiedler_handle hh, int32_t level, int64_t *row_ptr, int
         }
     }
     if (row_ptr) row_ptr[n] = off;
+    return FIEDLER_OK;
+    API_END
+}
+
+int fiedler_level_time(fiedler_handle hh, int32_t level, int32_t op, int32_t reps,
+                       double *ms_per_rep, double *bytes_per_rep) {
+    API_BEGIN
+    FDL_REQUIRE(hh && ms_per_rep && reps > 0, FIEDLER_ERR_ARG, "bad argument");
+    Handle &h = *reinterpret_cast<Handle *>(hh);
+    FDL_REQUIRE(level >= 0 && level < (int)h.levels.size(), FIEDLER_ERR_ARG, "bad level");
+    FDL_REQUIRE(op == FIEDLER_OP_GS_SWEEPS || op == FIEDLER_OP_POWER || op == FIEDLER_OP_RAYLEIGH,
+                FIEDLER_ERR_ARG, "bad op");
+    FDL_CK(cudaSetDevice(h.device));
+    time_level_op(h, level, op, reps, ms_per_rep, bytes_per_rep);
     return FIEDLER_OK;
     API_END
 }

@@ -31,7 +31,14 @@ struct Error : std::runtime_error {
                                    " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
     } while (0)
 
-#define FDL_LAUNCH_CK() FDL_CK(cudaGetLastError())
+// Every kernel launch site is followed by FDL_LAUNCH_CK(), which also counts
+// the launch (reported as fiedler_info.setup_launches / launches).
+extern thread_local long long g_launch_count;
+#define FDL_LAUNCH_CK()                 \
+    do {                                \
+        ::fdl::g_launch_count++;        \
+        FDL_CK(cudaGetLastError());     \
+    } while (0)
 
 #define FDL_REQUIRE(cond, code, msg)                                                      \
     do {                                                                                  \

@@ -72,6 +72,7 @@ struct Handle {
     DBuf result;             // {lambda2, residual, ...} (device)
     int row_grid = kNumSMs * 8;   // CTAs of a row pass
     double setup_ms = 0.0;
+    int setup_launches = 0;
     // captured solve graph and the options it was captured with
     cudaGraphExec_t gexec = nullptr;
     int g_gs = -1, g_pi = -1, g_piJ = -1;
@@ -95,5 +96,7 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg);
 // Single-operation entry (fiedler_level_apply); vectors in solve numbering on device.
 void apply_level_op(Handle &h, int level, int op, int count, const double *x_in, double *x_out,
                     double *scal_host);
+// fiedler_level_time: CUDA-event timing of `reps` back-to-back row passes
+void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, double *bytes_per_rep);
 
 }  // namespace fdl

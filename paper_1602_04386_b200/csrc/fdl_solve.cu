@@ -530,3 +530,57 @@ void apply_level_op(Handle &h, int level, int op, int count, const double *x_in,
 }
 
 }  // namespace fdl
+
+namespace fdl {
+// ----------------------------------------------------------------- fiedler_level_time
+void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, double *bytes_per_rep) {
+    const Level &L = h.levels[level];
+    cudaStream_t st = h.stream;
+    ensure_solve_buffers(h, 8);
+    Enq e{h, st};
+    double *xa = h.xa.as<double>(), *xb = h.xb.as<double>();
+    double *s0 = e.slot(0), *s1 = e.slot(1);
+    // finite, non-constant input: the counter-based uniform vector
+    k_rand<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(L.n, L.perm.as<int>(), 7, xa, s0,
+                                                           h.partials.as<double>(), h.counter.as<unsigned>());
+    FDL_LAUNCH_CK();
+    k_set_slot<<<1, 1, 0, st>>>(s1, 1.0, 1.0);
+    FDL_LAUNCH_CK();
+    auto one = [&]() {
+        if (op == FIEDLER_OP_GS_SWEEPS) {
+            e.gs(L, xa, 1, nullptr);
+        } else if (op == FIEDLER_OP_POWER) {
+            e.pi(L, xa, xb, s0, e.slot(2));
+        } else {
+            PassArgs a{};
+            a.x = xa;
+            a.in_stat = s0;
+            a.n = L.n;
+            a.perm = L.perm.as<int>();
+            a.vnat = h.vnat.as<double>();
+            a.sign = s1 + 2;
+            a.result = h.result.as<double>();
+            e.rowpass<OP_RQ>(L, 0, L.nitems, a);
+        }
+    };
+    one();  // warm-up
+    cudaEvent_t a, b;
+    FDL_CK(cudaEventCreate(&a));
+    FDL_CK(cudaEventCreate(&b));
+    FDL_CK(cudaEventRecord(a, st));
+    for (int r = 0; r < reps; r++) one();
+    FDL_CK(cudaEventRecord(b, st));
+    FDL_CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    FDL_CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_per_rep = ms / reps;
+    if (bytes_per_rep) {
+        double n = L.n, nnz = L.nnz;
+        double bytes = 4.0 * (n + 1) + 12.0 * nnz + 8.0 * n + 8.0 * n;
+        if (op == FIEDLER_OP_RAYLEIGH) bytes += 4.0 * n;   // perm read (the 8n write replaces z write)
+        *bytes_per_rep = bytes;
+    }
+}
+}  // namespace fdl
