@@ -164,8 +164,10 @@ __global__ void k_heavy_init(int n, const int *rp, const int *ci, const double *
         if (v < n && sw_lane_ == 0) {
             m[v] = bj;
             ptr[v] = bj;
-            if (bj >= 0) list[atomicAdd(count, 1)] = (int)v;
         }
+        const bool app = v < n && sw_lane_ == 0 && bj >= 0;
+        const int slot = warp_append(app, count);
+        if (app) list[slot] = (int)v;
     }
 }
 
@@ -206,13 +208,13 @@ __global__ void k_repoint(const int *list, const int *count, const int *rp, cons
             }
         }
         argmax_reduce<W>(bw, bh, bj);
-        if (sw_lane_ == 0) {
-            if (rescan) {
-                ptr[v] = bj;
-                if (bj >= 0) keep = true;
-            }
-            if (keep) newlist[atomicAdd(newcount, 1)] = v;
+        if (sw_lane_ == 0 && rescan) {
+            ptr[v] = bj;
+            if (bj >= 0) keep = true;
         }
+        const bool app = sw_lane_ == 0 && keep;
+        const int slot = warp_append(app, newcount);
+        if (app) newlist[slot] = v;
     }
 }
 
@@ -539,10 +541,10 @@ __global__ void k_color_round(const int *list, const int *count, const int *rp, 
             any_big = __any_sync(0xffffffffu, need_big);
         }
         (void)big;
-        if (v >= 0 && sw_lane_ == 0) {
-            if (notready) newlist[atomicAdd(newcount, 1)] = v;
-            else vcolor[v] = col;
-        }
+        if (v >= 0 && sw_lane_ == 0 && !notready) vcolor[v] = col;
+        const bool app = v >= 0 && sw_lane_ == 0 && notready;
+        const int slot = warp_append(app, newcount);
+        if (app) newlist[slot] = v;
     }
 }
 
