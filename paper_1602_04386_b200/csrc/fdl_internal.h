@@ -14,16 +14,18 @@
 
 namespace fdl {
 
-// Row classes of the solve layout (by adjacency nonzeros of the row).
-constexpr int kShortMax = 32;    // class 0: staged through shared-memory tiles
-constexpr int kMediumMax = 1024; // class 1: one warp per row; class 2: one CTA per row
-constexpr int kNumKinds = 3;
-constexpr int kTileNnz = 2048;   // nonzeros per short-row tile (target)
-constexpr int kTileCap = kTileNnz + kShortMax;
-constexpr int kRowsPerMedItem = 8;
+// Tile decomposition of the row passes.  A tile is a
+// run of consecutive rows whose "coordinate" rp[r] + r starts inside a window
+// of kTileT units, so a tile holds at most kTileT rows and its short rows
+// (<= kShortMax nonzeros) end within kTileT + kShortMax nonzeros of the tile's
+// first nonzero: that range is staged into shared memory by bulk copies.
+constexpr int kShortMax = 32;    // longer rows are reduced by a warp from global memory
+constexpr int kTileT = 2048;     // coordinate window per tile
+constexpr int kStageCap = kTileT + kShortMax;
+constexpr int kPadBytes = 64;    // slack after every staged array (bulk copies round up to 16 B)
 
-// A work item of the row-pass kernels: x = kind, y = first row, z = end row.
-using Item = int4;
+// A tile: x = first row, y = end row (exclusive).
+using Tile = int2;
 
 // Natural-numbering CSR of one level during setup.
 struct NatGraph {
@@ -37,22 +39,28 @@ struct NatGraph {
 
 struct Level {
     int n = 0, nnz = 0;
-    // solve layout
-    DBuf rp, ci, w;          // permuted CSR (columns in permuted numbering, order kept)
+    // GS layout: rows sorted by (colour, natural id); every colour is one
+    // contiguous row range; columns in solve numbering (= GS row order).
+    DBuf rp, ci, w;
+    // PI / RQ layout: rows in NATURAL order (spatial locality of the x gathers),
+    // columns in solve numbering; row v's own value / output sits at inv[v].
+    DBuf rpN, ciN, wN;
     DBuf perm;               // int32 [n]: solve row -> natural id
     DBuf inv;                // int32 [n]: natural id -> solve row
     DBuf qp;                 // int32 [n]: solve row -> solve row of its aggregate on level+1
     // natural-numbering setup results kept for fiedler_level_export
     DBuf q_nat, mate_nat, color_nat;
-    // work items: all colours back to back; colour c owns [citem[c], citem[c+1])
-    DBuf items;
-    std::vector<int> citem;
+    // tiles: GS tiles of all colours back to back (colour c owns
+    // [ctile[c], ctile[c+1])), then the natural-order tiles [ctile[ncolors], ntiles)
+    DBuf tiles;
+    std::vector<int> ctile;
     int ncolors = 0;
-    int nitems = 0;
-    int max_item_rows = 0;
+    int ntiles = 0;
     double shift = 0.0;      // c of c I - L: 2 max_i d_i (R8)
     int match_rounds = 0;
     int color_rounds = 0;
+    int gs_tile_begin(int c) const { return ctile[c]; }
+    int nat_tile_begin() const { return ctile[ncolors]; }
 };
 
 struct Handle {

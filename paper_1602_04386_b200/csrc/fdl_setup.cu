@@ -582,11 +582,9 @@ static int color_graph(const NatGraph &g, uint64_t salt, DBuf &color, int &round
 }
 
 // ================================================================= solve layout
-__global__ void k_kind_keys(int n, const int *rp, const int *color, unsigned *keys, int *vals) {
+__global__ void k_color_keys(int n, const int *color, unsigned *keys, int *vals) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        int d = rp[v + 1] - rp[v];
-        int kind = d <= kShortMax ? 0 : (d <= kMediumMax ? 1 : 2);
-        keys[v] = (unsigned)(color[v] * kNumKinds + kind);
+        keys[v] = (unsigned)color[v];
         vals[v] = v;
     }
 }
@@ -604,6 +602,7 @@ __global__ void k_inv_and_deg(int n, const int *perm, const int *rp, int *inv, i
     }
 }
 
+// GS layout rows: row t = natural row perm[t], columns renumbered by inv, order kept
 template <int W>
 __global__ void k_permute_rows(int n, const int *perm, const int *inv, const int *rp, const int *ci,
                                const double *w, const int *rpp, int *cip, double *wp) {
@@ -617,6 +616,19 @@ __global__ void k_permute_rows(int n, const int *perm, const int *inv, const int
             }
         }
     }
+}
+
+// PI/RQ layout: natural rows, columns renumbered by inv (a pure stream)
+__global__ void k_renumber_cols(int nnz, const int *inv, const int *ci, const double *w, int *cin,
+                                double *wn) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x) {
+        cin[k] = inv[ci[k]];
+        wn[k] = w[k];
+    }
+}
+
+__global__ void k_copy_i32(int n, const int *a, int *b) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = a[i];
 }
 
 // max_i d_i with d_i summed in stored (= natural ascending) order, as the oracle
@@ -637,24 +649,27 @@ __global__ void k_gather_i32(int k, const int *src, const int *idx, int *out) {
         out[i] = src[idx[i]];
 }
 
-// short-row tiles of a segment [s0, s1): tile t holds the rows whose first
-// nonzero lies in [P0 + t*kTileNnz, P0 + (t+1)*kTileNnz)
-__device__ __forceinline__ int lower_bound_rows(const int *rp, int lo, int hi, int target) {
+// Tiles of the row range [s0, s1): tile t holds the rows whose coordinate
+// rp[r] + r lies in [C0 + t*kTileT, C0 + (t+1)*kTileT), C0 = rp[s0] + s0.
+// The coordinate is strictly increasing in r, so the bounds are binary searches.
+__device__ __forceinline__ int lower_bound_coord(const int *rp, int lo, int hi, long long target) {
     while (lo < hi) {
         int mid = (lo + hi) >> 1;
-        if (rp[mid] < target) lo = mid + 1; else hi = mid;
+        if ((long long)rp[mid] + mid < target) lo = mid + 1; else hi = mid;
     }
     return lo;
 }
 
-__global__ void k_tiles(const int *rp, int s0, int s1, int ntiles, Item *out) {
-    int P0 = rp[s0];
+__global__ void k_make_tiles(const int *rp, int s0, int s1, int ntiles, Tile *out) {
+    const long long C0 = (long long)rp[s0] + s0;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
-        int a = t == 0 ? s0 : lower_bound_rows(rp, s0, s1, P0 + t * kTileNnz);
-        int b = (t + 1 == ntiles) ? s1 : lower_bound_rows(rp, s0, s1, P0 + (t + 1) * kTileNnz);
-        out[t] = make_int4(0, a, b, 0);
+        int a = t == 0 ? s0 : lower_bound_coord(rp, s0, s1, C0 + (long long)t * kTileT);
+        int b = (t + 1 == ntiles) ? s1 : lower_bound_coord(rp, s0, s1, C0 + (long long)(t + 1) * kTileT);
+        out[t] = make_int2(a, b);
     }
 }
+
+static int tiles_for(long long coord_span) { return std::max(1, (int)((coord_span + kTileT - 1) / kTileT)); }
 
 static void build_layout(const NatGraph &g, const int *color_nat, int ncolors, Level &L,
                          cudaStream_t st) {
@@ -663,14 +678,14 @@ static void build_layout(const NatGraph &g, const int *color_nat, int ncolors, L
     L.n = n;
     L.nnz = g.nnz;
     L.ncolors = ncolors;
-    const int nkeys = ncolors * kNumKinds;
+    // ---- GS layout: rows sorted (stably) by colour
     DBuf keys((size_t)n * 4, st);
     L.perm.alloc((size_t)n * 4, st);
-    k_kind_keys<<<grid_for(n), 256, 0, st>>>(n, g.rp, color_nat, keys.as<unsigned>(), L.perm.as<int>());
+    k_color_keys<<<grid_for(n), 256, 0, st>>>(n, color_nat, keys.as<unsigned>(), L.perm.as<int>());
     FDL_LAUNCH_CK();
-    radix_sort_u32_i32(keys.as<unsigned>(), L.perm.as<int>(), n, bits_for(nkeys - 1), st);
-    DBuf segstart((size_t)(nkeys + 1) * 4, st);
-    FDL_CK(cudaMemsetAsync(segstart.p, 0xff, (size_t)(nkeys + 1) * 4, st));
+    radix_sort_u32_i32(keys.as<unsigned>(), L.perm.as<int>(), n, bits_for(ncolors - 1), st);
+    DBuf segstart((size_t)(ncolors + 1) * 4, st);
+    FDL_CK(cudaMemsetAsync(segstart.p, 0xff, (size_t)(ncolors + 1) * 4, st));
     k_seg_starts<<<grid_for(n), 256, 0, st>>>(n, keys.as<unsigned>(), segstart.as<int>());
     FDL_LAUNCH_CK();
     keys.release();
@@ -678,72 +693,76 @@ static void build_layout(const NatGraph &g, const int *color_nat, int ncolors, L
     DBuf degp((size_t)n * 4, st);
     k_inv_and_deg<<<grid_for(n), 256, 0, st>>>(n, L.perm.as<int>(), g.rp, L.inv.as<int>(), degp.as<int>());
     FDL_LAUNCH_CK();
-    L.rp.alloc((size_t)(n + 1) * 4, st);
+    L.rp.alloc((size_t)(n + 1) * 4 + kPadBytes, st);
     scan_exclusive(degp.as<int>(), L.rp.as<int>(), n, L.rp.as<int>() + n, st);
     degp.release();
-    L.ci.alloc((size_t)std::max(g.nnz, 1) * 4, st);
-    L.w.alloc((size_t)std::max(g.nnz, 1) * 8, st);
+    const size_t ci_bytes = (size_t)std::max(g.nnz, 1) * 4 + kPadBytes;
+    const size_t w_bytes = (size_t)std::max(g.nnz, 1) * 8 + kPadBytes;
+    L.ci.alloc(ci_bytes, st);
+    L.w.alloc(w_bytes, st);
     DISPATCH_W(avg, (k_permute_rows<W><<<sub_grid(n, W), 256, 0, st>>>(
                          n, L.perm.as<int>(), L.inv.as<int>(), g.rp, g.ci, g.w, L.rp.as<int>(),
                          L.ci.as<int>(), L.w.as<double>())));
     FDL_LAUNCH_CK();
+    // ---- PI/RQ layout: natural rows, solve-numbered columns
+    L.rpN.alloc((size_t)(n + 1) * 4 + kPadBytes, st);
+    L.ciN.alloc(ci_bytes, st);
+    L.wN.alloc(w_bytes, st);
+    k_copy_i32<<<grid_for(n + 1), 256, 0, st>>>(n + 1, g.rp, L.rpN.as<int>());
+    FDL_LAUNCH_CK();
+    if (g.nnz) {
+        k_renumber_cols<<<grid_for(g.nnz, 256, kNumSMs * 16), 256, 0, st>>>(
+            g.nnz, L.inv.as<int>(), g.ci, g.w, L.ciN.as<int>(), L.wN.as<double>());
+        FDL_LAUNCH_CK();
+    }
     DBuf dmax(8, st);
     FDL_CK(cudaMemsetAsync(dmax.p, 0, 8, st));
-    k_degree_max<<<grid_for(n, 256, kNumSMs * 8), 256, 0, st>>>(n, L.rp.as<int>(), L.w.as<double>(),
+    k_degree_max<<<grid_for(n, 256, kNumSMs * 8), 256, 0, st>>>(n, g.rp, g.w,
                                                                dmax.as<unsigned long long>());
     FDL_LAUNCH_CK();
 
-    // segment boundaries -> host
-    std::vector<int> seg(nkeys + 1);
-    FDL_CK(cudaMemcpyAsync(seg.data(), segstart.p, (size_t)(nkeys + 1) * 4, cudaMemcpyDeviceToHost, st));
+    // colour segment boundaries and their nonzero offsets -> host
+    std::vector<int> seg(ncolors + 1);
+    FDL_CK(cudaMemcpyAsync(seg.data(), segstart.p, (size_t)(ncolors + 1) * 4, cudaMemcpyDeviceToHost, st));
     double dm = 0.0;
     FDL_CK(cudaMemcpyAsync(&dm, dmax.p, 8, cudaMemcpyDeviceToHost, st));
     FDL_CK(cudaStreamSynchronize(st));
     L.shift = 2.0 * dm;
-    seg[nkeys] = n;
-    for (int k = nkeys - 1; k >= 0; k--)
+    seg[ncolors] = n;
+    for (int k = ncolors - 1; k >= 0; k--)
         if (seg[k] < 0) seg[k] = seg[k + 1];
-    // nnz offsets at segment starts
-    DBuf sidx((size_t)(nkeys + 1) * 4, st), sval((size_t)(nkeys + 1) * 4, st);
-    FDL_CK(cudaMemcpyAsync(sidx.p, seg.data(), (size_t)(nkeys + 1) * 4, cudaMemcpyHostToDevice, st));
-    k_gather_i32<<<1, 256, 0, st>>>(nkeys + 1, L.rp.as<int>(), sidx.as<int>(), sval.as<int>());
+    DBuf sidx((size_t)(ncolors + 1) * 4, st), sval((size_t)(ncolors + 1) * 4, st);
+    FDL_CK(cudaMemcpyAsync(sidx.p, seg.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
+    k_gather_i32<<<1, 256, 0, st>>>(ncolors + 1, L.rp.as<int>(), sidx.as<int>(), sval.as<int>());
     FDL_LAUNCH_CK();
-    std::vector<int> segnnz(nkeys + 1);
-    FDL_CK(cudaMemcpyAsync(segnnz.data(), sval.p, (size_t)(nkeys + 1) * 4, cudaMemcpyDeviceToHost, st));
+    std::vector<int> segnnz(ncolors + 1);
+    FDL_CK(cudaMemcpyAsync(segnnz.data(), sval.p, (size_t)(ncolors + 1) * 4, cudaMemcpyDeviceToHost, st));
     FDL_CK(cudaStreamSynchronize(st));
 
-    // work items, colour by colour: short tiles, medium groups, long rows
-    std::vector<Item> host_items;
-    struct TileJob { int s0, s1, ntiles, at; };
-    std::vector<TileJob> jobs;
-    L.citem.assign(ncolors + 1, 0);
-    L.max_item_rows = 0;
+    // tiles: GS colours, then the natural-order pass
+    L.ctile.assign(ncolors + 1, 0);
+    int nt = 0;
+    std::vector<int> cnt(ncolors + 1);
     for (int c = 0; c < ncolors; c++) {
-        L.citem[c] = (int)host_items.size();
-        int s0 = seg[c * 3 + 0], s1 = seg[c * 3 + 1];
-        if (s1 > s0) {
-            int nz = segnnz[c * 3 + 1] - segnnz[c * 3 + 0];
-            int nt = std::max(1, div_up(nz, kTileNnz));
-            jobs.push_back({s0, s1, nt, (int)host_items.size()});
-            host_items.resize(host_items.size() + nt, make_int4(0, 0, 0, 0));
+        L.ctile[c] = nt;
+        long long span = (long long)(segnnz[c + 1] + seg[c + 1]) - (segnnz[c] + seg[c]);
+        cnt[c] = seg[c + 1] > seg[c] ? tiles_for(span) : 0;
+        nt += cnt[c];
+    }
+    L.ctile[ncolors] = nt;
+    cnt[ncolors] = tiles_for((long long)g.nnz + n);
+    nt += cnt[ncolors];
+    L.ntiles = nt;
+    L.tiles.alloc((size_t)nt * sizeof(Tile), st);
+    for (int c = 0; c < ncolors; c++)
+        if (cnt[c]) {
+            k_make_tiles<<<grid_for(cnt[c]), 256, 0, st>>>(L.rp.as<int>(), seg[c], seg[c + 1], cnt[c],
+                                                           L.tiles.as<Tile>() + L.ctile[c]);
+            FDL_LAUNCH_CK();
         }
-        int m0 = seg[c * 3 + 1], m1 = seg[c * 3 + 2];
-        for (int r = m0; r < m1; r += kRowsPerMedItem)
-            host_items.push_back(make_int4(1, r, std::min(r + kRowsPerMedItem, m1), 0));
-        int l0 = seg[c * 3 + 2], l1 = seg[c * 3 + 3];
-        for (int r = l0; r < l1; r++) host_items.push_back(make_int4(2, r, r + 1, 0));
-    }
-    L.citem[ncolors] = (int)host_items.size();
-    L.nitems = (int)host_items.size();
-    L.items.alloc((size_t)std::max(L.nitems, 1) * sizeof(Item), st);
-    FDL_CK(cudaMemcpyAsync(L.items.p, host_items.data(), (size_t)L.nitems * sizeof(Item),
-                           cudaMemcpyHostToDevice, st));
-    for (auto &j : jobs) {
-        k_tiles<<<grid_for(j.ntiles), 256, 0, st>>>(L.rp.as<int>(), j.s0, j.s1, j.ntiles,
-                                                    L.items.as<Item>() + j.at);
-        FDL_LAUNCH_CK();
-    }
-    FDL_CK(cudaStreamSynchronize(st));  // host_items must outlive the copy
+    k_make_tiles<<<grid_for(cnt[ncolors]), 256, 0, st>>>(L.rpN.as<int>(), 0, n, cnt[ncolors],
+                                                         L.tiles.as<Tile>() + L.ctile[ncolors]);
+    FDL_LAUNCH_CK();
 }
 
 // ================================================================= connectivity (coarsest level)

@@ -1,23 +1,31 @@
 // fdl_solve.cu -- Steps 2-3 of Algorithm 3 and the final
-// Rayleigh quotient, as row-pass kernels over the solve layout.
+// Rayleigh quotient, as tile-pass kernels over the two solve layouts.
 //
-// One row-pass kernel serves the three HBM-bound sweeps of the path:
+// One tile-pass kernel serves the three HBM-bound sweeps of the path:
 //   OP_GS  multicolour Gauss-Seidel on L x = 0 (Algorithm 2 line 87 with
-//          b = 0: x_i = sum_j w_ij x_j / d_i, in place, one colour per launch);
+//          b = 0: x_i = sum_j w_ij x_j / d_i, in place, one colour per launch),
+//          over the GS layout (rows sorted by colour);
 //   OP_PI  one step of power iteration on c I - L with deflation (R5, R8):
 //          z_i = [c (y_i - mu) + sum_j w_ij (y_j - y_i)] / sigma, where (mu, sigma)
 //          are the mean / deflated norm of y from the previous pass (lazy
 //          deflate + normalise: the whole step is ONE pass over the level);
 //   OP_RQ  Rayleigh quotient of v = s (z - mu) / sigma with the edge form
-//          sum_ij w_ij (z_i - z_j)^2 (R7), ||L v||, and v scattered to natural order.
+//          sum_ij w_ij (z_i - z_j)^2 (R7), ||L v||, and v written in natural order.
+//   PI and RQ walk the rows in NATURAL order (columns in solve numbering, own
+//   value / output at inv[v]) so the x gathers of neighbouring rows stay
+//   L2-local; GS walks its colour's contiguous row range.
 // d_i = sum_j w_ij is recomputed on the fly from the streamed weights (no
 // degree array is read).  Every pass produces its reductions with a
 // deterministic two-level tree (per-CTA partials, last CTA folds them in
 // fixed order), so results are bit-reproducible run to run.
 //
-// Work decomposition (fdl_internal.h): short rows (<= 32 nnz) in tiles of
-// ~2048 nonzeros whose column/weight streams are staged through shared memory
-// with coalesced loads, medium rows one warp each, long rows one CTA each.
+// Data movement: persistent CTAs walk their tiles (fdl_internal.h) with a
+// two-stage pipeline: while a tile is computed, one thread has already issued
+// the bulk copies (cp.async.bulk, TMA engine, L2 evict-first hint) of the next
+// tile's column and weight streams into the other shared-memory stage, tracked
+// by an mbarrier with a transaction count.  Rows with <= 32 nonzeros are
+// reduced by one thread from shared memory; longer rows by a warp (or, for a
+// row longer than a tile, the whole CTA) straight from global memory.
 #include <algorithm>
 #include <cmath>
 
@@ -26,10 +34,23 @@
 namespace fdl {
 
 enum { OP_GS = 0, OP_PI = 1, OP_RQ = 2 };
-constexpr int kRowThreads = 256;
+constexpr int kPassThreads = 256;
+constexpr int kPassWarps = kPassThreads / 32;
 constexpr int kNumStats = 3;
+constexpr int kCiBuf = kStageCap + 8;   // + start alignment (<= 3) + 16-byte round-up (<= 3)
+constexpr int kWBuf = kStageCap + 4;    // + start alignment (<= 1) + round-up (<= 1)
 
-struct LevelView {
+struct __align__(16) StageBuf {
+    double w[kWBuf];
+    int ci[kCiBuf];
+};
+struct __align__(16) PassSmem {
+    StageBuf st[2];
+    unsigned long long bar[2];
+};
+static_assert(sizeof(double) * kWBuf % 16 == 0 && sizeof(int) * kCiBuf % 16 == 0, "stage alignment");
+
+struct CsrView {
     int n;
     const int *rp;
     const int *ci;
@@ -39,6 +60,7 @@ struct LevelView {
 struct PassArgs {
     const double *x;        // input (GS: in/out)
     double *y;              // output (PI)
+    const int *oidx;        // PI/RQ: natural row -> solve position of its own value / output
     const double *in_stat;  // slot of the input vector: [2]=mu, [3]=sigma
     double *out_stat;       // slot receiving S, Q, mu, sigma
     int stat_mode;          // bit0: first contribution (assign), bit1: last (finalise), bit2: wanted
@@ -46,11 +68,54 @@ struct PassArgs {
     double shift;           // c
     double *partials;       // [grid][kNumStats]
     unsigned *counter;
-    const int *perm;        // RQ: solve row -> natural id
     double *vnat;           // RQ: output vector, natural order
     const double *sign;     // RQ: +-1
     double *result;         // RQ: {lambda2, residual}
 };
+
+// ----------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// bulk copy global -> shared (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar, unsigned long long pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ unsigned round16(unsigned b) { return (b + 15u) & ~15u; }
 
 // ----------------------------------------------------------------- per-row math
 template <int OP> struct RowAcc {
@@ -62,11 +127,24 @@ template <int OP> struct RowAcc {
         else { double d = own - xj; a = fma(wk * d, d, a); b = fma(wk, d, b); }
     }
     __device__ __forceinline__ void merge(const RowAcc &o) { a += o.a; b += o.b; }
+    __device__ __forceinline__ void warp_sum() {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (OP != OP_PI) b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+    }
 };
 
 struct Scal {
     double mu, inv_sigma, sigma, sign;
 };
+
+// own value of row r (PI / RQ: natural row r lives at solve position oidx[r])
+template <int OP>
+__device__ __forceinline__ double own_of(int r, const PassArgs &a) {
+    return OP == OP_GS ? 0.0 : a.x[a.oidx[r]];
+}
 
 // row epilogue: write result, accumulate statistics st[0..2]
 template <int OP>
@@ -79,12 +157,12 @@ __device__ __forceinline__ void row_finish(int r, const RowAcc<OP> &acc, const P
         st[1] = fma(xn, xn, st[1]);
     } else if (OP == OP_PI) {
         double z = (a.shift * (acc.own - sc.mu) + acc.a) * sc.inv_sigma;
-        a.y[r] = z;
+        a.y[a.oidx[r]] = z;
         st[0] += z;
         st[1] = fma(z, z, st[1]);
     } else {
         double zc = acc.own - sc.mu;
-        a.vnat[a.perm[r]] = sc.sign * zc * sc.inv_sigma;
+        a.vnat[r] = sc.sign * zc * sc.inv_sigma;
         double lv = acc.b * sc.inv_sigma;
         st[0] += acc.a;
         st[1] = fma(zc, zc, st[1]);
@@ -157,14 +235,21 @@ __device__ __forceinline__ void finish_stats(const double tot[kNumStats], double
     }
 }
 
-// ----------------------------------------------------------------- the row pass
+// ----------------------------------------------------------------- the tile pass
 template <int OP>
-__global__ void __launch_bounds__(kRowThreads) k_rowpass(const Item *__restrict__ items, int nitems,
-                                                         LevelView L, PassArgs a) {
-    __shared__ int s_ci[kTileCap];
-    __shared__ double s_w[kTileCap];
-    __shared__ RowAcc<OP> s_red[kRowThreads / 32];
+__global__ void __launch_bounds__(kPassThreads) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
+                                                           CsrView L, PassArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PassSmem &S = *reinterpret_cast<PassSmem *>(smem_raw);
+    __shared__ RowAcc<OP> s_red[kPassWarps];
+    const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const double *__restrict__ x = a.x;
+    if (tid == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
     Scal sc{0.0, 1.0, 1.0, 1.0};
     if (OP != OP_GS) {
         sc.mu = a.in_stat[2];
@@ -173,64 +258,96 @@ __global__ void __launch_bounds__(kRowThreads) k_rowpass(const Item *__restrict_
         if (OP == OP_RQ) sc.sign = *a.sign;
     }
     double st[kNumStats] = {0.0, 0.0, 0.0};
-    const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    unsigned long long pol = 0;
+    if (tid == 0) pol = evict_first_policy();
 
-    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const Item item = items[it];
-        if (item.x == 0) {
-            // ---- short rows: stage the tile's column/weight streams in smem
-            const int r0 = item.y, r1 = item.z;
-            const int e0 = L.rp[r0], e1 = L.rp[r1];
-            const int cnt = e1 - e0;
-            for (int k = tid; k < cnt; k += kRowThreads) {
-                s_ci[k] = __ldcs(L.ci + e0 + k);
-                s_w[k] = __ldcs(L.w + e0 + k);
-            }
-            __syncthreads();
-            for (int r = r0 + tid; r < r1; r += kRowThreads) {
-                const int b = L.rp[r] - e0, e = L.rp[r + 1] - e0;
-                RowAcc<OP> acc;
-                if (OP != OP_GS) acc.own = x[r];
-                for (int k = b; k < e; k++) acc.add(s_w[k], __ldg(x + s_ci[k]));
-                row_finish<OP>(r, acc, a, sc, st);
-            }
-            __syncthreads();
-        } else if (item.x == 1) {
-            // ---- medium rows: one warp per row
-            const int r = item.y + warp;
-            if (r < item.z) {
-                const int b = L.rp[r], e = L.rp[r + 1];
-                RowAcc<OP> acc;
-                if (OP != OP_GS) acc.own = x[r];
-                for (int k = b + lane; k < e; k += 32) acc.add(__ldcs(L.w + k), __ldg(x + __ldcs(L.ci + k)));
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    acc.a += __shfl_xor_sync(0xffffffffu, acc.a, o);
-                    acc.b += __shfl_xor_sync(0xffffffffu, acc.b, o);
-                }
-                if (lane == 0) row_finish<OP>(r, acc, a, sc, st);
-            }
+    // one thread stages the streams of tile `ti` into stage `b`
+    auto issue = [&](int ti, int b) {
+        const Tile t = tiles[ti];
+        const int e0 = L.rp[t.x], e1 = L.rp[t.y];
+        const int cnt = min(e1 - e0, kStageCap);
+        if (cnt > 0) {
+            const int a4 = e0 & ~3, a2 = e0 & ~1;
+            const unsigned bci = round16((unsigned)(e0 + cnt - a4) * 4u);
+            const unsigned bw = round16((unsigned)(e0 + cnt - a2) * 8u);
+            mbar_arrive_expect_tx(&S.bar[b], bci + bw);
+            bulk_g2s(S.st[b].ci, L.ci + a4, bci, &S.bar[b], pol);
+            bulk_g2s(S.st[b].w, L.w + a2, bw, &S.bar[b], pol);
         } else {
-            // ---- long rows: one CTA per row
-            const int r = item.y;
-            const int b = L.rp[r], e = L.rp[r + 1];
-            RowAcc<OP> acc;
-            if (OP != OP_GS) acc.own = x[r];
-            for (int k = b + tid; k < e; k += kRowThreads) acc.add(__ldcs(L.w + k), __ldg(x + __ldcs(L.ci + k)));
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                acc.a += __shfl_xor_sync(0xffffffffu, acc.a, o);
-                acc.b += __shfl_xor_sync(0xffffffffu, acc.b, o);
-            }
-            if (lane == 0) s_red[warp] = acc;
-            __syncthreads();
-            if (tid == 0) {
-                RowAcc<OP> t = s_red[0];
-                for (int k = 1; k < kRowThreads / 32; k++) t.merge(s_red[k]);
-                row_finish<OP>(r, t, a, sc, st);
-            }
-            __syncthreads();
+            mbar_arrive_expect_tx(&S.bar[b], 0u);
         }
+    };
+
+    int it = 0;
+    if (tid == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, it++) {
+        const int b = it & 1;
+        if (tid == 0 && ti + (int)gridDim.x < ntiles) {
+            fence_proxy_async();   // generic reads of stage b^1 (previous tile) before async writes
+            issue(ti + gridDim.x, b ^ 1);
+        }
+        const Tile t = tiles[ti];
+        const int e0 = L.rp[t.x];
+        const int a4 = e0 & ~3, a2 = e0 & ~1;
+        const int *__restrict__ sci = S.st[b].ci - a4;   // index with the global entry number
+        const double *__restrict__ sw = S.st[b].w - a2;
+        // prefetch the first row's offsets before waiting for the stage
+        int r = t.x + tid;
+        int rb = 0, re = 0;
+        if (r < t.y) { rb = L.rp[r]; re = L.rp[r + 1]; }
+        mbar_wait(&S.bar[b], (unsigned)(it >> 1) & 1u);
+        int has_long = 0;
+        for (; r < t.y;) {
+            if (re - rb <= kShortMax) {
+                RowAcc<OP> acc;
+                if (OP != OP_GS) acc.own = own_of<OP>(r, a);
+                for (int k = rb; k < re; k++) acc.add(sw[k], __ldg(x + sci[k]));
+                row_finish<OP>(r, acc, a, sc, st);
+            } else {
+                has_long = 1;
+            }
+            r += kPassThreads;
+            if (r < t.y) { rb = L.rp[r]; re = L.rp[r + 1]; }
+        }
+        if (__syncthreads_or(has_long)) {
+            // rows with > 32 nonzeros: one warp each, from global memory; a row longer
+            // than a tile is necessarily the tile's last row and gets the whole CTA
+            const int last = t.y - 1;
+            const int last_len = L.rp[t.y] - L.rp[last];
+            const bool cta_last = last_len > kTileT;
+            for (int base = t.x + warp * 32; base < t.y; base += kPassThreads) {
+                const int rr = base + lane;
+                int len = 0;
+                if (rr < t.y) len = L.rp[rr + 1] - L.rp[rr];
+                unsigned m = __ballot_sync(0xffffffffu, len > kShortMax && !(cta_last && rr == last));
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int row = base + src;
+                    const int kb = L.rp[row], ke = L.rp[row + 1];
+                    RowAcc<OP> acc;
+                    if (OP != OP_GS) acc.own = own_of<OP>(row, a);
+                    for (int k = kb + lane; k < ke; k += 32) acc.add(__ldcs(L.w + k), __ldg(x + __ldcs(L.ci + k)));
+                    acc.warp_sum();
+                    if (lane == 0) row_finish<OP>(row, acc, a, sc, st);
+                }
+            }
+            if (cta_last) {
+                const int kb = L.rp[last], ke = L.rp[t.y];
+                RowAcc<OP> acc;
+                if (OP != OP_GS) acc.own = own_of<OP>(last, a);
+                for (int k = kb + tid; k < ke; k += kPassThreads) acc.add(__ldcs(L.w + k), __ldg(x + __ldcs(L.ci + k)));
+                acc.warp_sum();
+                if (lane == 0) s_red[warp] = acc;
+                __syncthreads();
+                if (tid == 0) {
+                    RowAcc<OP> tot = s_red[0];
+                    for (int k = 1; k < kPassWarps; k++) tot.merge(s_red[k]);
+                    row_finish<OP>(last, tot, a, sc, st);
+                }
+            }
+        }
+        __syncthreads();   // stage b may be overwritten by the copy issued next iteration
     }
     if (OP == OP_GS && !(a.stat_mode & 4)) return;   // uniform: statistics not wanted
     grid_reduce(st, a.partials, a.counter, [&](const double *tot) {
@@ -317,21 +434,26 @@ __global__ void k_normalise(int n, double *z, const double *slot) {
 }
 
 // ----------------------------------------------------------------- host-side schedule
+constexpr size_t kPassSmemBytes = sizeof(PassSmem);
+
 struct Enq {
     Handle &h;
     cudaStream_t st;
     int launches = 0;
     double *slot(int k) { return h.scal.as<double>() + 4 * k; }
 
+    // OP over tiles [tb, te) of level L (GS: GS layout; PI/RQ: natural layout)
     template <int OP>
-    void rowpass(const Level &L, int ib, int ie, PassArgs a) {
-        int ni = ie - ib;
-        if (ni <= 0) return;
-        int grid = std::min(ni, h.row_grid);
+    void pass(const Level &L, int tb, int te, PassArgs a) {
+        int nt = te - tb;
+        if (nt <= 0) return;
+        int grid = std::min(nt, h.row_grid);
         a.partials = h.partials.as<double>();
         a.counter = h.counter.as<unsigned>();
-        LevelView v{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()};
-        k_rowpass<OP><<<grid, kRowThreads, 0, st>>>(L.items.as<Item>() + ib, ni, v, a);
+        CsrView v = OP == OP_GS ? CsrView{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()}
+                                : CsrView{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
+        if (OP != OP_GS) a.oidx = L.inv.as<int>();
+        k_tilepass<OP><<<grid, kPassThreads, kPassSmemBytes, st>>>(L.tiles.as<Tile>() + tb, nt, v, a);
         FDL_LAUNCH_CK();
         launches++;
     }
@@ -344,7 +466,7 @@ struct Enq {
                 bool want = (s == sweeps - 1) && out_slot;
                 a.out_stat = out_slot;
                 a.stat_mode = want ? (4 | (c == 0 ? 1 : 0) | (c == L.ncolors - 1 ? 2 : 0)) : 0;
-                rowpass<OP_GS>(L, L.citem[c], L.citem[c + 1], a);
+                pass<OP_GS>(L, L.ctile[c], L.ctile[c + 1], a);
             }
     }
     void pi(const Level &L, const double *x, double *y, const double *in_slot, double *out_slot) {
@@ -356,7 +478,17 @@ struct Enq {
         a.stat_mode = 7;
         a.n = L.n;
         a.shift = L.shift;
-        rowpass<OP_PI>(L, 0, L.nitems, a);
+        pass<OP_PI>(L, L.nat_tile_begin(), L.ntiles, a);
+    }
+    void rq(const Level &L, const double *x, const double *in_slot, double *vnat, const double *sign) {
+        PassArgs a{};
+        a.x = x;
+        a.in_stat = in_slot;
+        a.n = L.n;
+        a.vnat = vnat;
+        a.sign = sign;
+        a.result = h.result.as<double>();
+        pass<OP_RQ>(L, L.nat_tile_begin(), L.ntiles, a);
     }
     void prolong(const Level &L, const double *xc, double *y, double *out_slot) {
         k_prolong<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(
@@ -397,16 +529,24 @@ int prepare_solve(Handle &h, const SolveCfg &cfg) {
     return 0;
 }
 
+// CTAs of a pass: resident CTAs per SM x SMs (persistent tile loop)
 int rowpass_grid() {
+    static int cached = 0;
+    if (cached) return cached;
+    const int smem = (int)kPassSmemBytes;
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_RQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int b0 = 0, b1 = 0, b2 = 0;
-    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_rowpass<OP_GS>, kRowThreads, 0));
-    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_rowpass<OP_PI>, kRowThreads, 0));
-    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_rowpass<OP_RQ>, kRowThreads, 0));
+    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_tilepass<OP_GS>, kPassThreads, smem));
+    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_tilepass<OP_PI>, kPassThreads, smem));
+    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_tilepass<OP_RQ>, kPassThreads, smem));
     int b = std::max(1, std::min(b0, std::min(b1, b2)));
     int dev = 0, sms = kNumSMs;
     FDL_CK(cudaGetDevice(&dev));
     FDL_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    return sms * b;
+    cached = sms * b;
+    return cached;
 }
 
 int enqueue_solve(Handle &h, const SolveCfg &cfg) {
@@ -455,15 +595,7 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
     k_sign<<<1, 32, 0, h.stream>>>(L0.n, L0.inv.as<int>(), cur, cur_slot, sgn);
     FDL_LAUNCH_CK();
     e.launches++;
-    PassArgs a{};
-    a.x = cur;
-    a.in_stat = cur_slot;
-    a.n = L0.n;
-    a.perm = L0.perm.as<int>();
-    a.vnat = h.vnat.as<double>();
-    a.sign = sgn;
-    a.result = h.result.as<double>();
-    e.rowpass<OP_RQ>(L0, 0, L0.nitems, a);
+    e.rq(L0, cur, cur_slot, h.vnat.as<double>(), sgn);
     FDL_REQUIRE(sl <= nslots, FIEDLER_ERR_INTERNAL, "slot overflow");
     return e.launches;
 }
@@ -481,10 +613,12 @@ void apply_level_op(Handle &h, int level, int op, int count, const double *x_in,
     if (op == FIEDLER_OP_PROLONG) {
         const Level &C = h.levels[level + 1];
         k_gather_f64<<<grid_for(C.n), 256, 0, st>>>(C.n, C.perm.as<int>(), x_in, xa);
+        FDL_LAUNCH_CK();
         e.prolong(L, xa, xb, s0);
         k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), xb, x_out);
         FDL_LAUNCH_CK();
         FDL_CK(cudaMemcpyAsync(res, s0, 32, cudaMemcpyDeviceToHost, st));
+        FDL_CK(cudaStreamSynchronize(st));
         if (scal_host) { scal_host[0] = res[2]; scal_host[1] = res[3]; }
     } else {
         k_gather_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), x_in, xa);
@@ -494,33 +628,34 @@ void apply_level_op(Handle &h, int level, int op, int count, const double *x_in,
             k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), xa, x_out);
             FDL_LAUNCH_CK();
             FDL_CK(cudaMemcpyAsync(res, s0, 32, cudaMemcpyDeviceToHost, st));
+            FDL_CK(cudaStreamSynchronize(st));
             if (scal_host) { scal_host[0] = res[2]; scal_host[1] = res[3]; }
         } else if (op == FIEDLER_OP_POWER) {
             k_set_slot<<<1, 1, 0, st>>>(s0, 0.0, 1.0);
+            FDL_LAUNCH_CK();
             double *cur = xa, *oth = xb, *cs = s0, *ns = s1;
             for (int k = 0; k < count; k++) {
                 e.pi(L, cur, oth, cs, ns);
                 std::swap(cur, oth);
                 std::swap(cs, ns);
             }
-            if (count > 0) k_normalise<<<grid_for(L.n), 256, 0, st>>>(L.n, cur, cs);
+            if (count > 0) {
+                k_normalise<<<grid_for(L.n), 256, 0, st>>>(L.n, cur, cs);
+                FDL_LAUNCH_CK();
+            }
             k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), cur, x_out);
             FDL_LAUNCH_CK();
             FDL_CK(cudaMemcpyAsync(res, cs, 32, cudaMemcpyDeviceToHost, st));
+            FDL_CK(cudaStreamSynchronize(st));
             if (scal_host) { scal_host[0] = res[2]; scal_host[1] = res[3]; }
         } else if (op == FIEDLER_OP_RAYLEIGH) {
             k_set_slot<<<1, 1, 0, st>>>(s0, 0.0, 1.0);
-            k_set_slot<<<1, 1, 0, st>>>(s1, 1.0, 1.0);   // sign = slot1[0]... use [2]
-            PassArgs a{};
-            a.x = xa;
-            a.in_stat = s0;
-            a.n = L.n;
-            a.perm = L.perm.as<int>();
-            a.vnat = xb;     // scratch (natural order)
-            a.sign = s1 + 2;
-            a.result = h.result.as<double>();
-            e.rowpass<OP_RQ>(L, 0, L.nitems, a);
+            FDL_LAUNCH_CK();
+            k_set_slot<<<1, 1, 0, st>>>(s1, 1.0, 1.0);   // sign = +1 at s1[2]
+            FDL_LAUNCH_CK();
+            e.rq(L, xa, s0, xb, s1 + 2);                 // xb: natural-order scratch
             FDL_CK(cudaMemcpyAsync(res, h.result.p, 24, cudaMemcpyDeviceToHost, st));
+            FDL_CK(cudaStreamSynchronize(st));
             if (scal_host) { scal_host[0] = res[0]; scal_host[1] = res[1]; }
         } else {
             throw Error(FIEDLER_ERR_ARG, "unknown op");
@@ -529,9 +664,6 @@ void apply_level_op(Handle &h, int level, int op, int count, const double *x_in,
     FDL_CK(cudaStreamSynchronize(st));
 }
 
-}  // namespace fdl
-
-namespace fdl {
 // ----------------------------------------------------------------- fiedler_level_time
 void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, double *bytes_per_rep) {
     const Level &L = h.levels[level];
@@ -547,21 +679,9 @@ void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, d
     k_set_slot<<<1, 1, 0, st>>>(s1, 1.0, 1.0);
     FDL_LAUNCH_CK();
     auto one = [&]() {
-        if (op == FIEDLER_OP_GS_SWEEPS) {
-            e.gs(L, xa, 1, nullptr);
-        } else if (op == FIEDLER_OP_POWER) {
-            e.pi(L, xa, xb, s0, e.slot(2));
-        } else {
-            PassArgs a{};
-            a.x = xa;
-            a.in_stat = s0;
-            a.n = L.n;
-            a.perm = L.perm.as<int>();
-            a.vnat = h.vnat.as<double>();
-            a.sign = s1 + 2;
-            a.result = h.result.as<double>();
-            e.rowpass<OP_RQ>(L, 0, L.nitems, a);
-        }
+        if (op == FIEDLER_OP_GS_SWEEPS) e.gs(L, xa, 1, nullptr);
+        else if (op == FIEDLER_OP_POWER) e.pi(L, xa, xb, s0, e.slot(2));
+        else e.rq(L, xa, s0, h.vnat.as<double>(), s1 + 2);
     };
     one();  // warm-up
     cudaEvent_t a, b;
@@ -577,10 +697,11 @@ void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, d
     cudaEventDestroy(b);
     *ms_per_rep = ms / reps;
     if (bytes_per_rep) {
+        // algorithmic bytes of one pass: row offsets, columns
+        // and weights once, the input vector once, the output vector once
         double n = L.n, nnz = L.nnz;
-        double bytes = 4.0 * (n + 1) + 12.0 * nnz + 8.0 * n + 8.0 * n;
-        if (op == FIEDLER_OP_RAYLEIGH) bytes += 4.0 * n;   // perm read (the 8n write replaces z write)
-        *bytes_per_rep = bytes;
+        *bytes_per_rep = 4.0 * (n + 1) + 12.0 * nnz + 8.0 * n + 8.0 * n;
     }
 }
+
 }  // namespace fdl
