@@ -116,6 +116,30 @@ def random_connected(n: int, extra: int, seed: int, wlo: float = 0.0, whi: float
     return csr_from_edges(n, a, b, w, "rand%d_%d" % (n, seed))
 
 
+def hub_graph(n: int, chords: int, hubs: int = 1, seed: int = 0) -> CSRGraph:
+    """`hubs` hub vertices joined to every other vertex, plus `chords` random
+    edges among the non-hub vertices; weights uniform (0, 1].  Exercises rows
+    and aggregates far longer than a warp (power-law extremes)."""
+    rng = np.random.default_rng(seed)
+    us, vs = [], []
+    for h in range(hubs):
+        others = np.arange(hubs, n)
+        us.append(np.full(others.size, h)); vs.append(others)
+    a = rng.integers(hubs, n, chords)
+    b = rng.integers(hubs, n, chords)
+    us.append(a); vs.append(b)
+    if hubs > 1:
+        hh = np.triu_indices(hubs, 1)
+        us.append(hh[0]); vs.append(hh[1])
+    u = np.concatenate(us); v = np.concatenate(vs)
+    keep = u != v
+    lo, hi = np.minimum(u[keep], v[keep]), np.maximum(u[keep], v[keep])
+    key = np.unique(lo * n + hi)
+    lo, hi = key // n, key % n
+    w = 1.0 - rng.random(lo.size)
+    return csr_from_edges(n, lo, hi, w, "hub%d_%d" % (n, hubs))
+
+
 def _grid_weights(rng, size, weights, lo, hi, mu, sigma):
     if weights == "unit":
         return np.ones(size)

@@ -3,6 +3,9 @@
 // solve schedule, and error translation.  All numerical work is in
 // fdl_setup.cu / fdl_solve.cu kernels; there is no CPU fallback.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -12,6 +15,25 @@
 namespace fdl {
 
 thread_local std::string g_last_error;
+
+bool trace_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = std::getenv("FIEDLER_TRACE");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+
+void trace_mark(cudaStream_t st, const char *what) {
+    if (!trace_enabled()) return;
+    static thread_local auto last = std::chrono::steady_clock::now();
+    if (st) cudaStreamSynchronize(st);
+    auto now = std::chrono::steady_clock::now();
+    double ms = std::chrono::duration<double, std::milli>(now - last).count();
+    std::fprintf(stderr, "[fiedler trace] %-40s %9.3f ms\n", what, ms);
+    last = now;
+}
 thread_local long long g_launch_count = 0;
 
 void set_error(const std::string &m) { g_last_error = m; }
@@ -51,15 +73,20 @@ struct EventTimer {
 };
 
 static void check_device(int dev) {
+    // the capability check runs once per device (cudaGetDeviceProperties costs ~10 ms)
+    static int checked[64] = {0};
     int count = 0;
     FDL_CK(cudaGetDeviceCount(&count));
-    FDL_REQUIRE(dev >= 0 && dev < count, FIEDLER_ERR_CUDA, "no such CUDA device");
+    FDL_REQUIRE(dev >= 0 && dev < count && dev < 64, FIEDLER_ERR_CUDA, "no such CUDA device");
     FDL_CK(cudaSetDevice(dev));
-    cudaDeviceProp p;
-    FDL_CK(cudaGetDeviceProperties(&p, dev));
-    FDL_REQUIRE(p.major == 10, FIEDLER_ERR_CUDA,
-                "libfiedler is built for sm_100a (B200); device is sm_" + std::to_string(p.major) +
-                    std::to_string(p.minor));
+    if (checked[dev]) return;
+    int major = 0, minor = 0;
+    FDL_CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    FDL_CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+    FDL_REQUIRE(major == 10, FIEDLER_ERR_CUDA,
+                "libfiedler is built for sm_100a (B200); device is sm_" + std::to_string(major) +
+                    std::to_string(minor));
+    checked[dev] = 1;
     static bool pool_done = false;
     if (!pool_done) {
         cudaMemPool_t pool;
@@ -139,7 +166,9 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     FDL_REQUIRE(o.coarsest_size >= 2 && o.max_levels >= 1 && o.max_levels <= FIEDLER_MAX_LEVELS &&
                     o.gs_sweeps >= 0 && o.power_iters >= 0,
                 FIEDLER_ERR_ARG, "invalid options");
+    trace_mark(nullptr, "create: enter");
     check_device(o.device);
+    trace_mark(nullptr, "create: check_device");
 
     std::unique_ptr<Handle> h(new Handle());
     h->device = o.device;
@@ -179,9 +208,11 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     g0.rp = g0.own_rp.as<int>();
     if (o.validate) validate_input(n, nnz, g0.rp, g0.ci, g0.w, st);
     h->n0 = (int)n;
+    trace_mark(st, "create: input staging");
     const long long l0 = g_launch_count;
     build_hierarchy(*h, std::move(g0));
     prepare_solve(*h, cfg_of(o));
+    trace_mark(st, "create: prepare_solve");
     h->setup_launches = (int)(g_launch_count - l0);
     h->setup_ms = timer.stop_ms();
     *out = reinterpret_cast<fiedler_handle>(h.release());
@@ -210,6 +241,7 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
     cudaStream_t st = h.stream;
     SolveCfg cfg = cfg_of(o);
     prepare_solve(h, cfg);
+    trace_mark(st, "solve: enter");
     EventTimer timer(st);
     int launches = 0;
     if (o.use_graph) {
@@ -232,6 +264,7 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
             h.g_gs = cfg.gs; h.g_pi = cfg.pi; h.g_piJ = cfg.piJ; h.g_seed = cfg.seed;
             h.g_launches = launches;
         }
+        trace_mark(st, "solve: capture+instantiate");
         FDL_CK(cudaGraphLaunch(h.gexec, st));
         launches = h.g_launches;
     } else {
@@ -246,6 +279,7 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
     FDL_CK(cudaMemcpyAsync(res, h.result.p, sizeof(res), cudaMemcpyDeviceToHost, st));
     double ms = timer.stop_ms();
     FDL_CK(cudaStreamSynchronize(st));
+    trace_mark(st, "solve: run+copy");
     if (lambda2) *lambda2 = res[0];
     if (info) {
         std::memset(info, 0, sizeof(*info));
@@ -273,7 +307,10 @@ int fiedler_destroy(fiedler_handle hh) {
     if (!hh) return FIEDLER_OK;
     Handle *h = reinterpret_cast<Handle *>(hh);
     cudaSetDevice(h->device);
+    trace_mark(nullptr, "destroy: enter");
+    cudaStream_t st = h->own_stream ? nullptr : h->stream;
     delete h;
+    trace_mark(st, "destroy: done");
     return FIEDLER_OK;
     API_END
 }

@@ -45,6 +45,13 @@ extern thread_local long long g_launch_count;
         if (!(cond)) throw ::fdl::Error((code), (msg));                                   \
     } while (0)
 
+// ----------------------------------------------------------------- tracing
+// FIEDLER_TRACE=1 in the environment: every trace_mark() synchronises the
+// stream and prints the wall time since the previous mark to stderr
+// (diagnostics only; off by default, zero cost when off).
+bool trace_enabled();
+void trace_mark(cudaStream_t st, const char *what);
+
 // ----------------------------------------------------------------- memory
 // Stream-ordered device buffer (cudaMallocAsync pool; capture-safe frees are
 // never issued inside a captured region).
@@ -135,8 +142,13 @@ __device__ __forceinline__ int warp_append(bool pred, int *count) {
 void scan_exclusive(const int *in, int *out, int64_t n, int *total, cudaStream_t st);
 // Stable LSD radix sort of (key, value) pairs on bits [0, bits); result in keys/vals.
 void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStream_t st);
+void radix_sort_u64_i32(unsigned long long *keys, int *vals, int64_t n, int bits, cudaStream_t st);
 void radix_sort_u64_f64(unsigned long long *keys, double *vals, int64_t n, int bits,
                         cudaStream_t st);
+// Stream compaction: out[k] = (in ? in[i] : i) for the k-th i in [0, n) with
+// flags[i] != 0 (order kept); *d_count (device) = number kept.  flags are 0/1.
+void compact_flagged(const int *in, const int *flags, int64_t n, int *out, int *d_count,
+                     cudaStream_t st);
 // Device-wide max of an int array (n >= 1) into *out (device).
 void reduce_max_i32(const int *in, int64_t n, int *out, cudaStream_t st);
 

@@ -224,9 +224,31 @@ static void radix_sort_impl(K *keys, V *vals, int64_t n, int bits, cudaStream_t 
 void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStream_t st) {
     radix_sort_impl<unsigned, int>(keys, vals, n, bits, st);
 }
+void radix_sort_u64_i32(unsigned long long *keys, int *vals, int64_t n, int bits, cudaStream_t st) {
+    radix_sort_impl<unsigned long long, int>(keys, vals, n, bits, st);
+}
 void radix_sort_u64_f64(unsigned long long *keys, double *vals, int64_t n, int bits,
                         cudaStream_t st) {
     radix_sort_impl<unsigned long long, double>(keys, vals, n, bits, st);
+}
+
+// =============================================================== compaction
+__global__ void k_compact(const int *in, const int *flags, const int *pos, int64_t n, int *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (flags[i]) out[pos[i]] = in ? in[i] : (int)i;
+}
+
+void compact_flagged(const int *in, const int *flags, int64_t n, int *out, int *d_count,
+                     cudaStream_t st) {
+    if (n <= 0) {
+        FDL_CK(cudaMemsetAsync(d_count, 0, sizeof(int), st));
+        return;
+    }
+    DBuf pos((size_t)n * sizeof(int), st);
+    scan_exclusive(flags, pos.as<int>(), n, d_count, st);
+    k_compact<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(in, flags, pos.as<int>(), n, out);
+    FDL_LAUNCH_CK();
 }
 
 // =============================================================== max

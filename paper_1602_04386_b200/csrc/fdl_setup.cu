@@ -144,10 +144,11 @@ void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32,
 
 // ================================================================= heavy edge coarsening
 // m(v) = heaviest neighbour in the strict order (w, hash); also the first
-// handshake pointer.  Vertices with neighbours enter the work list.
+// handshake pointer.  Vertices with neighbours are flagged for the work list
+// (compacted by a prefix scan: no single-address atomics, list stays sorted).
 template <int W>
 __global__ void k_heavy_init(int n, const int *rp, const int *ci, const double *w, uint64_t salt,
-                             int *m, int *ptr, int *list, int *count) {
+                             int *m, int *ptr, int *flag) {
     SUBWARP_LOOP(W, n, v) {
         double bw = 0.0;
         unsigned long long bh = 0;
@@ -164,10 +165,8 @@ __global__ void k_heavy_init(int n, const int *rp, const int *ci, const double *
         if (v < n && sw_lane_ == 0) {
             m[v] = bj;
             ptr[v] = bj;
+            flag[v] = bj >= 0;
         }
-        const bool app = v < n && sw_lane_ == 0 && bj >= 0;
-        const int slot = warp_append(app, count);
-        if (app) list[slot] = (int)v;
     }
 }
 
@@ -184,8 +183,7 @@ __global__ void k_match_mutual(const int *list, const int *count, const int *ptr
 // re-point vertices whose target got matched at their heaviest FREE neighbour
 template <int W>
 __global__ void k_repoint(const int *list, const int *count, const int *rp, const int *ci,
-                          const double *w, uint64_t salt, int *ptr, const int *mate, int *newlist,
-                          int *newcount) {
+                          const double *w, uint64_t salt, int *ptr, const int *mate, int *keepflag) {
     const int cnt = *count;
     SUBWARP_LOOP(W, cnt, idx) {
         int v = idx < cnt ? list[idx] : -1;
@@ -212,9 +210,7 @@ __global__ void k_repoint(const int *list, const int *count, const int *rp, cons
             ptr[v] = bj;
             if (bj >= 0) keep = true;
         }
-        const bool app = sw_lane_ == 0 && keep;
-        const int slot = warp_append(app, newcount);
-        if (app) newlist[slot] = v;
+        if (sw_lane_ == 0 && idx < cnt) keepflag[idx] = keep;
     }
 }
 
@@ -252,15 +248,16 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
     const int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
     DBuf m((size_t)n * 4, st), ptr((size_t)n * 4, st), la((size_t)n * 4, st), lb((size_t)n * 4, st),
-        cnt(2 * sizeof(int), st);
+        fl((size_t)n * 4, st), cnt(2 * sizeof(int), st);
     q.alloc((size_t)n * 4, st);
     mate.alloc((size_t)n * 4, st);
     FDL_CK(cudaMemsetAsync(mate.p, 0xff, (size_t)n * 4, st));
     FDL_CK(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(int), st));
     int *ca = cnt.as<int>(), *cb = cnt.as<int>() + 1;
     DISPATCH_W(avg, (k_heavy_init<W><<<sub_grid(n, W), 256, 0, st>>>(
-                         n, g.rp, g.ci, g.w, salt, m.as<int>(), ptr.as<int>(), la.as<int>(), ca)));
+                         n, g.rp, g.ci, g.w, salt, m.as<int>(), ptr.as<int>(), fl.as<int>())));
     FDL_LAUNCH_CK();
+    compact_flagged(nullptr, fl.as<int>(), n, la.as<int>(), ca, st);
     int *L0 = la.as<int>(), *L1 = lb.as<int>();
     int active = read_int(ca, st);
     rounds = 0;
@@ -269,10 +266,10 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
         FDL_REQUIRE(rounds < 100000, FIEDLER_ERR_INTERNAL, "matching did not terminate");
         k_match_mutual<<<grid_for(active), 256, 0, st>>>(L0, ca, ptr.as<int>(), mate.as<int>());
         FDL_LAUNCH_CK();
-        FDL_CK(cudaMemsetAsync(cb, 0, sizeof(int), st));
         DISPATCH_W(avg, (k_repoint<W><<<sub_grid(active, W), 256, 0, st>>>(
-                             L0, ca, g.rp, g.ci, g.w, salt, ptr.as<int>(), mate.as<int>(), L1, cb)));
+                             L0, ca, g.rp, g.ci, g.w, salt, ptr.as<int>(), mate.as<int>(), fl.as<int>())));
         FDL_LAUNCH_CK();
+        compact_flagged(L0, fl.as<int>(), active, L1, cb, st);
         std::swap(L0, L1);
         std::swap(ca, cb);
         active = read_int(ca, st);
@@ -293,49 +290,91 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
     return th[0];
 }
 
+__global__ void k_seg_starts(int n, const unsigned *keys, int *segstart) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        if (t == 0 || keys[t] != keys[t - 1]) segstart[keys[t]] = t;
+}
+
 // ================================================================= Galerkin product
-template <int W>
-__global__ void k_gal_count(int n, const int *rp, const int *ci, const int *q, int *cnt) {
-    SUBWARP_LOOP(W, n, i) {
-        int c = 0;
-        if (i < n) {
-            int qi = q[i];
-            for (int k = rp[i] + sw_lane_; k < rp[i + 1]; k += W) {
-                int j = ci[k];
-                c += (j > i && q[j] != qi);
-            }
-        }
-        c = sub_sum<W>(c);
-        if (i < n && sw_lane_ == 0) cnt[i] = c;
+// I L I^T with the R3 summation order, computed per COARSE ROW
+// from the aggregate members (no global sort of all contributions):
+//   1. members of every aggregate, sorted by (aggregate, vertex): a stable
+//      radix sort of (q[v], v) -- n elements, not nnz;
+//   2. every member m emits, for each neighbour j in another aggregate B, the
+//      contribution (key = B << 32 | kpos, w_mj), where kpos is the CSR
+//      position of the edge's (lo -> hi) entry, lo = min(m, j): the R3 order
+//      of the fine edges {i < j} is exactly ascending kpos;
+//   3. each coarse row A sorts its contributions by key (registers for <= 16,
+//      a warp in shared memory for <= 256, a global two-key radix sort for the
+//      rare longer rows) and left-folds every run of equal B in kpos order --
+//      the oracle's fold, computed independently and identically on both sides
+//      of the pair, so W_c is symmetric bit for bit;
+//   4. prefix scan of the row lengths and a compacting copy give the CSR.
+constexpr int kGalSmall = 16;
+constexpr int kGalMid = 256;
+
+__global__ void k_member_keys(int n, const int *q, unsigned *keys, int *vals) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        keys[v] = (unsigned)q[v];
+        vals[v] = v;
     }
 }
 
+__global__ void k_set_at(int *p, int idx, int v) { p[idx] = v; }
+
+// contributions of member position t (vertex m = mem[t]): neighbours outside q[m]
 template <int W>
-__global__ void k_gal_emit(int n, const int *rp, const int *ci, const double *w, const int *q,
-                           const int *off, int bitsB, unsigned long long *keys, double *vals) {
-    SUBWARP_LOOP(W, n, i) {
+__global__ void k_gal_member_count(int n, const int *mem, const int *rp, const int *ci, const int *q,
+                                   int *cnt) {
+    SUBWARP_LOOP(W, n, t) {
+        int c = 0;
+        if (t < n) {
+            const int m = mem[t];
+            const int qm = q[m];
+            for (int k = rp[m] + sw_lane_; k < rp[m + 1]; k += W) c += (q[ci[k]] != qm);
+        }
+        c = sub_sum<W>(c);
+        if (t < n && sw_lane_ == 0) cnt[t] = c;
+    }
+}
+
+// position of `target` in the ascending row [b, e) of ci (it exists: symmetry)
+__device__ __forceinline__ int find_in_row(const int *ci, int b, int e, int target) {
+    int lo = b, hi = e - 1;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (ci[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <int W>
+__global__ void k_gal_member_emit(int n, const int *mem, const int *rp, const int *ci, const double *w,
+                                  const int *q, const int *coff, unsigned long long *keys,
+                                  double *vals) {
+    SUBWARP_LOOP(W, n, t) {
         const unsigned sub_mask = (W == 32) ? 0xffffffffu
                                             : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
-        int qi = 0, b = 0, e = 0, o = 0;
-        if (i < n) { qi = q[i]; b = rp[i]; e = rp[i + 1]; o = off[i]; }
-        int len = e - b;
+        int m = 0, qm = 0, b = 0, e = 0, o = 0;
+        if (t < n) { m = mem[t]; qm = q[m]; b = rp[m]; e = rp[m + 1]; o = coff[t]; }
+        const int len = e - b;
         int maxlen = len;   // warp-wide max: the ballot below needs all 32 lanes
 #pragma unroll
         for (int s = 16; s; s >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, s));
-        for (int t = 0; t < maxlen; t += W) {   // uniform within the warp
-            int k = b + t + sw_lane_;
+        for (int tt = 0; tt < maxlen; tt += W) {   // uniform within the warp
+            const int k = b + tt + sw_lane_;
             bool f = false;
             int j = 0, qj = 0;
-            if (t + sw_lane_ < len) {
+            if (tt + sw_lane_ < len) {
                 j = ci[k];
                 qj = q[j];
-                f = (j > i && qj != qi);
+                f = (qj != qm);
             }
-            unsigned bal = __ballot_sync(0xffffffffu, f) & sub_mask;
+            const unsigned bal = __ballot_sync(0xffffffffu, f) & sub_mask;
             if (f) {
-                int rank = __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
-                unsigned A = min(qi, qj), B = max(qi, qj);
-                keys[o + rank] = ((unsigned long long)A << bitsB) | B;
+                const int rank = __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+                const int kpos = m < j ? k : find_in_row(ci, rp[j], rp[j + 1], m);
+                keys[o + rank] = ((unsigned long long)(unsigned)qj << 32) | (unsigned)kpos;
                 vals[o + rank] = w[k];
             }
             o += __popc(bal);
@@ -343,139 +382,307 @@ __global__ void k_gal_emit(int n, const int *rp, const int *ci, const double *w,
     }
 }
 
-__global__ void k_run_heads(const unsigned long long *keys, int E, int *head) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < E; t += gridDim.x * blockDim.x)
-        head[t] = (t == 0 || keys[t] != keys[t - 1]);
-}
-
-// sequential left fold of each run (R3 order = the stable-sorted visit order)
-__global__ void k_run_fold(const unsigned long long *keys, const double *vals, int E,
-                           const int *head, const int *runid, int bitsB, int *pA, int *pB,
-                           double *pw) {
-    const unsigned long long maskB = (1ull << bitsB) - 1ull;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < E; t += gridDim.x * blockDim.x) {
-        if (!head[t]) continue;
-        double s = vals[t];
-        for (int u = t + 1; u < E && !head[u]; u++) s += vals[u];
-        int r = runid[t];
-        unsigned long long k = keys[t];
-        pA[r] = (int)(k >> bitsB);
-        pB[r] = (int)(k & maskB);
-        pw[r] = s;
+// rows with <= kGalSmall contributions: register bitonic sort + sequential fold.
+// Longer rows are flagged for the mid (warp) or big (global) path.
+__global__ void __launch_bounds__(256) k_gal_rows_small(int c, const int *mrp, const int *coff,
+                                                        const unsigned long long *keys, const double *vals,
+                                                        int *outB, double *outW, int *deg, int *midflag,
+                                                        int *bigflag) {
+    for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
+        const int sb = coff[mrp[A]], se = coff[mrp[A + 1]];
+        const int s = se - sb;
+        midflag[A] = (s > kGalSmall && s <= kGalMid);
+        bigflag[A] = (s > kGalMid);
+        if (s > kGalSmall) continue;
+        unsigned long long k[kGalSmall];
+        double v[kGalSmall];
+#pragma unroll
+        for (int i = 0; i < kGalSmall; i++) {
+            k[i] = i < s ? keys[sb + i] : ~0ull;
+            v[i] = i < s ? vals[sb + i] : 0.0;
+        }
+#pragma unroll
+        for (int kk = 2; kk <= kGalSmall; kk <<= 1)
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+                for (int i = 0; i < kGalSmall; i++) {
+                    const int l = i ^ jj;
+                    if (l > i) {
+                        const bool up = (i & kk) == 0;
+                        if ((k[i] > k[l]) == up) {
+                            unsigned long long tk = k[i]; k[i] = k[l]; k[l] = tk;
+                            double tv = v[i]; v[i] = v[l]; v[l] = tv;
+                        }
+                    }
+                }
+        int runs = 0;
+        unsigned curB = 0;
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < kGalSmall; i++) {
+            if (i < s) {
+                const unsigned B = (unsigned)(k[i] >> 32);
+                if (i == 0) { curB = B; acc = v[i]; }
+                else if (B != curB) {
+                    outB[sb + runs] = (int)curB; outW[sb + runs] = acc; runs++;
+                    curB = B; acc = v[i];
+                } else {
+                    acc += v[i];
+                }
+            }
+        }
+        if (s > 0) { outB[sb + runs] = (int)curB; outW[sb + runs] = acc; runs++; }
+        deg[A] = runs;
     }
 }
 
-__global__ void k_pair_counts(int P, const int *pA, const int *pB, int *upcnt, int *lowcnt,
-                              int *firstA) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < P; r += gridDim.x * blockDim.x) {
-        atomicAdd(&upcnt[pA[r]], 1);
-        atomicAdd(&lowcnt[pB[r]], 1);
-        if (r == 0 || pA[r] != pA[r - 1]) firstA[pA[r]] = r;
+// rows with kGalSmall < s <= kGalMid contributions: one warp each, bitonic sort in shared memory
+constexpr int kGalMidWarps = 8;
+__global__ void __launch_bounds__(kGalMidWarps * 32) k_gal_rows_mid(const int *list, const int *count,
+                                                                    const int *mrp, const int *coff,
+                                                                    const unsigned long long *keys,
+                                                                    const double *vals, int *outB,
+                                                                    double *outW, int *deg) {
+    __shared__ unsigned long long sk[kGalMidWarps][kGalMid];
+    __shared__ double sv[kGalMidWarps][kGalMid];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const int cnt = *count;
+    unsigned long long *K = sk[warp];
+    double *V = sv[warp];
+    for (int idx = blockIdx.x * kGalMidWarps + warp; idx < cnt; idx += gridDim.x * kGalMidWarps) {
+        const int A = list[idx];
+        const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb;
+        int N = 32;
+        while (N < s) N <<= 1;
+        for (int i = lane; i < N; i += 32) {
+            K[i] = i < s ? keys[sb + i] : ~0ull;
+            V[i] = i < s ? vals[sb + i] : 0.0;
+        }
+        __syncwarp();
+        for (int kk = 2; kk <= N; kk <<= 1)
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                for (int i = lane; i < N; i += 32) {
+                    const int l = i ^ jj;
+                    if (l > i) {
+                        const bool up = (i & kk) == 0;
+                        if ((K[i] > K[l]) == up) {
+                            unsigned long long tk = K[i]; K[i] = K[l]; K[l] = tk;
+                            double tv = V[i]; V[i] = V[l]; V[l] = tv;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        // runs: heads in order, the head lane folds its run sequentially
+        int base = 0;
+        for (int c0 = 0; c0 < s; c0 += 32) {
+            const int i = c0 + lane;
+            const bool head = i < s && (i == 0 || (K[i] >> 32) != (K[i - 1] >> 32));
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                const int r = base + __popc(hm & ((1u << lane) - 1u));
+                double acc = V[i];
+                for (int u = i + 1; u < s && (K[u] >> 32) == (K[i] >> 32); u++) acc += V[u];
+                outB[sb + r] = (int)(K[i] >> 32);
+                outW[sb + r] = acc;
+            }
+            base += __popc(hm);
+        }
+        if (lane == 0) deg[A] = base;
+        __syncwarp();
     }
 }
 
-__global__ void k_add(int n, const int *a, const int *b, int *out) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        out[i] = a[i] + b[i];
-}
-
-__global__ void k_fill_upper(int P, const int *pA, const int *pB, const double *pw, const int *crp,
-                             const int *lowcnt, const int *firstA, int *cci, double *cw) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < P; r += gridDim.x * blockDim.x) {
-        int A = pA[r];
-        int pos = crp[A] + lowcnt[A] + (r - firstA[A]);
-        cci[pos] = pB[r];
-        cw[pos] = pw[r];
+// ---- rows with more than kGalMid contributions: global two-key radix sort
+__global__ void k_big_sizes(int h, const int *list, const int *mrp, const int *coff, int *sz) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < h; r += gridDim.x * blockDim.x) {
+        const int A = list[r];
+        sz[r] = coff[mrp[A + 1]] - coff[mrp[A]];
     }
 }
 
-__global__ void k_pairs_by_B(int P, const int *pB, unsigned *keys, int *vals) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < P; r += gridDim.x * blockDim.x) {
-        keys[r] = (unsigned)pB[r];
-        vals[r] = r;
+// one CTA per big row: gather its segment into the concatenated arrays
+__global__ void k_big_gather(int h, const int *list, const int *mrp, const int *coff, const int *boff,
+                             const unsigned long long *keys, unsigned long long *ckey, int *cidx,
+                             unsigned *crank, int *cdst) {
+    for (int r = blockIdx.x; r < h; r += gridDim.x) {
+        const int A = list[r];
+        const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb, o = boff[r];
+        for (int i = threadIdx.x; i < s; i += blockDim.x) {
+            ckey[o + i] = keys[sb + i];
+            cidx[o + i] = o + i;
+            crank[o + i] = (unsigned)r;
+            cdst[o + i] = sb + i;
+        }
     }
 }
 
-__global__ void k_first_of_runs_u32(int P, const unsigned *keys, int *first) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < P; t += gridDim.x * blockDim.x)
-        if (t == 0 || keys[t] != keys[t - 1]) first[keys[t]] = t;
+__global__ void k_big_rank_of(int E, const int *idx, const unsigned *crank, unsigned *rank2) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < E; p += gridDim.x * blockDim.x)
+        rank2[p] = crank[idx[p]];
 }
 
-__global__ void k_fill_lower(int P, const unsigned *sB, const int *sr, const int *pA,
-                             const double *pw, const int *crp, const int *firstB, int *cci,
-                             double *cw) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < P; t += gridDim.x * blockDim.x) {
-        int B = (int)sB[t];
-        int r = sr[t];
-        int pos = crp[B] + (t - firstB[B]);
-        cci[pos] = pA[r];
-        cw[pos] = pw[r];
+// sorted element p (original concatenated index idx[p]) lands at the p-th slot of
+// the row segments (segments are concatenated in rank order)
+__global__ void k_big_place(int E, const int *idx, const int *cdst, const int *srcpos,
+                            const unsigned long long *keys, const double *vals,
+                            unsigned long long *keys2, double *vals2) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < E; p += gridDim.x * blockDim.x) {
+        const int from = srcpos[idx[p]];
+        keys2[cdst[p]] = keys[from];
+        vals2[cdst[p]] = vals[from];
+    }
+}
+
+// one CTA per big row: heads, block scan for run indices, sequential fold per run
+__global__ void __launch_bounds__(256) k_big_fold(int h, const int *list, const int *mrp,
+                                                  const int *coff, const unsigned long long *keys,
+                                                  const double *vals, int *outB, double *outW,
+                                                  int *deg) {
+    __shared__ int s_warp[8];
+    __shared__ int s_base;
+    for (int r = blockIdx.x; r < h; r += gridDim.x) {
+        const int A = list[r];
+        const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb;
+        if (threadIdx.x == 0) s_base = 0;
+        __syncthreads();
+        for (int c0 = 0; c0 < s; c0 += blockDim.x) {
+            const int i = c0 + threadIdx.x;
+            const bool head = i < s && (i == 0 || (keys[sb + i] >> 32) != (keys[sb + i - 1] >> 32));
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            const int warp = threadIdx.x >> 5;
+            if (lane_id() == 0) s_warp[warp] = __popc(hm);
+            __syncthreads();
+            int before = s_base;
+            for (int q = 0; q < warp; q++) before += s_warp[q];
+            if (head) {
+                const int ri = before + __popc(hm & ((1u << lane_id()) - 1u));
+                const unsigned long long B = keys[sb + i] >> 32;
+                double acc = vals[sb + i];
+                for (int u = i + 1; u < s && (keys[sb + u] >> 32) == B; u++) acc += vals[sb + u];
+                outB[sb + ri] = (int)B;
+                outW[sb + ri] = acc;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int q = 0; q < (int)(blockDim.x >> 5); q++) s_base += s_warp[q];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) deg[A] = s_base;
+        __syncthreads();
+    }
+}
+
+template <int W>
+__global__ void k_gal_write(int c, const int *mrp, const int *coff, const int *crp, const int *outB,
+                            const double *outW, int *cci, double *cw) {
+    SUBWARP_LOOP(W, c, A) {
+        if (A < c) {
+            const int sb = coff[mrp[A]], o = crp[A], d = crp[A + 1] - o;
+            for (int i = sw_lane_; i < d; i += W) {
+                cci[o + i] = outB[sb + i];
+                cw[o + i] = outW[sb + i];
+            }
+        }
     }
 }
 
 static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st) {
     const int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
-    const int bitsB = bits_for(c - 1);
-    DBuf cnt((size_t)n * 4, st), off((size_t)n * 4, st), tot(4, st);
-    DISPATCH_W(avg, (k_gal_count<W><<<sub_grid(n, W), 256, 0, st>>>(n, g.rp, g.ci, q, cnt.as<int>())));
-    FDL_LAUNCH_CK();
-    scan_exclusive(cnt.as<int>(), off.as<int>(), n, tot.as<int>(), st);
-    const int E = read_int(tot.as<int>(), st);
     NatGraph out;
     out.n = c;
     out.own_rp.alloc((size_t)(c + 1) * 4, st);
-    if (E == 0) {
-        FDL_CK(cudaMemsetAsync(out.own_rp.p, 0, (size_t)(c + 1) * 4, st));
-        out.nnz = 0;
-        out.rp = out.own_rp.as<int>();
-        return out;
+    // 1. members sorted by (aggregate, vertex); mrp = aggregate offsets
+    DBuf mkeys((size_t)n * 4, st), mem((size_t)n * 4, st), mrp((size_t)(c + 1) * 4, st);
+    k_member_keys<<<grid_for(n), 256, 0, st>>>(n, q, mkeys.as<unsigned>(), mem.as<int>());
+    FDL_LAUNCH_CK();
+    radix_sort_u32_i32(mkeys.as<unsigned>(), mem.as<int>(), n, bits_for(c - 1), st);
+    k_seg_starts<<<grid_for(n), 256, 0, st>>>(n, mkeys.as<unsigned>(), mrp.as<int>());
+    FDL_LAUNCH_CK();
+    k_set_at<<<1, 1, 0, st>>>(mrp.as<int>(), c, n);
+    FDL_LAUNCH_CK();
+    mkeys.release();
+    // 2. contributions in member order
+    DBuf cnt((size_t)n * 4, st), coff((size_t)(n + 1) * 4, st);
+    DISPATCH_W(avg, (k_gal_member_count<W><<<sub_grid(n, W), 256, 0, st>>>(
+                         n, mem.as<int>(), g.rp, g.ci, q, cnt.as<int>())));
+    FDL_LAUNCH_CK();
+    scan_exclusive(cnt.as<int>(), coff.as<int>(), n, coff.as<int>() + n, st);
+    cnt.release();
+    const int E = read_int(coff.as<int>() + n, st);
+    DBuf keys((size_t)std::max(E, 1) * 8, st), vals((size_t)std::max(E, 1) * 8, st);
+    if (E > 0) {
+        DISPATCH_W(avg, (k_gal_member_emit<W><<<sub_grid(n, W), 256, 0, st>>>(
+                             n, mem.as<int>(), g.rp, g.ci, g.w, q, coff.as<int>(),
+                             keys.as<unsigned long long>(), vals.as<double>())));
+        FDL_LAUNCH_CK();
     }
-    DBuf keys((size_t)E * 8, st), vals((size_t)E * 8, st);
-    DISPATCH_W(avg, (k_gal_emit<W><<<sub_grid(n, W), 256, 0, st>>>(
-                         n, g.rp, g.ci, g.w, q, off.as<int>(), bitsB,
-                         keys.as<unsigned long long>(), vals.as<double>())));
+    mem.release();
+    // 3. per-row sort + fold
+    DBuf outB((size_t)std::max(E, 1) * 4, st), outW((size_t)std::max(E, 1) * 8, st),
+        deg((size_t)(c + 1) * 4, st), midf((size_t)c * 4, st), bigf((size_t)c * 4, st),
+        lists((size_t)c * 4 * 2, st), lcnt(8, st);
+    k_gal_rows_small<<<grid_for(c, 256, kNumSMs * 8), 256, 0, st>>>(
+        c, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(), vals.as<double>(),
+        outB.as<int>(), outW.as<double>(), deg.as<int>(), midf.as<int>(), bigf.as<int>());
     FDL_LAUNCH_CK();
-    radix_sort_u64_f64(keys.as<unsigned long long>(), vals.as<double>(), E, 2 * bitsB, st);
-    DBuf head((size_t)E * 4, st), runid((size_t)E * 4, st);
-    k_run_heads<<<grid_for(E), 256, 0, st>>>(keys.as<unsigned long long>(), E, head.as<int>());
-    FDL_LAUNCH_CK();
-    scan_exclusive(head.as<int>(), runid.as<int>(), E, tot.as<int>(), st);
-    const int P = read_int(tot.as<int>(), st);
-    DBuf pA((size_t)P * 4, st), pB((size_t)P * 4, st), pw((size_t)P * 8, st);
-    k_run_fold<<<grid_for(E), 256, 0, st>>>(keys.as<unsigned long long>(), vals.as<double>(), E,
-                                            head.as<int>(), runid.as<int>(), bitsB, pA.as<int>(),
-                                            pB.as<int>(), pw.as<double>());
-    FDL_LAUNCH_CK();
-    keys.release(); vals.release(); head.release(); runid.release();
-    DBuf upcnt((size_t)c * 4, st), lowcnt((size_t)c * 4, st), firstA((size_t)c * 4, st),
-        rowcnt((size_t)c * 4, st);
-    FDL_CK(cudaMemsetAsync(upcnt.p, 0, (size_t)c * 4, st));
-    FDL_CK(cudaMemsetAsync(lowcnt.p, 0, (size_t)c * 4, st));
-    k_pair_counts<<<grid_for(P), 256, 0, st>>>(P, pA.as<int>(), pB.as<int>(), upcnt.as<int>(),
-                                               lowcnt.as<int>(), firstA.as<int>());
-    FDL_LAUNCH_CK();
-    k_add<<<grid_for(c), 256, 0, st>>>(c, upcnt.as<int>(), lowcnt.as<int>(), rowcnt.as<int>());
-    FDL_LAUNCH_CK();
-    scan_exclusive(rowcnt.as<int>(), out.own_rp.as<int>(), c, out.own_rp.as<int>() + c, st);
-    out.nnz = 2 * P;
-    out.own_ci.alloc((size_t)out.nnz * 4, st);
-    out.own_w.alloc((size_t)out.nnz * 8, st);
-    k_fill_upper<<<grid_for(P), 256, 0, st>>>(P, pA.as<int>(), pB.as<int>(), pw.as<double>(),
-                                              out.own_rp.as<int>(), lowcnt.as<int>(),
-                                              firstA.as<int>(), out.own_ci.as<int>(),
-                                              out.own_w.as<double>());
-    FDL_LAUNCH_CK();
-    DBuf sB((size_t)P * 4, st), sr((size_t)P * 4, st), firstB((size_t)c * 4, st);
-    k_pairs_by_B<<<grid_for(P), 256, 0, st>>>(P, pB.as<int>(), sB.as<unsigned>(), sr.as<int>());
-    FDL_LAUNCH_CK();
-    radix_sort_u32_i32(sB.as<unsigned>(), sr.as<int>(), P, bitsB, st);
-    k_first_of_runs_u32<<<grid_for(P), 256, 0, st>>>(P, sB.as<unsigned>(), firstB.as<int>());
-    FDL_LAUNCH_CK();
-    k_fill_lower<<<grid_for(P), 256, 0, st>>>(P, sB.as<unsigned>(), sr.as<int>(), pA.as<int>(),
-                                              pw.as<double>(), out.own_rp.as<int>(),
-                                              firstB.as<int>(), out.own_ci.as<int>(),
-                                              out.own_w.as<double>());
+    int *midlist = lists.as<int>(), *biglist = lists.as<int>() + c;
+    compact_flagged(nullptr, midf.as<int>(), c, midlist, lcnt.as<int>(), st);
+    compact_flagged(nullptr, bigf.as<int>(), c, biglist, lcnt.as<int>() + 1, st);
+    int hc[2];
+    FDL_CK(cudaMemcpyAsync(hc, lcnt.p, 8, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaStreamSynchronize(st));
+    if (hc[0] > 0) {
+        k_gal_rows_mid<<<std::min(div_up(hc[0], kGalMidWarps), kNumSMs * 8), kGalMidWarps * 32, 0, st>>>(
+            midlist, lcnt.as<int>(), mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
+            vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
+        FDL_LAUNCH_CK();
+    }
+    const int h = hc[1];
+    if (h > 0) {
+        DBuf sz((size_t)h * 4, st), boff((size_t)(h + 1) * 4, st);
+        k_big_sizes<<<grid_for(h), 256, 0, st>>>(h, biglist, mrp.as<int>(), coff.as<int>(), sz.as<int>());
+        FDL_LAUNCH_CK();
+        scan_exclusive(sz.as<int>(), boff.as<int>(), h, boff.as<int>() + h, st);
+        const int EB = read_int(boff.as<int>() + h, st);
+        DBuf ckey((size_t)EB * 8, st), cidx((size_t)EB * 4, st), crank((size_t)EB * 4, st),
+            cdst((size_t)EB * 4, st), srcpos((size_t)EB * 4, st);
+        k_big_gather<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
+            h, biglist, mrp.as<int>(), coff.as<int>(), boff.as<int>(), keys.as<unsigned long long>(),
+            ckey.as<unsigned long long>(), cidx.as<int>(), crank.as<unsigned>(), cdst.as<int>());
+        FDL_LAUNCH_CK();
+        // srcpos[o] = original position of concatenated element o (= cdst before sorting)
+        FDL_CK(cudaMemcpyAsync(srcpos.p, cdst.p, (size_t)EB * 4, cudaMemcpyDeviceToDevice, st));
+        // LSD: (B, kpos) first, then the row rank (stable)
+        radix_sort_u64_i32(ckey.as<unsigned long long>(), cidx.as<int>(), EB, 32 + bits_for(c - 1), st);
+        DBuf rank2((size_t)EB * 4, st);
+        k_big_rank_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), crank.as<unsigned>(),
+                                                    rank2.as<unsigned>());
+        FDL_LAUNCH_CK();
+        radix_sort_u32_i32(rank2.as<unsigned>(), cidx.as<int>(), EB, bits_for(h - 1), st);
+        DBuf keys2((size_t)E * 8, st), vals2((size_t)E * 8, st);
+        k_big_place<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), cdst.as<int>(), srcpos.as<int>(),
+                                                  keys.as<unsigned long long>(), vals.as<double>(),
+                                                  keys2.as<unsigned long long>(), vals2.as<double>());
+        FDL_LAUNCH_CK();
+        k_big_fold<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
+            h, biglist, mrp.as<int>(), coff.as<int>(), keys2.as<unsigned long long>(), vals2.as<double>(),
+            outB.as<int>(), outW.as<double>(), deg.as<int>());
+        FDL_LAUNCH_CK();
+    }
+    keys.release();
+    vals.release();
+    // 4. CSR assembly
+    scan_exclusive(deg.as<int>(), out.own_rp.as<int>(), c, out.own_rp.as<int>() + c, st);
+    out.nnz = read_int(out.own_rp.as<int>() + c, st);
+    out.own_ci.alloc((size_t)std::max(out.nnz, 1) * 4, st);
+    out.own_w.alloc((size_t)std::max(out.nnz, 1) * 8, st);
+    const double cavg = c ? (double)out.nnz / c : 0.0;
+    DISPATCH_W(cavg, (k_gal_write<W><<<sub_grid(c, W), 256, 0, st>>>(
+                          c, mrp.as<int>(), coff.as<int>(), out.own_rp.as<int>(), outB.as<int>(),
+                          outW.as<double>(), out.own_ci.as<int>(), out.own_w.as<double>())));
     FDL_LAUNCH_CK();
     out.rp = out.own_rp.as<int>();
     out.ci = out.own_ci.as<int>();
@@ -490,7 +697,7 @@ __device__ __forceinline__ bool higher_prio(uint64_t pu, int u, uint64_t pv, int
 
 template <int W>
 __global__ void k_color_round(const int *list, const int *count, const int *rp, const int *ci,
-                              uint64_t salt, int *color, int *newlist, int *newcount) {
+                              uint64_t salt, int *color, int *notready_flag) {
     const int cnt = *count;
     volatile int *vcolor = color;
     SUBWARP_LOOP(W, cnt, idx) {
@@ -541,10 +748,10 @@ __global__ void k_color_round(const int *list, const int *count, const int *rp, 
             any_big = __any_sync(0xffffffffu, need_big);
         }
         (void)big;
-        if (v >= 0 && sw_lane_ == 0 && !notready) vcolor[v] = col;
-        const bool app = v >= 0 && sw_lane_ == 0 && notready;
-        const int slot = warp_append(app, newcount);
-        if (app) newlist[slot] = v;
+        if (v >= 0 && sw_lane_ == 0) {
+            if (!notready) vcolor[v] = col;
+            notready_flag[idx] = notready;
+        }
     }
 }
 
@@ -557,7 +764,7 @@ static int color_graph(const NatGraph &g, uint64_t salt, DBuf &color, int &round
     const double avg = n ? (double)g.nnz / n : 0.0;
     color.alloc((size_t)n * 4, st);
     FDL_CK(cudaMemsetAsync(color.p, 0xff, (size_t)n * 4, st));
-    DBuf la((size_t)n * 4, st), lb((size_t)n * 4, st), cnt(8, st);
+    DBuf la((size_t)n * 4, st), lb((size_t)n * 4, st), fl((size_t)n * 4, st), cnt(8, st);
     k_iota<<<grid_for(n), 256, 0, st>>>(n, la.as<int>());
     FDL_LAUNCH_CK();
     int *ca = cnt.as<int>(), *cb = cnt.as<int>() + 1;
@@ -568,10 +775,10 @@ static int color_graph(const NatGraph &g, uint64_t salt, DBuf &color, int &round
     while (active > 0) {
         rounds++;
         FDL_REQUIRE(rounds < 1000000, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
-        FDL_CK(cudaMemsetAsync(cb, 0, sizeof(int), st));
         DISPATCH_W(avg, (k_color_round<W><<<sub_grid(active, W), 256, 0, st>>>(
-                             L0, ca, g.rp, g.ci, salt, color.as<int>(), L1, cb)));
+                             L0, ca, g.rp, g.ci, salt, color.as<int>(), fl.as<int>())));
         FDL_LAUNCH_CK();
+        compact_flagged(L0, fl.as<int>(), active, L1, cb, st);
         std::swap(L0, L1);
         std::swap(ca, cb);
         active = read_int(ca, st);
@@ -589,10 +796,6 @@ __global__ void k_color_keys(int n, const int *color, unsigned *keys, int *vals)
     }
 }
 
-__global__ void k_seg_starts(int n, const unsigned *keys, int *segstart) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-        if (t == 0 || keys[t] != keys[t - 1]) segstart[keys[t]] = t;
-}
 
 __global__ void k_inv_and_deg(int n, const int *perm, const int *rp, int *inv, int *degp) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
@@ -800,6 +1003,7 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
         NatGraph next;
         if (coarsen) {
             int c = hec_parallel(cur, salt_match(o.seed, ell), L.q_nat, L.mate_nat, L.match_rounds, st);
+            trace_mark(st, ell == 0 ? "L0 matching" : "Lk matching");
             // stall guard (R9): stop when HEC no longer shrinks the graph
             if ((double)c > 0.95 * (double)cur.n || c < 2) {
                 coarsen = false;
@@ -807,10 +1011,13 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
                 L.mate_nat.release();
             } else {
                 next = galerkin(cur, L.q_nat.as<int>(), c, st);
+                trace_mark(st, ell == 0 ? "L0 galerkin" : "Lk galerkin");
             }
         }
         int ncol = color_graph(cur, salt_color(o.seed, ell), L.color_nat, L.color_rounds, st);
+        trace_mark(st, ell == 0 ? "L0 colouring" : "Lk colouring");
         build_layout(cur, L.color_nat.as<int>(), ncol, L, st);
+        trace_mark(st, ell == 0 ? "L0 layout" : "Lk layout");
         h.levels.push_back(std::move(L));
         if (!coarsen) break;
         cur = std::move(next);
@@ -824,6 +1031,7 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
         FDL_LAUNCH_CK();
     }
     FDL_CK(cudaStreamSynchronize(st));
+    trace_mark(st, "compose qp");
     if (!coarsest_connected(h.levels[J], st))
         throw Error(FIEDLER_ERR_DISCONNECTED,
                     "graph is disconnected (lambda_2 = 0): the coarsest level splits into components");

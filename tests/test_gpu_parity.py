@@ -42,6 +42,7 @@ SMALL = {
     "path100": lambda: gg.path(100),
     "star40": lambda: gg.star(40),
     "complete30": lambda: gg.complete(30),
+    "hub3000_3hubs": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
     "tiny_p5": lambda: gg.path(5),
     "tiny_p3": lambda: gg.path(3),   # (P2 is degenerate for the Gershgorin shift: c = lambda_2)
 }
