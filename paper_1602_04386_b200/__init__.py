@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfiedler.so")
+# FIEDLER_LIB overrides the library (tuning sweeps of build variants only)
+LIB_PATH = os.environ.get("FIEDLER_LIB") or os.path.join(_HERE, "libfiedler.so")
 
 FIEDLER_OK = 0
 FIEDLER_ERR_ARG = -1

@@ -187,7 +187,7 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     NatGraph g0;
     g0.n = (int)n;
     g0.nnz = (int)nnz;
-    g0.own_rp.alloc((size_t)(n + 1) * 4, st);
+    g0.own_rp.alloc(padded((size_t)(n + 1) * 4), st);
     if (mem == FIEDLER_MEM_DEVICE) {
         convert_row_ptr(row_ptr, n, nnz, g0.own_rp.as<int>(), st);
         g0.ci = col_idx;
@@ -196,8 +196,8 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
         DBuf rp64((size_t)(n + 1) * 8, st);
         FDL_CK(cudaMemcpyAsync(rp64.p, row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st));
         convert_row_ptr(rp64.as<int64_t>(), n, nnz, g0.own_rp.as<int>(), st);
-        g0.own_ci.alloc((size_t)std::max<int64_t>(nnz, 1) * 4, st);
-        g0.own_w.alloc((size_t)std::max<int64_t>(nnz, 1) * 8, st);
+        g0.own_ci.alloc(padded((size_t)std::max<int64_t>(nnz, 1) * 4), st);
+        g0.own_w.alloc(padded((size_t)std::max<int64_t>(nnz, 1) * 8), st);
         if (nnz) {
             FDL_CK(cudaMemcpyAsync(g0.own_ci.p, col_idx, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
             FDL_CK(cudaMemcpyAsync(g0.own_w.p, weights, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));

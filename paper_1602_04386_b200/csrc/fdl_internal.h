@@ -20,7 +20,17 @@ namespace fdl {
 // (<= kShortMax nonzeros) end within kTileT + kShortMax nonzeros of the tile's
 // first nonzero: that range is staged into shared memory by bulk copies.
 constexpr int kShortMax = 32;    // longer rows are reduced by a warp from global memory
-constexpr int kTileT = 2048;     // coordinate window per tile
+#ifndef FDL_TILE_T
+#define FDL_TILE_T 2048
+#endif
+#ifndef FDL_STAGES
+#define FDL_STAGES 2
+#endif
+#ifndef FDL_PASS_MINB
+#define FDL_PASS_MINB 4
+#endif
+constexpr int kTileT = FDL_TILE_T;    // coordinate window per tile
+constexpr int kStages = FDL_STAGES;   // depth of the bulk-copy pipeline of a row pass
 constexpr int kStageCap = kTileT + kShortMax;
 constexpr int kPadBytes = 64;    // slack after every staged array (bulk copies round up to 16 B)
 
@@ -42,12 +52,12 @@ struct Level {
     // GS layout: rows sorted by (colour, natural id); every colour is one
     // contiguous row range; columns in solve numbering (= GS row order).
     DBuf rp, ci, w;
-    // PI / RQ layout: rows in NATURAL order (spatial locality of the x gathers),
-    // columns in solve numbering; row v's own value / output sits at inv[v].
+    // PI / RQ layout: the level's natural CSR itself (natural rows and columns;
+    // vectors of the power iteration live in natural numbering).
     DBuf rpN, ciN, wN;
-    DBuf perm;               // int32 [n]: solve row -> natural id
-    DBuf inv;                // int32 [n]: natural id -> solve row
-    DBuf qp;                 // int32 [n]: solve row -> solve row of its aggregate on level+1
+    DBuf perm;               // int32 [n]: GS row -> natural id
+    DBuf inv;                // int32 [n]: natural id -> GS row
+    DBuf qg;                 // int32 [n]: GS row -> natural id of its aggregate on level+1
     // natural-numbering setup results kept for fiedler_level_export
     DBuf q_nat, mate_nat, color_nat;
     // tiles: GS tiles of all colours back to back (colour c owns
@@ -93,6 +103,8 @@ struct Handle {
 void validate_input(int64_t n, int64_t nnz, const int *rp32, const int *ci, const double *w,
                     cudaStream_t st);
 void build_hierarchy(Handle &h, NatGraph &&g0);
+// allocation size of an array that the row passes stage with bulk copies
+inline size_t padded(size_t bytes) { return bytes + kPadBytes; }
 
 // fdl_solve.cu
 struct SolveCfg {

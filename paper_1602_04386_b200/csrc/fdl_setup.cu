@@ -18,6 +18,8 @@
 #include <cstring>
 #include <queue>
 
+#include <cooperative_groups.h>
+
 #include "fdl_internal.h"
 
 namespace fdl {
@@ -143,75 +145,129 @@ void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32,
 }
 
 // ================================================================= heavy edge coarsening
-// m(v) = heaviest neighbour in the strict order (w, hash); also the first
-// handshake pointer.  Vertices with neighbours are flagged for the work list
-// (compacted by a prefix scan: no single-address atomics, list stays sorted).
-template <int W>
-__global__ void k_heavy_init(int n, const int *rp, const int *ci, const double *w, uint64_t salt,
-                             int *m, int *ptr, int *flag) {
-    SUBWARP_LOOP(W, n, v) {
-        double bw = 0.0;
-        unsigned long long bh = 0;
-        int bj = -1;
-        if (v < n) {
-            for (int k = rp[v] + sw_lane_; k < rp[v + 1]; k += W) {
-                int j = ci[k];
-                double x = w[k];
-                unsigned long long h = edge_hash(salt, (int)v, j);
-                if (bj < 0 || x > bw || (x == bw && h > bh)) { bw = x; bh = h; bj = j; }
-            }
+// The handshake rounds run inside ONE cooperative kernel per level (grid-wide
+// barriers between phases, no host round trip per round).  Work lists are
+// appended through a per-CTA shared-memory buffer (one global atomic per
+// flush); list order is irrelevant to every consumer, so results are
+// deterministic.
+namespace cg = cooperative_groups;
+constexpr int kCoopThreads = 256;
+constexpr int kAppendCap = 2048;
+constexpr int kMaxRounds = 4096;
+
+struct CtaAppend {
+    int *buf;
+    int *n;
+    int *base;
+    __device__ __forceinline__ void push(int v) { buf[atomicAdd(n, 1)] = v; }
+    // all threads; call after __syncthreads()
+    __device__ __forceinline__ void flush(int *out, int *gcount) {
+        const int cnt = *n;
+        if (cnt == 0) return;
+        if (threadIdx.x == 0) *base = atomicAdd(gcount, cnt);
+        __syncthreads();
+        const int b = *base;
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) out[b + i] = buf[i];
+        __syncthreads();
+        if (threadIdx.x == 0) *n = 0;
+        __syncthreads();
+    }
+};
+
+// heaviest neighbour of v in the strict order (w, hash) among neighbours with
+// skip(j) == false (sub-warp of W lanes; all lanes return the same result)
+template <int W, class Skip>
+__device__ __forceinline__ int heaviest(int v, const int *rp, const int *ci, const double *w,
+                                        uint64_t salt, int lane, Skip skip) {
+    double bw = 0.0;
+    unsigned long long bh = 0;
+    int bj = -1;
+    if (v >= 0)
+        for (int k = rp[v] + lane; k < rp[v + 1]; k += W) {
+            const int j = ci[k];
+            if (skip(j)) continue;
+            const double x = w[k];
+            const unsigned long long h = edge_hash(salt, v, j);
+            if (bj < 0 || x > bw || (x == bw && h > bh)) { bw = x; bh = h; bj = j; }
         }
-        argmax_reduce<W>(bw, bh, bj);
-        if (v < n && sw_lane_ == 0) {
+    argmax_reduce<W>(bw, bh, bj);
+    return bj;
+}
+
+// counts[r] = length of the work list of round r (zeroed by the host); the
+// lists ping-pong between la and lb.  rounds_out[0] = handshake rounds.
+template <int W>
+__global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *rp, const int *ci,
+                                                             const double *w, uint64_t salt, int *m,
+                                                             int *ptr, int *mate, int *la, int *lb,
+                                                             int *counts, int *rounds_out) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int s_buf[kAppendCap];
+    __shared__ int s_n, s_base;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    CtaAppend app{s_buf, &s_n, &s_base};
+    const int lane = threadIdx.x & (W - 1);
+    const int per_block = kCoopThreads / W;
+    // round 0: m(v) = heaviest neighbour = first handshake pointer; vertices with
+    // a neighbour enter the list
+    for (long long base = (long long)blockIdx.x * per_block; base < n;
+         base += (long long)gridDim.x * per_block) {
+        const long long idx = base + threadIdx.x / W;
+        const int v = idx < n ? (int)idx : -1;
+        const int bj = heaviest<W>(v, rp, ci, w, salt, lane, [](int) { return false; });
+        if (v >= 0 && lane == 0) {
             m[v] = bj;
             ptr[v] = bj;
-            flag[v] = bj >= 0;
+            if (bj >= 0) app.push(v);
         }
+        __syncthreads();
+        if (s_n > kAppendCap - kCoopThreads) app.flush(la, counts);
     }
-}
-
-// handshake: mutual pointers match
-__global__ void k_match_mutual(const int *list, const int *count, const int *ptr, int *mate) {
-    int cnt = *count;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-        int v = list[i];
-        int p = ptr[v];
-        if (p >= 0 && ptr[p] == v) mate[v] = p;
-    }
-}
-
-// re-point vertices whose target got matched at their heaviest FREE neighbour
-template <int W>
-__global__ void k_repoint(const int *list, const int *count, const int *rp, const int *ci,
-                          const double *w, uint64_t salt, int *ptr, const int *mate, int *keepflag) {
-    const int cnt = *count;
-    SUBWARP_LOOP(W, cnt, idx) {
-        int v = idx < cnt ? list[idx] : -1;
-        bool keep = false, rescan = false;
-        if (v >= 0 && mate[v] < 0) {
-            int p = ptr[v];
-            if (mate[p] < 0) keep = true;
-            else rescan = true;
+    __syncthreads();
+    app.flush(la, counts);
+    grid.sync();
+    int *in = la, *out = lb;
+    int r = 0;
+    int cnt = *(volatile int *)&counts[0];
+    while (cnt > 0 && r + 1 < kMaxRounds) {
+        // (a) mutual pointers match
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+            const int v = in[i];
+            const int p = ptr[v];
+            if (p >= 0 && ptr[p] == v) mate[v] = p;
         }
-        double bw = 0.0;
-        unsigned long long bh = 0;
-        int bj = -1;
-        if (rescan) {
-            for (int k = rp[v] + sw_lane_; k < rp[v + 1]; k += W) {
-                int j = ci[k];
-                if (mate[j] >= 0) continue;
-                double x = w[k];
-                unsigned long long h = edge_hash(salt, v, j);
-                if (bj < 0 || x > bw || (x == bw && h > bh)) { bw = x; bh = h; bj = j; }
+        grid.sync();
+        // (b) unmatched vertices whose target got matched re-point at their
+        //     heaviest FREE neighbour; the ones still pointing somewhere stay
+        int *gcount = counts + r + 1;
+        for (long long base = (long long)blockIdx.x * per_block; base < cnt;
+             base += (long long)gridDim.x * per_block) {
+            const long long idx = base + threadIdx.x / W;
+            const int v = idx < cnt ? in[idx] : -1;
+            bool keep = false, rescan = false;
+            if (v >= 0 && mate[v] < 0) {
+                if (mate[ptr[v]] < 0) keep = true;
+                else rescan = true;
             }
+            const int bj = heaviest<W>(rescan ? v : -1, rp, ci, w, salt, lane,
+                                       [&](int j) { return mate[j] >= 0; });
+            if (lane == 0 && rescan) {
+                ptr[v] = bj;
+                keep = bj >= 0;
+            }
+            if (lane == 0 && keep) app.push(v);
+            __syncthreads();
+            if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
         }
-        argmax_reduce<W>(bw, bh, bj);
-        if (sw_lane_ == 0 && rescan) {
-            ptr[v] = bj;
-            if (bj >= 0) keep = true;
-        }
-        if (sw_lane_ == 0 && idx < cnt) keepflag[idx] = keep;
+        __syncthreads();
+        app.flush(out, gcount);
+        grid.sync();
+        r++;
+        cnt = *(volatile int *)gcount;
+        int *t = in; in = out; out = t;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
 }
 
 __global__ void k_leaders(int n, const int *m, const int *mate, int *leader, int *flag, int *err) {
@@ -242,38 +298,45 @@ static int read_int(const int *dptr, cudaStream_t st) {
     return h;
 }
 
+// cooperative launch with every CTA co-resident (grid = SMs x resident CTAs)
+template <class K>
+static void coop_launch(K kernel, void **args, cudaStream_t st) {
+    static int grid = 0;   // one cache per kernel instantiation
+    if (!grid) {
+        int per_sm = 0, dev = 0, sms = kNumSMs;
+        FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kCoopThreads, 0));
+        FDL_CK(cudaGetDevice(&dev));
+        FDL_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        FDL_REQUIRE(per_sm > 0, FIEDLER_ERR_CUDA, "cooperative kernel cannot be resident");
+        grid = per_sm * sms;
+    }
+    FDL_CK(cudaLaunchCooperativeKernel((const void *)kernel, dim3(grid), dim3(kCoopThreads), args, 0, st));
+    FDL_LAUNCH_CK();
+}
+
 // Returns the number of aggregates c; fills q (natural), mate.
 static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, int &rounds,
                         cudaStream_t st) {
-    const int n = g.n;
+    int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
     DBuf m((size_t)n * 4, st), ptr((size_t)n * 4, st), la((size_t)n * 4, st), lb((size_t)n * 4, st),
-        fl((size_t)n * 4, st), cnt(2 * sizeof(int), st);
+        counts((size_t)(kMaxRounds + 1) * 4, st);
     q.alloc((size_t)n * 4, st);
     mate.alloc((size_t)n * 4, st);
     FDL_CK(cudaMemsetAsync(mate.p, 0xff, (size_t)n * 4, st));
-    FDL_CK(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(int), st));
-    int *ca = cnt.as<int>(), *cb = cnt.as<int>() + 1;
-    DISPATCH_W(avg, (k_heavy_init<W><<<sub_grid(n, W), 256, 0, st>>>(
-                         n, g.rp, g.ci, g.w, salt, m.as<int>(), ptr.as<int>(), fl.as<int>())));
-    FDL_LAUNCH_CK();
-    compact_flagged(nullptr, fl.as<int>(), n, la.as<int>(), ca, st);
-    int *L0 = la.as<int>(), *L1 = lb.as<int>();
-    int active = read_int(ca, st);
-    rounds = 0;
-    while (active > 0) {
-        rounds++;
-        FDL_REQUIRE(rounds < 100000, FIEDLER_ERR_INTERNAL, "matching did not terminate");
-        k_match_mutual<<<grid_for(active), 256, 0, st>>>(L0, ca, ptr.as<int>(), mate.as<int>());
-        FDL_LAUNCH_CK();
-        DISPATCH_W(avg, (k_repoint<W><<<sub_grid(active, W), 256, 0, st>>>(
-                             L0, ca, g.rp, g.ci, g.w, salt, ptr.as<int>(), mate.as<int>(), fl.as<int>())));
-        FDL_LAUNCH_CK();
-        compact_flagged(L0, fl.as<int>(), active, L1, cb, st);
-        std::swap(L0, L1);
-        std::swap(ca, cb);
-        active = read_int(ca, st);
+    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 1) * 4, st));
+    {
+        const int *rp = g.rp, *ci = g.ci;
+        const double *w = g.w;
+        int *pm = m.as<int>(), *pp = ptr.as<int>(), *pmate = mate.as<int>(), *pa = la.as<int>(),
+            *pb = lb.as<int>(), *pc = counts.as<int>(), *pr = counts.as<int>() + kMaxRounds;
+        void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pa, &pb, &pc, &pr};
+        DISPATCH_W(avg, coop_launch(k_match_coop<W>, args, st));
     }
+    rounds = read_int(counts.as<int>() + kMaxRounds, st);
+    FDL_REQUIRE(rounds >= 0, FIEDLER_ERR_INTERNAL, "matching did not terminate");
+    la.release();
+    lb.release();
     // leaders, prefix scan numbering
     DBuf leader((size_t)n * 4, st), flag((size_t)n * 4, st), id((size_t)n * 4, st), tot(8, st);
     FDL_CK(cudaMemsetAsync(tot.p, 0, 8, st));
@@ -593,7 +656,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     const double avg = n ? (double)g.nnz / n : 0.0;
     NatGraph out;
     out.n = c;
-    out.own_rp.alloc((size_t)(c + 1) * 4, st);
+    out.own_rp.alloc(padded((size_t)(c + 1) * 4), st);
     // 1. members sorted by (aggregate, vertex); mrp = aggregate offsets
     DBuf mkeys((size_t)n * 4, st), mem((size_t)n * 4, st), mrp((size_t)(c + 1) * 4, st);
     k_member_keys<<<grid_for(n), 256, 0, st>>>(n, q, mkeys.as<unsigned>(), mem.as<int>());
@@ -677,8 +740,8 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     // 4. CSR assembly
     scan_exclusive(deg.as<int>(), out.own_rp.as<int>(), c, out.own_rp.as<int>() + c, st);
     out.nnz = read_int(out.own_rp.as<int>() + c, st);
-    out.own_ci.alloc((size_t)std::max(out.nnz, 1) * 4, st);
-    out.own_w.alloc((size_t)std::max(out.nnz, 1) * 8, st);
+    out.own_ci.alloc(padded((size_t)std::max(out.nnz, 1) * 4), st);
+    out.own_w.alloc(padded((size_t)std::max(out.nnz, 1) * 8), st);
     const double cavg = c ? (double)out.nnz / c : 0.0;
     DISPATCH_W(cavg, (k_gal_write<W><<<sub_grid(c, W), 256, 0, st>>>(
                           c, mrp.as<int>(), coff.as<int>(), out.own_rp.as<int>(), outB.as<int>(),
@@ -691,101 +754,125 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
 }
 
 // ================================================================= colouring (R4)
+// Jones-Plassmann rounds = the greedy first-fit colouring in decreasing
+// priority (pi(v), v), pi(v) = splitmix64(salt ^ v): a vertex takes the
+// smallest colour not used by a higher-priority neighbour as soon as all of
+// them are coloured, which fixes every colour independently of the schedule.
+// All rounds run in one cooperative kernel per level.
 __device__ __forceinline__ bool higher_prio(uint64_t pu, int u, uint64_t pv, int v) {
     return pu > pv || (pu == pv && u > v);
 }
 
+// one JP step for vertex v (sub-warp of W lanes; v < 0 = idle lanes, which still
+// take part in the warp-wide votes).  Returns 1 if v is not ready yet.
 template <int W>
-__global__ void k_color_round(const int *list, const int *count, const int *rp, const int *ci,
-                              uint64_t salt, int *color, int *notready_flag) {
-    const int cnt = *count;
-    volatile int *vcolor = color;
-    SUBWARP_LOOP(W, cnt, idx) {
-        int v = idx < cnt ? list[idx] : -1;
-        int notready = 0;
-        unsigned long long mask = 0ull;
-        int big = 0;
-        uint64_t pv = 0;
-        int b = 0, e = 0;
-        if (v >= 0) {
-            pv = splitmix64(salt ^ (uint64_t)v);
-            b = rp[v];
-            e = rp[v + 1];
-            for (int k = b + sw_lane_; k < e; k += W) {
-                int u = ci[k];
-                if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
-                int cu = vcolor[u];
-                if (cu < 0) notready = 1;
-                else if (cu < 64) mask |= 1ull << cu;
-                else big = 1;
-            }
-        }
-#pragma unroll
-        for (int o = W / 2; o; o >>= 1) {
-            notready |= __shfl_xor_sync(0xffffffffu, notready, o, W);
-            big |= __shfl_xor_sync(0xffffffffu, big, o, W);
-            mask |= __shfl_xor_sync(0xffffffffu, mask, o, W);
-        }
-        int col = -1;
-        if (v >= 0 && !notready) {
-            if (~mask) col = __ffsll((long long)~mask) - 1;
-        }
-        // rare: all of 0..63 taken -> scan further windows (sub-warp cooperative)
-        int need_big = (v >= 0 && !notready && col < 0) ? 1 : 0;
-        int any_big = __any_sync(0xffffffffu, need_big);   // warp-uniform loop below
-        for (int wb = 64; any_big; wb += 64) {
-            unsigned long long m2 = 0ull;
-            if (need_big)
-                for (int k = b + sw_lane_; k < e; k += W) {
-                    int u = ci[k];
-                    if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
-                    int cu = vcolor[u];
-                    if (cu >= wb && cu < wb + 64) m2 |= 1ull << (cu - wb);
-                }
-#pragma unroll
-            for (int o = W / 2; o; o >>= 1) m2 |= __shfl_xor_sync(0xffffffffu, m2, o, W);
-            if (need_big && ~m2) { col = wb + __ffsll((long long)~m2) - 1; need_big = 0; }
-            any_big = __any_sync(0xffffffffu, need_big);
-        }
-        (void)big;
-        if (v >= 0 && sw_lane_ == 0) {
-            if (!notready) vcolor[v] = col;
-            notready_flag[idx] = notready;
+__device__ __forceinline__ int color_item(int v, const int *rp, const int *ci, uint64_t salt,
+                                          volatile int *vcolor, int lane) {
+    int notready = 0;
+    unsigned long long mask = 0ull;
+    uint64_t pv = 0;
+    int b = 0, e = 0;
+    if (v >= 0) {
+        pv = splitmix64(salt ^ (uint64_t)v);
+        b = rp[v];
+        e = rp[v + 1];
+        for (int k = b + lane; k < e; k += W) {
+            const int u = ci[k];
+            if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+            const int cu = vcolor[u];
+            if (cu < 0) notready = 1;
+            else if (cu < 64) mask |= 1ull << cu;
         }
     }
+#pragma unroll
+    for (int o = W / 2; o; o >>= 1) {
+        notready |= __shfl_xor_sync(0xffffffffu, notready, o, W);
+        mask |= __shfl_xor_sync(0xffffffffu, mask, o, W);
+    }
+    int col = -1;
+    if (v >= 0 && !notready && ~mask) col = __ffsll((long long)~mask) - 1;
+    // rare: all of 0..63 taken -> scan further windows (sub-warp cooperative)
+    int need_big = (v >= 0 && !notready && col < 0) ? 1 : 0;
+    int any_big = __any_sync(0xffffffffu, need_big);   // warp-uniform loop below
+    for (int wb = 64; any_big; wb += 64) {
+        unsigned long long m2 = 0ull;
+        if (need_big)
+            for (int k = b + lane; k < e; k += W) {
+                const int u = ci[k];
+                if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+                const int cu = vcolor[u];
+                if (cu >= wb && cu < wb + 64) m2 |= 1ull << (cu - wb);
+            }
+#pragma unroll
+        for (int o = W / 2; o; o >>= 1) m2 |= __shfl_xor_sync(0xffffffffu, m2, o, W);
+        if (need_big && ~m2) { col = wb + __ffsll((long long)~m2) - 1; need_big = 0; }
+        any_big = __any_sync(0xffffffffu, need_big);
+    }
+    if (v >= 0 && lane == 0 && !notready) vcolor[v] = col;
+    return notready;
 }
 
-__global__ void k_iota(int n, int *a) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+template <int W>
+__global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *rp, const int *ci,
+                                                             uint64_t salt, int *color, int *la, int *lb,
+                                                             int *counts, int *rounds_out) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int s_buf[kAppendCap];
+    __shared__ int s_n, s_base;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    CtaAppend app{s_buf, &s_n, &s_base};
+    volatile int *vcolor = color;
+    const int lane = threadIdx.x & (W - 1);
+    const int per_block = kCoopThreads / W;
+    const int *in = nullptr;   // round 0: every vertex
+    int *out = la;
+    int cnt = n, r = 0;
+    while (cnt > 0 && r < kMaxRounds) {
+        int *gcount = counts + r;
+        for (long long base = (long long)blockIdx.x * per_block; base < cnt;
+             base += (long long)gridDim.x * per_block) {
+            const long long idx = base + threadIdx.x / W;
+            const int v = idx < cnt ? (in ? in[idx] : (int)idx) : -1;
+            const int nr = color_item<W>(v, rp, ci, salt, vcolor, lane);
+            if (v >= 0 && lane == 0 && nr) app.push(v);
+            __syncthreads();
+            if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
+        }
+        __syncthreads();
+        app.flush(out, gcount);
+        grid.sync();
+        cnt = *(volatile int *)gcount;
+        r++;
+        in = out;
+        out = (out == la) ? lb : la;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
 }
 
 static int color_graph(const NatGraph &g, uint64_t salt, DBuf &color, int &rounds, cudaStream_t st) {
-    const int n = g.n;
+    int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
     color.alloc((size_t)n * 4, st);
     FDL_CK(cudaMemsetAsync(color.p, 0xff, (size_t)n * 4, st));
-    DBuf la((size_t)n * 4, st), lb((size_t)n * 4, st), fl((size_t)n * 4, st), cnt(8, st);
-    k_iota<<<grid_for(n), 256, 0, st>>>(n, la.as<int>());
-    FDL_LAUNCH_CK();
-    int *ca = cnt.as<int>(), *cb = cnt.as<int>() + 1;
-    FDL_CK(cudaMemcpyAsync(ca, &n, sizeof(int), cudaMemcpyHostToDevice, st));
-    int *L0 = la.as<int>(), *L1 = lb.as<int>();
-    int active = n;
-    rounds = 0;
-    while (active > 0) {
-        rounds++;
-        FDL_REQUIRE(rounds < 1000000, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
-        DISPATCH_W(avg, (k_color_round<W><<<sub_grid(active, W), 256, 0, st>>>(
-                             L0, ca, g.rp, g.ci, salt, color.as<int>(), fl.as<int>())));
-        FDL_LAUNCH_CK();
-        compact_flagged(L0, fl.as<int>(), active, L1, cb, st);
-        std::swap(L0, L1);
-        std::swap(ca, cb);
-        active = read_int(ca, st);
+    DBuf la((size_t)n * 4, st), lb((size_t)n * 4, st), counts((size_t)(kMaxRounds + 1) * 4, st);
+    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 1) * 4, st));
+    {
+        const int *rp = g.rp, *ci = g.ci;
+        int *pcol = color.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(), *pc = counts.as<int>(),
+            *pr = counts.as<int>() + kMaxRounds;
+        void *args[] = {&n, &rp, &ci, &salt, &pcol, &pa, &pb, &pc, &pr};
+        DISPATCH_W(avg, coop_launch(k_color_coop<W>, args, st));
     }
     DBuf mx(4, st);
     reduce_max_i32(color.as<int>(), n, mx.as<int>(), st);
-    return read_int(mx.as<int>(), st) + 1;
+    int h[2];
+    FDL_CK(cudaMemcpyAsync(&h[0], counts.as<int>() + kMaxRounds, 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaMemcpyAsync(&h[1], mx.p, 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaStreamSynchronize(st));
+    rounds = h[0];
+    FDL_REQUIRE(rounds >= 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
+    return h[1] + 1;
 }
 
 // ================================================================= solve layout
@@ -818,15 +905,6 @@ __global__ void k_permute_rows(int n, const int *perm, const int *inv, const int
                 wp[o + k] = w[b + k];
             }
         }
-    }
-}
-
-// PI/RQ layout: natural rows, columns renumbered by inv (a pure stream)
-__global__ void k_renumber_cols(int nnz, const int *inv, const int *ci, const double *w, int *cin,
-                                double *wn) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x) {
-        cin[k] = inv[ci[k]];
-        wn[k] = w[k];
     }
 }
 
@@ -874,7 +952,7 @@ __global__ void k_make_tiles(const int *rp, int s0, int s1, int ntiles, Tile *ou
 
 static int tiles_for(long long coord_span) { return std::max(1, (int)((coord_span + kTileT - 1) / kTileT)); }
 
-static void build_layout(const NatGraph &g, const int *color_nat, int ncolors, Level &L,
+static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &L,
                          cudaStream_t st) {
     const int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
@@ -907,17 +985,8 @@ static void build_layout(const NatGraph &g, const int *color_nat, int ncolors, L
                          n, L.perm.as<int>(), L.inv.as<int>(), g.rp, g.ci, g.w, L.rp.as<int>(),
                          L.ci.as<int>(), L.w.as<double>())));
     FDL_LAUNCH_CK();
-    // ---- PI/RQ layout: natural rows, solve-numbered columns
-    L.rpN.alloc((size_t)(n + 1) * 4 + kPadBytes, st);
-    L.ciN.alloc(ci_bytes, st);
-    L.wN.alloc(w_bytes, st);
-    k_copy_i32<<<grid_for(n + 1), 256, 0, st>>>(n + 1, g.rp, L.rpN.as<int>());
-    FDL_LAUNCH_CK();
-    if (g.nnz) {
-        k_renumber_cols<<<grid_for(g.nnz, 256, kNumSMs * 16), 256, 0, st>>>(
-            g.nnz, L.inv.as<int>(), g.ci, g.w, L.ciN.as<int>(), L.wN.as<double>());
-        FDL_LAUNCH_CK();
-    }
+    // ---- PI/RQ layout: the natural CSR (taken over from the setup graph when it
+    // owns padded storage, copied otherwise) -- see take_natural() below
     DBuf dmax(8, st);
     FDL_CK(cudaMemsetAsync(dmax.p, 0, 8, st));
     k_degree_max<<<grid_for(n, 256, kNumSMs * 8), 256, 0, st>>>(n, g.rp, g.w,
@@ -941,6 +1010,22 @@ static void build_layout(const NatGraph &g, const int *color_nat, int ncolors, L
     std::vector<int> segnnz(ncolors + 1);
     FDL_CK(cudaMemcpyAsync(segnnz.data(), sval.p, (size_t)(ncolors + 1) * 4, cudaMemcpyDeviceToHost, st));
     FDL_CK(cudaStreamSynchronize(st));
+
+    // natural CSR for the PI / RQ passes
+    auto take = [&](DBuf &own, const void *ptr, size_t bytes, DBuf &dst) {
+        if (own.p && own.p == ptr && own.bytes >= padded(bytes)) {
+            dst = std::move(own);
+        } else {
+            dst.alloc(padded(bytes), st);
+            if (bytes) FDL_CK(cudaMemcpyAsync(dst.p, ptr, bytes, cudaMemcpyDeviceToDevice, st));
+        }
+    };
+    take(g.own_rp, g.rp, (size_t)(n + 1) * 4, L.rpN);
+    take(g.own_ci, g.ci, (size_t)g.nnz * 4, L.ciN);
+    take(g.own_w, g.w, (size_t)g.nnz * 8, L.wN);
+    g.rp = L.rpN.as<int>();
+    g.ci = L.ciN.as<int>();
+    g.w = L.wN.as<double>();
 
     // tiles: GS colours, then the natural-order pass
     L.ctile.assign(ncolors + 1, 0);
@@ -987,9 +1072,9 @@ static bool coarsest_connected(const Level &L, cudaStream_t st) {
     return cnt == L.n;
 }
 
-__global__ void k_compose_qp(int n, const int *perm, const int *q_nat, const int *inv_coarse, int *qp) {
+__global__ void k_compose_qg(int n, const int *perm, const int *q_nat, int *qg) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-        qp[t] = inv_coarse[q_nat[perm[t]]];
+        qg[t] = q_nat[perm[t]];
 }
 
 void build_hierarchy(Handle &h, NatGraph &&g0) {
@@ -1025,9 +1110,9 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
     const int J = (int)h.levels.size() - 1;
     for (int ell = 0; ell < J; ell++) {
         Level &L = h.levels[ell];
-        L.qp.alloc((size_t)L.n * 4, st);
-        k_compose_qp<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), L.q_nat.as<int>(),
-                                                    h.levels[ell + 1].inv.as<int>(), L.qp.as<int>());
+        L.qg.alloc((size_t)L.n * 4, st);
+        k_compose_qg<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), L.q_nat.as<int>(),
+                                                    L.qg.as<int>());
         FDL_LAUNCH_CK();
     }
     FDL_CK(cudaStreamSynchronize(st));

@@ -11,9 +11,10 @@
 //          deflate + normalise: the whole step is ONE pass over the level);
 //   OP_RQ  Rayleigh quotient of v = s (z - mu) / sigma with the edge form
 //          sum_ij w_ij (z_i - z_j)^2 (R7), ||L v||, and v written in natural order.
-//   PI and RQ walk the rows in NATURAL order (columns in solve numbering, own
-//   value / output at inv[v]) so the x gathers of neighbouring rows stay
-//   L2-local; GS walks its colour's contiguous row range.
+//   PI and RQ work on the level's natural CSR with vectors in natural
+//   numbering (coalesced own/output streams, L2-local gathers); GS works on
+//   the GS layout (rows sorted by colour) in GS numbering, and its result is
+//   permuted to natural numbering once per level.
 // d_i = sum_j w_ij is recomputed on the fly from the streamed weights (no
 // degree array is read).  Every pass produces its reductions with a
 // deterministic two-level tree (per-CTA partials, last CTA folds them in
@@ -34,7 +35,10 @@
 namespace fdl {
 
 enum { OP_GS = 0, OP_PI = 1, OP_RQ = 2 };
-constexpr int kPassThreads = 256;
+#ifndef FDL_PASS_THREADS
+#define FDL_PASS_THREADS 256
+#endif
+constexpr int kPassThreads = FDL_PASS_THREADS;
 constexpr int kPassWarps = kPassThreads / 32;
 constexpr int kNumStats = 3;
 constexpr int kCiBuf = kStageCap + 8;   // + start alignment (<= 3) + 16-byte round-up (<= 3)
@@ -45,8 +49,8 @@ struct __align__(16) StageBuf {
     int ci[kCiBuf];
 };
 struct __align__(16) PassSmem {
-    StageBuf st[2];
-    unsigned long long bar[2];
+    StageBuf st[kStages];
+    unsigned long long bar[kStages];
 };
 static_assert(sizeof(double) * kWBuf % 16 == 0 && sizeof(int) * kCiBuf % 16 == 0, "stage alignment");
 
@@ -60,7 +64,6 @@ struct CsrView {
 struct PassArgs {
     const double *x;        // input (GS: in/out)
     double *y;              // output (PI)
-    const int *oidx;        // PI/RQ: natural row -> solve position of its own value / output
     const double *in_stat;  // slot of the input vector: [2]=mu, [3]=sigma
     double *out_stat;       // slot receiving S, Q, mu, sigma
     int stat_mode;          // bit0: first contribution (assign), bit1: last (finalise), bit2: wanted
@@ -140,10 +143,10 @@ struct Scal {
     double mu, inv_sigma, sigma, sign;
 };
 
-// own value of row r (PI / RQ: natural row r lives at solve position oidx[r])
+// own value of row r (PI / RQ)
 template <int OP>
 __device__ __forceinline__ double own_of(int r, const PassArgs &a) {
-    return OP == OP_GS ? 0.0 : a.x[a.oidx[r]];
+    return OP == OP_GS ? 0.0 : a.x[r];
 }
 
 // row epilogue: write result, accumulate statistics st[0..2]
@@ -157,7 +160,7 @@ __device__ __forceinline__ void row_finish(int r, const RowAcc<OP> &acc, const P
         st[1] = fma(xn, xn, st[1]);
     } else if (OP == OP_PI) {
         double z = (a.shift * (acc.own - sc.mu) + acc.a) * sc.inv_sigma;
-        a.y[a.oidx[r]] = z;
+        a.y[r] = z;
         st[0] += z;
         st[1] = fma(z, z, st[1]);
     } else {
@@ -237,7 +240,7 @@ __device__ __forceinline__ void finish_stats(const double tot[kNumStats], double
 
 // ----------------------------------------------------------------- the tile pass
 template <int OP>
-__global__ void __launch_bounds__(kPassThreads) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
+__global__ void __launch_bounds__(kPassThreads, FDL_PASS_MINB) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
                                                            CsrView L, PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem &S = *reinterpret_cast<PassSmem *>(smem_raw);
@@ -245,8 +248,8 @@ __global__ void __launch_bounds__(kPassThreads) k_tilepass(const Tile *__restric
     const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const double *__restrict__ x = a.x;
     if (tid == 0) {
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
+#pragma unroll
+        for (int k = 0; k < kStages; k++) mbar_init(&S.bar[k], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -278,36 +281,87 @@ __global__ void __launch_bounds__(kPassThreads) k_tilepass(const Tile *__restric
         }
     };
 
+    // ring of kStages stages: iteration `it` consumes stage it % kStages and first
+    // refills the stage consumed in iteration it-1 with the tile kStages-1 ahead
+    if (tid == 0)
+        for (int k = 0; k < kStages - 1; k++) {
+            const int tk = blockIdx.x + k * gridDim.x;
+            if (tk < ntiles) issue(tk, k);
+        }
     int it = 0;
-    if (tid == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, it++) {
-        const int b = it & 1;
-        if (tid == 0 && ti + (int)gridDim.x < ntiles) {
-            fence_proxy_async();   // generic reads of stage b^1 (previous tile) before async writes
-            issue(ti + gridDim.x, b ^ 1);
+        const int b = it % kStages;
+        const int ahead = ti + (kStages - 1) * (int)gridDim.x;
+        if (tid == 0 && ahead < ntiles) {
+            fence_proxy_async();   // generic reads of that stage (previous tile) before async writes
+            issue(ahead, (it + kStages - 1) % kStages);
         }
         const Tile t = tiles[ti];
         const int e0 = L.rp[t.x];
         const int a4 = e0 & ~3, a2 = e0 & ~1;
         const int *__restrict__ sci = S.st[b].ci - a4;   // index with the global entry number
         const double *__restrict__ sw = S.st[b].w - a2;
-        // prefetch the first row's offsets before waiting for the stage
-        int r = t.x + tid;
-        int rb = 0, re = 0;
-        if (r < t.y) { rb = L.rp[r]; re = L.rp[r + 1]; }
-        mbar_wait(&S.bar[b], (unsigned)(it >> 1) & 1u);
-        int has_long = 0;
-        for (; r < t.y;) {
-            if (re - rb <= kShortMax) {
-                RowAcc<OP> acc;
-                if (OP != OP_GS) acc.own = own_of<OP>(r, a);
-                for (int k = rb; k < re; k++) acc.add(sw[k], __ldg(x + sci[k]));
-                row_finish<OP>(r, acc, a, sc, st);
-            } else {
-                has_long = 1;
+        // Each thread takes rows in pairs (r, r + kPassThreads): the gathers of both
+        // rows are in flight together.  The first pair's offsets and own values are
+        // requested before waiting for the stage.
+        int r0 = t.x + tid;
+        int b0 = 0, e0r = 0, b1 = 0, e1r = 0;
+        double own0 = 0.0, own1 = 0.0;
+        auto fetch = [&](int rr0) {
+            const int rr1 = rr0 + kPassThreads;
+            b0 = e0r = b1 = e1r = 0;
+            if (rr0 < t.y) {
+                b0 = L.rp[rr0];
+                e0r = L.rp[rr0 + 1];
+                if (OP != OP_GS) own0 = own_of<OP>(rr0, a);
             }
-            r += kPassThreads;
-            if (r < t.y) { rb = L.rp[r]; re = L.rp[r + 1]; }
+            if (rr1 < t.y) {
+                b1 = L.rp[rr1];
+                e1r = L.rp[rr1 + 1];
+                if (OP != OP_GS) own1 = own_of<OP>(rr1, a);
+            }
+        };
+        fetch(r0);
+        mbar_wait(&S.bar[b], (unsigned)(it / kStages) & 1u);
+        int has_long = 0;
+        for (; r0 < t.y; r0 += 2 * kPassThreads) {
+            if (r0 != t.x + tid) fetch(r0);
+            const int r1 = r0 + kPassThreads;
+            const bool v1 = r1 < t.y;
+            const bool s0 = e0r - b0 <= kShortMax;
+            const bool s1 = v1 && e1r - b1 <= kShortMax;
+            if (!s0 || (v1 && !s1)) has_long = 1;
+            RowAcc<OP> acc0, acc1;
+            acc0.own = own0;
+            acc1.own = own1;
+            const int n0 = s0 ? e0r - b0 : 0, n1 = s1 ? e1r - b1 : 0;
+            const int len = max(n0, n1);
+            // 4 entries of each row per step, all 8 gathers in flight together; each
+            // row still accumulates in its sequential entry order
+            for (int j = 0; j < len; j += 4) {
+                int c0[4], c1[4];
+                double w0[4], w1[4], x0[4], x1[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const bool ok0 = j + i < n0, ok1 = j + i < n1;
+                    c0[i] = ok0 ? sci[b0 + j + i] : 0;
+                    w0[i] = ok0 ? sw[b0 + j + i] : 0.0;
+                    c1[i] = ok1 ? sci[b1 + j + i] : 0;
+                    w1[i] = ok1 ? sw[b1 + j + i] : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    x0[i] = (j + i < n0) ? __ldg(x + c0[i]) : 0.0;
+                    x1[i] = (j + i < n1) ? __ldg(x + c1[i]) : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    if (j + i < n0) acc0.add(w0[i], x0[i]);
+                    if (j + i < n1) acc1.add(w1[i], x1[i]);
+                }
+            }
+            if (s0) row_finish<OP>(r0, acc0, a, sc, st);
+            if (s1) row_finish<OP>(r1, acc1, a, sc, st);
         }
         if (__syncthreads_or(has_long)) {
             // rows with > 32 nonzeros: one warp each, from global memory; a row longer
@@ -366,6 +420,8 @@ __global__ void __launch_bounds__(kPassThreads) k_tilepass(const Tile *__restric
 
 // ----------------------------------------------------------------- small kernels
 // prolongation y^j = I^T y^{j+1} + statistics of y^j
+// prolongation y^j = I^T y^{j+1}: y[i] = xc[map[i]], xc in the
+// coarse level's natural numbering; map = q (natural output) or q o perm (GS output)
 __global__ void __launch_bounds__(256) k_prolong(int n, const int *__restrict__ qp,
                                                  const double *__restrict__ xc, double *__restrict__ y,
                                                  double *slot, double *partials, unsigned *counter) {
@@ -380,13 +436,13 @@ __global__ void __launch_bounds__(256) k_prolong(int n, const int *__restrict__ 
 }
 
 // rand(n_J) in natural order, counter-based (R6)
-__global__ void __launch_bounds__(256) k_rand(int n, const int *__restrict__ perm, uint64_t seed,
+__global__ void __launch_bounds__(256) k_rand(int n, uint64_t seed,
                                               double *__restrict__ y, double *slot, double *partials,
                                               unsigned *counter) {
     const uint64_t s0 = splitmix64(seed ^ kTagRand);
     double st[kNumStats] = {0.0, 0.0, 0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        double v = (double)(splitmix64(s0 + (uint64_t)perm[i]) >> 11) * 0x1.0p-53;
+        double v = (double)(splitmix64(s0 + (uint64_t)i) >> 11) * 0x1.0p-53;
         y[i] = v;
         st[0] += v;
         st[1] = fma(v, v, st[1]);
@@ -395,12 +451,11 @@ __global__ void __launch_bounds__(256) k_rand(int n, const int *__restrict__ per
 }
 
 // sign convention: first nonzero entry (natural order) of v = (z - mu)/sigma positive
-__global__ void k_sign(int n, const int *__restrict__ inv, const double *__restrict__ z,
-                       const double *slot, double *sign) {
+__global__ void k_sign(int n, const double *__restrict__ z, const double *slot, double *sign) {
     const double mu = slot[2];
     for (int base = 0; base < n; base += 32) {
         int i = base + lane_id();
-        double v = i < n ? z[inv[i]] - mu : 0.0;
+        double v = i < n ? z[i] - mu : 0.0;
         unsigned nz = __ballot_sync(0xffffffffu, v != 0.0);
         if (nz) {
             int src = __ffs(nz) - 1;
@@ -410,6 +465,13 @@ __global__ void k_sign(int n, const int *__restrict__ inv, const double *__restr
         }
     }
     if (lane_id() == 0) *sign = 1.0;
+}
+
+// GS numbering -> natural numbering: dst[v] = src[inv[v]] (coalesced writes)
+__global__ void __launch_bounds__(256) k_gs_to_nat(int n, const int *__restrict__ inv,
+                                                   const double *__restrict__ src, double *__restrict__ dst) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        dst[v] = __ldg(src + __ldcs(inv + v));
 }
 
 __global__ void k_set_slot(double *slot, double mu, double sigma) {
@@ -452,7 +514,6 @@ struct Enq {
         a.counter = h.counter.as<unsigned>();
         CsrView v = OP == OP_GS ? CsrView{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()}
                                 : CsrView{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
-        if (OP != OP_GS) a.oidx = L.inv.as<int>();
         k_tilepass<OP><<<grid, kPassThreads, kPassSmemBytes, st>>>(L.tiles.as<Tile>() + tb, nt, v, a);
         FDL_LAUNCH_CK();
         launches++;
@@ -490,9 +551,14 @@ struct Enq {
         a.result = h.result.as<double>();
         pass<OP_RQ>(L, L.nat_tile_begin(), L.ntiles, a);
     }
-    void prolong(const Level &L, const double *xc, double *y, double *out_slot) {
+    void prolong(const Level &L, const int *map, const double *xc, double *y, double *out_slot) {
         k_prolong<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(
-            L.n, L.qp.as<int>(), xc, y, out_slot, h.partials.as<double>(), h.counter.as<unsigned>());
+            L.n, map, xc, y, out_slot, h.partials.as<double>(), h.counter.as<unsigned>());
+        FDL_LAUNCH_CK();
+        launches++;
+    }
+    void to_nat(const Level &L, const double *xg, double *xn) {
+        k_gs_to_nat<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(L.n, L.inv.as<int>(), xg, xn);
         FDL_LAUNCH_CK();
         launches++;
     }
@@ -560,7 +626,7 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
     const Level &LJ = h.levels[J];
     double *cur_slot = e.slot(sl++);
     k_rand<<<grid_for(LJ.n, 256, h.row_grid), 256, 0, h.stream>>>(
-        LJ.n, LJ.perm.as<int>(), cfg.seed, xa, cur_slot, h.partials.as<double>(), h.counter.as<unsigned>());
+        LJ.n, cfg.seed, xa, cur_slot, h.partials.as<double>(), h.counter.as<unsigned>());
     FDL_LAUNCH_CK();
     e.launches++;
     double *cur = xa, *oth = xb;
@@ -574,13 +640,19 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
     for (int ell = J - 1; ell >= 0; ell--) {
         const Level &L = h.levels[ell];
         double *ps = e.slot(sl++);
-        e.prolong(L, cur, oth, ps);
-        std::swap(cur, oth);
-        cur_slot = ps;
         if (cfg.gs > 0) {
+            // prolong straight into GS numbering, sweep, return to natural numbering
+            e.prolong(L, L.qg.as<int>(), cur, oth, ps);
+            std::swap(cur, oth);
             double *gsl = e.slot(sl++);
             e.gs(L, cur, cfg.gs, gsl);
+            e.to_nat(L, cur, oth);
+            std::swap(cur, oth);
             cur_slot = gsl;
+        } else {
+            e.prolong(L, L.q_nat.as<int>(), cur, oth, ps);
+            std::swap(cur, oth);
+            cur_slot = ps;
         }
         for (int k = 0; k < cfg.pi; k++) {
             double *ns = e.slot(sl++);
@@ -592,7 +664,7 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
     // ---- Rayleigh quotient on level 0 (+ vector in natural order)
     const Level &L0 = h.levels[0];
     double *sgn = e.slot(sl++);
-    k_sign<<<1, 32, 0, h.stream>>>(L0.n, L0.inv.as<int>(), cur, cur_slot, sgn);
+    k_sign<<<1, 32, 0, h.stream>>>(L0.n, cur, cur_slot, sgn);
     FDL_LAUNCH_CK();
     e.launches++;
     e.rq(L0, cur, cur_slot, h.vnat.as<double>(), sgn);
@@ -612,17 +684,18 @@ void apply_level_op(Handle &h, int level, int op, int count, const double *x_in,
     double res[4] = {0, 0, 0, 0};
     if (op == FIEDLER_OP_PROLONG) {
         const Level &C = h.levels[level + 1];
-        k_gather_f64<<<grid_for(C.n), 256, 0, st>>>(C.n, C.perm.as<int>(), x_in, xa);
-        FDL_LAUNCH_CK();
-        e.prolong(L, xa, xb, s0);
-        k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), xb, x_out);
-        FDL_LAUNCH_CK();
+        FDL_CK(cudaMemcpyAsync(xa, x_in, (size_t)C.n * 8, cudaMemcpyDeviceToDevice, st));
+        e.prolong(L, L.q_nat.as<int>(), xa, x_out, s0);
         FDL_CK(cudaMemcpyAsync(res, s0, 32, cudaMemcpyDeviceToHost, st));
         FDL_CK(cudaStreamSynchronize(st));
         if (scal_host) { scal_host[0] = res[2]; scal_host[1] = res[3]; }
     } else {
-        k_gather_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), x_in, xa);
-        FDL_LAUNCH_CK();
+        if (op == FIEDLER_OP_GS_SWEEPS) {   // natural -> GS numbering
+            k_gather_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), x_in, xa);
+            FDL_LAUNCH_CK();
+        } else {
+            FDL_CK(cudaMemcpyAsync(xa, x_in, (size_t)L.n * 8, cudaMemcpyDeviceToDevice, st));
+        }
         if (op == FIEDLER_OP_GS_SWEEPS) {
             e.gs(L, xa, count, s0);
             k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), xa, x_out);
@@ -643,8 +716,7 @@ void apply_level_op(Handle &h, int level, int op, int count, const double *x_in,
                 k_normalise<<<grid_for(L.n), 256, 0, st>>>(L.n, cur, cs);
                 FDL_LAUNCH_CK();
             }
-            k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), cur, x_out);
-            FDL_LAUNCH_CK();
+            FDL_CK(cudaMemcpyAsync(x_out, cur, (size_t)L.n * 8, cudaMemcpyDeviceToDevice, st));
             FDL_CK(cudaMemcpyAsync(res, cs, 32, cudaMemcpyDeviceToHost, st));
             FDL_CK(cudaStreamSynchronize(st));
             if (scal_host) { scal_host[0] = res[2]; scal_host[1] = res[3]; }
@@ -673,7 +745,7 @@ void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, d
     double *xa = h.xa.as<double>(), *xb = h.xb.as<double>();
     double *s0 = e.slot(0), *s1 = e.slot(1);
     // finite, non-constant input: the counter-based uniform vector
-    k_rand<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(L.n, L.perm.as<int>(), 7, xa, s0,
+    k_rand<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(L.n, 7, xa, s0,
                                                            h.partials.as<double>(), h.counter.as<unsigned>());
     FDL_LAUNCH_CK();
     k_set_slot<<<1, 1, 0, st>>>(s1, 1.0, 1.0);
