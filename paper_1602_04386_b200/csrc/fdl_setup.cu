@@ -160,9 +160,15 @@ struct CtaAppend {
     int *n;
     int *base;
     __device__ __forceinline__ void push(int v) { buf[atomicAdd(n, 1)] = v; }
+    // push that spills straight to the global list when the buffer is full
+    __device__ __forceinline__ void push_safe(int v, int *out, int *gcount) {
+        const int p = atomicAdd(n, 1);
+        if (p < kAppendCap) buf[p] = v;
+        else out[atomicAdd(gcount, 1)] = v;
+    }
     // all threads; call after __syncthreads()
     __device__ __forceinline__ void flush(int *out, int *gcount) {
-        const int cnt = *n;
+        const int cnt = min(*n, kAppendCap);
         if (cnt == 0) return;
         if (threadIdx.x == 0) *base = atomicAdd(gcount, cnt);
         __syncthreads();
@@ -194,13 +200,25 @@ __device__ __forceinline__ int heaviest(int v, const int *rp, const int *ci, con
     return bj;
 }
 
+// strict edge order of R2: (w, hash) descending
+__device__ __forceinline__ bool edge_greater(double wa, unsigned long long ha, double wb,
+                                             unsigned long long hb) {
+    return wa > wb || (wa == wb && ha > hb);
+}
+
+// Rows up to kSortSlots * W entries get their neighbours ranked once in the
+// strict edge order (nbr[rp[v] + rank] = neighbour): re-pointing to the
+// heaviest FREE neighbour is then a cursor advance.  Longer rows are rescanned.
+constexpr int kSortSlots = 4;
+
 // counts[r] = length of the work list of round r (zeroed by the host); the
 // lists ping-pong between la and lb.  rounds_out[0] = handshake rounds.
 template <int W>
 __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *rp, const int *ci,
                                                              const double *w, uint64_t salt, int *m,
-                                                             int *ptr, int *mate, int *la, int *lb,
-                                                             int *counts, int *rounds_out) {
+                                                             int *ptr, int *mate, int *nbr, int *cursor,
+                                                             int *la, int *lb, int *counts,
+                                                             int *rounds_out) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
@@ -209,16 +227,65 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
     CtaAppend app{s_buf, &s_n, &s_base};
     const int lane = threadIdx.x & (W - 1);
     const int per_block = kCoopThreads / W;
-    // round 0: m(v) = heaviest neighbour = first handshake pointer; vertices with
-    // a neighbour enter the list
+    // round 0: rank every short row's neighbours; m(v) = heaviest neighbour =
+    // the first handshake pointer; vertices with a neighbour enter the list
     for (long long base = (long long)blockIdx.x * per_block; base < n;
          base += (long long)gridDim.x * per_block) {
         const long long idx = base + threadIdx.x / W;
         const int v = idx < n ? (int)idx : -1;
-        const int bj = heaviest<W>(v, rp, ci, w, salt, lane, [](int) { return false; });
+        int b = 0, deg = 0;
+        if (v >= 0) { b = rp[v]; deg = rp[v + 1] - b; }
+        const bool sortable = deg <= kSortSlots * W;
+        int bj;
+        const bool ranked = __all_sync(0xffffffffu, v < 0 || sortable);   // warp-uniform
+        if (ranked) {
+            double wv[kSortSlots];
+            unsigned long long hv[kSortSlots];
+            int cv[kSortSlots], rank[kSortSlots];
+#pragma unroll
+            for (int i = 0; i < kSortSlots; i++) {
+                const int j = lane + i * W;
+                rank[i] = 0;
+                cv[i] = -1;
+                wv[i] = 0.0;
+                hv[i] = 0ull;
+                if (j < deg) {
+                    cv[i] = ci[b + j];
+                    wv[i] = w[b + j];
+                    hv[i] = edge_hash(salt, v, cv[i]);
+                }
+            }
+            // rank = number of entries of the row greater than this one
+#pragma unroll
+            for (int sl = 0; sl < kSortSlots; sl++)
+#pragma unroll
+                for (int src = 0; src < W; src++) {
+                    const int j = sl * W + src;
+                    const double wj = __shfl_sync(0xffffffffu, wv[sl], src, W);
+                    const unsigned long long hj = __shfl_sync(0xffffffffu, hv[sl], src, W);
+                    if (j < deg)
+#pragma unroll
+                        for (int i = 0; i < kSortSlots; i++)
+                            rank[i] += edge_greater(wj, hj, wv[i], hv[i]);
+                }
+            int top = -1;
+#pragma unroll
+            for (int i = 0; i < kSortSlots; i++)
+                if (cv[i] >= 0) {
+                    nbr[b + rank[i]] = cv[i];
+                    if (rank[i] == 0) top = cv[i];
+                }
+            // the heaviest neighbour sits in exactly one lane of the sub-warp
+#pragma unroll
+            for (int o = W / 2; o; o >>= 1) top = max(top, __shfl_xor_sync(0xffffffffu, top, o, W));
+            bj = top;
+        } else {
+            bj = heaviest<W>(v, rp, ci, w, salt, lane, [](int) { return false; });
+        }
         if (v >= 0 && lane == 0) {
             m[v] = bj;
             ptr[v] = bj;
+            cursor[v] = ranked ? 0 : -1;
             if (bj >= 0) app.push(v);
         }
         __syncthreads();
@@ -239,20 +306,31 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
         }
         grid.sync();
         // (b) unmatched vertices whose target got matched re-point at their
-        //     heaviest FREE neighbour; the ones still pointing somewhere stay
+        //     heaviest FREE neighbour (cursor advance, or a rescan for long rows)
         int *gcount = counts + r + 1;
         for (long long base = (long long)blockIdx.x * per_block; base < cnt;
              base += (long long)gridDim.x * per_block) {
             const long long idx = base + threadIdx.x / W;
             const int v = idx < cnt ? in[idx] : -1;
-            bool keep = false, rescan = false;
+            bool keep = false, moved = false;
+            int cur = -1;
             if (v >= 0 && mate[v] < 0) {
                 if (mate[ptr[v]] < 0) keep = true;
-                else rescan = true;
+                else { moved = true; cur = cursor[v]; }
             }
-            const int bj = heaviest<W>(rescan ? v : -1, rp, ci, w, salt, lane,
+            int bj = -1;
+            const bool rescan = moved && cur < 0;
+            if (moved && cur >= 0 && lane == 0) {
+                const int b = rp[v], deg = rp[v + 1] - b;
+                int c = cur + 1;
+                while (c < deg && mate[nbr[b + c]] >= 0) c++;
+                bj = c < deg ? nbr[b + c] : -1;
+                cursor[v] = c;
+            }
+            const int bs = heaviest<W>(rescan ? v : -1, rp, ci, w, salt, lane,
                                        [&](int j) { return mate[j] >= 0; });
-            if (lane == 0 && rescan) {
+            if (rescan) bj = bs;
+            if (lane == 0 && moved) {
                 ptr[v] = bj;
                 keep = bj >= 0;
             }
@@ -320,6 +398,7 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
     int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
     DBuf m((size_t)n * 4, st), ptr((size_t)n * 4, st), la((size_t)n * 4, st), lb((size_t)n * 4, st),
+        nbr((size_t)std::max(g.nnz, 1) * 4, st), cursor((size_t)n * 4, st),
         counts((size_t)(kMaxRounds + 1) * 4, st);
     q.alloc((size_t)n * 4, st);
     mate.alloc((size_t)n * 4, st);
@@ -328,15 +407,18 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
     {
         const int *rp = g.rp, *ci = g.ci;
         const double *w = g.w;
-        int *pm = m.as<int>(), *pp = ptr.as<int>(), *pmate = mate.as<int>(), *pa = la.as<int>(),
-            *pb = lb.as<int>(), *pc = counts.as<int>(), *pr = counts.as<int>() + kMaxRounds;
-        void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pa, &pb, &pc, &pr};
+        int *pm = m.as<int>(), *pp = ptr.as<int>(), *pmate = mate.as<int>(), *pn = nbr.as<int>(),
+            *pcur = cursor.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(), *pc = counts.as<int>(),
+            *pr = counts.as<int>() + kMaxRounds;
+        void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr};
         DISPATCH_W(avg, coop_launch(k_match_coop<W>, args, st));
     }
     rounds = read_int(counts.as<int>() + kMaxRounds, st);
     FDL_REQUIRE(rounds >= 0, FIEDLER_ERR_INTERNAL, "matching did not terminate");
     la.release();
     lb.release();
+    nbr.release();
+    cursor.release();
     // leaders, prefix scan numbering
     DBuf leader((size_t)n * 4, st), flag((size_t)n * 4, st), id((size_t)n * 4, st), tot(8, st);
     FDL_CK(cudaMemsetAsync(tot.p, 0, 8, st));
@@ -361,8 +443,7 @@ __global__ void k_seg_starts(int n, const unsigned *keys, int *segstart) {
 // ================================================================= Galerkin product
 // I L I^T with the R3 summation order, computed per COARSE ROW
 // from the aggregate members (no global sort of all contributions):
-//   1. members of every aggregate, sorted by (aggregate, vertex): a stable
-//      radix sort of (q[v], v) -- n elements, not nnz;
+//   1. members of every aggregate (counting sort by aggregate id; n elements);
 //   2. every member m emits, for each neighbour j in another aggregate B, the
 //      contribution (key = B << 32 | kpos, w_mj), where kpos is the CSR
 //      position of the edge's (lo -> hi) entry, lo = min(m, j): the R3 order
@@ -376,10 +457,15 @@ __global__ void k_seg_starts(int n, const unsigned *keys, int *segstart) {
 constexpr int kGalSmall = 16;
 constexpr int kGalMid = 256;
 
-__global__ void k_member_keys(int n, const int *q, unsigned *keys, int *vals) {
+__global__ void k_member_count(int n, const int *q, int *cnt) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        atomicAdd(&cnt[q[v]], 1);
+}
+
+__global__ void k_member_fill(int n, const int *q, const int *mrp, int *fill, int *mem) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        keys[v] = (unsigned)q[v];
-        vals[v] = v;
+        const int A = q[v];
+        mem[mrp[A] + atomicAdd(&fill[A], 1)] = v;
     }
 }
 
@@ -657,16 +743,19 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     NatGraph out;
     out.n = c;
     out.own_rp.alloc(padded((size_t)(c + 1) * 4), st);
-    // 1. members sorted by (aggregate, vertex); mrp = aggregate offsets
-    DBuf mkeys((size_t)n * 4, st), mem((size_t)n * 4, st), mrp((size_t)(c + 1) * 4, st);
-    k_member_keys<<<grid_for(n), 256, 0, st>>>(n, q, mkeys.as<unsigned>(), mem.as<int>());
+    // 1. members grouped by aggregate (counting sort with atomics; the order
+    //    inside an aggregate is irrelevant: step 3 sorts by (B, kpos))
+    DBuf mem((size_t)n * 4, st), mrp((size_t)(c + 1) * 4, st), mfill((size_t)c * 4, st);
+    FDL_CK(cudaMemsetAsync(mrp.p, 0, (size_t)(c + 1) * 4, st));
+    FDL_CK(cudaMemsetAsync(mfill.p, 0, (size_t)c * 4, st));
+    k_member_count<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(n, q, mfill.as<int>());
     FDL_LAUNCH_CK();
-    radix_sort_u32_i32(mkeys.as<unsigned>(), mem.as<int>(), n, bits_for(c - 1), st);
-    k_seg_starts<<<grid_for(n), 256, 0, st>>>(n, mkeys.as<unsigned>(), mrp.as<int>());
+    scan_exclusive(mfill.as<int>(), mrp.as<int>(), c, mrp.as<int>() + c, st);
+    FDL_CK(cudaMemsetAsync(mfill.p, 0, (size_t)c * 4, st));
+    k_member_fill<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(n, q, mrp.as<int>(), mfill.as<int>(),
+                                                                  mem.as<int>());
     FDL_LAUNCH_CK();
-    k_set_at<<<1, 1, 0, st>>>(mrp.as<int>(), c, n);
-    FDL_LAUNCH_CK();
-    mkeys.release();
+    mfill.release();
     // 2. contributions in member order
     DBuf cnt((size_t)n * 4, st), coff((size_t)(n + 1) * 4, st);
     DISPATCH_W(avg, (k_gal_member_count<W><<<sub_grid(n, W), 256, 0, st>>>(
@@ -812,40 +901,77 @@ __device__ __forceinline__ int color_item(int v, const int *rp, const int *ci, u
     return notready;
 }
 
+// Topological (DAG) form of the same greedy colouring: indeg[v] = number of
+// higher-priority neighbours; a vertex is coloured once all of them are, then
+// it releases its lower-priority neighbours.  Every vertex and edge is handled
+// a constant number of times (the round-based JP rescans waiting vertices).
 template <int W>
 __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *rp, const int *ci,
-                                                             uint64_t salt, int *color, int *la, int *lb,
-                                                             int *counts, int *rounds_out) {
+                                                             uint64_t salt, int *color, int *indeg,
+                                                             int *la, int *lb, int *counts,
+                                                             int *rounds_out) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     CtaAppend app{s_buf, &s_n, &s_base};
-    volatile int *vcolor = color;
     const int lane = threadIdx.x & (W - 1);
     const int per_block = kCoopThreads / W;
-    const int *in = nullptr;   // round 0: every vertex
-    int *out = la;
-    int cnt = n, r = 0;
-    while (cnt > 0 && r < kMaxRounds) {
-        int *gcount = counts + r;
+    // round 0: in-degrees in the priority DAG; sources form the first list
+    for (long long base = (long long)blockIdx.x * per_block; base < n;
+         base += (long long)gridDim.x * per_block) {
+        const long long idx = base + threadIdx.x / W;
+        const int v = idx < n ? (int)idx : -1;
+        int c = 0;
+        if (v >= 0) {
+            const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+            for (int k = rp[v] + lane; k < rp[v + 1]; k += W) {
+                const int u = ci[k];
+                c += higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v);
+            }
+        }
+        c = sub_sum<W>(c);
+        if (v >= 0 && lane == 0) {
+            indeg[v] = c;
+            if (c == 0) app.push(v);
+        }
+        __syncthreads();
+        if (s_n > kAppendCap - kCoopThreads) app.flush(la, counts);
+    }
+    __syncthreads();
+    app.flush(la, counts);
+    grid.sync();
+    int *in = la, *out = lb;
+    int r = 0;
+    int cnt = *(volatile int *)&counts[0];
+    while (cnt > 0 && r + 1 < kMaxRounds) {
+        int *gcount = counts + r + 1;
         for (long long base = (long long)blockIdx.x * per_block; base < cnt;
              base += (long long)gridDim.x * per_block) {
             const long long idx = base + threadIdx.x / W;
-            const int v = idx < cnt ? (in ? in[idx] : (int)idx) : -1;
-            const int nr = color_item<W>(v, rp, ci, salt, vcolor, lane);
-            if (v >= 0 && lane == 0 && nr) app.push(v);
+            const int v = idx < cnt ? in[idx] : -1;
+            // all higher-priority neighbours are coloured: first fit
+            if (color_item<W>(v, rp, ci, salt, color, lane) && lane == 0)
+                rounds_out[1] = 1;   // impossible: a released vertex had an uncoloured predecessor
+            // release the lower-priority neighbours
+            if (v >= 0) {
+                const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+                for (int k = rp[v] + lane; k < rp[v + 1]; k += W) {
+                    const int u = ci[k];
+                    if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+                    if (atomicSub(&indeg[u], 1) == 1) app.push_safe(u, out, gcount);
+                }
+            }
             __syncthreads();
             if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
         }
         __syncthreads();
         app.flush(out, gcount);
         grid.sync();
-        cnt = *(volatile int *)gcount;
         r++;
-        in = out;
-        out = (out == la) ? lb : la;
+        cnt = *(volatile int *)gcount;
+        int *t = in; in = out; out = t;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
 }
@@ -855,24 +981,25 @@ static int color_graph(const NatGraph &g, uint64_t salt, DBuf &color, int &round
     const double avg = n ? (double)g.nnz / n : 0.0;
     color.alloc((size_t)n * 4, st);
     FDL_CK(cudaMemsetAsync(color.p, 0xff, (size_t)n * 4, st));
-    DBuf la((size_t)n * 4, st), lb((size_t)n * 4, st), counts((size_t)(kMaxRounds + 1) * 4, st);
-    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 1) * 4, st));
+    DBuf la((size_t)n * 4, st), lb((size_t)n * 4, st), indeg((size_t)n * 4, st),
+        counts((size_t)(kMaxRounds + 2) * 4, st);
+    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 2) * 4, st));
     {
         const int *rp = g.rp, *ci = g.ci;
-        int *pcol = color.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(), *pc = counts.as<int>(),
-            *pr = counts.as<int>() + kMaxRounds;
-        void *args[] = {&n, &rp, &ci, &salt, &pcol, &pa, &pb, &pc, &pr};
+        int *pcol = color.as<int>(), *pin = indeg.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(),
+            *pc = counts.as<int>(), *pr = counts.as<int>() + kMaxRounds;
+        void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr};
         DISPATCH_W(avg, coop_launch(k_color_coop<W>, args, st));
     }
     DBuf mx(4, st);
     reduce_max_i32(color.as<int>(), n, mx.as<int>(), st);
-    int h[2];
-    FDL_CK(cudaMemcpyAsync(&h[0], counts.as<int>() + kMaxRounds, 4, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaMemcpyAsync(&h[1], mx.p, 4, cudaMemcpyDeviceToHost, st));
+    int h[3];
+    FDL_CK(cudaMemcpyAsync(&h[0], counts.as<int>() + kMaxRounds, 8, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaMemcpyAsync(&h[2], mx.p, 4, cudaMemcpyDeviceToHost, st));
     FDL_CK(cudaStreamSynchronize(st));
     rounds = h[0];
-    FDL_REQUIRE(rounds >= 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
-    return h[1] + 1;
+    FDL_REQUIRE(rounds >= 0 && h[1] == 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
+    return h[2] + 1;
 }
 
 // ================================================================= solve layout
@@ -892,14 +1019,15 @@ __global__ void k_inv_and_deg(int n, const int *perm, const int *rp, int *inv, i
     }
 }
 
-// GS layout rows: row t = natural row perm[t], columns renumbered by inv, order kept
+// GS layout rows: natural row v is copied to GS row inv[v] with its columns
+// renumbered by inv (order kept).  Walking natural rows keeps the reads and the
+// inv gathers streaming; the writes form one sequential stream per colour.
 template <int W>
-__global__ void k_permute_rows(int n, const int *perm, const int *inv, const int *rp, const int *ci,
-                               const double *w, const int *rpp, int *cip, double *wp) {
-    SUBWARP_LOOP(W, n, t) {
-        if (t < n) {
-            int v = perm[t];
-            int b = rp[v], e = rp[v + 1], o = rpp[t];
+__global__ void k_permute_rows(int n, const int *inv, const int *rp, const int *ci, const double *w,
+                               const int *rpp, int *cip, double *wp) {
+    SUBWARP_LOOP(W, n, v) {
+        if (v < n) {
+            const int b = rp[v], e = rp[v + 1], o = rpp[inv[v]];
             for (int k = sw_lane_; k < e - b; k += W) {
                 cip[o + k] = inv[ci[b + k]];
                 wp[o + k] = w[b + k];
@@ -982,7 +1110,7 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     L.ci.alloc(ci_bytes, st);
     L.w.alloc(w_bytes, st);
     DISPATCH_W(avg, (k_permute_rows<W><<<sub_grid(n, W), 256, 0, st>>>(
-                         n, L.perm.as<int>(), L.inv.as<int>(), g.rp, g.ci, g.w, L.rp.as<int>(),
+                         n, L.inv.as<int>(), g.rp, g.ci, g.w, L.rp.as<int>(),
                          L.ci.as<int>(), L.w.as<double>())));
     FDL_LAUNCH_CK();
     // ---- PI/RQ layout: the natural CSR (taken over from the setup graph when it

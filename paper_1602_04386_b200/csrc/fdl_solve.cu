@@ -240,7 +240,7 @@ __device__ __forceinline__ void finish_stats(const double tot[kNumStats], double
 
 // ----------------------------------------------------------------- the tile pass
 template <int OP>
-__global__ void __launch_bounds__(kPassThreads, FDL_PASS_MINB) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
+__global__ void __launch_bounds__(kPassThreads, (OP == OP_RQ ? FDL_PASS_MINB - 1 : FDL_PASS_MINB)) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
                                                            CsrView L, PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem &S = *reinterpret_cast<PassSmem *>(smem_raw);
@@ -498,6 +498,10 @@ __global__ void k_normalise(int n, double *z, const double *slot) {
 // ----------------------------------------------------------------- host-side schedule
 constexpr size_t kPassSmemBytes = sizeof(PassSmem);
 
+// CTAs of a pass: resident CTAs per SM x SMs (persistent tile loop), per OP
+static int g_pass_grid[3] = {0, 0, 0};
+static int pass_grid(int op) { return g_pass_grid[op]; }
+
 struct Enq {
     Handle &h;
     cudaStream_t st;
@@ -509,7 +513,7 @@ struct Enq {
     void pass(const Level &L, int tb, int te, PassArgs a) {
         int nt = te - tb;
         if (nt <= 0) return;
-        int grid = std::min(nt, h.row_grid);
+        int grid = std::min(nt, pass_grid(OP));
         a.partials = h.partials.as<double>();
         a.counter = h.counter.as<unsigned>();
         CsrView v = OP == OP_GS ? CsrView{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()}
@@ -595,7 +599,7 @@ int prepare_solve(Handle &h, const SolveCfg &cfg) {
     return 0;
 }
 
-// CTAs of a pass: resident CTAs per SM x SMs (persistent tile loop)
+// returns the largest pass grid (sizes the partial-sum buffer)
 int rowpass_grid() {
     static int cached = 0;
     if (cached) return cached;
@@ -607,11 +611,13 @@ int rowpass_grid() {
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_tilepass<OP_GS>, kPassThreads, smem));
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_tilepass<OP_PI>, kPassThreads, smem));
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_tilepass<OP_RQ>, kPassThreads, smem));
-    int b = std::max(1, std::min(b0, std::min(b1, b2)));
     int dev = 0, sms = kNumSMs;
     FDL_CK(cudaGetDevice(&dev));
     FDL_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    cached = sms * b;
+    g_pass_grid[OP_GS] = sms * std::max(1, b0);
+    g_pass_grid[OP_PI] = sms * std::max(1, b1);
+    g_pass_grid[OP_RQ] = sms * std::max(1, b2);
+    cached = sms * std::max(1, std::max(b0, std::max(b1, b2)));
     return cached;
 }
 
