@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <queue>
 
@@ -52,6 +53,15 @@ template <int W> __device__ __forceinline__ int sub_sum(int v) {
     for (int o = W / 2; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, W);
     return v;
 }
+
+// cooperative kernels: thread-per-vertex below 8 neighbours (more independent
+// dependency chains in flight), sub-warps above
+#define DISPATCH_WC(avg, ...)                                   \
+    do {                                                        \
+        if ((avg) <= 8.5) { constexpr int W = 1; __VA_ARGS__; } \
+        else if ((avg) <= 18) { constexpr int W = 8; __VA_ARGS__; } \
+        else { constexpr int W = 32; __VA_ARGS__; }             \
+    } while (0)
 
 #define DISPATCH_W(avg, ...)                                    \
     do {                                                        \
@@ -155,6 +165,16 @@ constexpr int kCoopThreads = 256;
 constexpr int kAppendCap = 2048;
 constexpr int kMaxRounds = 4096;
 
+// FIEDLER_TRACE: per-phase device timestamps of the cooperative kernels
+__device__ unsigned long long *g_round_ts = nullptr;
+__device__ __forceinline__ void round_stamp(int i) {
+    if (g_round_ts && blockIdx.x == 0 && threadIdx.x == 0 && i < 2 * kMaxRounds) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_round_ts[i] = t;
+    }
+}
+
 struct CtaAppend {
     int *buf;
     int *n;
@@ -209,7 +229,7 @@ __device__ __forceinline__ bool edge_greater(double wa, unsigned long long ha, d
 // Rows up to kSortSlots * W entries get their neighbours ranked once in the
 // strict edge order (nbr[rp[v] + rank] = neighbour): re-pointing to the
 // heaviest FREE neighbour is then a cursor advance.  Longer rows are rescanned.
-constexpr int kSortSlots = 4;
+template <int W> struct SortSlots { static constexpr int value = W == 1 ? 8 : 4; };
 
 // counts[r] = length of the work list of round r (zeroed by the host); the
 // lists ping-pong between la and lb.  rounds_out[0] = handshake rounds.
@@ -225,6 +245,8 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     CtaAppend app{s_buf, &s_n, &s_base};
+    int stamp = 0;
+    round_stamp(stamp++);
     const int lane = threadIdx.x & (W - 1);
     const int per_block = kCoopThreads / W;
     // round 0: rank every short row's neighbours; m(v) = heaviest neighbour =
@@ -235,6 +257,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
         const int v = idx < n ? (int)idx : -1;
         int b = 0, deg = 0;
         if (v >= 0) { b = rp[v]; deg = rp[v + 1] - b; }
+        constexpr int kSortSlots = SortSlots<W>::value;
         const bool sortable = deg <= kSortSlots * W;
         int bj;
         const bool ranked = __all_sync(0xffffffffu, v < 0 || sortable);   // warp-uniform
@@ -294,6 +317,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
     __syncthreads();
     app.flush(la, counts);
     grid.sync();
+    round_stamp(stamp++);
     int *in = la, *out = lb;
     int r = 0;
     int cnt = *(volatile int *)&counts[0];
@@ -305,6 +329,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
             if (p >= 0 && ptr[p] == v) mate[v] = p;
         }
         grid.sync();
+        round_stamp(stamp++);
         // (b) unmatched vertices whose target got matched re-point at their
         //     heaviest FREE neighbour (cursor advance, or a rescan for long rows)
         int *gcount = counts + r + 1;
@@ -341,6 +366,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
         __syncthreads();
         app.flush(out, gcount);
         grid.sync();
+        round_stamp(stamp++);
         r++;
         cnt = *(volatile int *)gcount;
         int *t = in; in = out; out = t;
@@ -375,6 +401,39 @@ static int read_int(const int *dptr, cudaStream_t st) {
     FDL_CK(cudaStreamSynchronize(st));
     return h;
 }
+
+// trace mode: arm the timestamp buffer before a cooperative kernel, print after
+struct RoundTrace {
+    DBuf buf;
+    cudaStream_t st;
+    const char *name;
+    explicit RoundTrace(cudaStream_t s, const char *nm) : st(s), name(nm) {
+        if (!trace_enabled()) return;
+        buf.alloc((size_t)2 * kMaxRounds * 8, st);
+        FDL_CK(cudaMemsetAsync(buf.p, 0, (size_t)2 * kMaxRounds * 8, st));
+        void *p = buf.p;
+        FDL_CK(cudaMemcpyToSymbolAsync(g_round_ts, &p, sizeof(p), 0, cudaMemcpyHostToDevice, st));
+    }
+    void report(const int *d_counts) {
+        if (!trace_enabled()) return;
+        std::vector<unsigned long long> ts(2 * kMaxRounds);
+        std::vector<int> cnt(64);
+        FDL_CK(cudaMemcpyAsync(ts.data(), buf.p, ts.size() * 8, cudaMemcpyDeviceToHost, st));
+        FDL_CK(cudaMemcpyAsync(cnt.data(), d_counts, cnt.size() * 4, cudaMemcpyDeviceToHost, st));
+        void *z = nullptr;
+        FDL_CK(cudaMemcpyToSymbolAsync(g_round_ts, &z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+        FDL_CK(cudaStreamSynchronize(st));
+        std::string line = std::string("[fiedler trace]   ") + name + " phases(us):";
+        for (int i = 1; i < 2 * kMaxRounds && ts[i]; i++) {
+            char tmp[64];
+            std::snprintf(tmp, sizeof(tmp), " %.0f", (ts[i] - ts[i - 1]) * 1e-3);
+            line += tmp;
+        }
+        line += "  lists:";
+        for (int i = 0; i < 64 && (i == 0 || cnt[i - 1]); i++) line += " " + std::to_string(cnt[i]);
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
+};
 
 // cooperative launch with every CTA co-resident (grid = SMs x resident CTAs)
 template <class K>
@@ -411,7 +470,9 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
             *pcur = cursor.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(), *pc = counts.as<int>(),
             *pr = counts.as<int>() + kMaxRounds;
         void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr};
-        DISPATCH_W(avg, coop_launch(k_match_coop<W>, args, st));
+        RoundTrace tr(st, "match");
+        DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st));
+        tr.report(counts.as<int>());
     }
     rounds = read_int(counts.as<int>() + kMaxRounds, st);
     FDL_REQUIRE(rounds >= 0, FIEDLER_ERR_INTERNAL, "matching did not terminate");
@@ -916,6 +977,8 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     CtaAppend app{s_buf, &s_n, &s_base};
+    int stamp = 0;
+    round_stamp(stamp++);
     const int lane = threadIdx.x & (W - 1);
     const int per_block = kCoopThreads / W;
     // round 0: in-degrees in the priority DAG; sources form the first list
@@ -942,6 +1005,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     __syncthreads();
     app.flush(la, counts);
     grid.sync();
+    round_stamp(stamp++);
     int *in = la, *out = lb;
     int r = 0;
     int cnt = *(volatile int *)&counts[0];
@@ -951,16 +1015,68 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
              base += (long long)gridDim.x * per_block) {
             const long long idx = base + threadIdx.x / W;
             const int v = idx < cnt ? in[idx] : -1;
-            // all higher-priority neighbours are coloured: first fit
-            if (color_item<W>(v, rp, ci, salt, color, lane) && lane == 0)
-                rounds_out[1] = 1;   // impossible: a released vertex had an uncoloured predecessor
-            // release the lower-priority neighbours
-            if (v >= 0) {
-                const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
-                for (int k = rp[v] + lane; k < rp[v + 1]; k += W) {
-                    const int u = ci[k];
-                    if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
-                    if (atomicSub(&indeg[u], 1) == 1) app.push_safe(u, out, gcount);
+            if (W == 1) {
+                // one pass over the row, 8 entries at a time with every load and
+                // atomic of the chunk in flight: the colours of the higher-priority
+                // neighbours (all final) and the release of the lower-priority ones
+                // (they read colour(v) only after the round's grid barrier)
+                if (v >= 0) {
+                    const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+                    const int b = rp[v], e = rp[v + 1];
+                    unsigned long long mask = 0ull;
+                    int big = 0;
+                    for (int k = b; k < e; k += 8) {
+                        int u8[8], r8[8];
+                        bool hi8[8];
+#pragma unroll
+                        for (int i = 0; i < 8; i++) u8[i] = k + i < e ? ci[k + i] : -1;
+#pragma unroll
+                        for (int i = 0; i < 8; i++) {
+                            hi8[i] = u8[i] >= 0 &&
+                                     higher_prio(splitmix64(salt ^ (uint64_t)u8[i]), u8[i], pv, v);
+                            r8[i] = 0;
+                            if (u8[i] >= 0) r8[i] = hi8[i] ? color[u8[i]] : atomicSub(&indeg[u8[i]], 1);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; i++) {
+                            if (u8[i] < 0) continue;
+                            if (hi8[i]) {
+                                if (r8[i] < 0) rounds_out[1] = 1;   // impossible: uncoloured predecessor
+                                else if (r8[i] < 64) mask |= 1ull << r8[i];
+                                else big = 1;
+                            } else if (r8[i] == 1) {
+                                app.push_safe(u8[i], out, gcount);
+                            }
+                        }
+                    }
+                    int col = ~mask ? __ffsll((long long)~mask) - 1 : -1;
+                    (void)big;
+                    if (col < 0) {   // rare: colours 0..63 all taken by higher neighbours
+                        for (int wb = 64;; wb += 64) {
+                            unsigned long long m2 = 0ull;
+                            for (int k = b; k < e; k++) {
+                                const int u = ci[k];
+                                if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+                                const int cu = color[u];
+                                if (cu >= wb && cu < wb + 64) m2 |= 1ull << (cu - wb);
+                            }
+                            if (~m2) { col = wb + __ffsll((long long)~m2) - 1; break; }
+                        }
+                    }
+                    color[v] = col;
+                }
+            } else {
+                // all higher-priority neighbours are coloured: first fit
+                if (color_item<W>(v, rp, ci, salt, color, lane) && lane == 0)
+                    rounds_out[1] = 1;   // impossible: a released vertex had an uncoloured predecessor
+                // release the lower-priority neighbours
+                if (v >= 0) {
+                    const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+                    for (int k = rp[v] + lane; k < rp[v + 1]; k += W) {
+                        const int u = ci[k];
+                        if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+                        if (atomicSub(&indeg[u], 1) == 1) app.push_safe(u, out, gcount);
+                    }
                 }
             }
             __syncthreads();
@@ -969,6 +1085,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
         __syncthreads();
         app.flush(out, gcount);
         grid.sync();
+        round_stamp(stamp++);
         r++;
         cnt = *(volatile int *)gcount;
         int *t = in; in = out; out = t;
@@ -989,7 +1106,9 @@ static int color_graph(const NatGraph &g, uint64_t salt, DBuf &color, int &round
         int *pcol = color.as<int>(), *pin = indeg.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(),
             *pc = counts.as<int>(), *pr = counts.as<int>() + kMaxRounds;
         void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr};
-        DISPATCH_W(avg, coop_launch(k_color_coop<W>, args, st));
+        RoundTrace tr(st, "colour");
+        DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st));
+        tr.report(counts.as<int>());
     }
     DBuf mx(4, st);
     reduce_max_i32(color.as<int>(), n, mx.as<int>(), st);

@@ -32,6 +32,16 @@ def orc_graph(orc, g):
     return orc.Graph.from_csr(g.n, g.rp, g.ci, g.w)
 
 
+def clique_with_tail(k, tail):
+    """K_k (more than 64 colours) hanging off a long path: low average degree,
+    so the thread-per-vertex kernels meet a > 64-colour neighbourhood."""
+    iu = np.triu_indices(k, 1)
+    u = np.r_[iu[0], np.arange(k - 1, k + tail - 1)]
+    v = np.r_[iu[1], np.arange(k, k + tail)]
+    w = 0.5 + (np.arange(u.size) % 7) / 7.0
+    return gg.csr_from_edges(k + tail, u, v, w, "clique%d_tail%d" % (k, tail))
+
+
 SMALL = {
     "grid32_unit(config0)": lambda: gg.grid2d(32, "unit"),
     "grid50x37_uniform": lambda: gg.grid2d(50, "uniform", seed=7, mx=37),
@@ -43,6 +53,7 @@ SMALL = {
     "star40": lambda: gg.star(40),
     "complete30": lambda: gg.complete(30),
     "hub3000_3hubs": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
+    "clique70_tail2000": lambda: clique_with_tail(70, 2000),
     "tiny_p5": lambda: gg.path(5),
     "tiny_p3": lambda: gg.path(3),   # (P2 is degenerate for the Gershgorin shift: c = lambda_2)
 }
