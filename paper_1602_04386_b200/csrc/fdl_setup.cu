@@ -441,13 +441,27 @@ static void coop_launch(K kernel, void **args, cudaStream_t st) {
     static int grid = 0;   // one cache per kernel instantiation
     if (!grid) {
         int per_sm = 0, dev = 0, sms = kNumSMs;
+        // a small shared-memory carveout: these kernels live on L1-cached gathers
+        FDL_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
         FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kCoopThreads, 0));
         FDL_CK(cudaGetDevice(&dev));
         FDL_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         FDL_REQUIRE(per_sm > 0, FIEDLER_ERR_CUDA, "cooperative kernel cannot be resident");
         grid = per_sm * sms;
     }
-    FDL_CK(cudaLaunchCooperativeKernel((const void *)kernel, dim3(grid), dim3(kCoopThreads), args, 0, st));
+    // the kernels are grid-size agnostic: if the driver finds fewer co-resident
+    // CTAs than the occupancy query promised, retry with a smaller grid
+    for (;;) {
+        cudaError_t e = cudaLaunchCooperativeKernel((const void *)kernel, dim3(grid), dim3(kCoopThreads),
+                                                    args, 0, st);
+        if (e == cudaErrorCooperativeLaunchTooLarge && grid > kNumSMs) {
+            (void)cudaGetLastError();
+            grid = grid * 3 / 4;
+            continue;
+        }
+        FDL_CK(e);
+        break;
+    }
     FDL_LAUNCH_CK();
 }
 
@@ -592,58 +606,80 @@ __global__ void k_gal_member_emit(int n, const int *mem, const int *rp, const in
     }
 }
 
-// rows with <= kGalSmall contributions: register bitonic sort + sequential fold.
-// Longer rows are flagged for the mid (warp) or big (global) path.
+// rows with <= CAP contributions: register bitonic sort + sequential fold.
+// The CAP = 8 pass runs over every row and sorts out the rest: rows with
+// 8 < s <= 16 (a CAP = 16 pass over that list), kGalSmall < s <= kGalMid (warp
+// path) and longer (global path).
+template <int CAP>
+__device__ __forceinline__ void gal_row_sort_fold(int s, int sb, const unsigned long long *keys,
+                                                  const double *vals, int *outB, double *outW,
+                                                  int *deg_out) {
+    unsigned long long k[CAP];
+    double v[CAP];
+#pragma unroll
+    for (int i = 0; i < CAP; i++) {
+        k[i] = i < s ? keys[sb + i] : ~0ull;
+        v[i] = i < s ? vals[sb + i] : 0.0;
+    }
+#pragma unroll
+    for (int kk = 2; kk <= CAP; kk <<= 1)
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+            for (int i = 0; i < CAP; i++) {
+                const int l = i ^ jj;
+                if (l > i) {
+                    const bool up = (i & kk) == 0;
+                    if ((k[i] > k[l]) == up) {
+                        unsigned long long tk = k[i]; k[i] = k[l]; k[l] = tk;
+                        double tv = v[i]; v[i] = v[l]; v[l] = tv;
+                    }
+                }
+            }
+    int runs = 0;
+    unsigned curB = 0;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < CAP; i++) {
+        if (i < s) {
+            const unsigned B = (unsigned)(k[i] >> 32);
+            if (i == 0) { curB = B; acc = v[i]; }
+            else if (B != curB) {
+                outB[sb + runs] = (int)curB; outW[sb + runs] = acc; runs++;
+                curB = B; acc = v[i];
+            } else {
+                acc += v[i];
+            }
+        }
+    }
+    if (s > 0) { outB[sb + runs] = (int)curB; outW[sb + runs] = acc; runs++; }
+    *deg_out = runs;
+}
+
 __global__ void __launch_bounds__(256) k_gal_rows_small(int c, const int *mrp, const int *coff,
                                                         const unsigned long long *keys, const double *vals,
-                                                        int *outB, double *outW, int *deg, int *midflag,
-                                                        int *bigflag) {
+                                                        int *outB, double *outW, int *deg, int *f16,
+                                                        int *midflag, int *bigflag) {
     for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
         const int sb = coff[mrp[A]], se = coff[mrp[A + 1]];
         const int s = se - sb;
+        f16[A] = (s > 8 && s <= kGalSmall);
         midflag[A] = (s > kGalSmall && s <= kGalMid);
         bigflag[A] = (s > kGalMid);
-        if (s > kGalSmall) continue;
-        unsigned long long k[kGalSmall];
-        double v[kGalSmall];
-#pragma unroll
-        for (int i = 0; i < kGalSmall; i++) {
-            k[i] = i < s ? keys[sb + i] : ~0ull;
-            v[i] = i < s ? vals[sb + i] : 0.0;
-        }
-#pragma unroll
-        for (int kk = 2; kk <= kGalSmall; kk <<= 1)
-#pragma unroll
-            for (int jj = kk >> 1; jj > 0; jj >>= 1)
-#pragma unroll
-                for (int i = 0; i < kGalSmall; i++) {
-                    const int l = i ^ jj;
-                    if (l > i) {
-                        const bool up = (i & kk) == 0;
-                        if ((k[i] > k[l]) == up) {
-                            unsigned long long tk = k[i]; k[i] = k[l]; k[l] = tk;
-                            double tv = v[i]; v[i] = v[l]; v[l] = tv;
-                        }
-                    }
-                }
-        int runs = 0;
-        unsigned curB = 0;
-        double acc = 0.0;
-#pragma unroll
-        for (int i = 0; i < kGalSmall; i++) {
-            if (i < s) {
-                const unsigned B = (unsigned)(k[i] >> 32);
-                if (i == 0) { curB = B; acc = v[i]; }
-                else if (B != curB) {
-                    outB[sb + runs] = (int)curB; outW[sb + runs] = acc; runs++;
-                    curB = B; acc = v[i];
-                } else {
-                    acc += v[i];
-                }
-            }
-        }
-        if (s > 0) { outB[sb + runs] = (int)curB; outW[sb + runs] = acc; runs++; }
-        deg[A] = runs;
+        if (s > 8) continue;
+        gal_row_sort_fold<8>(s, sb, keys, vals, outB, outW, &deg[A]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_gal_rows_16(const int *list, const int *count, const int *mrp,
+                                                     const int *coff, const unsigned long long *keys,
+                                                     const double *vals, int *outB, double *outW,
+                                                     int *deg) {
+    const int cnt = *count;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const int A = list[i];
+        const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb;
+        gal_row_sort_fold<kGalSmall>(s, sb, keys, vals, outB, outW, &deg[A]);
     }
 }
 
@@ -819,7 +855,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     mfill.release();
     // 2. contributions in member order
     DBuf cnt((size_t)n * 4, st), coff((size_t)(n + 1) * 4, st);
-    DISPATCH_W(avg, (k_gal_member_count<W><<<sub_grid(n, W), 256, 0, st>>>(
+    DISPATCH_WC(avg, (k_gal_member_count<W><<<sub_grid(n, W), 256, 0, st>>>(
                          n, mem.as<int>(), g.rp, g.ci, q, cnt.as<int>())));
     FDL_LAUNCH_CK();
     scan_exclusive(cnt.as<int>(), coff.as<int>(), n, coff.as<int>() + n, st);
@@ -827,7 +863,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     const int E = read_int(coff.as<int>() + n, st);
     DBuf keys((size_t)std::max(E, 1) * 8, st), vals((size_t)std::max(E, 1) * 8, st);
     if (E > 0) {
-        DISPATCH_W(avg, (k_gal_member_emit<W><<<sub_grid(n, W), 256, 0, st>>>(
+        DISPATCH_WC(avg, (k_gal_member_emit<W><<<sub_grid(n, W), 256, 0, st>>>(
                              n, mem.as<int>(), g.rp, g.ci, g.w, q, coff.as<int>(),
                              keys.as<unsigned long long>(), vals.as<double>())));
         FDL_LAUNCH_CK();
@@ -835,18 +871,25 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     mem.release();
     // 3. per-row sort + fold
     DBuf outB((size_t)std::max(E, 1) * 4, st), outW((size_t)std::max(E, 1) * 8, st),
-        deg((size_t)(c + 1) * 4, st), midf((size_t)c * 4, st), bigf((size_t)c * 4, st),
-        lists((size_t)c * 4 * 2, st), lcnt(8, st);
+        deg((size_t)(c + 1) * 4, st), f16((size_t)c * 4, st), midf((size_t)c * 4, st),
+        bigf((size_t)c * 4, st), lists((size_t)c * 4 * 3, st), lcnt(16, st);
     k_gal_rows_small<<<grid_for(c, 256, kNumSMs * 8), 256, 0, st>>>(
         c, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(), vals.as<double>(),
-        outB.as<int>(), outW.as<double>(), deg.as<int>(), midf.as<int>(), bigf.as<int>());
+        outB.as<int>(), outW.as<double>(), deg.as<int>(), f16.as<int>(), midf.as<int>(), bigf.as<int>());
     FDL_LAUNCH_CK();
-    int *midlist = lists.as<int>(), *biglist = lists.as<int>() + c;
+    int *midlist = lists.as<int>(), *biglist = lists.as<int>() + c, *list16 = lists.as<int>() + 2 * c;
     compact_flagged(nullptr, midf.as<int>(), c, midlist, lcnt.as<int>(), st);
     compact_flagged(nullptr, bigf.as<int>(), c, biglist, lcnt.as<int>() + 1, st);
-    int hc[2];
-    FDL_CK(cudaMemcpyAsync(hc, lcnt.p, 8, cudaMemcpyDeviceToHost, st));
+    compact_flagged(nullptr, f16.as<int>(), c, list16, lcnt.as<int>() + 2, st);
+    int hc[3];
+    FDL_CK(cudaMemcpyAsync(hc, lcnt.p, 12, cudaMemcpyDeviceToHost, st));
     FDL_CK(cudaStreamSynchronize(st));
+    if (hc[2] > 0) {
+        k_gal_rows_16<<<grid_for(hc[2], 256, kNumSMs * 8), 256, 0, st>>>(
+            list16, lcnt.as<int>() + 2, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
+            vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
+        FDL_LAUNCH_CK();
+    }
     if (hc[0] > 0) {
         k_gal_rows_mid<<<std::min(div_up(hc[0], kGalMidWarps), kNumSMs * 8), kGalMidWarps * 32, 0, st>>>(
             midlist, lcnt.as<int>(), mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
@@ -893,7 +936,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     out.own_ci.alloc(padded((size_t)std::max(out.nnz, 1) * 4), st);
     out.own_w.alloc(padded((size_t)std::max(out.nnz, 1) * 8), st);
     const double cavg = c ? (double)out.nnz / c : 0.0;
-    DISPATCH_W(cavg, (k_gal_write<W><<<sub_grid(c, W), 256, 0, st>>>(
+    DISPATCH_WC(cavg, (k_gal_write<W><<<sub_grid(c, W), 256, 0, st>>>(
                           c, mrp.as<int>(), coff.as<int>(), out.own_rp.as<int>(), outB.as<int>(),
                           outW.as<double>(), out.own_ci.as<int>(), out.own_w.as<double>())));
     FDL_LAUNCH_CK();
