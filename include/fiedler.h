@@ -177,11 +177,79 @@ FIEDLER_API int fiedler_level_apply(fiedler_handle h, int32_t level, int32_t op,
  *   FIEDLER_OP_RAYLEIGH  one Rayleigh-quotient row pass per rep.
  * *ms_per_rep = mean device time of one rep; *bytes_per_rep (may be NULL) =
  * the ALGORITHMIC HBM bytes of one rep (4(n+1) row
- * offsets + 12 per adjacency nonzero + 8n vector read + 8n vector written,
- * + 4n + 8n for the Rayleigh pass's natural-order output).  The level's solve
- * buffers are used as scratch; call between solves, not during one. */
+ * offsets + 12 per adjacency nonzero + 8n vector read + 8n vector written).
+ * The level's solve buffers are used as scratch; call between solves, not
+ * during one. */
 FIEDLER_API int fiedler_level_time(fiedler_handle h, int32_t level, int32_t op, int32_t reps,
                                    double *ms_per_rep, double *bytes_per_rep);
+
+/* ---------------------------------------------------------------------------
+ * Row-partitioned solve across ranks (one process per GPU).
+ *
+ * Every rank holds the whole hierarchy (fiedler_create is deterministic, so
+ * all ranks build the same one).  A partitioned level gives rank r the
+ * contiguous natural rows [row_begin, row_end) (balanced by rows + nonzeros);
+ * every pass of the solve then runs on the rank's own rows only, and the
+ * caller moves the bytes between ranks with its collectives library
+ * (paper_1602_04386_b200/dist.py: torch.distributed over NCCL):
+ *   - halo exchange: after a pass, the values of the rank's rows that other
+ *     ranks read (send lists) go to them, and the rank receives the values of
+ *     its ghost rows (recv lists);  peer-major, ascending row order, so rank
+ *     p's send list to rank r equals rank r's recv list from rank p;
+ *   - all-reduce (sum) of the pass statistics, then FIEDLER_DOP_FINALISE;
+ *   - all-gather of a level's final vector before the next finer level.
+ * Reading of the paper (R2-R8) and the arithmetic per row are those of
+ * fiedler_solve; only the summation order of the global sums differs.
+ *
+ * Vectors are device arrays of the level's size in one of two numberings:
+ * natural (the level's own vertex ids) or GS (the multicolour order used by
+ * the Gauss-Seidel sweeps; FIEDLER_DOP_PROLONG / _TO_NAT convert).
+ * Statistic slots are device arrays of 4 doubles.
+ * ------------------------------------------------------------------------- */
+#define FIEDLER_MAX_RANKS 64
+
+typedef struct fiedler_dist_plan_info {
+    int64_t n;                                   /* level size                     */
+    int32_t nranks, rank, colors;
+    int64_t row_begin, row_end;                  /* rows of this rank              */
+    int64_t row_bounds[FIEDLER_MAX_RANKS + 1];   /* rows of every rank             */
+    int64_t send_count[FIEDLER_MAX_RANKS];       /* halo entries sent to each rank */
+    int64_t recv_count[FIEDLER_MAX_RANKS];       /* ghost entries from each rank   */
+    int64_t send_total, recv_total;
+} fiedler_dist_plan_info;
+
+/* Build (or rebuild) the plan of `level` for (nranks, rank); nranks == 1 gives
+ * the replicated (whole-level) plan.  Synchronises the handle's stream.
+ * Errors: ARG (bad level / nranks outside [1, FIEDLER_MAX_RANKS] / rank). */
+FIEDLER_API int fiedler_dist_plan(fiedler_handle h, int32_t level, int32_t nranks, int32_t rank,
+                                  fiedler_dist_plan_info *info);
+
+#define FIEDLER_DOP_RAND 1          /* y (natural) = rand(n) (R6, seed = arg); stat = partial (S, Q)     */
+#define FIEDLER_DOP_PROLONG 2       /* y = I^T x for own + ghost rows; x = FULL vector of level+1
+                                       (natural); arg 0: y natural, 1: y GS; stat = partial (S, Q)     */
+#define FIEDLER_DOP_GS_COLOUR 3     /* one GS pass over own rows of colour arg; x (GS) in place          */
+#define FIEDLER_DOP_TO_NAT 4        /* y (natural) = x (GS) on own rows; stat = partial (S, Q)            */
+#define FIEDLER_DOP_POWER 5         /* y = one power step of x on own rows; stat_in = finalised slot of x;
+                                       stat = partial (S, Q) of y                                       */
+#define FIEDLER_DOP_FINALISE 6      /* stat: (S, Q) -> (S, Q, mean, deflated norm) of the level          */
+#define FIEDLER_DOP_FIRST_NONZERO 7 /* stat[0] = 2 i + (v_i < 0) for the first own row i with
+                                       v_i = x_i - mean != 0 (stat_in = slot of x), else 2^60        */
+#define FIEDLER_DOP_SIGN 8          /* stat[2] = +-1 from the reduced key in stat[0]                     */
+#define FIEDLER_DOP_RAYLEIGH 9      /* own rows: y (natural) = sign (x - mean)/norm; stat = partial
+                                       (edge form, sum (x - mean)^2, ||L (x - mean)||^2);
+                                       stat_in = slot of x, sign read at sign_slot[2] (arg ignored)     */
+#define FIEDLER_DOP_FINALISE_RQ 10  /* stat (reduced partials) -> {lambda2, residual, ||v||}, using
+                                       stat_in = slot of x                                              */
+#define FIEDLER_DOP_HALO_PACK 11    /* y (send buffer) = x at the send rows; arg 0: x natural, 1: GS     */
+#define FIEDLER_DOP_HALO_UNPACK 12  /* y at the ghost rows = x (recv buffer); arg 0: y natural, 1: GS    */
+
+/* Enqueue one operation of the partitioned solve on `stream` (NULL = the
+ * handle's stream) for the plan last built on `level`.  Never synchronises.
+ * x / y / stat / stat_in / sign_slot: device pointers (unused ones may be
+ * NULL).  Errors: ARG (no plan on level, bad op), CUDA. */
+FIEDLER_API int fiedler_dist_op(fiedler_handle h, int32_t level, int32_t op, int64_t arg,
+                                const double *x, double *y, double *stat, const double *stat_in,
+                                const double *sign_slot, void *stream);
 
 #ifdef __cplusplus
 }

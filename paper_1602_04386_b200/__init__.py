@@ -36,9 +36,24 @@ FIEDLER_OP_POWER = 2
 FIEDLER_OP_PROLONG = 3
 FIEDLER_OP_RAYLEIGH = 4
 
+FIEDLER_MAX_RANKS = 64
+FIEDLER_DOP_RAND = 1
+FIEDLER_DOP_PROLONG = 2
+FIEDLER_DOP_GS_COLOUR = 3
+FIEDLER_DOP_TO_NAT = 4
+FIEDLER_DOP_POWER = 5
+FIEDLER_DOP_FINALISE = 6
+FIEDLER_DOP_FIRST_NONZERO = 7
+FIEDLER_DOP_SIGN = 8
+FIEDLER_DOP_RAYLEIGH = 9
+FIEDLER_DOP_FINALISE_RQ = 10
+FIEDLER_DOP_HALO_PACK = 11
+FIEDLER_DOP_HALO_UNPACK = 12
+
 EXPORTED = ("fiedler_default_opts", "fiedler_create", "fiedler_solve", "fiedler_destroy",
             "fiedler_last_error", "fiedler_num_levels", "fiedler_level_size",
-            "fiedler_level_export", "fiedler_level_apply", "fiedler_level_time")
+            "fiedler_level_export", "fiedler_level_apply", "fiedler_level_time",
+            "fiedler_dist_plan", "fiedler_dist_op")
 
 
 class fiedler_opts(ctypes.Structure):
@@ -64,6 +79,16 @@ class fiedler_info(ctypes.Structure):
         return [dict(n=self.level_n[i], nnz=self.level_nnz[i], colors=self.level_colors[i],
                      match_rounds=self.level_match_rounds[i], shift=self.level_shift[i])
                 for i in range(self.num_levels)]
+
+
+class fiedler_dist_plan_info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("colors", ctypes.c_int32),
+                ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("row_bounds", ctypes.c_int64 * (FIEDLER_MAX_RANKS + 1)),
+                ("send_count", ctypes.c_int64 * FIEDLER_MAX_RANKS),
+                ("recv_count", ctypes.c_int64 * FIEDLER_MAX_RANKS),
+                ("send_total", ctypes.c_int64), ("recv_total", ctypes.c_int64)]
 
 
 class FiedlerError(RuntimeError):
@@ -107,6 +132,10 @@ def _load():
         lib.fiedler_level_time.restype = ctypes.c_int
         lib.fiedler_level_time.argtypes = [P, i32, i32, i32, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double)]
+        lib.fiedler_dist_plan.restype = ctypes.c_int
+        lib.fiedler_dist_plan.argtypes = [P, i32, i32, i32, ctypes.POINTER(fiedler_dist_plan_info)]
+        lib.fiedler_dist_op.restype = ctypes.c_int
+        lib.fiedler_dist_op.argtypes = [P, i32, i32, i64, P, P, P, P, P, P]
         lib.fiedler_level_apply.restype = ctypes.c_int
         lib.fiedler_level_apply.argtypes = [P, i32, i32, i32, P, P, i32, ctypes.POINTER(ctypes.c_double)]
         _lib = lib
@@ -221,6 +250,29 @@ def fiedler_level_time(handle, level, op, reps=20):
     ms, by = ctypes.c_double(), ctypes.c_double()
     _check(_load().fiedler_level_time(handle, level, op, reps, ctypes.byref(ms), ctypes.byref(by)))
     return ms.value, by.value
+
+
+def fiedler_dist_plan(handle, level, nranks, rank) -> fiedler_dist_plan_info:
+    """Row partition + halo plan of `level` for (nranks, rank) (include/fiedler.h)."""
+    info = fiedler_dist_plan_info()
+    _check(_load().fiedler_dist_plan(handle, level, nranks, rank, ctypes.byref(info)))
+    return info
+
+
+def fiedler_dist_op(handle, level, op, arg=0, x=None, y=None, stat=None, stat_in=None, sign_slot=None,
+                    stream=None):
+    """Enqueue one partitioned-solve operation; array arguments are CUDA tensors
+    (float64) or raw device pointers, `stream` a cudaStream_t (int) or None."""
+    def ptr(t):
+        if t is None:
+            return None
+        if isinstance(t, int):
+            return t
+        if t.dtype.itemsize != 8 or not t.is_cuda or not t.is_contiguous():
+            raise TypeError("expected a contiguous CUDA float64 tensor")
+        return t.data_ptr()
+    _check(_load().fiedler_dist_op(handle, level, op, int(arg), ptr(x), ptr(y), ptr(stat), ptr(stat_in),
+                                   ptr(sign_slot), stream))
 
 
 class FiedlerSolver:

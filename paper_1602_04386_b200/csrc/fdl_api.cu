@@ -427,4 +427,29 @@ int fiedler_level_apply(fiedler_handle hh, int32_t level, int32_t op, int32_t co
     API_END
 }
 
+int fiedler_dist_plan(fiedler_handle hh, int32_t level, int32_t nranks, int32_t rank,
+                      fiedler_dist_plan_info *info) {
+    API_BEGIN
+    FDL_REQUIRE(hh, FIEDLER_ERR_ARG, "NULL handle");
+    Handle &h = *reinterpret_cast<Handle *>(hh);
+    FDL_REQUIRE(level >= 0 && level < (int)h.levels.size(), FIEDLER_ERR_ARG, "bad level");
+    FDL_REQUIRE(nranks >= 1 && nranks <= FIEDLER_MAX_RANKS && rank >= 0 && rank < nranks, FIEDLER_ERR_ARG,
+                "bad nranks / rank");
+    FDL_CK(cudaSetDevice(h.device));
+    dist_plan(h, level, nranks, rank, info);
+    return FIEDLER_OK;
+    API_END
+}
+
+int fiedler_dist_op(fiedler_handle hh, int32_t level, int32_t op, int64_t arg, const double *x, double *y,
+                    double *stat, const double *stat_in, const double *sign_slot, void *stream) {
+    API_BEGIN
+    FDL_REQUIRE(hh, FIEDLER_ERR_ARG, "NULL handle");
+    Handle &h = *reinterpret_cast<Handle *>(hh);
+    FDL_REQUIRE(level >= 0 && level < (int)h.levels.size(), FIEDLER_ERR_ARG, "bad level");
+    dist_op(h, level, op, arg, x, y, stat, stat_in, sign_slot, stream ? (cudaStream_t)stream : h.stream);
+    return FIEDLER_OK;
+    API_END
+}
+
 }  // extern "C"

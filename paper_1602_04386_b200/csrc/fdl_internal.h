@@ -47,6 +47,21 @@ struct NatGraph {
     DBuf own_rp, own_ci, own_w;  // storage when owned by the library
 };
 
+// Row partition of one level for the partitioned solve (fiedler_dist_plan).
+struct DistPlan {
+    bool valid = false;
+    int nranks = 1, rank = 0;
+    int r0 = 0, r1 = 0;                  // own natural rows
+    std::vector<int64_t> bounds;         // [nranks + 1] natural row bounds of every rank
+    DBuf tilesN;                         // own natural tiles (PI / RQ)
+    int ntN = 0;
+    DBuf tilesGS;                        // own GS tiles, colour c at [ctile[c], ctile[c+1])
+    std::vector<int> ctile;
+    DBuf send_idx, recv_idx;             // natural ids, peer-major, ascending within a peer
+    std::vector<int64_t> send_cnt, recv_cnt;
+    int send_total = 0, recv_total = 0;
+};
+
 struct Level {
     int n = 0, nnz = 0;
     // GS layout: rows sorted by (colour, natural id); every colour is one
@@ -64,6 +79,8 @@ struct Level {
     // [ctile[c], ctile[c+1])), then the natural-order tiles [ctile[ncolors], ntiles)
     DBuf tiles;
     std::vector<int> ctile;
+    std::vector<int> seg;    // [ncolors + 1] GS row range of every colour
+    DistPlan dist;
     int ncolors = 0;
     int ntiles = 0;
     double shift = 0.0;      // c of c I - L: 2 max_i d_i (R8)
@@ -116,6 +133,10 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg);
 // Single-operation entry (fiedler_level_apply); vectors in solve numbering on device.
 void apply_level_op(Handle &h, int level, int op, int count, const double *x_in, double *x_out,
                     double *scal_host);
+// partitioned solve (fiedler_dist_plan / fiedler_dist_op)
+void dist_plan(Handle &h, int level, int nranks, int rank, fiedler_dist_plan_info *info);
+void dist_op(Handle &h, int level, int op, int64_t arg, const double *x, double *y, double *stat,
+             const double *stat_in, const double *sign_slot, cudaStream_t st);
 // fiedler_level_time: CUDA-event timing of `reps` back-to-back row passes
 void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, double *bytes_per_rep);
 

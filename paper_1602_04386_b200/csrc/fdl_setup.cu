@@ -1318,6 +1318,7 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     g.w = L.wN.as<double>();
 
     // tiles: GS colours, then the natural-order pass
+    L.seg = seg;
     L.ctile.assign(ncolors + 1, 0);
     int nt = 0;
     std::vector<int> cnt(ncolors + 1);

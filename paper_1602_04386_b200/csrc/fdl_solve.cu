@@ -29,6 +29,7 @@
 // row longer than a tile, the whole CTA) straight from global memory.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "fdl_internal.h"
 
@@ -73,7 +74,8 @@ struct PassArgs {
     unsigned *counter;
     double *vnat;           // RQ: output vector, natural order
     const double *sign;     // RQ: +-1
-    double *result;         // RQ: {lambda2, residual}
+    double *result;         // RQ: {lambda2, residual, ||v||}, or the raw sums if rq_raw
+    int rq_raw;             // RQ: write the raw partial sums (partitioned solve)
 };
 
 // ----------------------------------------------------------------- PTX helpers
@@ -405,7 +407,11 @@ __global__ void __launch_bounds__(kPassThreads, (OP == OP_RQ ? FDL_PASS_MINB - 1
     }
     if (OP == OP_GS && !(a.stat_mode & 4)) return;   // uniform: statistics not wanted
     grid_reduce(st, a.partials, a.counter, [&](const double *tot) {
-        if (OP == OP_RQ) {
+        if (OP == OP_RQ && a.rq_raw) {
+            a.result[0] = tot[0];
+            a.result[1] = tot[1];
+            a.result[2] = tot[2];
+        } else if (OP == OP_RQ) {
             double lam = 0.5 * tot[0] / tot[1];
             double vn2 = tot[1] * sc.inv_sigma * sc.inv_sigma;   // ||v||^2
             double res2 = tot[2] - lam * lam * vn2;
@@ -419,7 +425,6 @@ __global__ void __launch_bounds__(kPassThreads, (OP == OP_RQ ? FDL_PASS_MINB - 1
 }
 
 // ----------------------------------------------------------------- small kernels
-// prolongation y^j = I^T y^{j+1} + statistics of y^j
 // prolongation y^j = I^T y^{j+1}: y[i] = xc[map[i]], xc in the
 // coarse level's natural numbering; map = q (natural output) or q o perm (GS output)
 __global__ void __launch_bounds__(256) k_prolong(int n, const int *__restrict__ qp,
@@ -508,19 +513,22 @@ struct Enq {
     int launches = 0;
     double *slot(int k) { return h.scal.as<double>() + 4 * k; }
 
-    // OP over tiles [tb, te) of level L (GS: GS layout; PI/RQ: natural layout)
+    // OP over the tiles [tiles, tiles + nt) of level L (GS: GS layout; PI/RQ: natural layout)
     template <int OP>
-    void pass(const Level &L, int tb, int te, PassArgs a) {
-        int nt = te - tb;
+    void pass_tiles(const Level &L, const Tile *tiles, int nt, PassArgs a) {
         if (nt <= 0) return;
         int grid = std::min(nt, pass_grid(OP));
         a.partials = h.partials.as<double>();
         a.counter = h.counter.as<unsigned>();
         CsrView v = OP == OP_GS ? CsrView{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()}
                                 : CsrView{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
-        k_tilepass<OP><<<grid, kPassThreads, kPassSmemBytes, st>>>(L.tiles.as<Tile>() + tb, nt, v, a);
+        k_tilepass<OP><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
         FDL_LAUNCH_CK();
         launches++;
+    }
+    template <int OP>
+    void pass(const Level &L, int tb, int te, PassArgs a) {
+        pass_tiles<OP>(L, L.tiles.as<Tile>() + tb, te - tb, a);
     }
     void gs(const Level &L, double *x, int sweeps, double *out_slot) {
         for (int s = 0; s < sweeps; s++)
@@ -779,6 +787,431 @@ void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, d
         // and weights once, the input vector once, the output vector once
         double n = L.n, nnz = L.nnz;
         *bytes_per_rep = 4.0 * (n + 1) + 12.0 * nnz + 8.0 * n + 8.0 * n;
+    }
+}
+
+}  // namespace fdl
+
+// =================================================================== partitioned solve
+// fiedler_dist_plan / fiedler_dist_op (include/fiedler.h).
+namespace fdl {
+
+__device__ __forceinline__ int lower_bound_coord_d(const int *rp, int lo, int hi, long long target) {
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((long long)rp[mid] + mid < target) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// bounds[k] = first natural row whose coordinate rp[r] + r reaches k (n + nnz) / nranks
+__global__ void k_dist_bounds(const int *rp, int n, int nranks, int *bounds) {
+    const int k = threadIdx.x;
+    if (k > nranks) return;
+    const long long total = (long long)rp[n] + n;
+    bounds[k] = k == 0 ? 0 : (k == nranks ? n : lower_bound_coord_d(rp, 0, n, total * k / nranks));
+}
+
+// own GS rows of colour c: [lower_bound(perm_c, r0), lower_bound(perm_c, r1)) inside the
+// colour's segment (natural ids ascend within a colour)
+__global__ void k_dist_colour_ranges(const int *perm, const int *seg, int ncol, int r0, int r1, int *ab) {
+    const int c = threadIdx.x;
+    if (c >= ncol) return;
+    for (int side = 0; side < 2; side++) {
+        int lo = seg[c], hi = seg[c + 1];
+        const int target = side ? r1 : r0;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (perm[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        ab[2 * c + side] = lo;
+    }
+}
+
+__global__ void k_make_tiles_d(const int *rp, int s0, int s1, int ntiles, Tile *out) {
+    const long long C0 = (long long)rp[s0] + s0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+        int a = t == 0 ? s0 : lower_bound_coord_d(rp, s0, s1, C0 + (long long)t * kTileT);
+        int b = (t + 1 == ntiles) ? s1 : lower_bound_coord_d(rp, s0, s1, C0 + (long long)(t + 1) * kTileT);
+        out[t] = make_int2(a, b);
+    }
+}
+
+__device__ __forceinline__ int owner_of(int u, const int *bounds, int nranks) {
+    int p = 0;
+    while (p + 1 < nranks && u >= bounds[p + 1]) p++;
+    return p;
+}
+
+// ghosts: neighbours of own rows outside [r0, r1); peer masks of own rows
+__global__ void k_dist_mark(const int *rp, const int *ci, int r0, int r1, const int *bounds, int nranks,
+                            int rank, int *ghost_flag, unsigned long long *peer_mask) {
+    for (int v = r0 + blockIdx.x * blockDim.x + threadIdx.x; v < r1; v += gridDim.x * blockDim.x) {
+        unsigned long long m = 0ull;
+        for (int k = rp[v]; k < rp[v + 1]; k++) {
+            const int u = ci[k];
+            if (u < r0 || u >= r1) {
+                ghost_flag[u] = 1;
+                m |= 1ull << owner_of(u, bounds, nranks);
+            }
+        }
+        peer_mask[v - r0] = m & ~(1ull << rank);
+    }
+}
+
+__global__ void k_mask_bit(const unsigned long long *mask, int cnt, int p, int *flag) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+        flag[i] = (int)((mask[i] >> p) & 1ull);
+}
+
+__global__ void k_add_offset(int *a, int cnt, int off) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) a[i] += off;
+}
+
+// number of sorted list entries below each bound
+__global__ void k_count_below(const int *list, const int *cnt, const int *bounds, int nb, int *pos) {
+    const int k = threadIdx.x;
+    if (k >= nb) return;
+    int lo = 0, hi = *cnt;
+    const int target = bounds[k];
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (list[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    pos[k] = lo;
+}
+
+static int read_i(const int *d, cudaStream_t st) {
+    int h;
+    FDL_CK(cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaStreamSynchronize(st));
+    return h;
+}
+
+void dist_plan(Handle &h, int level, int nranks, int rank, fiedler_dist_plan_info *info) {
+    Level &L = h.levels[level];
+    cudaStream_t st = h.stream;
+    DistPlan &P = L.dist;
+    P = DistPlan();
+    P.nranks = nranks;
+    P.rank = rank;
+    const int n = L.n;
+    DBuf db((size_t)(nranks + 1) * 4, st);
+    k_dist_bounds<<<1, 128, 0, st>>>(L.rpN.as<int>(), n, nranks, db.as<int>());
+    FDL_LAUNCH_CK();
+    std::vector<int> b(nranks + 1);
+    FDL_CK(cudaMemcpyAsync(b.data(), db.p, (size_t)(nranks + 1) * 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaStreamSynchronize(st));
+    P.bounds.assign(b.begin(), b.end());
+    P.r0 = b[rank];
+    P.r1 = b[rank + 1];
+    // own natural tiles
+    int rr[2];
+    FDL_CK(cudaMemcpyAsync(&rr[0], L.rpN.as<int>() + P.r0, 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaMemcpyAsync(&rr[1], L.rpN.as<int>() + P.r1, 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaStreamSynchronize(st));
+    const long long spanN = (long long)(rr[1] + P.r1) - (rr[0] + P.r0);
+    P.ntN = P.r1 > P.r0 ? (int)((spanN + kTileT - 1) / kTileT) : 0;
+    P.tilesN.alloc((size_t)std::max(P.ntN, 1) * sizeof(Tile), st);
+    if (P.ntN) {
+        k_make_tiles_d<<<grid_for(P.ntN), 256, 0, st>>>(L.rpN.as<int>(), P.r0, P.r1, P.ntN, P.tilesN.as<Tile>());
+        FDL_LAUNCH_CK();
+    }
+    // own GS tiles per colour
+    const int nc = L.ncolors;
+    DBuf dseg((size_t)(nc + 1) * 4, st), dab((size_t)2 * nc * 4, st);
+    FDL_CK(cudaMemcpyAsync(dseg.p, L.seg.data(), (size_t)(nc + 1) * 4, cudaMemcpyHostToDevice, st));
+    k_dist_colour_ranges<<<1, 128, 0, st>>>(L.perm.as<int>(), dseg.as<int>(), nc, P.r0, P.r1, dab.as<int>());
+    FDL_LAUNCH_CK();
+    std::vector<int> ab(2 * nc);
+    FDL_CK(cudaMemcpyAsync(ab.data(), dab.p, (size_t)2 * nc * 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaStreamSynchronize(st));
+    std::vector<int> cnt(nc, 0);
+    P.ctile.assign(nc + 1, 0);
+    int nt = 0;
+    for (int c = 0; c < nc; c++) {
+        P.ctile[c] = nt;
+        const int a0 = ab[2 * c], a1 = ab[2 * c + 1];
+        if (a1 > a0) {
+            int q[2];
+            FDL_CK(cudaMemcpyAsync(&q[0], L.rp.as<int>() + a0, 4, cudaMemcpyDeviceToHost, st));
+            FDL_CK(cudaMemcpyAsync(&q[1], L.rp.as<int>() + a1, 4, cudaMemcpyDeviceToHost, st));
+            FDL_CK(cudaStreamSynchronize(st));
+            const long long span = (long long)(q[1] + a1) - (q[0] + a0);
+            cnt[c] = (int)((span + kTileT - 1) / kTileT);
+            if (cnt[c] < 1) cnt[c] = 1;
+        }
+        nt += cnt[c];
+    }
+    P.ctile[nc] = nt;
+    P.tilesGS.alloc((size_t)std::max(nt, 1) * sizeof(Tile), st);
+    for (int c = 0; c < nc; c++)
+        if (cnt[c]) {
+            k_make_tiles_d<<<grid_for(cnt[c]), 256, 0, st>>>(L.rp.as<int>(), ab[2 * c], ab[2 * c + 1], cnt[c],
+                                                             P.tilesGS.as<Tile>() + P.ctile[c]);
+            FDL_LAUNCH_CK();
+        }
+    // halo plan
+    P.send_cnt.assign(nranks, 0);
+    P.recv_cnt.assign(nranks, 0);
+    if (nranks > 1) {
+        const int own = P.r1 - P.r0;
+        DBuf gflag((size_t)std::max(n, 1) * 4, st), mask((size_t)std::max(own, 1) * 8, st),
+            glist((size_t)std::max(n, 1) * 4, st), gcnt(8, st), pos((size_t)(nranks + 1) * 4, st);
+        FDL_CK(cudaMemsetAsync(gflag.p, 0, (size_t)n * 4, st));
+        if (own > 0) {
+            k_dist_mark<<<grid_for(own), 256, 0, st>>>(L.rpN.as<int>(), L.ciN.as<int>(), P.r0, P.r1, db.as<int>(),
+                                                       nranks, rank, gflag.as<int>(), mask.as<unsigned long long>());
+            FDL_LAUNCH_CK();
+        }
+        compact_flagged(nullptr, gflag.as<int>(), n, glist.as<int>(), gcnt.as<int>(), st);
+        k_count_below<<<1, 128, 0, st>>>(glist.as<int>(), gcnt.as<int>(), db.as<int>(), nranks + 1, pos.as<int>());
+        FDL_LAUNCH_CK();
+        std::vector<int> hp(nranks + 1);
+        FDL_CK(cudaMemcpyAsync(hp.data(), pos.p, (size_t)(nranks + 1) * 4, cudaMemcpyDeviceToHost, st));
+        FDL_CK(cudaStreamSynchronize(st));
+        P.recv_total = hp[nranks] - hp[0];
+        for (int p = 0; p < nranks; p++) P.recv_cnt[p] = hp[p + 1] - hp[p];
+        P.recv_idx.alloc((size_t)std::max(P.recv_total, 1) * 4, st);
+        if (P.recv_total)
+            FDL_CK(cudaMemcpyAsync(P.recv_idx.p, glist.as<int>() + hp[0], (size_t)P.recv_total * 4,
+                                   cudaMemcpyDeviceToDevice, st));
+        // send lists, peer-major
+        std::vector<DBuf> parts;
+        std::vector<int> pc(nranks, 0);
+        DBuf flag((size_t)std::max(own, 1) * 4, st);
+        for (int p = 0; p < nranks; p++) {
+            if (p == rank || own == 0) continue;
+            parts.emplace_back((size_t)own * 4, st);
+            DBuf &part = parts.back();
+            k_mask_bit<<<grid_for(own), 256, 0, st>>>(mask.as<unsigned long long>(), own, p, flag.as<int>());
+            FDL_LAUNCH_CK();
+            compact_flagged(nullptr, flag.as<int>(), own, part.as<int>(), gcnt.as<int>() + 1, st);
+            pc[p] = read_i(gcnt.as<int>() + 1, st);
+            if (pc[p]) {
+                k_add_offset<<<grid_for(pc[p]), 256, 0, st>>>(part.as<int>(), pc[p], P.r0);
+                FDL_LAUNCH_CK();
+            }
+        }
+        P.send_total = 0;
+        for (int p = 0; p < nranks; p++) { P.send_cnt[p] = pc[p]; P.send_total += pc[p]; }
+        P.send_idx.alloc((size_t)std::max(P.send_total, 1) * 4, st);
+        int off = 0, k = 0;
+        for (int p = 0; p < nranks; p++) {
+            if (p == rank || own == 0) continue;
+            if (pc[p])
+                FDL_CK(cudaMemcpyAsync(P.send_idx.as<int>() + off, parts[k].p, (size_t)pc[p] * 4,
+                                       cudaMemcpyDeviceToDevice, st));
+            off += pc[p];
+            k++;
+        }
+    }
+    FDL_CK(cudaStreamSynchronize(st));
+    P.valid = true;
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->n = n;
+        info->nranks = nranks;
+        info->rank = rank;
+        info->colors = nc;
+        info->row_begin = P.r0;
+        info->row_end = P.r1;
+        for (int p = 0; p <= nranks; p++) info->row_bounds[p] = P.bounds[p];
+        for (int p = 0; p < nranks; p++) {
+            info->send_count[p] = P.send_cnt[p];
+            info->recv_count[p] = P.recv_cnt[p];
+        }
+        info->send_total = P.send_total;
+        info->recv_total = P.recv_total;
+    }
+}
+
+// ---- op kernels
+// y = I^T x on own rows [r0, r1) and on the ghost rows; natural row v goes to
+// y[v] (natural) or y[inv[v]] (GS); partial (S, Q) over the own rows
+__global__ void __launch_bounds__(256) k_dist_prolong(int r0, int r1, const int *__restrict__ ghosts, int ng,
+                                                      const int *__restrict__ q, const int *__restrict__ inv,
+                                                      const double *__restrict__ xc, double *__restrict__ y,
+                                                      double *slot, double *partials, unsigned *counter) {
+    double st[kNumStats] = {0.0, 0.0, 0.0};
+    const int own = r1 - r0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < own + ng; i += gridDim.x * blockDim.x) {
+        const int v = i < own ? r0 + i : ghosts[i - own];
+        const double val = __ldg(xc + q[v]);
+        y[inv ? inv[v] : v] = val;
+        if (i < own) {
+            st[0] += val;
+            st[1] = fma(val, val, st[1]);
+        }
+    }
+    grid_reduce(st, partials, counter, [&](const double *tot) { finish_stats(tot, slot, 1, 1); });
+}
+
+// y[v] = x[inv[v]] on own rows; partial (S, Q)
+__global__ void __launch_bounds__(256) k_dist_to_nat(int r0, int r1, const int *__restrict__ inv,
+                                                     const double *__restrict__ x, double *__restrict__ y,
+                                                     double *slot, double *partials, unsigned *counter) {
+    double st[kNumStats] = {0.0, 0.0, 0.0};
+    for (int v = r0 + blockIdx.x * blockDim.x + threadIdx.x; v < r1; v += gridDim.x * blockDim.x) {
+        const double val = __ldg(x + inv[v]);
+        y[v] = val;
+        st[0] += val;
+        st[1] = fma(val, val, st[1]);
+    }
+    grid_reduce(st, partials, counter, [&](const double *tot) { finish_stats(tot, slot, 1, 1); });
+}
+
+__global__ void k_dist_finalise(double *slot, int n) {
+    const double tot[kNumStats] = {slot[0], slot[1], 0.0};
+    finish_stats(tot, slot, 1 | 2, n);
+}
+
+__global__ void k_dist_finalise_rq(double *slot, const double *xs) {
+    const double is = 1.0 / xs[3];
+    const double lam = 0.5 * slot[0] / slot[1];
+    const double vn2 = slot[1] * is * is;
+    const double res2 = slot[2] - lam * lam * vn2;
+    slot[0] = lam;
+    slot[1] = sqrt(fmax(res2, 0.0));
+    slot[2] = sqrt(vn2);
+}
+
+// first own row with x - mean != 0: key = 2 i + (negative)
+__global__ void k_dist_first_nonzero(int r0, int r1, const double *__restrict__ x, const double *xs,
+                                     double *out) {
+    const double mu = xs[2];
+    double key = 1152921504606846976.0;   // 2^60
+    for (int base = r0; base < r1; base += 32) {
+        const int i = base + lane_id();
+        const double v = i < r1 ? x[i] - mu : 0.0;
+        const unsigned nz = __ballot_sync(0xffffffffu, v != 0.0);
+        if (nz) {
+            const int src = __ffs(nz) - 1;
+            const double f = __shfl_sync(0xffffffffu, v, src);
+            key = 2.0 * (double)(base + src) + (f < 0.0 ? 1.0 : 0.0);
+            break;
+        }
+    }
+    if (lane_id() == 0) out[0] = key;
+}
+
+__global__ void k_dist_sign(double *slot) {
+    const double key = slot[0];
+    slot[2] = (key < 1152921504606846976.0 && fmod(key, 2.0) == 1.0) ? -1.0 : 1.0;
+}
+
+__global__ void k_dist_pack(const int *__restrict__ idx, int cnt, const int *__restrict__ inv,
+                            const double *__restrict__ x, double *__restrict__ buf) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const int v = idx[i];
+        buf[i] = x[inv ? inv[v] : v];
+    }
+}
+
+__global__ void k_dist_unpack(const int *__restrict__ idx, int cnt, const int *__restrict__ inv,
+                              const double *__restrict__ buf, double *__restrict__ y) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const int v = idx[i];
+        y[inv ? inv[v] : v] = buf[i];
+    }
+}
+
+void dist_op(Handle &h, int level, int op, int64_t arg, const double *x, double *y, double *stat,
+             const double *stat_in, const double *sign_slot, cudaStream_t st) {
+    const Level &L = h.levels[level];
+    const DistPlan &P = L.dist;
+    FDL_REQUIRE(P.valid, FIEDLER_ERR_ARG, "fiedler_dist_op: no plan on this level (call fiedler_dist_plan)");
+    ensure_solve_buffers(h, 8);
+    Enq e{h, st};
+    double *partials = h.partials.as<double>();
+    unsigned *counter = h.counter.as<unsigned>();
+    const int own = P.r1 - P.r0;
+    switch (op) {
+    case FIEDLER_DOP_RAND:
+        FDL_REQUIRE(P.nranks == 1, FIEDLER_ERR_ARG, "FIEDLER_DOP_RAND needs a replicated (1-rank) plan");
+        k_rand<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(L.n, (uint64_t)arg, y, stat, partials, counter);
+        FDL_LAUNCH_CK();
+        break;
+    case FIEDLER_DOP_PROLONG: {
+        FDL_REQUIRE(level + 1 < (int)h.levels.size(), FIEDLER_ERR_ARG, "no coarser level");
+        k_dist_prolong<<<grid_for(own + P.recv_total, 256, h.row_grid), 256, 0, st>>>(
+            P.r0, P.r1, P.recv_idx.as<int>(), P.recv_total, L.q_nat.as<int>(), arg ? L.inv.as<int>() : nullptr,
+            x, y, stat, partials, counter);
+        FDL_LAUNCH_CK();
+        break;
+    }
+    case FIEDLER_DOP_GS_COLOUR: {
+        FDL_REQUIRE(arg >= 0 && arg < L.ncolors, FIEDLER_ERR_ARG, "bad colour");
+        PassArgs a{};
+        a.x = x;
+        a.n = L.n;
+        a.stat_mode = 0;
+        e.pass_tiles<OP_GS>(L, P.tilesGS.as<Tile>() + P.ctile[arg], P.ctile[arg + 1] - P.ctile[arg], a);
+        break;
+    }
+    case FIEDLER_DOP_TO_NAT:
+        k_dist_to_nat<<<grid_for(std::max(own, 1), 256, h.row_grid), 256, 0, st>>>(
+            P.r0, P.r1, L.inv.as<int>(), x, y, stat, partials, counter);
+        FDL_LAUNCH_CK();
+        break;
+    case FIEDLER_DOP_POWER: {
+        PassArgs a{};
+        a.x = x;
+        a.y = y;
+        a.in_stat = stat_in;
+        a.out_stat = stat;
+        a.stat_mode = 4 | 1;   // assign the partial sums, the caller reduces and finalises
+        a.n = L.n;
+        a.shift = L.shift;
+        if (P.ntN) e.pass_tiles<OP_PI>(L, P.tilesN.as<Tile>(), P.ntN, a);
+        else FDL_CK(cudaMemsetAsync(stat, 0, 16, st));
+        break;
+    }
+    case FIEDLER_DOP_FINALISE:
+        k_dist_finalise<<<1, 1, 0, st>>>(stat, L.n);
+        FDL_LAUNCH_CK();
+        break;
+    case FIEDLER_DOP_FIRST_NONZERO:
+        k_dist_first_nonzero<<<1, 32, 0, st>>>(P.r0, P.r1, x, stat_in, stat);
+        FDL_LAUNCH_CK();
+        break;
+    case FIEDLER_DOP_SIGN:
+        k_dist_sign<<<1, 1, 0, st>>>(stat);
+        FDL_LAUNCH_CK();
+        break;
+    case FIEDLER_DOP_RAYLEIGH: {
+        PassArgs a{};
+        a.x = x;
+        a.in_stat = stat_in;
+        a.n = L.n;
+        a.vnat = y;
+        a.sign = sign_slot + 2;
+        a.result = stat;
+        a.rq_raw = 1;
+        if (P.ntN) e.pass_tiles<OP_RQ>(L, P.tilesN.as<Tile>(), P.ntN, a);
+        else FDL_CK(cudaMemsetAsync(stat, 0, 24, st));
+        break;
+    }
+    case FIEDLER_DOP_FINALISE_RQ:
+        k_dist_finalise_rq<<<1, 1, 0, st>>>(stat, stat_in);
+        FDL_LAUNCH_CK();
+        break;
+    case FIEDLER_DOP_HALO_PACK:
+        if (P.send_total) {
+            k_dist_pack<<<grid_for(P.send_total), 256, 0, st>>>(P.send_idx.as<int>(), P.send_total,
+                                                                 arg ? L.inv.as<int>() : nullptr, x, y);
+            FDL_LAUNCH_CK();
+        }
+        break;
+    case FIEDLER_DOP_HALO_UNPACK:
+        if (P.recv_total) {
+            k_dist_unpack<<<grid_for(P.recv_total), 256, 0, st>>>(P.recv_idx.as<int>(), P.recv_total,
+                                                                   arg ? L.inv.as<int>() : nullptr, x, y);
+            FDL_LAUNCH_CK();
+        }
+        break;
+    default:
+        throw Error(FIEDLER_ERR_ARG, "fiedler_dist_op: unknown op");
     }
 }
 

@@ -1,0 +1,117 @@
+"""GPU tests of the partitioned solve (fiedler_dist_plan / fiedler_dist_op +
+paper_1602_04386_b200/dist.py).  Several ranks run as threads of one process
+on one GPU (ThreadComm): their kernels never wait on one another -- every
+exchange is a host rendezvous after a device synchronisation."""
+import numpy as np
+import pytest
+
+import graphgen as gg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1602_04386_b200 as fd
+    from paper_1602_04386_b200 import build
+    build.build()
+    return fd
+
+
+GRAPHS = {
+    "grid64x45": lambda: gg.grid2d(64, "uniform", seed=3, mx=45),
+    "rmat12": lambda: gg.rmat(12, 16.0, seed=5),
+    "hub": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
+    "grid3d_14": lambda: gg.grid3d(14, "lognormal", seed=2),
+}
+
+
+def _handle(fd, g):
+    import torch
+    args = [torch.from_numpy(a).cuda() for a in (g.rp, g.ci, g.w)]
+    opts = fd.fiedler_default_opts(stream=torch.cuda.current_stream().cuda_stream)
+    return fd.fiedler_create(g.n, g.nnz, *args, opts)
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+def test_plans_match_reference(fd, orc, name):
+    """Row bounds, halo counts and the halo lists themselves (recovered through
+    HALO_PACK / HALO_UNPACK of index vectors) equal the reference plan."""
+    import torch
+    from dist_ref import ref_plan
+    g = GRAPHS[name]()
+    h = _handle(fd, g)
+    try:
+        levels = orc.build_hierarchy(orc.Graph.from_csr(g.n, g.rp, g.ci, g.w), orc.Config())
+        for lev in (0, 1):
+            L = levels[lev]
+            for world in (2, 3):
+                for rank in range(world):
+                    info = fd.fiedler_dist_plan(h, lev, world, rank)
+                    ref, sidx, ridx = ref_plan(L.g.rp, L.g.ci, L.ncolors, world, rank)
+                    assert [info.row_bounds[k] for k in range(world + 1)] == ref.bounds
+                    assert [info.send_count[k] for k in range(world)] == ref.send_count
+                    assert [info.recv_count[k] for k in range(world)] == ref.recv_count
+                    x = torch.arange(L.g.n, dtype=torch.float64, device="cuda")
+                    sb = torch.zeros(max(ref.send_total, 1), dtype=torch.float64, device="cuda")
+                    fd.fiedler_dist_op(h, lev, fd.FIEDLER_DOP_HALO_PACK, 0, x=x, y=sb)
+                    torch.cuda.synchronize()
+                    assert np.array_equal(sb[:ref.send_total].cpu().numpy().astype(np.int64), sidx)
+                    rb = torch.arange(max(ref.recv_total, 1), dtype=torch.float64, device="cuda")
+                    y = torch.full((L.g.n,), -1.0, dtype=torch.float64, device="cuda")
+                    fd.fiedler_dist_op(h, lev, fd.FIEDLER_DOP_HALO_UNPACK, 0, x=rb, y=y)
+                    torch.cuda.synchronize()
+                    got = y.cpu().numpy()
+                    pos = np.flatnonzero(got >= 0)
+                    assert np.array_equal(pos[np.argsort(got[pos])], ridx)
+    finally:
+        fd.fiedler_destroy(h)
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+def test_single_rank_equals_fiedler_solve(fd, orc, name):
+    import torch
+    from paper_1602_04386_b200.dist import LibOps, LocalComm, PartitionedSolver
+    g = GRAPHS[name]()
+    h = _handle(fd, g)
+    try:
+        vec = torch.empty(g.n, dtype=torch.float64, device="cuda")
+        lam_ref = fd.fiedler_solve(h, vec)
+        v, lam, _ = PartitionedSolver(LibOps(h, torch.device("cuda")), LocalComm()).solve()
+        torch.cuda.synchronize()
+        assert abs(lam - lam_ref) / lam_ref <= 1e-12
+        a, b = v.cpu().numpy(), vec.cpu().numpy()
+        assert 1 - abs(a @ b) / (np.linalg.norm(a) * np.linalg.norm(b)) <= 1e-12
+        assert np.allclose(a, b, rtol=0, atol=1e-10)
+    finally:
+        fd.fiedler_destroy(h)
+
+
+@pytest.mark.parametrize("name,world", [("grid64x45", 2), ("rmat12", 3), ("hub", 2), ("grid3d_14", 4)])
+def test_multi_rank_threads_match_oracle(fd, orc, name, world):
+    import torch
+    from dist_ref import ThreadComm, run_threads
+    from paper_1602_04386_b200.dist import LibOps, PartitionedSolver
+    g = GRAPHS[name]()
+    ref = orc.solve(orc.Graph.from_csr(g.n, g.rp, g.ci, g.w), orc.Config())
+
+    def rank_fn(rank, shared):
+        h = _handle(fd, g)
+        try:
+            solver = PartitionedSolver(LibOps(h, torch.device("cuda")),
+                                       ThreadComm(shared, rank, world, sync_cuda=True), min_rows=1)
+            v, lam, res = solver.solve()
+            torch.cuda.synchronize()
+            return v.cpu().numpy(), lam, sum(solver.part)
+        finally:
+            fd.fiedler_destroy(h)
+
+    out = run_threads(world, rank_fn)
+    for v, lam, nparts in out:
+        assert nparts >= 1
+        assert abs(lam - ref.lambda2) / ref.lambda2 <= 1e-10
+        cos = abs(float(v @ ref.vector)) / (np.linalg.norm(v) * np.linalg.norm(ref.vector))
+        assert 1 - cos <= 1e-10
+        assert np.allclose(v, ref.vector, rtol=0, atol=1e-9)
