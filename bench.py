@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--no-partitioned", action="store_true")
+    ap.add_argument("--partition-min-rows", type=int, default=1 << 20)
     return ap.parse_args()
 
 
@@ -169,6 +171,37 @@ def traffic_from_profiles():
     return None
 
 
+def partitioned_solve_timing(fd, g, rp, ci, w, dev, local, args, lam_single):
+    """Time the row-partitioned solve (paper_1602_04386_b200.dist) of the graph on
+    all ranks: device time of `steps` solves, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_1602_04386_b200.dist import LibOps, PartitionedSolver, TorchComm
+    h = fd.fiedler_create(g.n, g.nnz, rp, ci, w, fd.fiedler_default_opts(device=local, validate=0))
+    try:
+        ops = LibOps(h, dev)
+        solver = PartitionedSolver(ops, TorchComm(), min_rows=args.partition_min_rows)
+        _, lam, _ = solver.solve()           # warm-up
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ops.torch_stream)
+        for _ in range(args.steps):
+            _, lam, _ = solver.solve()
+        e1.record(ops.torch_stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return {"solve_ms": float(t.item()), "levels_partitioned": int(sum(solver.part)),
+                "min_rows": args.partition_min_rows,
+                "lambda2": lam, "lambda2_rel_diff_vs_1gpu": abs(lam - lam_single) / lam_single,
+                "note": "setup replicated on every rank; solve of one graph row-partitioned"}
+    finally:
+        fd.fiedler_destroy(h)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -283,6 +316,17 @@ def main():
     h2d = 8 * (n + 1) + 4 * nnz + 8 * nnz
     d2h = 8 * n + 8
 
+    # ---- N > 1: the row-partitioned solve of ONE graph across the ranks
+    # (setup replicated, fine levels partitioned, NCCL
+    # halo exchange / all-reduce / all-gather).  Reported beside the replica
+    # throughput; any failure is reported, not hidden.
+    partitioned = None
+    if dist and not args.no_partitioned:
+        try:
+            partitioned = partitioned_solve_timing(fd, g, rp, ci, w, dev, local, args, lam)
+        except Exception as exc:  # reported in the JSON line
+            partitioned = {"error": "%s: %s" % (type(exc).__name__, exc)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config)
@@ -312,6 +356,8 @@ def main():
             "gpu_launches": launches,
             "clocks": ck,
         }
+        if partitioned is not None:
+            line["partitioned"] = partitioned
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
