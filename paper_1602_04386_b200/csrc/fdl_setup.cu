@@ -168,11 +168,23 @@ constexpr int kMaxRounds = 4096;
 // FIEDLER_TRACE: per-phase device timestamps of the cooperative kernels
 __device__ unsigned long long *g_round_ts = nullptr;
 __device__ __forceinline__ void round_stamp(int i) {
-    if (g_round_ts && blockIdx.x == 0 && threadIdx.x == 0 && i < 2 * kMaxRounds) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && i < 2 * kMaxRounds && g_round_ts) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_round_ts[i] = t;
     }
+}
+
+// predicated atomic decrement (returns the old value, 0 when pred is false):
+// branch-free, so the decrements of a whole chunk are in flight together
+__device__ __forceinline__ int atom_dec_if(int *p, bool pred) {
+    int old = 0;
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q atom.global.add.s32 %0, [%1], -1;\n}\n"
+        : "+r"(old)
+        : "l"(p), "r"((int)pred)
+        : "memory");
+    return old;
 }
 
 struct CtaAppend {
@@ -1074,11 +1086,16 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
 #pragma unroll
                         for (int i = 0; i < 8; i++) u8[i] = k + i < e ? ci[k + i] : -1;
 #pragma unroll
-                        for (int i = 0; i < 8; i++) {
+                        for (int i = 0; i < 8; i++)
                             hi8[i] = u8[i] >= 0 &&
                                      higher_prio(splitmix64(salt ^ (uint64_t)u8[i]), u8[i], pv, v);
-                            r8[i] = 0;
-                            if (u8[i] >= 0) r8[i] = hi8[i] ? color[u8[i]] : atomicSub(&indeg[u8[i]], 1);
+#pragma unroll
+                        for (int i = 0; i < 8; i++) r8[i] = hi8[i] ? color[u8[i]] : 0;
+#pragma unroll
+                        for (int i = 0; i < 8; i++) {
+                            const bool lo = u8[i] >= 0 && !hi8[i];
+                            const int o = atom_dec_if(&indeg[lo ? u8[i] : 0], lo);
+                            if (lo) r8[i] = o;
                         }
 #pragma unroll
                         for (int i = 0; i < 8; i++) {
