@@ -532,10 +532,9 @@ __global__ void k_seg_starts(int n, const unsigned *keys, int *segstart) {
 // from the aggregate members (no global sort of all contributions):
 //   1. members of every aggregate (counting sort by aggregate id; n elements);
 //   2. every member m emits, for each neighbour j in another aggregate B, the
-//      contribution (key = B << 32 | kpos, w_mj), where kpos is the CSR
-//      position of the edge's (lo -> hi) entry, lo = min(m, j): the R3 order
-//      of the fine edges {i < j} is exactly ascending kpos;
-//   3. each coarse row A sorts its contributions by key (registers for <= 16,
+//      contribution (B, lo = min(m, j), hi = max(m, j), w_mj): the R3 order of
+//      the fine edges {i < j} is ascending (lo, hi);
+//   3. each coarse row A sorts its contributions by (B, lo, hi) (registers for <= 16,
 //      a warp in shared memory for <= 256, a global two-key radix sort for the
 //      rare longer rows) and left-folds every run of equal B in kpos order --
 //      the oracle's fold, computed independently and identically on both sides
@@ -574,20 +573,36 @@ __global__ void k_gal_member_count(int n, const int *mem, const int *rp, const i
     }
 }
 
-// position of `target` in the ascending row [b, e) of ci (it exists: symmetry)
-__device__ __forceinline__ int find_in_row(const int *ci, int b, int e, int target) {
-    int lo = b, hi = e - 1;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (ci[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
 
 template <int W>
 __global__ void k_gal_member_emit(int n, const int *mem, const int *rp, const int *ci, const double *w,
                                   const int *q, const int *coff, unsigned long long *keys,
-                                  double *vals) {
+                                  unsigned *keys2, double *vals) {
+    if (W == 1) {
+        // thread per member, 8 entries per step with their loads/gathers in flight
+        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+            const int m = mem[t];
+            const int qm = q[m], b = rp[m], e = rp[m + 1];
+            int o = coff[t];
+            for (int k = b; k < e; k += 8) {
+                int j8[8], q8[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) j8[i] = k + i < e ? ci[k + i] : -1;
+#pragma unroll
+                for (int i = 0; i < 8; i++) q8[i] = j8[i] >= 0 ? q[j8[i]] : qm;
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    if (q8[i] != qm) {
+                        const int lo = min(m, j8[i]), hi = max(m, j8[i]);
+                        keys[o] = ((unsigned long long)(unsigned)q8[i] << 32) | (unsigned)lo;
+                        keys2[o] = (unsigned)hi;
+                        vals[o] = w[k + i];
+                        o++;
+                    }
+            }
+        }
+        return;
+    }
     SUBWARP_LOOP(W, n, t) {
         const unsigned sub_mask = (W == 32) ? 0xffffffffu
                                             : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
@@ -609,8 +624,8 @@ __global__ void k_gal_member_emit(int n, const int *mem, const int *rp, const in
             const unsigned bal = __ballot_sync(0xffffffffu, f) & sub_mask;
             if (f) {
                 const int rank = __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
-                const int kpos = m < j ? k : find_in_row(ci, rp[j], rp[j + 1], m);
-                keys[o + rank] = ((unsigned long long)(unsigned)qj << 32) | (unsigned)kpos;
+                keys[o + rank] = ((unsigned long long)(unsigned)qj << 32) | (unsigned)min(m, j);
+                keys2[o + rank] = (unsigned)max(m, j);
                 vals[o + rank] = w[k];
             }
             o += __popc(bal);
@@ -624,15 +639,18 @@ __global__ void k_gal_member_emit(int n, const int *mem, const int *rp, const in
 // path) and longer (global path).
 template <int CAP>
 __device__ __forceinline__ void gal_row_sort_fold(int s, int sb, const unsigned long long *keys,
-                                                  const double *vals, int *outB, double *outW,
-                                                  int *deg_out) {
+                                                  const unsigned *keys2, const double *vals, int *outB,
+                                                  double *outW, int *deg_out) {
     unsigned long long k[CAP];
+    unsigned k2[CAP];
     double v[CAP];
 #pragma unroll
     for (int i = 0; i < CAP; i++) {
         k[i] = i < s ? keys[sb + i] : ~0ull;
+        k2[i] = i < s ? keys2[sb + i] : ~0u;
         v[i] = i < s ? vals[sb + i] : 0.0;
     }
+    // bitonic sort by (B, lo, hi): (B, lo) in k, hi in k2
 #pragma unroll
     for (int kk = 2; kk <= CAP; kk <<= 1)
 #pragma unroll
@@ -642,8 +660,10 @@ __device__ __forceinline__ void gal_row_sort_fold(int s, int sb, const unsigned 
                 const int l = i ^ jj;
                 if (l > i) {
                     const bool up = (i & kk) == 0;
-                    if ((k[i] > k[l]) == up) {
+                    const bool gt = k[i] > k[l] || (k[i] == k[l] && k2[i] > k2[l]);
+                    if (gt == up) {
                         unsigned long long tk = k[i]; k[i] = k[l]; k[l] = tk;
+                        unsigned t2 = k2[i]; k2[i] = k2[l]; k2[l] = t2;
                         double tv = v[i]; v[i] = v[l]; v[l] = tv;
                     }
                 }
@@ -669,7 +689,8 @@ __device__ __forceinline__ void gal_row_sort_fold(int s, int sb, const unsigned 
 }
 
 __global__ void __launch_bounds__(256) k_gal_rows_small(int c, const int *mrp, const int *coff,
-                                                        const unsigned long long *keys, const double *vals,
+                                                        const unsigned long long *keys, const unsigned *keys2,
+                                                        const double *vals,
                                                         int *outB, double *outW, int *deg, int *f16,
                                                         int *midflag, int *bigflag) {
     for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
@@ -679,19 +700,19 @@ __global__ void __launch_bounds__(256) k_gal_rows_small(int c, const int *mrp, c
         midflag[A] = (s > kGalSmall && s <= kGalMid);
         bigflag[A] = (s > kGalMid);
         if (s > 8) continue;
-        gal_row_sort_fold<8>(s, sb, keys, vals, outB, outW, &deg[A]);
+        gal_row_sort_fold<8>(s, sb, keys, keys2, vals, outB, outW, &deg[A]);
     }
 }
 
 __global__ void __launch_bounds__(256) k_gal_rows_16(const int *list, const int *count, const int *mrp,
                                                      const int *coff, const unsigned long long *keys,
-                                                     const double *vals, int *outB, double *outW,
+                                                     const unsigned *keys2, const double *vals, int *outB, double *outW,
                                                      int *deg) {
     const int cnt = *count;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
         const int A = list[i];
         const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb;
-        gal_row_sort_fold<kGalSmall>(s, sb, keys, vals, outB, outW, &deg[A]);
+        gal_row_sort_fold<kGalSmall>(s, sb, keys, keys2, vals, outB, outW, &deg[A]);
     }
 }
 
@@ -699,14 +720,16 @@ __global__ void __launch_bounds__(256) k_gal_rows_16(const int *list, const int 
 constexpr int kGalMidWarps = 8;
 __global__ void __launch_bounds__(kGalMidWarps * 32) k_gal_rows_mid(const int *list, const int *count,
                                                                     const int *mrp, const int *coff,
-                                                                    const unsigned long long *keys,
+                                                                    const unsigned long long *keys, const unsigned *keys2,
                                                                     const double *vals, int *outB,
                                                                     double *outW, int *deg) {
     __shared__ unsigned long long sk[kGalMidWarps][kGalMid];
+    __shared__ unsigned sk2[kGalMidWarps][kGalMid];
     __shared__ double sv[kGalMidWarps][kGalMid];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int cnt = *count;
     unsigned long long *K = sk[warp];
+    unsigned *K2 = sk2[warp];
     double *V = sv[warp];
     for (int idx = blockIdx.x * kGalMidWarps + warp; idx < cnt; idx += gridDim.x * kGalMidWarps) {
         const int A = list[idx];
@@ -715,6 +738,7 @@ __global__ void __launch_bounds__(kGalMidWarps * 32) k_gal_rows_mid(const int *l
         while (N < s) N <<= 1;
         for (int i = lane; i < N; i += 32) {
             K[i] = i < s ? keys[sb + i] : ~0ull;
+            K2[i] = i < s ? keys2[sb + i] : ~0u;
             V[i] = i < s ? vals[sb + i] : 0.0;
         }
         __syncwarp();
@@ -724,8 +748,10 @@ __global__ void __launch_bounds__(kGalMidWarps * 32) k_gal_rows_mid(const int *l
                     const int l = i ^ jj;
                     if (l > i) {
                         const bool up = (i & kk) == 0;
-                        if ((K[i] > K[l]) == up) {
+                        const bool gt = K[i] > K[l] || (K[i] == K[l] && K2[i] > K2[l]);
+                        if (gt == up) {
                             unsigned long long tk = K[i]; K[i] = K[l]; K[l] = tk;
+                            unsigned t2 = K2[i]; K2[i] = K2[l]; K2[l] = t2;
                             double tv = V[i]; V[i] = V[l]; V[l] = tv;
                         }
                     }
@@ -762,13 +788,12 @@ __global__ void k_big_sizes(int h, const int *list, const int *mrp, const int *c
 
 // one CTA per big row: gather its segment into the concatenated arrays
 __global__ void k_big_gather(int h, const int *list, const int *mrp, const int *coff, const int *boff,
-                             const unsigned long long *keys, unsigned long long *ckey, int *cidx,
-                             unsigned *crank, int *cdst) {
+                             const unsigned *keys2, unsigned *ck2, int *cidx, unsigned *crank, int *cdst) {
     for (int r = blockIdx.x; r < h; r += gridDim.x) {
         const int A = list[r];
         const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb, o = boff[r];
         for (int i = threadIdx.x; i < s; i += blockDim.x) {
-            ckey[o + i] = keys[sb + i];
+            ck2[o + i] = keys2[sb + i];
             cidx[o + i] = o + i;
             crank[o + i] = (unsigned)r;
             cdst[o + i] = sb + i;
@@ -781,15 +806,22 @@ __global__ void k_big_rank_of(int E, const int *idx, const unsigned *crank, unsi
         rank2[p] = crank[idx[p]];
 }
 
+// k1 of the concatenated element idx[p] (original position srcpos[idx[p]])
+__global__ void k_big_key1_of(int E, const int *idx, const int *srcpos, const unsigned long long *keys,
+                              unsigned long long *k1) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < E; p += gridDim.x * blockDim.x)
+        k1[p] = keys[srcpos[idx[p]]];
+}
+
 // sorted element p (original concatenated index idx[p]) lands at the p-th slot of
 // the row segments (segments are concatenated in rank order)
 __global__ void k_big_place(int E, const int *idx, const int *cdst, const int *srcpos,
                             const unsigned long long *keys, const double *vals,
-                            unsigned long long *keys2, double *vals2) {
+                            unsigned long long *keys_out, double *vals_out) {
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < E; p += gridDim.x * blockDim.x) {
         const int from = srcpos[idx[p]];
-        keys2[cdst[p]] = keys[from];
-        vals2[cdst[p]] = vals[from];
+        keys_out[cdst[p]] = keys[from];
+        vals_out[cdst[p]] = vals[from];
     }
 }
 
@@ -835,6 +867,22 @@ __global__ void __launch_bounds__(256) k_big_fold(int h, const int *list, const 
 template <int W>
 __global__ void k_gal_write(int c, const int *mrp, const int *coff, const int *crp, const int *outB,
                             const double *outW, int *cci, double *cw) {
+    if (W == 1) {
+        for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
+            const int sb = coff[mrp[A]], o = crp[A], d = crp[A + 1] - o;
+            for (int i = 0; i < d; i += 8) {   // 8 entries in flight per step
+                int b8[8];
+                double w8[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    if (i + k < d) { b8[k] = outB[sb + i + k]; w8[k] = outW[sb + i + k]; }
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    if (i + k < d) { cci[o + i + k] = b8[k]; cw[o + i + k] = w8[k]; }
+            }
+        }
+        return;
+    }
     SUBWARP_LOOP(W, c, A) {
         if (A < c) {
             const int sb = coff[mrp[A]], o = crp[A], d = crp[A + 1] - o;
@@ -873,11 +921,12 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     scan_exclusive(cnt.as<int>(), coff.as<int>(), n, coff.as<int>() + n, st);
     cnt.release();
     const int E = read_int(coff.as<int>() + n, st);
-    DBuf keys((size_t)std::max(E, 1) * 8, st), vals((size_t)std::max(E, 1) * 8, st);
+    DBuf keys((size_t)std::max(E, 1) * 8, st), keys2((size_t)std::max(E, 1) * 4, st),
+        vals((size_t)std::max(E, 1) * 8, st);
     if (E > 0) {
         DISPATCH_WC(avg, (k_gal_member_emit<W><<<sub_grid(n, W), 256, 0, st>>>(
                              n, mem.as<int>(), g.rp, g.ci, g.w, q, coff.as<int>(),
-                             keys.as<unsigned long long>(), vals.as<double>())));
+                             keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>())));
         FDL_LAUNCH_CK();
     }
     mem.release();
@@ -886,7 +935,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
         deg((size_t)(c + 1) * 4, st), f16((size_t)c * 4, st), midf((size_t)c * 4, st),
         bigf((size_t)c * 4, st), lists((size_t)c * 4 * 3, st), lcnt(16, st);
     k_gal_rows_small<<<grid_for(c, 256, kNumSMs * 8), 256, 0, st>>>(
-        c, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(), vals.as<double>(),
+        c, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>(),
         outB.as<int>(), outW.as<double>(), deg.as<int>(), f16.as<int>(), midf.as<int>(), bigf.as<int>());
     FDL_LAUNCH_CK();
     int *midlist = lists.as<int>(), *biglist = lists.as<int>() + c, *list16 = lists.as<int>() + 2 * c;
@@ -899,13 +948,13 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     if (hc[2] > 0) {
         k_gal_rows_16<<<grid_for(hc[2], 256, kNumSMs * 8), 256, 0, st>>>(
             list16, lcnt.as<int>() + 2, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
-            vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
+            keys2.as<unsigned>(), vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
         FDL_LAUNCH_CK();
     }
     if (hc[0] > 0) {
         k_gal_rows_mid<<<std::min(div_up(hc[0], kGalMidWarps), kNumSMs * 8), kGalMidWarps * 32, 0, st>>>(
             midlist, lcnt.as<int>(), mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
-            vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
+            keys2.as<unsigned>(), vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
         FDL_LAUNCH_CK();
     }
     const int h = hc[1];
@@ -915,32 +964,37 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
         FDL_LAUNCH_CK();
         scan_exclusive(sz.as<int>(), boff.as<int>(), h, boff.as<int>() + h, st);
         const int EB = read_int(boff.as<int>() + h, st);
-        DBuf ckey((size_t)EB * 8, st), cidx((size_t)EB * 4, st), crank((size_t)EB * 4, st),
-            cdst((size_t)EB * 4, st), srcpos((size_t)EB * 4, st);
+        DBuf ckey((size_t)EB * 8, st), ck2((size_t)EB * 4, st), cidx((size_t)EB * 4, st),
+            crank((size_t)EB * 4, st), cdst((size_t)EB * 4, st), srcpos((size_t)EB * 4, st);
         k_big_gather<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
-            h, biglist, mrp.as<int>(), coff.as<int>(), boff.as<int>(), keys.as<unsigned long long>(),
-            ckey.as<unsigned long long>(), cidx.as<int>(), crank.as<unsigned>(), cdst.as<int>());
+            h, biglist, mrp.as<int>(), coff.as<int>(), boff.as<int>(), keys2.as<unsigned>(),
+            ck2.as<unsigned>(), cidx.as<int>(), crank.as<unsigned>(), cdst.as<int>());
         FDL_LAUNCH_CK();
         // srcpos[o] = original position of concatenated element o (= cdst before sorting)
         FDL_CK(cudaMemcpyAsync(srcpos.p, cdst.p, (size_t)EB * 4, cudaMemcpyDeviceToDevice, st));
-        // LSD: (B, kpos) first, then the row rank (stable)
+        // LSD radix passes, least significant key first: hi, then (B, lo), then the row rank
+        radix_sort_u32_i32(ck2.as<unsigned>(), cidx.as<int>(), EB, 32, st);
+        k_big_key1_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), srcpos.as<int>(),
+                                                    keys.as<unsigned long long>(), ckey.as<unsigned long long>());
+        FDL_LAUNCH_CK();
         radix_sort_u64_i32(ckey.as<unsigned long long>(), cidx.as<int>(), EB, 32 + bits_for(c - 1), st);
         DBuf rank2((size_t)EB * 4, st);
         k_big_rank_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), crank.as<unsigned>(),
                                                     rank2.as<unsigned>());
         FDL_LAUNCH_CK();
         radix_sort_u32_i32(rank2.as<unsigned>(), cidx.as<int>(), EB, bits_for(h - 1), st);
-        DBuf keys2((size_t)E * 8, st), vals2((size_t)E * 8, st);
+        DBuf keys_s((size_t)E * 8, st), vals_s((size_t)E * 8, st);
         k_big_place<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), cdst.as<int>(), srcpos.as<int>(),
                                                   keys.as<unsigned long long>(), vals.as<double>(),
-                                                  keys2.as<unsigned long long>(), vals2.as<double>());
+                                                  keys_s.as<unsigned long long>(), vals_s.as<double>());
         FDL_LAUNCH_CK();
         k_big_fold<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
-            h, biglist, mrp.as<int>(), coff.as<int>(), keys2.as<unsigned long long>(), vals2.as<double>(),
+            h, biglist, mrp.as<int>(), coff.as<int>(), keys_s.as<unsigned long long>(), vals_s.as<double>(),
             outB.as<int>(), outW.as<double>(), deg.as<int>());
         FDL_LAUNCH_CK();
     }
     keys.release();
+    keys2.release();
     vals.release();
     // 4. CSR assembly
     scan_exclusive(deg.as<int>(), out.own_rp.as<int>(), c, out.own_rp.as<int>() + c, st);
