@@ -1,0 +1,215 @@
+"""Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py
+times (one fiedler_create + fiedler_solve through the C ABI, device input).
+
+* config 2 (R-MAT 2^20): the oracle solves it in tens of seconds, so the whole
+  result is compared (north-star bars) and the first coarse level bit-exactly.
+* configs 3 and 4 (16.7 M and 67 M vertices): outputs the oracle can compute
+  one by one and properties that characterise the method at any size:
+    - the returned vector: unit norm, orthogonal to 1, sign convention (R10),
+      and its Rayleigh quotient / residual recomputed by the oracle's C code;
+    - level 0 -> 1: the matching IS the greedy heaviest-first matching in the
+      strict (w, hash) order (R2) -- an edge is matched iff no heavier adjacent
+      edge is matched -- checked on every edge; aggregate numbering by leader
+      prefix scan and the join rule on every vertex;
+    - colours: the greedy first-fit colouring in priority order (R4) -- every
+      vertex has the smallest colour not used by a higher-priority neighbour;
+    - the coarse operator on sampled coarse rows: the R3 left fold of the fine
+      weights between the aggregates, bit for bit.
+"""
+import numpy as np
+import pytest
+
+import graphgen as gg
+
+pytestmark = pytest.mark.gpu
+
+M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(x):
+    x = x.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1602_04386_b200 as fd
+    from paper_1602_04386_b200 import build
+    build.build()
+    return fd
+
+
+def run_gpu(fd, g):
+    import torch
+    args = [torch.from_numpy(a).cuda() for a in (g.rp, g.ci, g.w)]
+    vec = torch.empty(g.n, dtype=torch.float64, device="cuda")
+    info = fd.fiedler_info()
+    h = fd.fiedler_create(g.n, g.nnz, *args, fd.fiedler_default_opts(validate=0))
+    lam = fd.fiedler_solve(h, vec, None, info)
+    ex0 = fd.fiedler_level_export(h, 0)
+    ex1 = fd.fiedler_level_export(h, 1)
+    fd.fiedler_destroy(h)
+    v = vec.cpu().numpy()
+    del args
+    torch.cuda.empty_cache()
+    return v, lam, info, ex0, ex1
+
+
+def check_vector(orc, g, v, lam, info):
+    assert np.linalg.norm(v) == pytest.approx(1.0, rel=1e-12)
+    assert abs(v.sum()) <= 1e-9 * np.sqrt(g.n)
+    assert v[np.flatnonzero(v)[0]] > 0
+    G = orc.Graph.from_csr(g.n, g.rp, g.ci, g.w)
+    assert orc.rayleigh(G, v) == pytest.approx(lam, rel=1e-10)
+    r = orc.laplacian_matvec(G, v) - lam * v
+    assert info.residual_norm == pytest.approx(float(np.linalg.norm(r)), rel=1e-6, abs=1e-7 * lam)
+
+
+def _row_chunks(rp, chunk=1 << 23):
+    n = rp.size - 1
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        yield r0, r1, int(rp[r0]), int(rp[r1])
+
+
+def _edge_hash(salt, rows, cols):
+    lo, hi = np.minimum(rows, cols), np.maximum(rows, cols)
+    return splitmix64(salt ^ ((lo.astype(np.uint64) << np.uint64(32)) | hi.astype(np.uint64)))
+
+
+def check_matching(orc, rp, ci, w, q, mate, seed=0):
+    """Greedy heaviest-first matching in the strict (w, hash) order (R2), the join
+    rule and the leader numbering, on every edge / vertex (row chunks)."""
+    n = rp.size - 1
+    salt = np.uint64(orc.salt_match(seed, 0))
+    mate = mate.astype(np.int64)
+    m = mate >= 0
+    assert np.array_equal(mate[mate[m]], np.flatnonzero(m))     # a matching
+    # weight/hash of each vertex's matched edge (-inf for unmatched)
+    mw = np.full(n, -np.inf)
+    mh = np.zeros(n, dtype=np.uint64)
+    heavy = np.full(n, -1, dtype=np.int64)
+
+    def heavier(wa, ha, wb, hb):
+        return (wa > wb) | ((wa == wb) & (ha > hb))
+
+    for r0, r1, e0, e1 in _row_chunks(rp):
+        rows = np.repeat(np.arange(r0, r1, dtype=np.int64), np.diff(rp[r0:r1 + 1]))
+        cols = ci[e0:e1].astype(np.int64)
+        h = _edge_hash(salt, rows, cols)
+        is_m = mate[rows] == cols
+        mw[rows[is_m]] = w[e0:e1][is_m]
+        mh[rows[is_m]] = h[is_m]
+        # heaviest neighbour per row in the (w, hash) order, without sorting
+        starts = rp[r0:r1] - e0
+        nz = np.diff(rp[r0:r1 + 1]) > 0
+        ww = w[e0:e1]
+        wmax = np.full(r1 - r0, -np.inf)
+        wmax[nz] = np.maximum.reduceat(ww, starts[nz])
+        cand = ww == wmax[rows - r0]
+        hc = np.where(cand, h, np.uint64(0))
+        hmax = np.zeros(r1 - r0, dtype=np.uint64)
+        hmax[nz] = np.maximum.reduceat(hc, starts[nz])
+        top = cand & (h == hmax[rows - r0])
+        heavy[rows[top]] = cols[top]
+    for r0, r1, e0, e1 in _row_chunks(rp):
+        rows = np.repeat(np.arange(r0, r1, dtype=np.int64), np.diff(rp[r0:r1 + 1]))
+        cols = ci[e0:e1].astype(np.int64)
+        h = _edge_hash(salt, rows, cols)
+        un = mate[rows] != cols
+        ww = w[e0:e1][un]
+        hh = h[un]
+        blocked = heavier(mw[rows[un]], mh[rows[un]], ww, hh) | heavier(mw[cols[un]], mh[cols[un]], ww, hh)
+        assert blocked.all(), "an unmatched edge has no heavier matched neighbour edge"
+    lone = (~m) & (heavy >= 0)
+    assert np.array_equal(q[lone], q[heavy[lone]])
+    leader = np.where(m, np.minimum(np.arange(n), mate), -1)
+    leader[lone] = leader[heavy[lone]]
+    iso = (~m) & (heavy < 0)
+    leader[iso] = np.flatnonzero(iso)
+    is_leader = leader == np.arange(n)
+    ids = np.cumsum(is_leader) - 1
+    assert np.array_equal(q, ids[leader])
+
+
+def check_coloring(orc, rp, ci, color, seed=0, level=0):
+    """Greedy first-fit colouring in decreasing priority (R4), on every vertex."""
+    n = rp.size - 1
+    salt = np.uint64(orc.salt_color(seed, level))
+    pri = splitmix64(salt ^ np.arange(n, dtype=np.uint64))
+    color = color.astype(np.int64)
+    maxc = int(color.max()) + 1
+    for r0, r1, e0, e1 in _row_chunks(rp):
+        rows = np.repeat(np.arange(r0, r1, dtype=np.int64), np.diff(rp[r0:r1 + 1]))
+        cols = ci[e0:e1].astype(np.int64)
+        assert (color[rows] != color[cols]).all(), "not a proper colouring"
+        higher = (pri[cols] > pri[rows]) | ((pri[cols] == pri[rows]) & (cols > rows))
+        used = np.zeros((r1 - r0, maxc + 1), dtype=bool)
+        used[rows[higher] - r0, color[cols[higher]]] = True
+        # smallest colour not used by a higher-priority neighbour
+        assert np.array_equal(np.argmin(used, axis=1), color[r0:r1])
+
+
+def check_galerkin_sample(rp, ci, w, q, ex1, nsample=4000, seed=0):
+    """Coarse rows = R3 left folds of the fine weights between aggregates."""
+    rng = np.random.default_rng(seed)
+    c = ex1["n"]
+    members = {}
+    sample = rng.choice(c, size=min(nsample, c), replace=False)
+    want = set(sample.tolist())
+    qs = q.astype(np.int64)
+    # members of the sampled aggregates
+    idx = np.flatnonzero(np.isin(qs, sample))
+    for v in idx:
+        members.setdefault(int(qs[v]), []).append(int(v))
+    for A in sample:
+        contrib = {}
+        for m in members[int(A)]:
+            for k in range(rp[m], rp[m + 1]):
+                j = int(ci[k])
+                B = int(qs[j])
+                if B != A:
+                    contrib.setdefault(B, []).append((min(m, j), max(m, j), w[k]))
+        cols = sorted(contrib)
+        vals = []
+        for B in cols:
+            terms = sorted(contrib[B])
+            s = terms[0][2]
+            for t in terms[1:]:
+                s += t[2]
+            vals.append(s)
+        b, e = ex1["rp"][A], ex1["rp"][A + 1]
+        assert list(ex1["ci"][b:e]) == cols
+        assert np.array_equal(ex1["w"][b:e].view(np.uint64), np.array(vals).view(np.uint64))
+
+
+def test_config2_full_parity(fd, orc):
+    g = gg.config(2)
+    v, lam, info, ex0, ex1 = run_gpu(fd, g)
+    ref = orc.solve(orc.Graph.from_csr(g.n, g.rp, g.ci, g.w), orc.Config())
+    assert info.num_levels == len(ref.levels)
+    assert abs(lam - ref.lambda2) / ref.lambda2 <= 1e-10
+    cos = abs(float(v @ ref.vector))
+    assert 1 - cos <= 1e-10
+    L0, L1 = ref.levels[0], ref.levels[1]
+    assert np.array_equal(ex0["agg"], L0.q) and np.array_equal(ex0["mate"], L0.mate)
+    assert np.array_equal(ex0["color"], L0.color)
+    assert np.array_equal(ex1["rp"], L1.g.rp) and np.array_equal(ex1["ci"], L1.g.ci)
+    assert np.array_equal(ex1["w"].view(np.uint64), L1.g.w.view(np.uint64))
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_properties(fd, orc, cfg):
+    g = gg.config(cfg)
+    v, lam, info, ex0, ex1 = run_gpu(fd, g)
+    check_vector(orc, g, v, lam, info)
+    q = ex0["agg"].astype(np.int64)
+    check_matching(orc, g.rp, g.ci, g.w, q, ex0["mate"])
+    check_coloring(orc, g.rp, g.ci, ex0["color"])
+    check_galerkin_sample(g.rp, g.ci, g.w, q, ex1)
