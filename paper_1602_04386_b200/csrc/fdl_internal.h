@@ -79,7 +79,10 @@ struct Level {
     // [ctile[c], ctile[c+1])), then the natural-order tiles [ctile[ncolors], ntiles)
     DBuf tiles;
     std::vector<int> ctile;
+    DBuf ctile_d;            // device copy of ctile
     std::vector<int> seg;    // [ncolors + 1] GS row range of every colour
+    DBuf seg_d;              // device copy of seg
+    int gs_tail_c0 = 0;      // colours [gs_tail_c0, ncolors) run in one single-CTA launch
     DistPlan dist;
     int ncolors = 0;
     int ntiles = 0;

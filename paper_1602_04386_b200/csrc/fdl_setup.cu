@@ -163,7 +163,7 @@ void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32,
 namespace cg = cooperative_groups;
 constexpr int kCoopThreads = 256;
 constexpr int kAppendCap = 2048;
-constexpr int kMaxRounds = 4096;
+constexpr int kMaxRounds = 1 << 16;   // JP depth can reach thousands on dense cores
 
 // FIEDLER_TRACE: per-phase device timestamps of the cooperative kernels
 __device__ unsigned long long *g_round_ts = nullptr;
@@ -1022,13 +1022,17 @@ __device__ __forceinline__ bool higher_prio(uint64_t pu, int u, uint64_t pv, int
     return pu > pv || (pu == pv && u > v);
 }
 
-// one JP step for vertex v (sub-warp of W lanes; v < 0 = idle lanes, which still
-// take part in the warp-wide votes).  Returns 1 if v is not ready yet.
+// First-fit colour of v from its higher-priority neighbours' colours (all final),
+// by a sub-warp of W lanes (v < 0: idle lanes, which still take part in the
+// warp-wide steps).  The used colours go into a shared-memory bitmap of the
+// sub-warp (kBmWords x 32 colours), so hundreds of colours cost one row scan;
+// only when all of them are taken does a windowed rescan look further.
+constexpr int kBmWords = 64;
 template <int W>
-__device__ __forceinline__ int color_item(int v, const int *rp, const int *ci, uint64_t salt,
-                                          volatile int *vcolor, int lane) {
-    int notready = 0;
-    unsigned long long mask = 0ull;
+__device__ __forceinline__ void color_first_fit(int v, const int *rp, const int *ci, uint64_t salt,
+                                                int *color, int lane, unsigned *bm) {
+    for (int i = lane; i < kBmWords; i += W) bm[i] = 0u;
+    __syncwarp();
     uint64_t pv = 0;
     int b = 0, e = 0;
     if (v >= 0) {
@@ -1038,28 +1042,28 @@ __device__ __forceinline__ int color_item(int v, const int *rp, const int *ci, u
         for (int k = b + lane; k < e; k += W) {
             const int u = ci[k];
             if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
-            const int cu = vcolor[u];
-            if (cu < 0) notready = 1;
-            else if (cu < 64) mask |= 1ull << cu;
+            const int cu = color[u];
+            if (cu < 32 * kBmWords) atomicOr(&bm[cu >> 5], 1u << (cu & 31));
         }
     }
-#pragma unroll
-    for (int o = W / 2; o; o >>= 1) {
-        notready |= __shfl_xor_sync(0xffffffffu, notready, o, W);
-        mask |= __shfl_xor_sync(0xffffffffu, mask, o, W);
+    __syncwarp();
+    int col = 0x7fffffff;
+    for (int i = lane; i < kBmWords; i += W) {
+        const unsigned fr = ~bm[i];
+        if (fr) { col = i * 32 + __ffs(fr) - 1; break; }
     }
-    int col = -1;
-    if (v >= 0 && !notready && ~mask) col = __ffsll((long long)~mask) - 1;
-    // rare: all of 0..63 taken -> scan further windows (sub-warp cooperative)
-    int need_big = (v >= 0 && !notready && col < 0) ? 1 : 0;
+#pragma unroll
+    for (int o = W / 2; o; o >>= 1) col = min(col, __shfl_xor_sync(0xffffffffu, col, o, W));
+    // rare: colours 0 .. 32 kBmWords - 1 all taken -> windows of 64 beyond
+    int need_big = (v >= 0 && col == 0x7fffffff) ? 1 : 0;
     int any_big = __any_sync(0xffffffffu, need_big);   // warp-uniform loop below
-    for (int wb = 64; any_big; wb += 64) {
+    for (int wb = 32 * kBmWords; any_big; wb += 64) {
         unsigned long long m2 = 0ull;
         if (need_big)
             for (int k = b + lane; k < e; k += W) {
                 const int u = ci[k];
                 if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
-                const int cu = vcolor[u];
+                const int cu = color[u];
                 if (cu >= wb && cu < wb + 64) m2 |= 1ull << (cu - wb);
             }
 #pragma unroll
@@ -1067,8 +1071,8 @@ __device__ __forceinline__ int color_item(int v, const int *rp, const int *ci, u
         if (need_big && ~m2) { col = wb + __ffsll((long long)~m2) - 1; need_big = 0; }
         any_big = __any_sync(0xffffffffu, need_big);
     }
-    if (v >= 0 && lane == 0 && !notready) vcolor[v] = col;
-    return notready;
+    if (v >= 0 && lane == 0) color[v] = col;
+    __syncwarp();
 }
 
 // Topological (DAG) form of the same greedy colouring: indeg[v] = number of
@@ -1083,6 +1087,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     cg::grid_group grid = cg::this_grid();
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
+    __shared__ unsigned s_bm[W > 1 ? kCoopThreads / W : 1][kBmWords];   // first-fit bitmaps
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     CtaAppend app{s_buf, &s_n, &s_base};
@@ -1181,8 +1186,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
                 }
             } else {
                 // all higher-priority neighbours are coloured: first fit
-                if (color_item<W>(v, rp, ci, salt, color, lane) && lane == 0)
-                    rounds_out[1] = 1;   // impossible: a released vertex had an uncoloured predecessor
+                color_first_fit<W>(v, rp, ci, salt, color, lane, s_bm[threadIdx.x / W]);
                 // release the lower-priority neighbours
                 if (v >= 0) {
                     const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
@@ -1390,6 +1394,18 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
 
     // tiles: GS colours, then the natural-order pass
     L.seg = seg;
+    L.seg_d.alloc((size_t)(ncolors + 1) * 4, st);
+    FDL_CK(cudaMemcpyAsync(L.seg_d.p, L.seg.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
+    // trailing colours small enough for the single-CTA GS kernel (<= kGsTailRows rows
+    // and nonzeros small enough together); a whole small level qualifies
+    {
+        constexpr int kGsTailRows = 16384;
+        int c0 = ncolors;
+        while (c0 > 0 && seg[ncolors] - seg[c0 - 1] <= kGsTailRows &&
+               (long long)segnnz[ncolors] - segnnz[c0 - 1] <= 16LL * kGsTailRows)
+            c0--;
+        L.gs_tail_c0 = c0;
+    }
     L.ctile.assign(ncolors + 1, 0);
     int nt = 0;
     std::vector<int> cnt(ncolors + 1);
@@ -1403,6 +1419,8 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     cnt[ncolors] = tiles_for((long long)g.nnz + n);
     nt += cnt[ncolors];
     L.ntiles = nt;
+    L.ctile_d.alloc((size_t)(ncolors + 1) * 4, st);
+    FDL_CK(cudaMemcpyAsync(L.ctile_d.p, L.ctile.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
     L.tiles.alloc((size_t)nt * sizeof(Tile), st);
     for (int c = 0; c < ncolors; c++)
         if (cnt[c]) {

@@ -31,9 +31,12 @@
 #include <cmath>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "fdl_internal.h"
 
 namespace fdl {
+namespace cg = cooperative_groups;
 
 enum { OP_GS = 0, OP_PI = 1, OP_RQ = 2 };
 #ifndef FDL_PASS_THREADS
@@ -41,6 +44,13 @@ enum { OP_GS = 0, OP_PI = 1, OP_RQ = 2 };
 #endif
 constexpr int kPassThreads = FDL_PASS_THREADS;
 constexpr int kPassWarps = kPassThreads / 32;
+// entries per row gathered together (x 2 rows in flight) and CTAs per SM, per
+// pass kind (tuned with tools/build_variants.py: the GS passes, with no own
+// value and a sparse colour sub-range, prefer a deeper chunk)
+template <int OP, int CH> struct PassTune {
+    static constexpr int chunk = CH ? CH : (OP == 0 ? 8 : 4);
+    static constexpr int min_blocks = (chunk == 4 && OP != 2) ? 4 : 3;
+};
 constexpr int kNumStats = 3;
 constexpr int kCiBuf = kStageCap + 8;   // + start alignment (<= 3) + 16-byte round-up (<= 3)
 constexpr int kWBuf = kStageCap + 4;    // + start alignment (<= 1) + round-up (<= 1)
@@ -241,20 +251,148 @@ __device__ __forceinline__ void finish_stats(const double tot[kNumStats], double
 }
 
 // ----------------------------------------------------------------- the tile pass
-template <int OP>
-__global__ void __launch_bounds__(kPassThreads, (OP == OP_RQ ? FDL_PASS_MINB - 1 : FDL_PASS_MINB)) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
-                                                           CsrView L, PassArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    PassSmem &S = *reinterpret_cast<PassSmem *>(smem_raw);
-    __shared__ RowAcc<OP> s_red[kPassWarps];
+// x gathers: through the read-only path, or L2-coherent (__ldcg) when x is
+// rewritten inside the same launch (the fused GS sweep)
+template <bool COHERENT>
+__device__ __forceinline__ double ldx(const double *p) {
+    return COHERENT ? __ldcg(p) : __ldg(p);
+}
+
+// one thread stages the column/weight streams of tile t into stage b
+__device__ __forceinline__ void issue_tile(PassSmem &S, const CsrView &L, Tile t, int b,
+                                           unsigned long long pol) {
+    const int e0 = L.rp[t.x], e1 = L.rp[t.y];
+    const int cnt = min(e1 - e0, kStageCap);
+    if (cnt > 0) {
+        const int a4 = e0 & ~3, a2 = e0 & ~1;
+        const unsigned bci = round16((unsigned)(e0 + cnt - a4) * 4u);
+        const unsigned bw = round16((unsigned)(e0 + cnt - a2) * 8u);
+        mbar_arrive_expect_tx(&S.bar[b], bci + bw);
+        bulk_g2s(S.st[b].ci, L.ci + a4, bci, &S.bar[b], pol);
+        bulk_g2s(S.st[b].w, L.w + a2, bw, &S.bar[b], pol);
+    } else {
+        mbar_arrive_expect_tx(&S.bar[b], 0u);
+    }
+}
+
+// Reduce the rows of tile t, whose streams land in stage b (mbarrier phase `phase`).
+// Rows <= 32 nonzeros: thread per row from shared memory, two rows per thread with
+// their gathers in flight together; longer rows: a warp each (round robin over the
+// warps) from global memory; a row longer than a tile (necessarily the tile's last)
+// gets the whole CTA.  Ends with a __syncthreads (stage b may then be refilled).
+template <int OP, int CH, bool COHERENT>
+__device__ __forceinline__ void tile_compute(const Tile t, PassSmem &S, int b, unsigned phase,
+                                             RowAcc<OP> *s_red, const CsrView &L, const PassArgs &a,
+                                             const Scal &sc, double st[kNumStats]) {
     const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const double *__restrict__ x = a.x;
-    if (tid == 0) {
+    const int e0 = L.rp[t.x];
+    const int a4 = e0 & ~3, a2 = e0 & ~1;
+    const int *__restrict__ sci = S.st[b].ci - a4;   // index with the global entry number
+    const double *__restrict__ sw = S.st[b].w - a2;
+    int r0 = t.x + tid;
+    int b0 = 0, e0r = 0, b1 = 0, e1r = 0;
+    double own0 = 0.0, own1 = 0.0;
+    auto fetch = [&](int rr0) {
+        const int rr1 = rr0 + kPassThreads;
+        b0 = e0r = b1 = e1r = 0;
+        if (rr0 < t.y) {
+            b0 = L.rp[rr0];
+            e0r = L.rp[rr0 + 1];
+            if (OP != OP_GS) own0 = own_of<OP>(rr0, a);
+        }
+        if (rr1 < t.y) {
+            b1 = L.rp[rr1];
+            e1r = L.rp[rr1 + 1];
+            if (OP != OP_GS) own1 = own_of<OP>(rr1, a);
+        }
+    };
+    fetch(r0);   // the first pair's offsets / own values are in flight during the wait
+    mbar_wait(&S.bar[b], phase);
+    int has_long = 0;
+    for (; r0 < t.y; r0 += 2 * kPassThreads) {
+        if (r0 != t.x + tid) fetch(r0);
+        const int r1 = r0 + kPassThreads;
+        const bool v1 = r1 < t.y;
+        const bool s0 = e0r - b0 <= kShortMax;
+        const bool s1 = v1 && e1r - b1 <= kShortMax;
+        if (!s0 || (v1 && !s1)) has_long = 1;
+        RowAcc<OP> acc0, acc1;
+        acc0.own = own0;
+        acc1.own = own1;
+        const int n0 = s0 ? e0r - b0 : 0, n1 = s1 ? e1r - b1 : 0;
+        const int len = max(n0, n1);
+        // kChunk entries of each row per step, all their gathers in flight together;
+        // each row still accumulates in its sequential entry order
+        constexpr int kChunk = PassTune<OP, CH>::chunk;
+        for (int j = 0; j < len; j += kChunk) {
+            int c0[kChunk], c1[kChunk];
+            double w0[kChunk], w1[kChunk], x0[kChunk], x1[kChunk];
+#pragma unroll
+            for (int i = 0; i < kChunk; i++) {
+                const bool ok0 = j + i < n0, ok1 = j + i < n1;
+                c0[i] = ok0 ? sci[b0 + j + i] : 0;
+                w0[i] = ok0 ? sw[b0 + j + i] : 0.0;
+                c1[i] = ok1 ? sci[b1 + j + i] : 0;
+                w1[i] = ok1 ? sw[b1 + j + i] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < kChunk; i++) {
+                x0[i] = (j + i < n0) ? ldx<COHERENT>(x + c0[i]) : 0.0;
+                x1[i] = (j + i < n1) ? ldx<COHERENT>(x + c1[i]) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < kChunk; i++) {
+                if (j + i < n0) acc0.add(w0[i], x0[i]);
+                if (j + i < n1) acc1.add(w1[i], x1[i]);
+            }
+        }
+        if (s0) row_finish<OP>(r0, acc0, a, sc, st);
+        if (s1) row_finish<OP>(r1, acc1, a, sc, st);
+    }
+    if (__syncthreads_or(has_long)) {
+        const int last = t.y - 1;
+        const bool cta_last = L.rp[t.y] - L.rp[last] > kTileT;
+        for (int row = t.x + warp; row < t.y; row += kPassWarps) {
+            const int kb = L.rp[row], ke = L.rp[row + 1];
+            if (ke - kb <= kShortMax || (cta_last && row == last)) continue;   // warp-uniform
+            RowAcc<OP> acc;
+            if (OP != OP_GS) acc.own = own_of<OP>(row, a);
+            for (int k = kb + lane; k < ke; k += 32)
+                acc.add(__ldcs(L.w + k), ldx<COHERENT>(x + __ldcs(L.ci + k)));
+            acc.warp_sum();
+            if (lane == 0) row_finish<OP>(row, acc, a, sc, st);
+        }
+        if (cta_last) {
+            const int kb = L.rp[last], ke = L.rp[t.y];
+            RowAcc<OP> acc;
+            if (OP != OP_GS) acc.own = own_of<OP>(last, a);
+            for (int k = kb + tid; k < ke; k += kPassThreads)
+                acc.add(__ldcs(L.w + k), ldx<COHERENT>(x + __ldcs(L.ci + k)));
+            acc.warp_sum();
+            if (lane == 0) s_red[warp] = acc;
+            __syncthreads();
+            if (tid == 0) {
+                RowAcc<OP> tot = s_red[0];
+                for (int k = 1; k < kPassWarps; k++) tot.merge(s_red[k]);
+                row_finish<OP>(last, tot, a, sc, st);
+            }
+        }
+    }
+    __syncthreads();   // stage b may be overwritten by the next copy
+}
+
+__device__ __forceinline__ void init_stages(PassSmem &S) {
+    if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < kStages; k++) mbar_init(&S.bar[k], 1);
         fence_mbar_init();
     }
     __syncthreads();
+}
+
+template <int OP>
+__device__ __forceinline__ Scal load_scal(const PassArgs &a) {
     Scal sc{0.0, 1.0, 1.0, 1.0};
     if (OP != OP_GS) {
         sc.mu = a.in_stat[2];
@@ -262,148 +400,36 @@ __global__ void __launch_bounds__(kPassThreads, (OP == OP_RQ ? FDL_PASS_MINB - 1
         sc.inv_sigma = 1.0 / sc.sigma;
         if (OP == OP_RQ) sc.sign = *a.sign;
     }
+    return sc;
+}
+
+template <int OP, int CH = 0>
+__global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
+                                                           CsrView L, PassArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PassSmem &S = *reinterpret_cast<PassSmem *>(smem_raw);
+    __shared__ RowAcc<OP> s_red[kPassWarps];
+    init_stages(S);
+    const Scal sc = load_scal<OP>(a);
     double st[kNumStats] = {0.0, 0.0, 0.0};
     unsigned long long pol = 0;
-    if (tid == 0) pol = evict_first_policy();
-
-    // one thread stages the streams of tile `ti` into stage `b`
-    auto issue = [&](int ti, int b) {
-        const Tile t = tiles[ti];
-        const int e0 = L.rp[t.x], e1 = L.rp[t.y];
-        const int cnt = min(e1 - e0, kStageCap);
-        if (cnt > 0) {
-            const int a4 = e0 & ~3, a2 = e0 & ~1;
-            const unsigned bci = round16((unsigned)(e0 + cnt - a4) * 4u);
-            const unsigned bw = round16((unsigned)(e0 + cnt - a2) * 8u);
-            mbar_arrive_expect_tx(&S.bar[b], bci + bw);
-            bulk_g2s(S.st[b].ci, L.ci + a4, bci, &S.bar[b], pol);
-            bulk_g2s(S.st[b].w, L.w + a2, bw, &S.bar[b], pol);
-        } else {
-            mbar_arrive_expect_tx(&S.bar[b], 0u);
-        }
-    };
-
+    if (threadIdx.x == 0) pol = evict_first_policy();
     // ring of kStages stages: iteration `it` consumes stage it % kStages and first
     // refills the stage consumed in iteration it-1 with the tile kStages-1 ahead
-    if (tid == 0)
+    if (threadIdx.x == 0)
         for (int k = 0; k < kStages - 1; k++) {
             const int tk = blockIdx.x + k * gridDim.x;
-            if (tk < ntiles) issue(tk, k);
+            if (tk < ntiles) issue_tile(S, L, tiles[tk], k, pol);
         }
     int it = 0;
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, it++) {
         const int b = it % kStages;
         const int ahead = ti + (kStages - 1) * (int)gridDim.x;
-        if (tid == 0 && ahead < ntiles) {
+        if (threadIdx.x == 0 && ahead < ntiles) {
             fence_proxy_async();   // generic reads of that stage (previous tile) before async writes
-            issue(ahead, (it + kStages - 1) % kStages);
+            issue_tile(S, L, tiles[ahead], (it + kStages - 1) % kStages, pol);
         }
-        const Tile t = tiles[ti];
-        const int e0 = L.rp[t.x];
-        const int a4 = e0 & ~3, a2 = e0 & ~1;
-        const int *__restrict__ sci = S.st[b].ci - a4;   // index with the global entry number
-        const double *__restrict__ sw = S.st[b].w - a2;
-        // Each thread takes rows in pairs (r, r + kPassThreads): the gathers of both
-        // rows are in flight together.  The first pair's offsets and own values are
-        // requested before waiting for the stage.
-        int r0 = t.x + tid;
-        int b0 = 0, e0r = 0, b1 = 0, e1r = 0;
-        double own0 = 0.0, own1 = 0.0;
-        auto fetch = [&](int rr0) {
-            const int rr1 = rr0 + kPassThreads;
-            b0 = e0r = b1 = e1r = 0;
-            if (rr0 < t.y) {
-                b0 = L.rp[rr0];
-                e0r = L.rp[rr0 + 1];
-                if (OP != OP_GS) own0 = own_of<OP>(rr0, a);
-            }
-            if (rr1 < t.y) {
-                b1 = L.rp[rr1];
-                e1r = L.rp[rr1 + 1];
-                if (OP != OP_GS) own1 = own_of<OP>(rr1, a);
-            }
-        };
-        fetch(r0);
-        mbar_wait(&S.bar[b], (unsigned)(it / kStages) & 1u);
-        int has_long = 0;
-        for (; r0 < t.y; r0 += 2 * kPassThreads) {
-            if (r0 != t.x + tid) fetch(r0);
-            const int r1 = r0 + kPassThreads;
-            const bool v1 = r1 < t.y;
-            const bool s0 = e0r - b0 <= kShortMax;
-            const bool s1 = v1 && e1r - b1 <= kShortMax;
-            if (!s0 || (v1 && !s1)) has_long = 1;
-            RowAcc<OP> acc0, acc1;
-            acc0.own = own0;
-            acc1.own = own1;
-            const int n0 = s0 ? e0r - b0 : 0, n1 = s1 ? e1r - b1 : 0;
-            const int len = max(n0, n1);
-            // 4 entries of each row per step, all 8 gathers in flight together; each
-            // row still accumulates in its sequential entry order
-            for (int j = 0; j < len; j += 4) {
-                int c0[4], c1[4];
-                double w0[4], w1[4], x0[4], x1[4];
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const bool ok0 = j + i < n0, ok1 = j + i < n1;
-                    c0[i] = ok0 ? sci[b0 + j + i] : 0;
-                    w0[i] = ok0 ? sw[b0 + j + i] : 0.0;
-                    c1[i] = ok1 ? sci[b1 + j + i] : 0;
-                    w1[i] = ok1 ? sw[b1 + j + i] : 0.0;
-                }
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    x0[i] = (j + i < n0) ? __ldg(x + c0[i]) : 0.0;
-                    x1[i] = (j + i < n1) ? __ldg(x + c1[i]) : 0.0;
-                }
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    if (j + i < n0) acc0.add(w0[i], x0[i]);
-                    if (j + i < n1) acc1.add(w1[i], x1[i]);
-                }
-            }
-            if (s0) row_finish<OP>(r0, acc0, a, sc, st);
-            if (s1) row_finish<OP>(r1, acc1, a, sc, st);
-        }
-        if (__syncthreads_or(has_long)) {
-            // rows with > 32 nonzeros: one warp each, from global memory; a row longer
-            // than a tile is necessarily the tile's last row and gets the whole CTA
-            const int last = t.y - 1;
-            const int last_len = L.rp[t.y] - L.rp[last];
-            const bool cta_last = last_len > kTileT;
-            for (int base = t.x + warp * 32; base < t.y; base += kPassThreads) {
-                const int rr = base + lane;
-                int len = 0;
-                if (rr < t.y) len = L.rp[rr + 1] - L.rp[rr];
-                unsigned m = __ballot_sync(0xffffffffu, len > kShortMax && !(cta_last && rr == last));
-                while (m) {
-                    const int src = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int row = base + src;
-                    const int kb = L.rp[row], ke = L.rp[row + 1];
-                    RowAcc<OP> acc;
-                    if (OP != OP_GS) acc.own = own_of<OP>(row, a);
-                    for (int k = kb + lane; k < ke; k += 32) acc.add(__ldcs(L.w + k), __ldg(x + __ldcs(L.ci + k)));
-                    acc.warp_sum();
-                    if (lane == 0) row_finish<OP>(row, acc, a, sc, st);
-                }
-            }
-            if (cta_last) {
-                const int kb = L.rp[last], ke = L.rp[t.y];
-                RowAcc<OP> acc;
-                if (OP != OP_GS) acc.own = own_of<OP>(last, a);
-                for (int k = kb + tid; k < ke; k += kPassThreads) acc.add(__ldcs(L.w + k), __ldg(x + __ldcs(L.ci + k)));
-                acc.warp_sum();
-                if (lane == 0) s_red[warp] = acc;
-                __syncthreads();
-                if (tid == 0) {
-                    RowAcc<OP> tot = s_red[0];
-                    for (int k = 1; k < kPassWarps; k++) tot.merge(s_red[k]);
-                    row_finish<OP>(last, tot, a, sc, st);
-                }
-            }
-        }
-        __syncthreads();   // stage b may be overwritten by the copy issued next iteration
+        tile_compute<OP, CH, false>(tiles[ti], S, b, (unsigned)(it / kStages) & 1u, s_red, L, a, sc, st);
     }
     if (OP == OP_GS && !(a.stat_mode & 4)) return;   // uniform: statistics not wanted
     grid_reduce(st, a.partials, a.counter, [&](const double *tot) {
@@ -422,6 +448,151 @@ __global__ void __launch_bounds__(kPassThreads, (OP == OP_RQ ? FDL_PASS_MINB - 1
             finish_stats(tot, a.out_stat, a.stat_mode, a.n);
         }
     });
+}
+
+// ----------------------------------------------------------------- single-CTA kernels
+// Small colours and small levels are launch-bound as grid-wide passes: one CTA
+// walks them with __syncthreads between the dependent steps instead.
+constexpr int kCtaThreads = 1024;
+constexpr int kCtaWarps = kCtaThreads / 32;
+
+// block-wide sum of 2 values (all threads get the totals)
+__device__ __forceinline__ void cta_sum2(double &a, double &b, double (*sm)[2]) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if (lane_id() == 0) { sm[w][0] = a; sm[w][1] = b; }
+    __syncthreads();
+    double ta = 0.0, tb = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); k++) { ta += sm[k][0]; tb += sm[k][1]; }
+    a = ta;
+    b = tb;
+    __syncthreads();
+}
+
+// GS colours [c0, ncolors) of `sweeps` sweeps (GS layout, x in place), one CTA:
+// short rows thread per row, long rows a warp each; a barrier between colours.
+// stat_mode as for the tile pass (statistics of the rows handled here).
+__global__ void __launch_bounds__(kCtaThreads) k_gs_tail(CsrView L, const int *__restrict__ seg, int c0,
+                                                         int ncolors, int sweeps, double *x, double *slot,
+                                                         int stat_mode, int n) {
+    __shared__ double sm[kCtaWarps][2];
+    const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    double S = 0.0, Q = 0.0;
+    for (int s = 0; s < sweeps; s++) {
+        const bool last = s == sweeps - 1;
+        for (int c = c0; c < ncolors; c++) {
+            const int a = seg[c], b = seg[c + 1];
+            int has_long = 0;
+            for (int r = a + tid; r < b; r += kCtaThreads) {
+                const int kb = L.rp[r], ke = L.rp[r + 1];
+                if (ke - kb > kShortMax) { has_long = 1; continue; }
+                double num = 0.0, den = 0.0;
+                for (int k = kb; k < ke; k++) {
+                    const double wk = L.w[k];
+                    num = fma(wk, x[L.ci[k]], num);
+                    den += wk;
+                }
+                const double xn = num / den;
+                x[r] = xn;
+                if (last) { S += xn; Q = fma(xn, xn, Q); }
+            }
+            if (__syncthreads_or(has_long)) {
+                for (int r = a + warp; r < b; r += kCtaWarps) {
+                    const int kb = L.rp[r], ke = L.rp[r + 1];
+                    if (ke - kb <= kShortMax) continue;
+                    double num = 0.0, den = 0.0;
+                    for (int k = kb + lane; k < ke; k += 32) {
+                        const double wk = L.w[k];
+                        num = fma(wk, x[L.ci[k]], num);
+                        den += wk;
+                    }
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) {
+                        num += __shfl_xor_sync(0xffffffffu, num, o);
+                        den += __shfl_xor_sync(0xffffffffu, den, o);
+                    }
+                    const double xn = num / den;
+                    if (lane == 0) {
+                        x[r] = xn;
+                        if (last) { S += xn; Q = fma(xn, xn, Q); }
+                    }
+                }
+            }
+            __syncthreads();   // colour c complete before colour c+1 reads it
+        }
+    }
+    if (!(stat_mode & 4)) return;
+    cta_sum2(S, Q, sm);
+    if (tid == 0) {
+        const double tot[kNumStats] = {S, Q, 0.0};
+        finish_stats(tot, slot, stat_mode, n);
+    }
+}
+
+// `iters` power steps on c I - L of a small level (natural CSR), one CTA:
+// z = (c (y - mu) + sum w (y_j - y_i)) / sigma with (mu, sigma) of the previous
+// vector, ping-pong between y0 and y1 (the result ends in y0 if iters is even);
+// in_slot = (mu, sigma) of y0 on entry, out_slot = statistics of the result.
+__global__ void __launch_bounds__(kCtaThreads) k_pi_small(CsrView L, double shift, int iters, double *y0,
+                                                          double *y1, const double *in_slot, double *out_slot) {
+    __shared__ double sm[kCtaWarps][2];
+    __shared__ double s_mu, s_isig;
+    const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    const int n = L.n;
+    if (tid == 0) { s_mu = in_slot[2]; s_isig = 1.0 / in_slot[3]; }
+    __syncthreads();
+    double *src = y0, *dst = y1;
+    double S = 0.0, Q = 0.0;
+    for (int it = 0; it < iters; it++) {
+        const double mu = s_mu, is = s_isig;
+        S = 0.0;
+        Q = 0.0;
+        int has_long = 0;
+        for (int r = tid; r < n; r += kCtaThreads) {
+            const int kb = L.rp[r], ke = L.rp[r + 1];
+            if (ke - kb > kShortMax) { has_long = 1; continue; }
+            const double own = src[r];
+            double acc = 0.0;
+            for (int k = kb; k < ke; k++) acc = fma(L.w[k], src[L.ci[k]] - own, acc);
+            const double z = (shift * (own - mu) + acc) * is;
+            dst[r] = z;
+            S += z;
+            Q = fma(z, z, Q);
+        }
+        if (__syncthreads_or(has_long)) {
+            for (int r = warp; r < n; r += kCtaWarps) {
+                const int kb = L.rp[r], ke = L.rp[r + 1];
+                if (ke - kb <= kShortMax) continue;
+                const double own = src[r];
+                double acc = 0.0;
+                for (int k = kb + lane; k < ke; k += 32) acc = fma(L.w[k], src[L.ci[k]] - own, acc);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) {
+                    const double z = (shift * (own - mu) + acc) * is;
+                    dst[r] = z;
+                    S += z;
+                    Q = fma(z, z, Q);
+                }
+            }
+        }
+        cta_sum2(S, Q, sm);   // also the barrier before the next step reads dst
+        if (tid == 0) {
+            const double m = S / (double)n;
+            s_mu = m;
+            s_isig = 1.0 / sqrt(fmax(Q - (double)n * m * m, 0.0));
+        }
+        __syncthreads();
+        double *t = src; src = dst; dst = t;
+    }
+    if (tid == 0) {
+        const double tot[kNumStats] = {S, Q, 0.0};
+        finish_stats(tot, out_slot, 1 | 2, n);
+    }
 }
 
 // ----------------------------------------------------------------- small kernels
@@ -503,8 +674,10 @@ __global__ void k_normalise(int n, double *z, const double *slot) {
 // ----------------------------------------------------------------- host-side schedule
 constexpr size_t kPassSmemBytes = sizeof(PassSmem);
 
+constexpr int kSmallPiRows = 4096;   // levels this small run all power steps in one CTA
+
 // CTAs of a pass: resident CTAs per SM x SMs (persistent tile loop), per OP
-static int g_pass_grid[3] = {0, 0, 0};
+static int g_pass_grid[4] = {0, 0, 0, 0};
 static int pass_grid(int op) { return g_pass_grid[op]; }
 
 struct Enq {
@@ -522,7 +695,13 @@ struct Enq {
         a.counter = h.counter.as<unsigned>();
         CsrView v = OP == OP_GS ? CsrView{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()}
                                 : CsrView{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
-        k_tilepass<OP><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
+        // GS: the chunk of 4 suits <= 4.5 neighbours per row, 8 the denser coarse levels
+        if (OP == OP_GS && L.nnz <= 4.5 * L.n) {
+            grid = std::min(nt, g_pass_grid[3]);
+            k_tilepass<OP_GS, 4><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
+        } else {
+            k_tilepass<OP><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
+        }
         FDL_LAUNCH_CK();
         launches++;
     }
@@ -530,17 +709,58 @@ struct Enq {
     void pass(const Level &L, int tb, int te, PassArgs a) {
         pass_tiles<OP>(L, L.tiles.as<Tile>() + tb, te - tb, a);
     }
+    // Colours [0, c0) as grid-wide tile passes, the small trailing colours
+    // [c0, ncolors) (<= kTailRows rows together) in one single-CTA launch per sweep;
+    // a small level (c0 == 0) does all its sweeps in one launch.
     void gs(const Level &L, double *x, int sweeps, double *out_slot) {
-        for (int s = 0; s < sweeps; s++)
-            for (int c = 0; c < L.ncolors; c++) {
+        if (sweeps <= 0) return;
+        const int c0 = L.gs_tail_c0;
+        CsrView v{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()};
+        if (c0 == 0) {
+            k_gs_tail<<<1, kCtaThreads, 0, st>>>(v, L.seg_d.as<int>(), 0, L.ncolors, sweeps, x, out_slot,
+                                                 out_slot ? (4 | 1 | 2) : 0, L.n);
+            FDL_LAUNCH_CK();
+            launches++;
+            return;
+        }
+        for (int s = 0; s < sweeps; s++) {
+            const bool want = (s == sweeps - 1) && out_slot;
+            for (int c = 0; c < c0; c++) {
                 PassArgs a{};
                 a.x = x;
                 a.n = L.n;
-                bool want = (s == sweeps - 1) && out_slot;
                 a.out_stat = out_slot;
-                a.stat_mode = want ? (4 | (c == 0 ? 1 : 0) | (c == L.ncolors - 1 ? 2 : 0)) : 0;
+                a.stat_mode = want ? (4 | (c == 0 ? 1 : 0) | (c0 == L.ncolors && c == c0 - 1 ? 2 : 0)) : 0;
                 pass<OP_GS>(L, L.ctile[c], L.ctile[c + 1], a);
             }
+            if (c0 < L.ncolors) {
+                k_gs_tail<<<1, kCtaThreads, 0, st>>>(v, L.seg_d.as<int>(), c0, L.ncolors, 1, x, out_slot,
+                                                     want ? (4 | 2) : 0, L.n);
+                FDL_LAUNCH_CK();
+                launches++;
+            }
+        }
+    }
+    // `iters` power steps from (cur, cur_slot); returns the buffer / slot of the result
+    void pi_iters(const Level &L, double *&cur, double *&oth, double *&cur_slot, int iters,
+                  double *(*next_slot)(void *), void *ctx) {
+        if (iters <= 0) return;
+        if (L.n <= kSmallPiRows) {
+            double *ns = next_slot(ctx);
+            CsrView v{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
+            k_pi_small<<<1, kCtaThreads, 0, st>>>(v, L.shift, iters, cur, oth, cur_slot, ns);
+            FDL_LAUNCH_CK();
+            launches++;
+            if (iters & 1) std::swap(cur, oth);
+            cur_slot = ns;
+            return;
+        }
+        for (int k = 0; k < iters; k++) {
+            double *ns = next_slot(ctx);
+            pi(L, cur, oth, cur_slot, ns);
+            std::swap(cur, oth);
+            cur_slot = ns;
+        }
     }
     void pi(const Level &L, const double *x, double *y, const double *in_slot, double *out_slot) {
         PassArgs a{};
@@ -615,6 +835,10 @@ int rowpass_grid() {
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_RQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+
+    int b3 = 0;
+    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_tilepass<OP_GS, 4>, kPassThreads, smem));
     int b0 = 0, b1 = 0, b2 = 0;
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_tilepass<OP_GS>, kPassThreads, smem));
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_tilepass<OP_PI>, kPassThreads, smem));
@@ -625,7 +849,8 @@ int rowpass_grid() {
     g_pass_grid[OP_GS] = sms * std::max(1, b0);
     g_pass_grid[OP_PI] = sms * std::max(1, b1);
     g_pass_grid[OP_RQ] = sms * std::max(1, b2);
-    cached = sms * std::max(1, std::max(b0, std::max(b1, b2)));
+    g_pass_grid[3] = sms * std::max(1, b3);
+    cached = sms * std::max(std::max(1, b3), std::max(b0, std::max(b1, b2)));
     return cached;
 }
 
@@ -644,12 +869,12 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
     FDL_LAUNCH_CK();
     e.launches++;
     double *cur = xa, *oth = xb;
-    for (int k = 0; k < cfg.piJ; k++) {
-        double *ns = e.slot(sl++);
-        e.pi(LJ, cur, oth, cur_slot, ns);
-        std::swap(cur, oth);
-        cur_slot = ns;
-    }
+    struct SlotCtx { Enq *e; int *sl; } sctx{&e, &sl};
+    auto next_slot = [](void *p) -> double * {
+        SlotCtx *c = static_cast<SlotCtx *>(p);
+        return c->e->slot((*c->sl)++);
+    };
+    e.pi_iters(LJ, cur, oth, cur_slot, cfg.piJ, next_slot, &sctx);
     // ---- cascadic refinement
     for (int ell = J - 1; ell >= 0; ell--) {
         const Level &L = h.levels[ell];
@@ -668,12 +893,7 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
             std::swap(cur, oth);
             cur_slot = ps;
         }
-        for (int k = 0; k < cfg.pi; k++) {
-            double *ns = e.slot(sl++);
-            e.pi(L, cur, oth, cur_slot, ns);
-            std::swap(cur, oth);
-            cur_slot = ns;
-        }
+        e.pi_iters(L, cur, oth, cur_slot, cfg.pi, next_slot, &sctx);
     }
     // ---- Rayleigh quotient on level 0 (+ vector in natural order)
     const Level &L0 = h.levels[0];
