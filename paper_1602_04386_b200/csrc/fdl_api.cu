@@ -45,6 +45,10 @@ Handle::~Handle() {
     xa.release(); xb.release(); vnat.release(); scal.release();
     partials.release(); counter.release(); result.release();
     if (stream) cudaStreamSynchronize(stream);
+    if (stream2) {
+        cudaStreamSynchronize(stream2);
+        cudaStreamDestroy(stream2);
+    }
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -181,6 +185,7 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
         h->own_stream = true;
     }
     cudaStream_t st = h->stream;
+    FDL_CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
     h->row_grid = rowpass_grid();
     EventTimer timer(st);
 

@@ -97,6 +97,7 @@ struct Handle {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    cudaStream_t stream2 = nullptr;   // setup: colourings overlapped with the coarsening chain
     fiedler_opts opts{};
     std::vector<Level> levels;
     int n0 = 0;

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <queue>
 
 #include <cooperative_groups.h>
@@ -449,7 +450,7 @@ struct RoundTrace {
 
 // cooperative launch with every CTA co-resident (grid = SMs x resident CTAs)
 template <class K>
-static void coop_launch(K kernel, void **args, cudaStream_t st) {
+static void coop_launch(K kernel, void **args, cudaStream_t st, int grid_div = 1) {
     static int grid = 0;   // one cache per kernel instantiation
     if (!grid) {
         int per_sm = 0, dev = 0, sms = kNumSMs;
@@ -464,8 +465,8 @@ static void coop_launch(K kernel, void **args, cudaStream_t st) {
     // the kernels are grid-size agnostic: if the driver finds fewer co-resident
     // CTAs than the occupancy query promised, retry with a smaller grid
     for (;;) {
-        cudaError_t e = cudaLaunchCooperativeKernel((const void *)kernel, dim3(grid), dim3(kCoopThreads),
-                                                    args, 0, st);
+        cudaError_t e = cudaLaunchCooperativeKernel((const void *)kernel, dim3(std::max(1, grid / grid_div)),
+                                                    dim3(kCoopThreads), args, 0, st);
         if (e == cudaErrorCooperativeLaunchTooLarge && grid > kNumSMs) {
             (void)cudaGetLastError();
             grid = grid * 3 / 4;
@@ -1211,31 +1212,55 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
 }
 
-static int color_graph(const NatGraph &g, uint64_t salt, DBuf &color, int &rounds, cudaStream_t st) {
+// The colouring of a level runs on the handle's second stream, overlapped with
+// the matching / Galerkin chain of the coarser levels on the main stream; its
+// colour count is read back only when the level's layout is built.
+#ifndef FDL_COLOUR_GRID_DIV
+#define FDL_COLOUR_GRID_DIV 2
+#endif
+constexpr int kColourGridDiv = FDL_COLOUR_GRID_DIV;
+
+struct ColourJob {
+    DBuf la, lb, indeg, counts, mx;
+};
+
+static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJob &job, cudaStream_t st) {
     int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
     color.alloc((size_t)n * 4, st);
     FDL_CK(cudaMemsetAsync(color.p, 0xff, (size_t)n * 4, st));
-    DBuf la((size_t)n * 4, st), lb((size_t)n * 4, st), indeg((size_t)n * 4, st),
-        counts((size_t)(kMaxRounds + 2) * 4, st);
-    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 2) * 4, st));
+    job.la.alloc((size_t)n * 4, st);
+    job.lb.alloc((size_t)n * 4, st);
+    job.indeg.alloc((size_t)n * 4, st);
+    job.counts.alloc((size_t)(kMaxRounds + 2) * 4, st);
+    FDL_CK(cudaMemsetAsync(job.counts.p, 0, (size_t)(kMaxRounds + 2) * 4, st));
     {
         const int *rp = g.rp, *ci = g.ci;
-        int *pcol = color.as<int>(), *pin = indeg.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(),
-            *pc = counts.as<int>(), *pr = counts.as<int>() + kMaxRounds;
+        int *pcol = color.as<int>(), *pin = job.indeg.as<int>(), *pa = job.la.as<int>(), *pb = job.lb.as<int>(),
+            *pc = job.counts.as<int>(), *pr = job.counts.as<int>() + kMaxRounds;
         void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr};
         RoundTrace tr(st, "colour");
-        DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st));
-        tr.report(counts.as<int>());
+        // half the co-resident grid: the other half stays free for the coarsening
+        // chain running concurrently on the main stream
+        DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridDiv));
+        tr.report(job.counts.as<int>());
     }
-    DBuf mx(4, st);
-    reduce_max_i32(color.as<int>(), n, mx.as<int>(), st);
+    job.mx.alloc(4, st);
+    reduce_max_i32(color.as<int>(), n, job.mx.as<int>(), st);
+    job.la.release();
+    job.lb.release();
+    job.indeg.release();
+}
+
+static int color_finish(ColourJob &job, int &rounds, cudaStream_t st) {
     int h[3];
-    FDL_CK(cudaMemcpyAsync(&h[0], counts.as<int>() + kMaxRounds, 8, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaMemcpyAsync(&h[2], mx.p, 4, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaMemcpyAsync(&h[0], job.counts.as<int>() + kMaxRounds, 8, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaMemcpyAsync(&h[2], job.mx.p, 4, cudaMemcpyDeviceToHost, st));
     FDL_CK(cudaStreamSynchronize(st));
     rounds = h[0];
     FDL_REQUIRE(rounds >= 0 && h[1] == 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
+    job.counts.release();
+    job.mx.release();
     return h[2] + 1;
 }
 
@@ -1458,35 +1483,58 @@ __global__ void k_compose_qg(int n, const int *perm, const int *q_nat, int *qg) 
 }
 
 void build_hierarchy(Handle &h, NatGraph &&g0) {
-    cudaStream_t st = h.stream;
+    cudaStream_t st = h.stream, sb = h.stream2;
     const fiedler_opts &o = h.opts;
     NatGraph cur = std::move(g0);
     h.levels.clear();
-    for (int ell = 0;; ell++) {
-        Level L;
-        bool coarsen = cur.n > o.coarsest_size && ell + 1 < o.max_levels;
-        NatGraph next;
-        if (coarsen) {
-            int c = hec_parallel(cur, salt_match(o.seed, ell), L.q_nat, L.mate_nat, L.match_rounds, st);
-            trace_mark(st, ell == 0 ? "L0 matching" : "Lk matching");
-            // stall guard (R9): stop when HEC no longer shrinks the graph
-            if ((double)c > 0.95 * (double)cur.n || c < 2) {
-                coarsen = false;
-                L.q_nat.release();
-                L.mate_nat.release();
-            } else {
-                next = galerkin(cur, L.q_nat.as<int>(), c, st);
-                trace_mark(st, ell == 0 ? "L0 galerkin" : "Lk galerkin");
+    std::vector<NatGraph> graphs;
+    std::vector<std::unique_ptr<ColourJob>> jobs;
+    cudaEvent_t ev;
+    FDL_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    try {
+        for (int ell = 0;; ell++) {
+            Level L;
+            // colouring of level ell on the second stream, once the level exists
+            FDL_CK(cudaEventRecord(ev, st));
+            FDL_CK(cudaStreamWaitEvent(sb, ev, 0));
+            jobs.emplace_back(new ColourJob());
+            color_launch(cur, salt_color(o.seed, ell), L.color_nat, *jobs.back(), sb);
+            bool coarsen = cur.n > o.coarsest_size && ell + 1 < o.max_levels;
+            NatGraph next;
+            if (coarsen) {
+                int c = hec_parallel(cur, salt_match(o.seed, ell), L.q_nat, L.mate_nat, L.match_rounds, st);
+                trace_mark(st, ell == 0 ? "L0 matching" : "Lk matching");
+                // stall guard (R9): stop when HEC no longer shrinks the graph
+                if ((double)c > 0.95 * (double)cur.n || c < 2) {
+                    coarsen = false;
+                    L.q_nat.release();
+                    L.mate_nat.release();
+                } else {
+                    next = galerkin(cur, L.q_nat.as<int>(), c, st);
+                    trace_mark(st, ell == 0 ? "L0 galerkin" : "Lk galerkin");
+                }
             }
+            h.levels.push_back(std::move(L));
+            graphs.push_back(std::move(cur));
+            if (!coarsen) break;
+            cur = std::move(next);
         }
-        int ncol = color_graph(cur, salt_color(o.seed, ell), L.color_nat, L.color_rounds, st);
-        trace_mark(st, ell == 0 ? "L0 colouring" : "Lk colouring");
-        build_layout(cur, L.color_nat.as<int>(), ncol, L, st);
-        trace_mark(st, ell == 0 ? "L0 layout" : "Lk layout");
-        h.levels.push_back(std::move(L));
-        if (!coarsen) break;
-        cur = std::move(next);
+        // layouts: the colourings must be complete (main stream waits for the second)
+        FDL_CK(cudaEventRecord(ev, sb));
+        FDL_CK(cudaStreamWaitEvent(st, ev, 0));
+        trace_mark(sb, "colourings (second stream)");
+        for (size_t ell = 0; ell < h.levels.size(); ell++) {
+            Level &L = h.levels[ell];
+            const int ncol = color_finish(*jobs[ell], L.color_rounds, sb);
+            build_layout(graphs[ell], L.color_nat.as<int>(), ncol, L, st);
+        }
+        trace_mark(st, "layouts");
+    } catch (...) {
+        cudaStreamSynchronize(sb);
+        cudaEventDestroy(ev);
+        throw;
     }
+    cudaEventDestroy(ev);
     const int J = (int)h.levels.size() - 1;
     for (int ell = 0; ell < J; ell++) {
         Level &L = h.levels[ell];
