@@ -122,20 +122,6 @@ inline int grid_for(int64_t threads, int block = 256, int cap = kNumSMs * 32) {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
-// Warp-aggregated append to a work list: ONE atomic per warp instead of one
-// per element (a single-address atomic per vertex serialises at L2).  Must be
-// called by all 32 lanes of the warp; returns the slot of a lane with
-// pred == true (undefined otherwise).  List order is not deterministic, which
-// is harmless: every consumer of these lists is order-independent.
-__device__ __forceinline__ int warp_append(bool pred, int *count) {
-    const unsigned m = __ballot_sync(0xffffffffu, pred);
-    if (m == 0u) return -1;
-    const int leader = __ffs(m) - 1;
-    int base = 0;
-    if (lane_id() == leader) base = atomicAdd(count, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    return base + __popc(m & ((1u << lane_id()) - 1u));
-}
 
 // ----------------------------------------------------------------- primitives (fdl_prims.cu)
 // Exclusive prefix sum of int32; `total` (device, may be null) receives the sum.
@@ -143,8 +129,6 @@ void scan_exclusive(const int *in, int *out, int64_t n, int *total, cudaStream_t
 // Stable LSD radix sort of (key, value) pairs on bits [0, bits); result in keys/vals.
 void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStream_t st);
 void radix_sort_u64_i32(unsigned long long *keys, int *vals, int64_t n, int bits, cudaStream_t st);
-void radix_sort_u64_f64(unsigned long long *keys, double *vals, int64_t n, int bits,
-                        cudaStream_t st);
 // Stream compaction: out[k] = (in ? in[i] : i) for the k-th i in [0, n) with
 // flags[i] != 0 (order kept); *d_count (device) = number kept.  flags are 0/1.
 void compact_flagged(const int *in, const int *flags, int64_t n, int *out, int *d_count,

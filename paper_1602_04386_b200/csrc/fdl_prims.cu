@@ -1,8 +1,9 @@
 // fdl_prims.cu -- hand-written device primitives: exclusive scan (reduce-then-
 // scan, 4096-element tiles, vectorised int4 traffic) and a stable LSD radix
 // sort (8-bit digits, 8192-element tiles, warp __match_any_sync ranking).
-// Used by the aggregate numbering (prefix scan of leader flags), the Galerkin
-// product (sort of coarse-pair keys) and the multicolour layout.
+// Used by the aggregate numbering (prefix scan of leader flags), work-list and
+// CSR offset scans everywhere, the Galerkin product's long-row path (two-key
+// radix sort) and the multicolour layout (sort by colour).
 #include <climits>
 
 #include "fdl_common.cuh"
@@ -226,10 +227,6 @@ void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStre
 }
 void radix_sort_u64_i32(unsigned long long *keys, int *vals, int64_t n, int bits, cudaStream_t st) {
     radix_sort_impl<unsigned long long, int>(keys, vals, n, bits, st);
-}
-void radix_sort_u64_f64(unsigned long long *keys, double *vals, int64_t n, int bits,
-                        cudaStream_t st) {
-    radix_sort_impl<unsigned long long, double>(keys, vals, n, bits, st);
 }
 
 // =============================================================== compaction

@@ -1,17 +1,18 @@
 // fdl_setup.cu -- Setup Phase of Algorithm 3 on the GPU.
 //
 //   per level l (natural numbering):
-//     heavy edge coarsening, parallel order (R2): locally-dominant handshake
-//       matching in the strict edge order (w, splitmix64 hash) -- equal to the
-//       greedy heaviest-first matching -- then unmatched vertices join the
-//       aggregate of their heaviest neighbour (Algorithm 1 line 13);
+//     heavy edge coarsening, parallel order (R2): the handshake matching in the
+//       strict edge order (w, splitmix64 hash) -- equal to the greedy
+//       heaviest-first matching -- as ONE cooperative launch (grid barriers
+//       between rounds), then unmatched vertices join the aggregate of their
+//       heaviest neighbour (Algorithm 1 line 13);
 //     aggregate numbering: exclusive prefix scan over leader flags;
-//     Galerkin product I L I^T with the R3 summation order:
-//       crossing fine edges -> (coarse pair key, w), stable radix sort,
-//       sequential left fold per pair, symmetric CSR assembly;
-//     Jones-Plassmann colouring = greedy first-fit colouring in decreasing
-//       hash priority (R4);
-//     solve layout: rows sorted by (colour, row class, natural id).
+//     Galerkin product I L I^T per coarse row from the aggregate
+//       members, folded in the R3 order (sort by (B, lo, hi) per row);
+//     greedy first-fit colouring in decreasing hash priority (R4), the DAG form
+//       of Jones-Plassmann, one cooperative launch on a second stream,
+//       overlapped with the coarsening chain;
+//     solve layouts: GS rows sorted by (colour, natural id) + the natural CSR.
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -555,8 +556,6 @@ __global__ void k_member_fill(int n, const int *q, const int *mrp, int *fill, in
         mem[mrp[A] + atomicAdd(&fill[A], 1)] = v;
     }
 }
-
-__global__ void k_set_at(int *p, int idx, int v) { p[idx] = v; }
 
 // contributions of member position t (vertex m = mem[t]): neighbours outside q[m]
 template <int W>
@@ -1296,10 +1295,6 @@ __global__ void k_permute_rows(int n, const int *inv, const int *rp, const int *
             }
         }
     }
-}
-
-__global__ void k_copy_i32(int n, const int *a, int *b) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = a[i];
 }
 
 // max_i d_i with d_i summed in stored (= natural ascending) order, as the oracle
