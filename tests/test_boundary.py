@@ -67,3 +67,47 @@ def test_no_gpu_means_loud_failure():
     with pytest.raises(p.FiedlerError) as e:
         p.fiedler_create(g.n, g.nnz, g.rp, g.ci, g.w)
     assert e.value.code == p.FIEDLER_ERR_CUDA
+
+
+def test_argument_errors_before_any_device_work():
+    """Argument checks of fiedler_create come before the device is touched, so
+    they return their documented codes on a machine without a GPU too."""
+    import numpy as np
+    import paper_1602_04386_b200 as p
+    rp = np.array([0, 1, 2], dtype=np.int64)
+    ci = np.array([1, 0], dtype=np.int32)
+    w = np.ones(2)
+    with pytest.raises(p.FiedlerError) as e:
+        p.fiedler_create(1, 0, np.zeros(2, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    assert e.value.code == p.FIEDLER_ERR_ARG                     # n < 2
+    with pytest.raises(p.FiedlerError) as e:
+        p.fiedler_create(2, -1, rp, ci, w)
+    assert e.value.code == p.FIEDLER_ERR_ARG                     # nnz < 0
+    with pytest.raises(p.FiedlerError) as e:
+        p.fiedler_create(1 << 31, 2, rp, ci, w)
+    assert e.value.code == p.FIEDLER_ERR_TOO_LARGE               # int32 offsets
+    bad = p.fiedler_default_opts(coarsest_size=1)
+    with pytest.raises(p.FiedlerError) as e:
+        p.fiedler_create(2, 2, rp, ci, w, bad)
+    assert e.value.code == p.FIEDLER_ERR_ARG                     # invalid options
+    lib = p._load()
+    import ctypes
+    h = ctypes.c_void_p()
+    assert lib.fiedler_create(2, 2, None, None, None, 0, None, ctypes.byref(h)) == p.FIEDLER_ERR_ARG
+    assert lib.fiedler_create(2, 2, rp.ctypes.data, ci.ctypes.data, w.ctypes.data, 7, None,
+                              ctypes.byref(h)) == p.FIEDLER_ERR_ARG   # bad memory kind
+    assert lib.fiedler_destroy(None) == p.FIEDLER_OK
+    assert lib.fiedler_solve(None, None, None, 0, None, None) == p.FIEDLER_ERR_ARG
+    assert lib.fiedler_dist_plan(None, 0, 1, 0, None) == p.FIEDLER_ERR_ARG
+    assert "handle" in p.fiedler_last_error().lower()
+
+
+def test_header_documents_every_entry_point():
+    """Each FIEDLER_API declaration in include/fiedler.h is preceded by a comment."""
+    hdr = open(os.path.join(ROOT, "include", "fiedler.h")).read()
+    import re
+    for sym in declared_symbols():
+        m = re.search(r"FIEDLER_API[^;(]*\b" + sym + r"\s*\(", hdr)
+        assert m, sym
+        before = hdr[:m.start()].rstrip()
+        assert before.endswith("*/"), sym
