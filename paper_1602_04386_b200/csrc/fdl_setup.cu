@@ -1075,6 +1075,82 @@ __device__ __forceinline__ void color_first_fit(int v, const int *rp, const int 
     __syncwarp();
 }
 
+// Heavy vertices (degree > kHeavyDeg, the hubs of power-law graphs) are handled
+// by the whole CTA instead of a sub-warp: otherwise one sub-warp walking a hub's
+// row would hold every other CTA at the round's grid barrier.
+constexpr int kHeavyDeg = 1024;
+constexpr int kHeavyCap = 512;
+
+__device__ __forceinline__ int cta_sum_int(int v, int *sm) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane_id() == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int t = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); k++) t += sm[k];
+    __syncthreads();
+    return t;
+}
+
+__device__ __forceinline__ int cta_min_int(int v, int *sm) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane_id() == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int t = 0x7fffffff;
+    for (int k = 0; k < (int)(blockDim.x >> 5); k++) t = min(t, sm[k]);
+    __syncthreads();
+    return t;
+}
+
+// number of higher-priority neighbours of v, whole CTA
+__device__ __forceinline__ int cta_indeg(int v, const int *rp, const int *ci, uint64_t salt, int *sm) {
+    const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+    int c = 0;
+    for (int k = rp[v] + threadIdx.x; k < rp[v + 1]; k += blockDim.x) {
+        const int u = ci[k];
+        c += higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v);
+    }
+    return cta_sum_int(c, sm);
+}
+
+// first-fit colour of v (all higher-priority neighbours coloured), whole CTA
+__device__ __forceinline__ void cta_first_fit(int v, const int *rp, const int *ci, uint64_t salt, int *color,
+                                              unsigned *bm, int *sm) {
+    for (int i = threadIdx.x; i < kBmWords; i += blockDim.x) bm[i] = 0u;
+    __syncthreads();
+    const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+    const int b = rp[v], e = rp[v + 1];
+    for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
+        const int u = ci[k];
+        if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+        const int cu = color[u];
+        if (cu < 32 * kBmWords) atomicOr(&bm[cu >> 5], 1u << (cu & 31));
+    }
+    __syncthreads();
+    int col = 0x7fffffff;
+    for (int i = threadIdx.x; i < kBmWords; i += blockDim.x)
+        if (~bm[i]) col = min(col, i * 32 + __ffs(~bm[i]) - 1);
+    col = cta_min_int(col, sm);
+    for (int wb = 32 * kBmWords; col == 0x7fffffff; wb += 32 * kBmWords) {   // rare
+        for (int i = threadIdx.x; i < kBmWords; i += blockDim.x) bm[i] = 0u;
+        __syncthreads();
+        for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
+            const int u = ci[k];
+            if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+            const int cu = color[u] - wb;
+            if (cu >= 0 && cu < 32 * kBmWords) atomicOr(&bm[cu >> 5], 1u << (cu & 31));
+        }
+        __syncthreads();
+        int c2 = 0x7fffffff;
+        for (int i = threadIdx.x; i < kBmWords; i += blockDim.x)
+            if (~bm[i]) c2 = min(c2, wb + i * 32 + __ffs(~bm[i]) - 1);
+        col = cta_min_int(c2, sm);
+    }
+    if (threadIdx.x == 0) color[v] = col;
+    __syncthreads();
+}
+
 // Topological (DAG) form of the same greedy colouring: indeg[v] = number of
 // higher-priority neighbours; a vertex is coloured once all of them are, then
 // it releases its lower-priority neighbours.  Every vertex and edge is handled
@@ -1088,7 +1164,10 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
     __shared__ unsigned s_bm[W > 1 ? kCoopThreads / W : 1][kBmWords];   // first-fit bitmaps
-    if (threadIdx.x == 0) s_n = 0;
+    __shared__ int s_heavy[W > 1 ? kHeavyCap : 1];
+    __shared__ int s_nh;
+    __shared__ int s_red[32];
+    if (threadIdx.x == 0) { s_n = 0; s_nh = 0; }
     __syncthreads();
     CtaAppend app{s_buf, &s_n, &s_base};
     int stamp = 0;
@@ -1099,7 +1178,11 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     for (long long base = (long long)blockIdx.x * per_block; base < n;
          base += (long long)gridDim.x * per_block) {
         const long long idx = base + threadIdx.x / W;
-        const int v = idx < n ? (int)idx : -1;
+        int v = idx < n ? (int)idx : -1;
+        if (W > 1 && v >= 0 && rp[v + 1] - rp[v] > kHeavyDeg) {   // the CTA does it below
+            if (lane == 0) s_heavy[atomicAdd(&s_nh, 1)] = v;
+            v = -1;
+        }
         int c = 0;
         if (v >= 0) {
             const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
@@ -1114,7 +1197,26 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
             if (c == 0) app.push(v);
         }
         __syncthreads();
+        if (W > 1 && s_nh > kHeavyCap - per_block) {
+            for (int i = 0; i < s_nh; i++) {
+                const int hv = s_heavy[i];
+                const int hc = cta_indeg(hv, rp, ci, salt, s_red);
+                if (threadIdx.x == 0) { indeg[hv] = hc; if (hc == 0) app.push(hv); }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s_nh = 0;
+            __syncthreads();
+        }
         if (s_n > kAppendCap - kCoopThreads) app.flush(la, counts);
+    }
+    if (W > 1) {
+        for (int i = 0; i < s_nh; i++) {
+            const int hv = s_heavy[i];
+            const int hc = cta_indeg(hv, rp, ci, salt, s_red);
+            if (threadIdx.x == 0) { indeg[hv] = hc; if (hc == 0) app.push(hv); }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_nh = 0;
     }
     __syncthreads();
     app.flush(la, counts);
@@ -1123,12 +1225,33 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     int *in = la, *out = lb;
     int r = 0;
     int cnt = *(volatile int *)&counts[0];
+    // the deferred heavy vertices of this CTA: colour, then release, whole CTA
+    auto heavy_round = [&](int *hout, int *hcount) {
+        const int nh = s_nh;   // read after a barrier
+        for (int i = 0; i < nh; i++) {
+            const int hv = s_heavy[i];
+            cta_first_fit(hv, rp, ci, salt, color, s_bm[0], s_red);
+            const uint64_t pv = splitmix64(salt ^ (uint64_t)hv);
+            for (int k = rp[hv] + threadIdx.x; k < rp[hv + 1]; k += blockDim.x) {
+                const int u = ci[k];
+                if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, hv)) continue;
+                if (atomicSub(&indeg[u], 1) == 1) app.push_safe(u, hout, hcount);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) s_nh = 0;
+        __syncthreads();
+    };
     while (cnt > 0 && r + 1 < kMaxRounds) {
         int *gcount = counts + r + 1;
         for (long long base = (long long)blockIdx.x * per_block; base < cnt;
              base += (long long)gridDim.x * per_block) {
             const long long idx = base + threadIdx.x / W;
-            const int v = idx < cnt ? in[idx] : -1;
+            int v = idx < cnt ? in[idx] : -1;
+            if (W > 1 && v >= 0 && rp[v + 1] - rp[v] > kHeavyDeg) {   // the CTA does it below
+                if (lane == 0) s_heavy[atomicAdd(&s_nh, 1)] = v;
+                v = -1;
+            }
             if (W == 1) {
                 // one pass over the row, 8 entries at a time with every load and
                 // atomic of the chunk in flight: the colours of the higher-priority
@@ -1198,8 +1321,13 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
                 }
             }
             __syncthreads();
+            if (W > 1 && s_nh > kHeavyCap - per_block) {
+                heavy_round(out, gcount);
+                __syncthreads();
+            }
             if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
         }
+        if (W > 1) heavy_round(out, gcount);
         __syncthreads();
         app.flush(out, gcount);
         grid.sync();
