@@ -1075,10 +1075,13 @@ __device__ __forceinline__ void color_first_fit(int v, const int *rp, const int 
     __syncwarp();
 }
 
-// Heavy vertices (degree > kHeavyDeg, the hubs of power-law graphs) are handled
+// Heavy vertices (degree > kHeavyDeg: hubs, dense coarse levels) are handled
 // by the whole CTA instead of a sub-warp: otherwise one sub-warp walking a hub's
 // row would hold every other CTA at the round's grid barrier.
-constexpr int kHeavyDeg = 1024;
+#ifndef FDL_HEAVY_DEG
+#define FDL_HEAVY_DEG 128
+#endif
+constexpr int kHeavyDeg = FDL_HEAVY_DEG;
 constexpr int kHeavyCap = 512;
 
 __device__ __forceinline__ int cta_sum_int(int v, int *sm) {

@@ -5,8 +5,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1602_04386_b200 import build as b  # noqa: E402
 
-VARIANTS = [dict(FDL_COLOUR_GRID_DIV=1), dict(FDL_COLOUR_GRID_DIV=2), dict(FDL_COLOUR_GRID_DIV=3),
-            dict(FDL_COLOUR_GRID_DIV=4)]
+VARIANTS = [dict(FDL_HEAVY_DEG=64), dict(FDL_HEAVY_DEG=128), dict(FDL_HEAVY_DEG=256), dict(FDL_HEAVY_DEG=1024)]
 out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build_variants")
 os.makedirs(out, exist_ok=True)
 for v in VARIANTS:
