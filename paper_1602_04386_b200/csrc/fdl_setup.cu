@@ -17,6 +17,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <queue>
@@ -542,13 +543,10 @@ __global__ void k_seg_starts(int n, const unsigned *keys, int *segstart) {
 //      the oracle's fold, computed independently and identically on both sides
 //      of the pair, so W_c is symmetric bit for bit;
 //   4. prefix scan of the row lengths and a compacting copy give the CSR.
+// Steps 2-3 have a direct form (no materialised contributions, see
+// k_gal_direct) taken whenever no coarse row exceeds kGalMid slots.
 constexpr int kGalSmall = 16;
 constexpr int kGalMid = 256;
-
-__global__ void k_member_count(int n, const int *q, int *cnt) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        atomicAdd(&cnt[q[v]], 1);
-}
 
 __global__ void k_member_fill(int n, const int *q, const int *mrp, int *fill, int *mem) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
@@ -637,20 +635,12 @@ __global__ void k_gal_member_emit(int n, const int *mem, const int *rp, const in
 // The CAP = 8 pass runs over every row and sorts out the rest: rows with
 // 8 < s <= 16 (a CAP = 16 pass over that list), kGalSmall < s <= kGalMid (warp
 // path) and longer (global path).
+// bitonic sort of CAP register entries by (B, lo, hi) -- (B, lo) in k, hi in
+// k2; empty slots hold k = ~0 and sort last -- then a left fold of every run
+// of equal B in that order; the runs go to outB/outW[0 ..), their count to *deg_out
 template <int CAP>
-__device__ __forceinline__ void gal_row_sort_fold(int s, int sb, const unsigned long long *keys,
-                                                  const unsigned *keys2, const double *vals, int *outB,
-                                                  double *outW, int *deg_out) {
-    unsigned long long k[CAP];
-    unsigned k2[CAP];
-    double v[CAP];
-#pragma unroll
-    for (int i = 0; i < CAP; i++) {
-        k[i] = i < s ? keys[sb + i] : ~0ull;
-        k2[i] = i < s ? keys2[sb + i] : ~0u;
-        v[i] = i < s ? vals[sb + i] : 0.0;
-    }
-    // bitonic sort by (B, lo, hi): (B, lo) in k, hi in k2
+__device__ __forceinline__ void sort_fold_regs(unsigned long long (&k)[CAP], unsigned (&k2)[CAP],
+                                               double (&v)[CAP], int *outB, double *outW, int *deg_out) {
 #pragma unroll
     for (int kk = 2; kk <= CAP; kk <<= 1)
 #pragma unroll
@@ -673,19 +663,39 @@ __device__ __forceinline__ void gal_row_sort_fold(int s, int sb, const unsigned 
     double acc = 0.0;
 #pragma unroll
     for (int i = 0; i < CAP; i++) {
-        if (i < s) {
+        if (k[i] != ~0ull) {
             const unsigned B = (unsigned)(k[i] >> 32);
             if (i == 0) { curB = B; acc = v[i]; }
             else if (B != curB) {
-                outB[sb + runs] = (int)curB; outW[sb + runs] = acc; runs++;
+                outB[runs] = (int)curB; outW[runs] = acc; runs++;
                 curB = B; acc = v[i];
             } else {
                 acc += v[i];
             }
         }
     }
-    if (s > 0) { outB[sb + runs] = (int)curB; outW[sb + runs] = acc; runs++; }
+    if (k[0] != ~0ull) { outB[runs] = (int)curB; outW[runs] = acc; runs++; }
     *deg_out = runs;
+}
+
+// rows with <= CAP contributions: register bitonic sort + sequential fold.
+// The CAP = 8 pass runs over every row and sorts out the rest: rows with
+// 8 < s <= 16 (a CAP = 16 pass over that list), kGalSmall < s <= kGalMid (warp
+// path) and longer (global path).
+template <int CAP>
+__device__ __forceinline__ void gal_row_sort_fold(int s, int sb, const unsigned long long *keys,
+                                                  const unsigned *keys2, const double *vals, int *outB,
+                                                  double *outW, int *deg_out) {
+    unsigned long long k[CAP];
+    unsigned k2[CAP];
+    double v[CAP];
+#pragma unroll
+    for (int i = 0; i < CAP; i++) {
+        k[i] = i < s ? keys[sb + i] : ~0ull;
+        k2[i] = i < s ? keys2[sb + i] : ~0u;
+        v[i] = i < s ? vals[sb + i] : 0.0;
+    }
+    sort_fold_regs<CAP>(k, k2, v, outB + sb, outW + sb, deg_out);
 }
 
 __global__ void __launch_bounds__(256) k_gal_rows_small(int c, const int *mrp, const int *coff,
@@ -865,11 +875,11 @@ __global__ void __launch_bounds__(256) k_big_fold(int h, const int *list, const 
 }
 
 template <int W>
-__global__ void k_gal_write(int c, const int *mrp, const int *coff, const int *crp, const int *outB,
+__global__ void k_gal_write(int c, const int *rowoff, const int *crp, const int *outB,
                             const double *outW, int *cci, double *cw) {
     if (W == 1) {
         for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
-            const int sb = coff[mrp[A]], o = crp[A], d = crp[A + 1] - o;
+            const int sb = rowoff[A], o = crp[A], d = crp[A + 1] - o;
             for (int i = 0; i < d; i += 8) {   // 8 entries in flight per step
                 int b8[8];
                 double w8[8];
@@ -885,13 +895,424 @@ __global__ void k_gal_write(int c, const int *mrp, const int *coff, const int *c
     }
     SUBWARP_LOOP(W, c, A) {
         if (A < c) {
-            const int sb = coff[mrp[A]], o = crp[A], d = crp[A + 1] - o;
+            const int sb = rowoff[A], o = crp[A], d = crp[A + 1] - o;
             for (int i = sw_lane_; i < d; i += W) {
                 cci[o + i] = outB[sb + i];
                 cw[o + i] = outW[sb + i];
             }
         }
     }
+}
+
+// ---- direct path (every row with <= kGalMid slots): the contributions are
+// read straight from the members' CSR rows, never materialised.  The SLOTS of
+// coarse row A are the fine entries (m, j) of its members m in member order,
+// T_A = sum of their degrees; a slot contributes (B = q(j), lo, hi, w_mj) when
+// B != A and is empty (key ~0, sorts last) otherwise.  Sorting all slots by
+// (B, lo, hi) and folding runs of B gives exactly the fold of the general path.
+__global__ void k_member_count_deg(int n, const int *q, const int *rp, unsigned long long *cnt_deg) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        atomicAdd(&cnt_deg[q[v]], (1ull << 32) | (unsigned)(rp[v + 1] - rp[v]));
+}
+
+__global__ void k_split_cnt_deg(int c, const unsigned long long *cnt_deg, int *mcnt, int *slots) {
+    for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
+        const unsigned long long x = cnt_deg[A];
+        mcnt[A] = (int)(x >> 32);
+        slots[A] = (int)(x & 0xffffffffu);
+    }
+}
+
+// class of a coarse row in the direct path: 0 = thread per row in a batch of 32
+// (k_gal_direct_batch), 1 = warp per row with one slot per lane, 2 = warp in
+// shared memory (<= kGalMid slots and members); 3 = too big for the direct path
+constexpr int kGalBatchMembers = 4;
+__device__ __forceinline__ int gal_class(int nm, int T) {
+    if (nm <= kGalBatchMembers && T <= 16) return 0;
+    if (nm <= 32 && T <= 32) return 1;
+    if (nm <= kGalMid && T <= kGalMid) return 2;
+    return 3;
+}
+
+__global__ void k_gal_classify(int c, const int *mrp, const int *toff, int *f32, int *fmid, int *fbig) {
+    for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
+        const int nm = mrp[A + 1] - mrp[A], T = toff[A + 1] - toff[A];
+        const int k = gal_class(nm, T);
+        f32[A] = k == 1;
+        fmid[A] = k == 2;
+        fbig[A] = k == 3;
+    }
+}
+
+// Sub-warp of W lanes per coarse row, lane s holding slot s: member table by
+// lanes, slot gathers coalesced along the member rows, bitonic sort across the
+// lanes by (B, lo, hi), then every head of a B run left-folds the run in order.
+template <int W, bool LIST>
+__global__ void __launch_bounds__(256) k_gal_direct_sw(int c, const int *list, const int *count, const int *mrp,
+                                                       const int *mem, const int *toff, const int *rp,
+                                                       const int *ci, const double *w, const int *q, int *outB,
+                                                       double *outW, int *deg) {
+    const int cnt = LIST ? *count : c;
+    const int lane = threadIdx.x & (W - 1);
+    const int wl = threadIdx.x & 31;
+    const unsigned sub = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << (wl & ~(W - 1)));
+    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x - wl) / W + wl / W; ;
+         base += (int64_t)gridDim.x * blockDim.x / W) {
+        // warp-uniform loop exit: the shuffles below need every lane of the warp
+        if (__all_sync(0xffffffffu, base >= cnt)) break;
+        const bool live = base < cnt;
+        const int A = live ? (LIST ? list[base] : (int)base) : 0;
+        int mb = 0, nm = 0, tb = 0, T = 0;
+        if (live) { mb = mrp[A]; nm = mrp[A + 1] - mb; tb = toff[A]; T = toff[A + 1] - tb; }
+        const bool mine = live && (LIST || gal_class(nm, T) == 0);
+        // member table: lane t holds member t, its row start and slot offset
+        int mv = 0, bv = 0, d = 0;
+        if (mine && lane < nm) { mv = mem[mb + lane]; bv = rp[mv]; d = rp[mv + 1] - bv; }
+        int pin = d;   // inclusive prefix of the member degrees
+#pragma unroll
+        for (int o = 1; o < W; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pin, o, W);
+            if (lane >= o) pin += y;
+        }
+        // member of slot `lane`: the number of members ending at or before it
+        int nmax = mine ? nm : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+        int t = 0;
+        for (int u = 0; u < nmax; u++) {
+            const int e = __shfl_sync(0xffffffffu, pin, u, W);
+            t += (u < nm && e <= lane);
+        }
+        t = min(t, W - 1);
+        const int m = __shfl_sync(0xffffffffu, mv, t, W);
+        const int b = __shfl_sync(0xffffffffu, bv, t, W);
+        const int ps = __shfl_sync(0xffffffffu, pin - d, t, W);
+        unsigned long long key = ~0ull;
+        unsigned k2 = ~0u;
+        double v = 0.0;
+        if (mine && lane < T) {
+            const int k = b + lane - ps;
+            const int j = ci[k];
+            const double x = w[k];
+            const int B = q[j];
+            if (B != A) {
+                key = ((unsigned long long)(unsigned)B << 32) | (unsigned)min(m, j);
+                k2 = (unsigned)max(m, j);
+                v = x;
+            }
+        }
+        // bitonic sort across the W lanes, ascending (B, lo, hi); empty slots last
+#pragma unroll
+        for (int kk = 2; kk <= W; kk <<= 1)
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, jj, W);
+                const unsigned ok2 = __shfl_xor_sync(0xffffffffu, k2, jj, W);
+                const double ov = __shfl_xor_sync(0xffffffffu, v, jj, W);
+                const bool up = (lane & kk) == 0;
+                const bool lower = (lane & jj) == 0;
+                const bool other_less = ok < key || (ok == key && ok2 < k2);
+                // the lower lane of an ascending pair keeps the smaller entry
+                if (other_less == (lower == up)) { key = ok; k2 = ok2; v = ov; }
+            }
+        const unsigned Bm = (unsigned)(key >> 32);
+        const unsigned Bprev = __shfl_up_sync(0xffffffffu, Bm, 1, W);
+        const bool head = key != ~0ull && (lane == 0 || Bprev != Bm);
+        // left fold of the run starting at a head, in order
+        double acc = v;
+        bool run = head;
+#pragma unroll
+        for (int u = 1; u < W; u++) {
+            const double x = __shfl_down_sync(0xffffffffu, v, u, W);
+            const unsigned bx = __shfl_down_sync(0xffffffffu, Bm, u, W);
+            run = run && lane + u < W && bx == Bm;
+            if (run) acc += x;
+        }
+        const unsigned hm = __ballot_sync(0xffffffffu, head) & sub;
+        if (head) {
+            const int r = __popc(hm & ((1u << wl) - 1u));
+            outB[tb + r] = (int)Bm;
+            outW[tb + r] = acc;
+        }
+        if (mine && lane == 0) deg[A] = __popc(hm);
+    }
+}
+
+// Sort-and-fold of one row's <= CAP slots (smem at P: coarse column B, or -1
+// for an edge inside the aggregate; lo = min(m, j); the weight) on ONE 64-bit
+// key per slot, (B << 33 | lo << 4 | slot).  The slot index breaks the ties of
+// (B, lo) in the order of hi, because the slots run through the members in
+// ascending order and every member row in ascending column order: equal lo is
+// either one member m < j with several neighbours j in B (slot order = j order)
+// or one neighbour j < m adjacent to several members (slot order = m order).
+// So the runs of B come out in the R3 order (lo, hi) and are left-folded.
+// Requires B < 2^27, vertex ids < 2^29 and ascending CSR rows (the input
+// contract of fiedler_create; every Galerkin output row ascends in B).
+template <int CAP>
+__device__ __forceinline__ void sort_fold_b64(const int *KB, const int *LO, const double *V, int P, int Tm,
+                                              int *outB, double *outW, int *deg_out) {
+    unsigned long long k[CAP];
+#pragma unroll
+    for (int s = 0; s < CAP; s++) {
+        const int B = s < Tm ? KB[P + s] : -1;
+        k[s] = B < 0 ? ~0ull
+                     : ((unsigned long long)B << 33) | ((unsigned long long)(unsigned)LO[P + s] << 4) |
+                           (unsigned long long)s;
+    }
+#pragma unroll
+    for (int kk = 2; kk <= CAP; kk <<= 1)
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+            for (int i = 0; i < CAP; i++) {
+                const int l = i ^ jj;
+                if (l > i) {
+                    const unsigned long long a = min(k[i], k[l]), b = max(k[i], k[l]);
+                    if ((i & kk) == 0) { k[i] = a; k[l] = b; } else { k[i] = b; k[l] = a; }
+                }
+            }
+    int runs = 0;
+    unsigned curB = 0;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < CAP; i++) {
+        if (k[i] != ~0ull) {
+            const unsigned B = (unsigned)(k[i] >> 33);
+            const double x = V[P + (int)(k[i] & 15u)];
+            if (i == 0) { curB = B; acc = x; }
+            else if (B != curB) {
+                outB[runs] = (int)curB; outW[runs] = acc; runs++;
+                curB = B; acc = x;
+            } else {
+                acc += x;
+            }
+        }
+    }
+    if (k[0] != ~0ull) { outB[runs] = (int)curB; outW[runs] = acc; runs++; }
+    *deg_out = runs;
+}
+
+// Batches of 32 consecutive coarse rows per warp, class 0 only: lane = row
+// reads its row's members and lays its slot descriptors (CSR position, row) out
+// in shared memory; the lanes then gather all slots of the batch together
+// (consecutive slots are consecutive CSR entries); finally every lane sorts and
+// folds its own row in registers (sort_fold_b64).  Without the b64 premises
+// (`b64` false) every row is appended to `redo` for the warp-per-row kernel.
+constexpr int kGalBatchWarps = 4;
+constexpr int kGalBatchSlots = 32 * 16;
+#ifndef FDL_GAL_UNROLL
+#define FDL_GAL_UNROLL 8
+#endif
+constexpr int kGalGatherUnroll = FDL_GAL_UNROLL;
+__global__ void __launch_bounds__(kGalBatchWarps * 32) k_gal_direct_batch(
+    int c, bool b64, const int *mrp, const int *mem, const int *toff, const int *rp, const int *ci,
+    const double *w, const int *q, int *outB, double *outW, int *deg, int *redo, int *redo_count) {
+    __shared__ int skb[kGalBatchWarps][kGalBatchSlots];
+    __shared__ int slo[kGalBatchWarps][kGalBatchSlots];
+    __shared__ double sv[kGalBatchWarps][kGalBatchSlots];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    int *KB = skb[warp];
+    int *LO = slo[warp];
+    double *V = sv[warp];
+    int *VA = reinterpret_cast<int *>(V);   // the slot's row during the gather
+    const int64_t nw = (int64_t)gridDim.x * kGalBatchWarps;
+    for (int64_t base = ((int64_t)blockIdx.x * kGalBatchWarps + warp) * 32; base < c; base += nw * 32) {
+        const int A = (int)(base + lane);
+        const bool live = A < c;
+        int mb = 0, nm = 0, tb = 0, T = 0;
+        if (live) { mb = mrp[A]; nm = mrp[A + 1] - mb; tb = toff[A]; T = toff[A + 1] - tb; }
+        const bool mine = live && gal_class(nm, T) == 0;
+        const int Tm = mine ? T : 0;
+        int P = Tm;   // inclusive, then exclusive prefix of the slot counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, P, o);
+            if (lane >= o) P += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, P, 31);
+        P -= Tm;
+        // members, their row starts and slot offsets
+        int m[kGalBatchMembers], b[kGalBatchMembers], p[kGalBatchMembers + 1];
+#pragma unroll
+        for (int t = 0; t < kGalBatchMembers; t++) m[t] = (mine && t < nm) ? mem[mb + t] : 0x7fffffff;
+        // members in ascending order (sort_fold_b64 relies on it)
+#pragma unroll
+        for (int kk = 2; kk <= kGalBatchMembers; kk <<= 1)
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+                for (int t = 0; t < kGalBatchMembers; t++) {
+                    const int l = t ^ jj;
+                    if (l > t) {
+                        const int lo = min(m[t], m[l]), hi = max(m[t], m[l]);
+                        if ((t & kk) == 0) { m[t] = lo; m[l] = hi; } else { m[t] = hi; m[l] = lo; }
+                    }
+                }
+        p[0] = 0;
+#pragma unroll
+        for (int t = 0; t < kGalBatchMembers; t++) {
+            const bool ok = mine && t < nm;
+            b[t] = ok ? rp[m[t]] : 0;
+            p[t + 1] = p[t] + (ok ? rp[m[t] + 1] - b[t] : 0);
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 16; s2++) {
+            if (s2 < Tm) {
+                int bt = b[0], pt = p[0], mt = m[0];
+#pragma unroll
+                for (int u = 1; u < kGalBatchMembers; u++)
+                    if (s2 >= p[u]) { bt = b[u]; pt = p[u]; mt = m[u]; }
+                KB[P + s2] = bt + s2 - pt;
+                LO[P + s2] = mt;
+                VA[2 * (P + s2)] = A;
+            }
+        }
+        __syncwarp();
+        // gather every slot of the batch, kGalGatherUnroll per lane in flight
+        for (int i0 = 0; i0 < total; i0 += 32 * kGalGatherUnroll) {
+            int kk[kGalGatherUnroll], aa[kGalGatherUnroll], jj[kGalGatherUnroll];
+            double xx[kGalGatherUnroll];
+#pragma unroll
+            for (int u = 0; u < kGalGatherUnroll; u++) {
+                const int i = i0 + u * 32 + lane;
+                const bool ok = i < total;
+                kk[u] = ok ? KB[i] : 0;
+                aa[u] = ok ? VA[2 * i] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < kGalGatherUnroll; u++) {
+                xx[u] = aa[u] >= 0 ? w[kk[u]] : 0.0;
+                jj[u] = aa[u] >= 0 ? ci[kk[u]] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kGalGatherUnroll; u++) kk[u] = aa[u] >= 0 ? q[jj[u]] : 0;
+#pragma unroll
+            for (int u = 0; u < kGalGatherUnroll; u++) {
+                const int i = i0 + u * 32 + lane;
+                if (aa[u] < 0) continue;
+                KB[i] = kk[u] != aa[u] ? kk[u] : -1;
+                LO[i] = min(LO[i], jj[u]);
+                V[i] = xx[u];
+            }
+        }
+        __syncwarp();
+        int d = 0;
+        if (b64) {
+            if (__all_sync(0xffffffffu, Tm <= 8)) {
+                if (mine) sort_fold_b64<8>(KB, LO, V, P, Tm, outB + tb, outW + tb, &d);
+            } else {
+                if (mine) sort_fold_b64<16>(KB, LO, V, P, Tm, outB + tb, outW + tb, &d);
+            }
+        }
+        const bool ok = b64;
+        if (mine) {
+            if (ok) deg[A] = d;
+            else redo[atomicAdd(redo_count, 1)] = A;
+        }
+        __syncwarp();
+    }
+}
+
+// warp per coarse row (<= kGalMid slots and members): member table and slots in
+// shared memory, bitonic sort there, heads of the B runs fold them in order
+constexpr int kGalDirectWarps = 4;
+__global__ void __launch_bounds__(kGalDirectWarps * 32) k_gal_direct_warp(
+    const int *list, const int *count, const int *mrp, const int *mem, const int *toff, const int *rp,
+    const int *ci, const double *w, const int *q, int *outB, double *outW, int *deg) {
+    __shared__ unsigned long long sk[kGalDirectWarps][kGalMid];
+    __shared__ unsigned sk2[kGalDirectWarps][kGalMid];
+    __shared__ double sv[kGalDirectWarps][kGalMid];
+    __shared__ int sm_m[kGalDirectWarps][kGalMid], sm_b[kGalDirectWarps][kGalMid],
+        sm_p[kGalDirectWarps][kGalMid];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const int cnt = *count;
+    unsigned long long *K = sk[warp];
+    unsigned *K2 = sk2[warp];
+    double *V = sv[warp];
+    int *Mm = sm_m[warp], *Mb = sm_b[warp], *Mp = sm_p[warp];
+    for (int idx = blockIdx.x * kGalDirectWarps + warp; idx < cnt; idx += gridDim.x * kGalDirectWarps) {
+        const int A = list[idx];
+        const int mb = mrp[A], nm = mrp[A + 1] - mb, tb = toff[A], T = toff[A + 1] - tb;
+        // member table with the exclusive prefix of the member degrees
+        int carry = 0;
+        for (int t0 = 0; t0 < nm; t0 += 32) {
+            const int t = t0 + lane;
+            int mv = 0, bv = 0, d = 0;
+            if (t < nm) { mv = mem[mb + t]; bv = rp[mv]; d = rp[mv + 1] - bv; }
+            int x = d;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (t < nm) { Mm[t] = mv; Mb[t] = bv; Mp[t] = carry + x - d; }
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        __syncwarp();
+        int N = 32;
+        while (N < T) N <<= 1;
+        for (int s = lane; s < N; s += 32) {
+            unsigned long long kk = ~0ull;
+            unsigned kk2 = ~0u;
+            double vv = 0.0;
+            if (s < T) {
+                int lo = 0, hi = nm - 1;   // last t with Mp[t] <= s
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (Mp[mid] <= s) lo = mid; else hi = mid - 1;
+                }
+                const int mv = Mm[lo], k = Mb[lo] + s - Mp[lo];
+                const int j = ci[k];
+                const int B = q[j];
+                if (B != A) {
+                    kk = ((unsigned long long)(unsigned)B << 32) | (unsigned)min(mv, j);
+                    kk2 = (unsigned)max(mv, j);
+                    vv = w[k];
+                }
+            }
+            K[s] = kk;
+            K2[s] = kk2;
+            V[s] = vv;
+        }
+        __syncwarp();
+        for (int kk = 2; kk <= N; kk <<= 1)
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                for (int i = lane; i < N; i += 32) {
+                    const int l = i ^ jj;
+                    if (l > i) {
+                        const bool up = (i & kk) == 0;
+                        const bool gt = K[i] > K[l] || (K[i] == K[l] && K2[i] > K2[l]);
+                        if (gt == up) {
+                            unsigned long long tk = K[i]; K[i] = K[l]; K[l] = tk;
+                            unsigned t2 = K2[i]; K2[i] = K2[l]; K2[l] = t2;
+                            double tv = V[i]; V[i] = V[l]; V[l] = tv;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        int base = 0;
+        for (int c0 = 0; c0 < N; c0 += 32) {
+            const int i = c0 + lane;
+            const bool head = K[i] != ~0ull && (i == 0 || (K[i] >> 32) != (K[i - 1] >> 32));
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                const int r = base + __popc(hm & ((1u << lane) - 1u));
+                double acc = V[i];
+                for (int u = i + 1; u < N && (K[u] >> 32) == (K[i] >> 32); u++) acc += V[u];
+                outB[tb + r] = (int)(K[i] >> 32);
+                outW[tb + r] = acc;
+            }
+            base += __popc(hm);
+        }
+        if (lane == 0) deg[A] = base;
+        __syncwarp();
+    }
+}
+
+__global__ void k_row_base(int c, const int *mrp, const int *coff, int *rowoff) {
+    for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x)
+        rowoff[A] = coff[mrp[A]];
 }
 
 static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st) {
@@ -902,100 +1323,169 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     out.own_rp.alloc(padded((size_t)(c + 1) * 4), st);
     // 1. members grouped by aggregate (counting sort with atomics; the order
     //    inside an aggregate is irrelevant: step 3 sorts by (B, kpos))
-    DBuf mem((size_t)n * 4, st), mrp((size_t)(c + 1) * 4, st), mfill((size_t)c * 4, st);
-    FDL_CK(cudaMemsetAsync(mrp.p, 0, (size_t)(c + 1) * 4, st));
-    FDL_CK(cudaMemsetAsync(mfill.p, 0, (size_t)c * 4, st));
-    k_member_count<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(n, q, mfill.as<int>());
-    FDL_LAUNCH_CK();
-    scan_exclusive(mfill.as<int>(), mrp.as<int>(), c, mrp.as<int>() + c, st);
+    //    with the slot count T_A = sum of the member degrees of every row
+    DBuf mem((size_t)n * 4, st), mrp((size_t)(c + 1) * 4, st), mfill((size_t)c * 4, st),
+        toff((size_t)(c + 1) * 4, st);
+    {
+        DBuf cd((size_t)c * 8, st), slots((size_t)c * 4, st);
+        FDL_CK(cudaMemsetAsync(cd.p, 0, (size_t)c * 8, st));
+        k_member_count_deg<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(n, q, g.rp,
+                                                                            cd.as<unsigned long long>());
+        FDL_LAUNCH_CK();
+        k_split_cnt_deg<<<grid_for(c), 256, 0, st>>>(c, cd.as<unsigned long long>(), mfill.as<int>(),
+                                                      slots.as<int>());
+        FDL_LAUNCH_CK();
+        scan_exclusive(mfill.as<int>(), mrp.as<int>(), c, mrp.as<int>() + c, st);
+        scan_exclusive(slots.as<int>(), toff.as<int>(), c, toff.as<int>() + c, st);
+    }
     FDL_CK(cudaMemsetAsync(mfill.p, 0, (size_t)c * 4, st));
     k_member_fill<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(n, q, mrp.as<int>(), mfill.as<int>(),
                                                                   mem.as<int>());
     FDL_LAUNCH_CK();
     mfill.release();
-    // 2. contributions in member order
-    DBuf cnt((size_t)n * 4, st), coff((size_t)(n + 1) * 4, st);
-    DISPATCH_WC(avg, (k_gal_member_count<W><<<sub_grid(n, W), 256, 0, st>>>(
-                         n, mem.as<int>(), g.rp, g.ci, q, cnt.as<int>())));
-    FDL_LAUNCH_CK();
-    scan_exclusive(cnt.as<int>(), coff.as<int>(), n, coff.as<int>() + n, st);
-    cnt.release();
-    const int E = read_int(coff.as<int>() + n, st);
-    DBuf keys((size_t)std::max(E, 1) * 8, st), keys2((size_t)std::max(E, 1) * 4, st),
-        vals((size_t)std::max(E, 1) * 8, st);
-    if (E > 0) {
-        DISPATCH_WC(avg, (k_gal_member_emit<W><<<sub_grid(n, W), 256, 0, st>>>(
-                             n, mem.as<int>(), g.rp, g.ci, g.w, q, coff.as<int>(),
-                             keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>())));
+    // rows by size class: the direct path takes the level when no row is too
+    // big for its warp kernel, the general path (steps 2-3) otherwise
+    DBuf deg((size_t)(c + 1) * 4, st), rowoff, outB, outW;
+    int dc[3] = {0, 0, 0};
+    DBuf dl((size_t)c * 4 * 2, st), dcnt(16, st);
+    FDL_CK(cudaMemsetAsync(dcnt.p, 0, 16, st));
+    {
+        DBuf f32((size_t)c * 4, st), fmid((size_t)c * 4, st), fbig((size_t)c * 4, st);
+        k_gal_classify<<<grid_for(c), 256, 0, st>>>(c, mrp.as<int>(), toff.as<int>(), f32.as<int>(),
+                                                    fmid.as<int>(), fbig.as<int>());
+        FDL_LAUNCH_CK();
+        compact_flagged(nullptr, f32.as<int>(), c, dl.as<int>(), dcnt.as<int>(), st);
+        compact_flagged(nullptr, fmid.as<int>(), c, dl.as<int>() + c, dcnt.as<int>() + 1, st);
+        compact_flagged(nullptr, fbig.as<int>(), c, dl.as<int>() + c, dcnt.as<int>() + 2, st);   // count only
+        FDL_CK(cudaMemcpyAsync(dc, dcnt.p, 12, cudaMemcpyDeviceToHost, st));
+        FDL_CK(cudaStreamSynchronize(st));
+    }
+    const bool direct = dc[2] == 0;
+    if (direct) {
+        outB.alloc((size_t)std::max(g.nnz, 1) * 4, st);
+        outW.alloc((size_t)std::max(g.nnz, 1) * 8, st);
+        // rows ascend: input contract.  FIEDLER_TEST_FULL_SORT=1 (tests) forces
+        // the fallback that very large levels take
+        const char *fs = std::getenv("FIEDLER_TEST_FULL_SORT");
+        const bool b64 = c < (1 << 27) && n < (1 << 29) && !(fs && fs[0] == '1');
+        DBuf redo(b64 ? 0 : (size_t)c * 4, st);
+        k_gal_direct_batch<<<std::min(div_up(c, 32 * kGalBatchWarps), kNumSMs * 32), kGalBatchWarps * 32, 0,
+                             st>>>(c, b64, mrp.as<int>(), mem.as<int>(), toff.as<int>(), g.rp, g.ci, g.w, q,
+                                   outB.as<int>(), outW.as<double>(), deg.as<int>(), redo.as<int>(),
+                                   dcnt.as<int>() + 3);
+        FDL_LAUNCH_CK();
+        if (!b64) {
+            // beyond the b64 key ranges: the class-0 rows take the full (B, lo, hi)
+            // sort (the kernel reads the list length on the device)
+            k_gal_direct_sw<32, true><<<kNumSMs * 8, 256, 0, st>>>(
+                c, redo.as<int>(), dcnt.as<int>() + 3, mrp.as<int>(), mem.as<int>(), toff.as<int>(), g.rp,
+                g.ci, g.w, q, outB.as<int>(), outW.as<double>(), deg.as<int>());
+            FDL_LAUNCH_CK();
+        }
+        if (dc[0] > 0) {
+            k_gal_direct_sw<32, true><<<grid_for((int64_t)dc[0] * 32, 256, kNumSMs * 16), 256, 0, st>>>(
+                c, dl.as<int>(), dcnt.as<int>(), mrp.as<int>(), mem.as<int>(), toff.as<int>(), g.rp, g.ci,
+                g.w, q, outB.as<int>(), outW.as<double>(), deg.as<int>());
+            FDL_LAUNCH_CK();
+        }
+        if (dc[1] > 0) {
+            k_gal_direct_warp<<<std::min(div_up(dc[1], kGalDirectWarps), kNumSMs * 16), kGalDirectWarps * 32,
+                                0, st>>>(dl.as<int>() + c, dcnt.as<int>() + 1, mrp.as<int>(), mem.as<int>(),
+                                         toff.as<int>(), g.rp, g.ci, g.w, q, outB.as<int>(), outW.as<double>(),
+                                         deg.as<int>());
+            FDL_LAUNCH_CK();
+        }
+        rowoff = std::move(toff);
+    } else {
+        toff.release();
+        // 2. contributions in member order
+        DBuf cnt((size_t)n * 4, st), coff((size_t)(n + 1) * 4, st);
+        DISPATCH_WC(avg, (k_gal_member_count<W><<<sub_grid(n, W), 256, 0, st>>>(
+                             n, mem.as<int>(), g.rp, g.ci, q, cnt.as<int>())));
+        FDL_LAUNCH_CK();
+        scan_exclusive(cnt.as<int>(), coff.as<int>(), n, coff.as<int>() + n, st);
+        cnt.release();
+        const int E = read_int(coff.as<int>() + n, st);
+        DBuf keys((size_t)std::max(E, 1) * 8, st), keys2((size_t)std::max(E, 1) * 4, st),
+            vals((size_t)std::max(E, 1) * 8, st);
+        if (E > 0) {
+            DISPATCH_WC(avg, (k_gal_member_emit<W><<<sub_grid(n, W), 256, 0, st>>>(
+                                 n, mem.as<int>(), g.rp, g.ci, g.w, q, coff.as<int>(),
+                                 keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>())));
+            FDL_LAUNCH_CK();
+        }
+        mem.release();
+        // 3. per-row sort + fold
+        outB.alloc((size_t)std::max(E, 1) * 4, st);
+        outW.alloc((size_t)std::max(E, 1) * 8, st);
+        DBuf f16((size_t)c * 4, st), midf((size_t)c * 4, st),
+            bigf((size_t)c * 4, st), lists((size_t)c * 4 * 3, st), lcnt(16, st);
+        k_gal_rows_small<<<grid_for(c, 256, kNumSMs * 8), 256, 0, st>>>(
+            c, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>(),
+            outB.as<int>(), outW.as<double>(), deg.as<int>(), f16.as<int>(), midf.as<int>(), bigf.as<int>());
+        FDL_LAUNCH_CK();
+        int *midlist = lists.as<int>(), *biglist = lists.as<int>() + c, *list16 = lists.as<int>() + 2 * c;
+        compact_flagged(nullptr, midf.as<int>(), c, midlist, lcnt.as<int>(), st);
+        compact_flagged(nullptr, bigf.as<int>(), c, biglist, lcnt.as<int>() + 1, st);
+        compact_flagged(nullptr, f16.as<int>(), c, list16, lcnt.as<int>() + 2, st);
+        int hc[3];
+        FDL_CK(cudaMemcpyAsync(hc, lcnt.p, 12, cudaMemcpyDeviceToHost, st));
+        FDL_CK(cudaStreamSynchronize(st));
+        if (hc[2] > 0) {
+            k_gal_rows_16<<<grid_for(hc[2], 256, kNumSMs * 8), 256, 0, st>>>(
+                list16, lcnt.as<int>() + 2, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
+                keys2.as<unsigned>(), vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
+            FDL_LAUNCH_CK();
+        }
+        if (hc[0] > 0) {
+            k_gal_rows_mid<<<std::min(div_up(hc[0], kGalMidWarps), kNumSMs * 8), kGalMidWarps * 32, 0, st>>>(
+                midlist, lcnt.as<int>(), mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
+                keys2.as<unsigned>(), vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
+            FDL_LAUNCH_CK();
+        }
+        const int h = hc[1];
+        if (h > 0) {
+            DBuf sz((size_t)h * 4, st), boff((size_t)(h + 1) * 4, st);
+            k_big_sizes<<<grid_for(h), 256, 0, st>>>(h, biglist, mrp.as<int>(), coff.as<int>(), sz.as<int>());
+            FDL_LAUNCH_CK();
+            scan_exclusive(sz.as<int>(), boff.as<int>(), h, boff.as<int>() + h, st);
+            const int EB = read_int(boff.as<int>() + h, st);
+            DBuf ckey((size_t)EB * 8, st), ck2((size_t)EB * 4, st), cidx((size_t)EB * 4, st),
+                crank((size_t)EB * 4, st), cdst((size_t)EB * 4, st), srcpos((size_t)EB * 4, st);
+            k_big_gather<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
+                h, biglist, mrp.as<int>(), coff.as<int>(), boff.as<int>(), keys2.as<unsigned>(),
+                ck2.as<unsigned>(), cidx.as<int>(), crank.as<unsigned>(), cdst.as<int>());
+            FDL_LAUNCH_CK();
+            // srcpos[o] = original position of concatenated element o (= cdst before sorting)
+            FDL_CK(cudaMemcpyAsync(srcpos.p, cdst.p, (size_t)EB * 4, cudaMemcpyDeviceToDevice, st));
+            // LSD radix passes, least significant key first: hi, then (B, lo), then the row rank
+            radix_sort_u32_i32(ck2.as<unsigned>(), cidx.as<int>(), EB, 32, st);
+            k_big_key1_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), srcpos.as<int>(),
+                                                        keys.as<unsigned long long>(), ckey.as<unsigned long long>());
+            FDL_LAUNCH_CK();
+            radix_sort_u64_i32(ckey.as<unsigned long long>(), cidx.as<int>(), EB, 32 + bits_for(c - 1), st);
+            DBuf rank2((size_t)EB * 4, st);
+            k_big_rank_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), crank.as<unsigned>(),
+                                                        rank2.as<unsigned>());
+            FDL_LAUNCH_CK();
+            radix_sort_u32_i32(rank2.as<unsigned>(), cidx.as<int>(), EB, bits_for(h - 1), st);
+            DBuf keys_s((size_t)E * 8, st), vals_s((size_t)E * 8, st);
+            k_big_place<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), cdst.as<int>(), srcpos.as<int>(),
+                                                      keys.as<unsigned long long>(), vals.as<double>(),
+                                                      keys_s.as<unsigned long long>(), vals_s.as<double>());
+            FDL_LAUNCH_CK();
+            k_big_fold<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
+                h, biglist, mrp.as<int>(), coff.as<int>(), keys_s.as<unsigned long long>(), vals_s.as<double>(),
+                outB.as<int>(), outW.as<double>(), deg.as<int>());
+            FDL_LAUNCH_CK();
+        }
+        keys.release();
+        keys2.release();
+        vals.release();
+        rowoff.alloc((size_t)c * 4, st);
+        k_row_base<<<grid_for(c), 256, 0, st>>>(c, mrp.as<int>(), coff.as<int>(), rowoff.as<int>());
         FDL_LAUNCH_CK();
     }
-    mem.release();
-    // 3. per-row sort + fold
-    DBuf outB((size_t)std::max(E, 1) * 4, st), outW((size_t)std::max(E, 1) * 8, st),
-        deg((size_t)(c + 1) * 4, st), f16((size_t)c * 4, st), midf((size_t)c * 4, st),
-        bigf((size_t)c * 4, st), lists((size_t)c * 4 * 3, st), lcnt(16, st);
-    k_gal_rows_small<<<grid_for(c, 256, kNumSMs * 8), 256, 0, st>>>(
-        c, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>(),
-        outB.as<int>(), outW.as<double>(), deg.as<int>(), f16.as<int>(), midf.as<int>(), bigf.as<int>());
-    FDL_LAUNCH_CK();
-    int *midlist = lists.as<int>(), *biglist = lists.as<int>() + c, *list16 = lists.as<int>() + 2 * c;
-    compact_flagged(nullptr, midf.as<int>(), c, midlist, lcnt.as<int>(), st);
-    compact_flagged(nullptr, bigf.as<int>(), c, biglist, lcnt.as<int>() + 1, st);
-    compact_flagged(nullptr, f16.as<int>(), c, list16, lcnt.as<int>() + 2, st);
-    int hc[3];
-    FDL_CK(cudaMemcpyAsync(hc, lcnt.p, 12, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
-    if (hc[2] > 0) {
-        k_gal_rows_16<<<grid_for(hc[2], 256, kNumSMs * 8), 256, 0, st>>>(
-            list16, lcnt.as<int>() + 2, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
-            keys2.as<unsigned>(), vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
-        FDL_LAUNCH_CK();
-    }
-    if (hc[0] > 0) {
-        k_gal_rows_mid<<<std::min(div_up(hc[0], kGalMidWarps), kNumSMs * 8), kGalMidWarps * 32, 0, st>>>(
-            midlist, lcnt.as<int>(), mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
-            keys2.as<unsigned>(), vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
-        FDL_LAUNCH_CK();
-    }
-    const int h = hc[1];
-    if (h > 0) {
-        DBuf sz((size_t)h * 4, st), boff((size_t)(h + 1) * 4, st);
-        k_big_sizes<<<grid_for(h), 256, 0, st>>>(h, biglist, mrp.as<int>(), coff.as<int>(), sz.as<int>());
-        FDL_LAUNCH_CK();
-        scan_exclusive(sz.as<int>(), boff.as<int>(), h, boff.as<int>() + h, st);
-        const int EB = read_int(boff.as<int>() + h, st);
-        DBuf ckey((size_t)EB * 8, st), ck2((size_t)EB * 4, st), cidx((size_t)EB * 4, st),
-            crank((size_t)EB * 4, st), cdst((size_t)EB * 4, st), srcpos((size_t)EB * 4, st);
-        k_big_gather<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
-            h, biglist, mrp.as<int>(), coff.as<int>(), boff.as<int>(), keys2.as<unsigned>(),
-            ck2.as<unsigned>(), cidx.as<int>(), crank.as<unsigned>(), cdst.as<int>());
-        FDL_LAUNCH_CK();
-        // srcpos[o] = original position of concatenated element o (= cdst before sorting)
-        FDL_CK(cudaMemcpyAsync(srcpos.p, cdst.p, (size_t)EB * 4, cudaMemcpyDeviceToDevice, st));
-        // LSD radix passes, least significant key first: hi, then (B, lo), then the row rank
-        radix_sort_u32_i32(ck2.as<unsigned>(), cidx.as<int>(), EB, 32, st);
-        k_big_key1_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), srcpos.as<int>(),
-                                                    keys.as<unsigned long long>(), ckey.as<unsigned long long>());
-        FDL_LAUNCH_CK();
-        radix_sort_u64_i32(ckey.as<unsigned long long>(), cidx.as<int>(), EB, 32 + bits_for(c - 1), st);
-        DBuf rank2((size_t)EB * 4, st);
-        k_big_rank_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), crank.as<unsigned>(),
-                                                    rank2.as<unsigned>());
-        FDL_LAUNCH_CK();
-        radix_sort_u32_i32(rank2.as<unsigned>(), cidx.as<int>(), EB, bits_for(h - 1), st);
-        DBuf keys_s((size_t)E * 8, st), vals_s((size_t)E * 8, st);
-        k_big_place<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), cdst.as<int>(), srcpos.as<int>(),
-                                                  keys.as<unsigned long long>(), vals.as<double>(),
-                                                  keys_s.as<unsigned long long>(), vals_s.as<double>());
-        FDL_LAUNCH_CK();
-        k_big_fold<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
-            h, biglist, mrp.as<int>(), coff.as<int>(), keys_s.as<unsigned long long>(), vals_s.as<double>(),
-            outB.as<int>(), outW.as<double>(), deg.as<int>());
-        FDL_LAUNCH_CK();
-    }
-    keys.release();
-    keys2.release();
-    vals.release();
     // 4. CSR assembly
     scan_exclusive(deg.as<int>(), out.own_rp.as<int>(), c, out.own_rp.as<int>() + c, st);
     out.nnz = read_int(out.own_rp.as<int>() + c, st);
@@ -1003,7 +1493,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     out.own_w.alloc(padded((size_t)std::max(out.nnz, 1) * 8), st);
     const double cavg = c ? (double)out.nnz / c : 0.0;
     DISPATCH_WC(cavg, (k_gal_write<W><<<sub_grid(c, W), 256, 0, st>>>(
-                          c, mrp.as<int>(), coff.as<int>(), out.own_rp.as<int>(), outB.as<int>(),
+                          c, rowoff.as<int>(), out.own_rp.as<int>(), outB.as<int>(),
                           outW.as<double>(), out.own_ci.as<int>(), out.own_w.as<double>())));
     FDL_LAUNCH_CK();
     out.rp = out.own_rp.as<int>();

@@ -42,6 +42,18 @@ def clique_with_tail(k, tail):
     return gg.csr_from_edges(k + tail, u, v, w, "clique%d_tail%d" % (k, tail))
 
 
+def unsorted_rows(g, seed):
+    """Same graph with the entries of every CSR row in a seeded random order
+    (violates the input contract: columns strictly increasing per row)."""
+    rng = np.random.default_rng(seed)
+    ci, w = g.ci.copy(), g.w.copy()
+    for v in range(g.n):
+        b, e = int(g.rp[v]), int(g.rp[v + 1])
+        p = b + rng.permutation(e - b)
+        ci[b:e], w[b:e] = g.ci[p], g.w[p]
+    return gg.CSRGraph(g.n, g.rp.copy(), ci, w, g.name + "_unsorted")
+
+
 SMALL = {
     "grid32_unit(config0)": lambda: gg.grid2d(32, "unit"),
     "grid50x37_uniform": lambda: gg.grid2d(50, "uniform", seed=7, mx=37),
@@ -78,6 +90,14 @@ def test_hierarchy_bit_exact(fd, orc, name):
                 assert np.array_equal(ex["mate"], L.mate), (name, ell)
     finally:
         fd.fiedler_destroy(h)
+
+
+@pytest.mark.parametrize("name", ["grid50x37_uniform", "grid3d_12_lognormal", "rand300"])
+def test_hierarchy_full_sort_fallback(fd, orc, name, monkeypatch):
+    """The Galerkin fallback of very large levels (full (B, lo, hi) sort of the
+    class-0 rows), forced on small graphs: still bit-exact."""
+    monkeypatch.setenv("FIEDLER_TEST_FULL_SORT", "1")
+    test_hierarchy_bit_exact(fd, orc, name)
 
 
 @pytest.mark.parametrize("name", ["grid32_unit(config0)", "grid3d_12_lognormal", "rmat12", "rand300"])
@@ -203,6 +223,15 @@ def test_rejects_disconnected(fd):
     with pytest.raises(fd.FiedlerError) as e:
         fd.fiedler_create(g.n, g.nnz, g.rp, g.ci, g.w)
     assert e.value.code == fd.FIEDLER_ERR_DISCONNECTED
+
+
+def test_rejects_unsorted_rows(fd):
+    # ascending rows are part of the contract (include/fiedler.h) and a
+    # premise of the direct Galerkin path: validation must catch them
+    g = unsorted_rows(gg.grid2d(12, "uniform", seed=9), 3)
+    with pytest.raises(fd.FiedlerError) as e:
+        fd.fiedler_create(g.n, g.nnz, g.rp, g.ci, g.w)
+    assert e.value.code == fd.FIEDLER_ERR_GRAPH
 
 
 def test_rejects_invalid_csr(fd):

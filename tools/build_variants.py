@@ -5,7 +5,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1602_04386_b200 import build as b  # noqa: E402
 
-VARIANTS = [dict(FDL_HEAVY_DEG=64), dict(FDL_HEAVY_DEG=128), dict(FDL_HEAVY_DEG=256), dict(FDL_HEAVY_DEG=1024)]
+# usage: python tools/build_variants.py "[dict(FDL_X=1), dict(FDL_X=2)]"
+VARIANTS = eval(sys.argv[1]) if len(sys.argv) > 1 else [dict(FDL_HEAVY_DEG=64), dict(FDL_HEAVY_DEG=128)]
 out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build_variants")
 os.makedirs(out, exist_ok=True)
 for v in VARIANTS:
