@@ -949,7 +949,8 @@ __global__ void k_gal_classify(int c, const int *mrp, const int *toff, int *f32,
 // lanes by (B, lo, hi), then every head of a B run left-folds the run in order.
 template <int W, bool LIST>
 __global__ void __launch_bounds__(256) k_gal_direct_sw(int c, const int *list, const int *count, const int *mrp,
-                                                       const int *mem, const int *toff, const int *rp,
+                                                       const int *mem, const int *toff, const int *rowoff,
+                                                       const int *rp,
                                                        const int *ci, const double *w, const int *q, int *outB,
                                                        double *outW, int *deg) {
     const int cnt = LIST ? *count : c;
@@ -963,7 +964,7 @@ __global__ void __launch_bounds__(256) k_gal_direct_sw(int c, const int *list, c
         const bool live = base < cnt;
         const int A = live ? (LIST ? list[base] : (int)base) : 0;
         int mb = 0, nm = 0, tb = 0, T = 0;
-        if (live) { mb = mrp[A]; nm = mrp[A + 1] - mb; tb = toff[A]; T = toff[A + 1] - tb; }
+        if (live) { mb = mrp[A]; nm = mrp[A + 1] - mb; T = toff[A + 1] - toff[A]; tb = rowoff[A]; }
         const bool mine = live && (LIST || gal_class(nm, T) == 0);
         // member table: lane t holds member t, its row start and slot offset
         int mv = 0, bv = 0, d = 0;
@@ -1040,7 +1041,7 @@ __global__ void __launch_bounds__(256) k_gal_direct_sw(int c, const int *list, c
 
 // Sort-and-fold of one row's <= CAP slots (smem at P: coarse column B, or -1
 // for an edge inside the aggregate; lo = min(m, j); the weight) on ONE 64-bit
-// key per slot, (B << 33 | lo << 4 | slot).  The slot index breaks the ties of
+// key per slot, (B << 33 | lo << 4 | slot), in batch_sort_fold below.  The slot index breaks the ties of
 // (B, lo) in the order of hi, because the slots run through the members in
 // ascending order and every member row in ascending column order: equal lo is
 // either one member m < j with several neighbours j in B (slot order = j order)
@@ -1048,9 +1049,14 @@ __global__ void __launch_bounds__(256) k_gal_direct_sw(int c, const int *list, c
 // So the runs of B come out in the R3 order (lo, hi) and are left-folded.
 // Requires B < 2^27, vertex ids < 2^29 and ascending CSR rows (the input
 // contract of fiedler_create; every Galerkin output row ascends in B).
+// All 32 lanes: lane rows with Tm > 0 are sorted and folded here; every lane
+// reserves `resv` output entries (its fold's run count when resv < 0) in the
+// batch's output block that starts at bbase, dense in lane order, and returns
+// its offset there in *off (its run count as the result).
 template <int CAP>
-__device__ __forceinline__ void sort_fold_b64(const int *KB, const int *LO, const double *V, int P, int Tm,
-                                              int *outB, double *outW, int *deg_out) {
+__device__ __forceinline__ int batch_sort_fold(const int *KB, const int *LO, const double *V, int P, int Tm,
+                                               int resv, int bbase, int lane, int *outB, double *outW,
+                                               int *off) {
     unsigned long long k[CAP];
 #pragma unroll
     for (int s = 0; s < CAP; s++) {
@@ -1071,7 +1077,21 @@ __device__ __forceinline__ void sort_fold_b64(const int *KB, const int *LO, cons
                     if ((i & kk) == 0) { k[i] = a; k[l] = b; } else { k[i] = b; k[l] = a; }
                 }
             }
-    int runs = 0;
+    int runs = k[0] != ~0ull;
+#pragma unroll
+    for (int i = 1; i < CAP; i++) runs += k[i] != ~0ull && (k[i] >> 33) != (k[i - 1] >> 33);
+    const int r = resv < 0 ? runs : resv;
+    int Q = r;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, Q, o);
+        if (lane >= o) Q += y;
+    }
+    Q += bbase - r;
+    *off = Q;
+    int *oB = outB + Q;
+    double *oW = outW + Q;
+    int nr = 0;
     unsigned curB = 0;
     double acc = 0.0;
 #pragma unroll
@@ -1081,23 +1101,25 @@ __device__ __forceinline__ void sort_fold_b64(const int *KB, const int *LO, cons
             const double x = V[P + (int)(k[i] & 15u)];
             if (i == 0) { curB = B; acc = x; }
             else if (B != curB) {
-                outB[runs] = (int)curB; outW[runs] = acc; runs++;
+                oB[nr] = (int)curB; oW[nr] = acc; nr++;
                 curB = B; acc = x;
             } else {
                 acc += x;
             }
         }
     }
-    if (k[0] != ~0ull) { outB[runs] = (int)curB; outW[runs] = acc; runs++; }
-    *deg_out = runs;
+    if (k[0] != ~0ull) { oB[nr] = (int)curB; oW[nr] = acc; }
+    return runs;
 }
 
 // Batches of 32 consecutive coarse rows per warp, class 0 only: lane = row
 // reads its row's members and lays its slot descriptors (CSR position, row) out
 // in shared memory; the lanes then gather all slots of the batch together
 // (consecutive slots are consecutive CSR entries); finally every lane sorts and
-// folds its own row in registers (sort_fold_b64).  Without the b64 premises
-// (`b64` false) every row is appended to `redo` for the warp-per-row kernel.
+// folds its own row in registers (batch_sort_fold) and writes it to the dense
+// output block of the batch (rowoff[A] = its offset; the other classes' rows
+// keep T_A entries reserved there).  Without the b64 premises (`b64` false)
+// every class-0 row is appended to `redo` for the warp-per-row kernel.
 constexpr int kGalBatchWarps = 4;
 constexpr int kGalBatchSlots = 32 * 16;
 #ifndef FDL_GAL_UNROLL
@@ -1106,7 +1128,7 @@ constexpr int kGalBatchSlots = 32 * 16;
 constexpr int kGalGatherUnroll = FDL_GAL_UNROLL;
 __global__ void __launch_bounds__(kGalBatchWarps * 32) k_gal_direct_batch(
     int c, bool b64, const int *mrp, const int *mem, const int *toff, const int *rp, const int *ci,
-    const double *w, const int *q, int *outB, double *outW, int *deg, int *redo, int *redo_count) {
+    const double *w, const int *q, int *outB, double *outW, int *deg, int *rowoff, int *redo, int *redo_count) {
     __shared__ int skb[kGalBatchWarps][kGalBatchSlots];
     __shared__ int slo[kGalBatchWarps][kGalBatchSlots];
     __shared__ double sv[kGalBatchWarps][kGalBatchSlots];
@@ -1196,17 +1218,18 @@ __global__ void __launch_bounds__(kGalBatchWarps * 32) k_gal_direct_batch(
             }
         }
         __syncwarp();
-        int d = 0;
-        if (b64) {
-            if (__all_sync(0xffffffffu, Tm <= 8)) {
-                if (mine) sort_fold_b64<8>(KB, LO, V, P, Tm, outB + tb, outW + tb, &d);
-            } else {
-                if (mine) sort_fold_b64<16>(KB, LO, V, P, Tm, outB + tb, outW + tb, &d);
-            }
-        }
-        const bool ok = b64;
+        // folded here: class-0 rows under the b64 premises; the rest reserve T
+        const int Tf = b64 ? Tm : 0;
+        const int resv = (mine && b64) ? -1 : (live ? T : 0);
+        const int bbase = __shfl_sync(0xffffffffu, tb, 0);   // toff of the batch's first row
+        int off, d;
+        if (__all_sync(0xffffffffu, Tf <= 8))
+            d = batch_sort_fold<8>(KB, LO, V, P, Tf, resv, bbase, lane, outB, outW, &off);
+        else
+            d = batch_sort_fold<16>(KB, LO, V, P, Tf, resv, bbase, lane, outB, outW, &off);
+        if (live) rowoff[A] = off;
         if (mine) {
-            if (ok) deg[A] = d;
+            if (b64) deg[A] = d;
             else redo[atomicAdd(redo_count, 1)] = A;
         }
         __syncwarp();
@@ -1217,8 +1240,8 @@ __global__ void __launch_bounds__(kGalBatchWarps * 32) k_gal_direct_batch(
 // shared memory, bitonic sort there, heads of the B runs fold them in order
 constexpr int kGalDirectWarps = 4;
 __global__ void __launch_bounds__(kGalDirectWarps * 32) k_gal_direct_warp(
-    const int *list, const int *count, const int *mrp, const int *mem, const int *toff, const int *rp,
-    const int *ci, const double *w, const int *q, int *outB, double *outW, int *deg) {
+    const int *list, const int *count, const int *mrp, const int *mem, const int *toff, const int *rowoff,
+    const int *rp, const int *ci, const double *w, const int *q, int *outB, double *outW, int *deg) {
     __shared__ unsigned long long sk[kGalDirectWarps][kGalMid];
     __shared__ unsigned sk2[kGalDirectWarps][kGalMid];
     __shared__ double sv[kGalDirectWarps][kGalMid];
@@ -1232,7 +1255,7 @@ __global__ void __launch_bounds__(kGalDirectWarps * 32) k_gal_direct_warp(
     int *Mm = sm_m[warp], *Mb = sm_b[warp], *Mp = sm_p[warp];
     for (int idx = blockIdx.x * kGalDirectWarps + warp; idx < cnt; idx += gridDim.x * kGalDirectWarps) {
         const int A = list[idx];
-        const int mb = mrp[A], nm = mrp[A + 1] - mb, tb = toff[A], T = toff[A + 1] - tb;
+        const int mb = mrp[A], nm = mrp[A + 1] - mb, tb = rowoff[A], T = toff[A + 1] - toff[A];
         // member table with the exclusive prefix of the member degrees
         int carry = 0;
         for (int t0 = 0; t0 < nm; t0 += 32) {
@@ -1369,33 +1392,34 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
         const char *fs = std::getenv("FIEDLER_TEST_FULL_SORT");
         const bool b64 = c < (1 << 27) && n < (1 << 29) && !(fs && fs[0] == '1');
         DBuf redo(b64 ? 0 : (size_t)c * 4, st);
+        rowoff.alloc((size_t)c * 4, st);
         k_gal_direct_batch<<<std::min(div_up(c, 32 * kGalBatchWarps), kNumSMs * 32), kGalBatchWarps * 32, 0,
                              st>>>(c, b64, mrp.as<int>(), mem.as<int>(), toff.as<int>(), g.rp, g.ci, g.w, q,
-                                   outB.as<int>(), outW.as<double>(), deg.as<int>(), redo.as<int>(),
-                                   dcnt.as<int>() + 3);
+                                   outB.as<int>(), outW.as<double>(), deg.as<int>(), rowoff.as<int>(),
+                                   redo.as<int>(), dcnt.as<int>() + 3);
         FDL_LAUNCH_CK();
         if (!b64) {
             // beyond the b64 key ranges: the class-0 rows take the full (B, lo, hi)
             // sort (the kernel reads the list length on the device)
             k_gal_direct_sw<32, true><<<kNumSMs * 8, 256, 0, st>>>(
-                c, redo.as<int>(), dcnt.as<int>() + 3, mrp.as<int>(), mem.as<int>(), toff.as<int>(), g.rp,
-                g.ci, g.w, q, outB.as<int>(), outW.as<double>(), deg.as<int>());
+                c, redo.as<int>(), dcnt.as<int>() + 3, mrp.as<int>(), mem.as<int>(), toff.as<int>(),
+                rowoff.as<int>(), g.rp, g.ci, g.w, q, outB.as<int>(), outW.as<double>(), deg.as<int>());
             FDL_LAUNCH_CK();
         }
         if (dc[0] > 0) {
             k_gal_direct_sw<32, true><<<grid_for((int64_t)dc[0] * 32, 256, kNumSMs * 16), 256, 0, st>>>(
-                c, dl.as<int>(), dcnt.as<int>(), mrp.as<int>(), mem.as<int>(), toff.as<int>(), g.rp, g.ci,
-                g.w, q, outB.as<int>(), outW.as<double>(), deg.as<int>());
+                c, dl.as<int>(), dcnt.as<int>(), mrp.as<int>(), mem.as<int>(), toff.as<int>(),
+                rowoff.as<int>(), g.rp, g.ci, g.w, q, outB.as<int>(), outW.as<double>(), deg.as<int>());
             FDL_LAUNCH_CK();
         }
         if (dc[1] > 0) {
             k_gal_direct_warp<<<std::min(div_up(dc[1], kGalDirectWarps), kNumSMs * 16), kGalDirectWarps * 32,
                                 0, st>>>(dl.as<int>() + c, dcnt.as<int>() + 1, mrp.as<int>(), mem.as<int>(),
-                                         toff.as<int>(), g.rp, g.ci, g.w, q, outB.as<int>(), outW.as<double>(),
-                                         deg.as<int>());
+                                         toff.as<int>(), rowoff.as<int>(), g.rp, g.ci, g.w, q, outB.as<int>(),
+                                         outW.as<double>(), deg.as<int>());
             FDL_LAUNCH_CK();
         }
-        rowoff = std::move(toff);
+        toff.release();
     } else {
         toff.release();
         // 2. contributions in member order
