@@ -166,7 +166,12 @@ void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32,
 namespace cg = cooperative_groups;
 constexpr int kCoopThreads = 256;
 constexpr int kAppendCap = 2048;
-constexpr int kMaxRounds = 1 << 16;   // JP depth can reach thousands on dense cores
+constexpr int kMaxRounds = 1 << 16;
+#ifndef FDL_MATCH_UNROLL
+#define FDL_MATCH_UNROLL 4
+#endif
+constexpr int kMatchUnroll = FDL_MATCH_UNROLL;
+static_assert(kAppendCap >= 2 * kMatchUnroll * kCoopThreads, "append buffer too small");   // JP depth can reach thousands on dense cores
 
 // FIEDLER_TRACE: per-phase device timestamps of the cooperative kernels
 __device__ unsigned long long *g_round_ts = nullptr;
@@ -337,17 +342,86 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
     int r = 0;
     int cnt = *(volatile int *)&counts[0];
     while (cnt > 0 && r + 1 < kMaxRounds) {
-        // (a) mutual pointers match
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-            const int v = in[i];
-            const int p = ptr[v];
-            if (p >= 0 && ptr[p] == v) mate[v] = p;
+        // (a) mutual pointers match (kMatchUnroll entries per thread in flight)
+        {
+            const int stride = gridDim.x * blockDim.x;
+            for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < cnt; i0 += stride * kMatchUnroll) {
+                int v[kMatchUnroll], p[kMatchUnroll];
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++) {
+                    const int i = i0 + u * stride;
+                    v[u] = i < cnt ? in[i] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++) p[u] = v[u] >= 0 ? ptr[v[u]] : -1;
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++)
+                    if (p[u] >= 0 && ptr[p[u]] == v[u]) mate[v[u]] = p[u];
+            }
         }
         grid.sync();
         round_stamp(stamp++);
         // (b) unmatched vertices whose target got matched re-point at their
         //     heaviest FREE neighbour (cursor advance, or a rescan for long rows)
         int *gcount = counts + r + 1;
+        if (W == 1) {
+            // thread per vertex, kMatchUnroll vertices per thread with their
+            // loads in flight together; long rows (no cursor) are rescanned
+            for (long long base = (long long)blockIdx.x * kCoopThreads * kMatchUnroll; base < cnt;
+                 base += (long long)gridDim.x * kCoopThreads * kMatchUnroll) {
+                int v[kMatchUnroll], mv[kMatchUnroll], p[kMatchUnroll], cur[kMatchUnroll], b[kMatchUnroll],
+                    e[kMatchUnroll], mp[kMatchUnroll], cand[kMatchUnroll], mc[kMatchUnroll];
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++) {
+                    const long long idx = base + u * kCoopThreads + threadIdx.x;
+                    v[u] = idx < cnt ? in[idx] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++) {
+                    const bool ok = v[u] >= 0;
+                    mv[u] = ok ? mate[v[u]] : 0;
+                    p[u] = ok ? ptr[v[u]] : 0;
+                    cur[u] = ok ? cursor[v[u]] : -1;
+                    b[u] = ok ? rp[v[u]] : 0;
+                    e[u] = ok ? rp[v[u] + 1] : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++) mp[u] = (v[u] >= 0 && mv[u] < 0) ? mate[p[u]] : -1;
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++) {
+                    const bool adv = v[u] >= 0 && mv[u] < 0 && mp[u] >= 0 && cur[u] >= 0;
+                    cur[u] += 1;
+                    cand[u] = (adv && b[u] + cur[u] < e[u]) ? nbr[b[u] + cur[u]] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++) mc[u] = cand[u] >= 0 ? mate[cand[u]] : -1;
+#pragma unroll
+                for (int u = 0; u < kMatchUnroll; u++) {
+                    if (v[u] < 0 || mv[u] >= 0) continue;
+                    bool keep = mp[u] < 0;
+                    if (!keep) {   // the target got matched: re-point
+                        int bj;
+                        if (cur[u] > 0) {   // ranked row: cursor advance from cur + 1
+                            int c = cur[u], j = cand[u], mj = mc[u];
+                            while (j >= 0 && mj >= 0) {
+                                c++;
+                                j = b[u] + c < e[u] ? nbr[b[u] + c] : -1;
+                                mj = j >= 0 ? mate[j] : -1;
+                            }
+                            bj = j;
+                            cursor[v[u]] = c;
+                        } else {
+                            bj = heaviest<1>(v[u], rp, ci, w, salt, 0, [&](int j) { return mate[j] >= 0; });
+                        }
+                        ptr[v[u]] = bj;
+                        keep = bj >= 0;
+                    }
+                    if (keep) app.push(v[u]);
+                }
+                __syncthreads();
+                if (s_n > kAppendCap - kMatchUnroll * kCoopThreads) app.flush(out, gcount);
+            }
+        } else
         for (long long base = (long long)blockIdx.x * per_block; base < cnt;
              base += (long long)gridDim.x * per_block) {
             const long long idx = base + threadIdx.x / W;
