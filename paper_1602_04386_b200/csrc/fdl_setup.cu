@@ -1992,41 +1992,83 @@ __global__ void k_color_keys(int n, const int *color, unsigned *keys, int *vals)
 
 
 __global__ void k_inv_and_deg(int n, const int *perm, const int *rp, int *inv, int *degp) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        int v = perm[t];
-        inv[v] = t;
-        degp[t] = rp[v + 1] - rp[v];
+    const int stride = gridDim.x * blockDim.x;
+    for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < n; t0 += 4 * stride) {
+        int v[4], d[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = t0 + u * stride < n ? perm[t0 + u * stride] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++) d[u] = v[u] >= 0 ? rp[v[u] + 1] - rp[v[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (v[u] >= 0) { inv[v[u]] = t0 + u * stride; degp[t0 + u * stride] = d[u]; }
     }
 }
 
 // GS layout rows: natural row v is copied to GS row inv[v] with its columns
 // renumbered by inv (order kept).  Walking natural rows keeps the reads and the
 // inv gathers streaming; the writes form one sequential stream per colour.
+// The sub-warp handles kPermRows rows per step with all their loads in flight,
+// and also yields max_i d_i (Gershgorin shift, R5) with every d_i summed in
+// stored (= natural ascending) order, as the oracle.
+constexpr int kPermRows = 4;
 template <int W>
 __global__ void k_permute_rows(int n, const int *inv, const int *rp, const int *ci, const double *w,
-                               const int *rpp, int *cip, double *wp) {
-    SUBWARP_LOOP(W, n, v) {
-        if (v < n) {
-            const int b = rp[v], e = rp[v + 1], o = rpp[inv[v]];
-            for (int k = sw_lane_; k < e - b; k += W) {
-                cip[o + k] = inv[ci[b + k]];
-                wp[o + k] = w[b + k];
+                               const int *rpp, int *cip, double *wp, unsigned long long *dmax) {
+    const int lane = threadIdx.x & (W - 1);
+    const unsigned smask = W == 32 ? 0xffffffffu : ((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1));
+    const int64_t nsub = (int64_t)gridDim.x * blockDim.x / W;
+    const int64_t sub = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / W;
+    double dm = 0.0;
+    for (int64_t r0 = sub; r0 < n; r0 += nsub * kPermRows) {
+        int b[kPermRows], e[kPermRows], iv[kPermRows], o[kPermRows], c[kPermRows];
+        double x[kPermRows];
+#pragma unroll
+        for (int u = 0; u < kPermRows; u++) {
+            const int64_t v = r0 + u * nsub;
+            const bool ok = v < n;
+            b[u] = ok ? rp[v] : 0;
+            e[u] = ok ? rp[v + 1] : 0;
+            iv[u] = ok ? inv[v] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPermRows; u++) {
+            o[u] = e[u] > b[u] ? rpp[iv[u]] : 0;
+            const bool ok = lane < e[u] - b[u];
+            c[u] = ok ? ci[b[u] + lane] : -1;
+            x[u] = ok ? w[b[u] + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPermRows; u++) {
+            if (c[u] >= 0) {
+                cip[o[u] + lane] = inv[c[u]];
+                wp[o[u] + lane] = x[u];
             }
         }
-    }
-}
-
-// max_i d_i with d_i summed in stored (= natural ascending) order, as the oracle
-__global__ void k_degree_max(int n, const int *rp, const double *w, unsigned long long *dmax) {
-    double m = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int k = rp[i]; k < rp[i + 1]; k++) s += w[k];
-        m = fmax(m, s);
+#pragma unroll
+        for (int u = 0; u < kPermRows; u++) {
+            // d_v = sum of the row in order: the first W entries, then the rest
+            double d = 0.0;
+#pragma unroll
+            for (int l = 0; l < W; l++) d += __shfl_sync(smask, x[u], l, W);
+            const int len = e[u] - b[u];
+            for (int k0 = W; k0 < len; k0 += W) {   // rows longer than W (uniform in the sub-warp)
+                const int k = k0 + lane;
+                double y = 0.0;
+                if (k < len) {
+                    cip[o[u] + k] = inv[ci[b[u] + k]];
+                    y = w[b[u] + k];
+                    wp[o[u] + k] = y;
+                }
+                const int cnt = min(W, len - k0);
+                for (int l = 0; l < cnt; l++) d += __shfl_sync(smask, y, l, W);
+            }
+            dm = fmax(dm, d);
+        }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane_id() == 0) atomicMax(dmax, (unsigned long long)__double_as_longlong(m));
+    for (int o2 = 16; o2; o2 >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o2));
+    if (lane_id() == 0) atomicMax(dmax, (unsigned long long)__double_as_longlong(dm));
 }
 
 __global__ void k_gather_i32(int k, const int *src, const int *idx, int *out) {
@@ -2085,17 +2127,14 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     const size_t w_bytes = (size_t)std::max(g.nnz, 1) * 8 + kPadBytes;
     L.ci.alloc(ci_bytes, st);
     L.w.alloc(w_bytes, st);
+    DBuf dmax(8, st);
+    FDL_CK(cudaMemsetAsync(dmax.p, 0, 8, st));
     DISPATCH_W(avg, (k_permute_rows<W><<<sub_grid(n, W), 256, 0, st>>>(
                          n, L.inv.as<int>(), g.rp, g.ci, g.w, L.rp.as<int>(),
-                         L.ci.as<int>(), L.w.as<double>())));
+                         L.ci.as<int>(), L.w.as<double>(), dmax.as<unsigned long long>())));
     FDL_LAUNCH_CK();
     // ---- PI/RQ layout: the natural CSR (taken over from the setup graph when it
     // owns padded storage, copied otherwise) -- see take_natural() below
-    DBuf dmax(8, st);
-    FDL_CK(cudaMemsetAsync(dmax.p, 0, 8, st));
-    k_degree_max<<<grid_for(n, 256, kNumSMs * 8), 256, 0, st>>>(n, g.rp, g.w,
-                                                               dmax.as<unsigned long long>());
-    FDL_LAUNCH_CK();
 
     // colour segment boundaries and their nonzero offsets -> host
     std::vector<int> seg(ncolors + 1);
