@@ -422,9 +422,10 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
                 if (s_n > kAppendCap - kMatchUnroll * kCoopThreads) app.flush(out, gcount);
             }
         } else
-        for (long long base = (long long)blockIdx.x * per_block; base < cnt;
-             base += (long long)gridDim.x * per_block) {
-            const long long idx = base + threadIdx.x / W;
+        // sub-warp slot s of CTA b takes entry base + s * gridDim + b: a short
+        // list (deep rounds of dense levels) is spread over all CTAs
+        for (long long base = 0; base < cnt; base += (long long)gridDim.x * per_block) {
+            const long long idx = base + (long long)(threadIdx.x / W) * gridDim.x + blockIdx.x;
             const int v = idx < cnt ? in[idx] : -1;
             bool keep = false, moved = false;
             int cur = -1;
@@ -1835,9 +1836,13 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     };
     while (cnt > 0 && r + 1 < kMaxRounds) {
         int *gcount = counts + r + 1;
-        for (long long base = (long long)blockIdx.x * per_block; base < cnt;
+        // W == 1: contiguous entries per CTA; W > 1: sub-warp slot s of CTA b
+        // takes entry base + s * gridDim + b, so a short list (the deep rounds
+        // of dense levels) is spread over all CTAs, at most one heavy vertex each
+        for (long long base = W == 1 ? (long long)blockIdx.x * per_block : 0; base < cnt;
              base += (long long)gridDim.x * per_block) {
-            const long long idx = base + threadIdx.x / W;
+            const long long idx = W == 1 ? base + threadIdx.x
+                                         : base + (long long)(threadIdx.x / W) * gridDim.x + blockIdx.x;
             int v = idx < cnt ? in[idx] : -1;
             if (W > 1 && v >= 0 && rp[v + 1] - rp[v] > kHeavyDeg) {   // the CTA does it below
                 if (lane == 0) s_heavy[atomicAdd(&s_nh, 1)] = v;
