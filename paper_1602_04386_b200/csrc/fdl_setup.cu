@@ -1935,6 +1935,155 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
     if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
 }
 
+// Small dense levels (n <= kSmallColourN, average degree >= 64: the coarse levels of power-law
+// graphs: hundreds of colours, priority DAGs ~n deep): the same topological JP
+// in ONE CTA, with colours, in-degrees and both work lists in shared memory
+// (shared-memory atomics, __syncthreads between rounds instead of grid
+// barriers).  A round takes its ready vertices kSmallChunk at a time and
+// spreads ALL their row entries over the CTA (8 loads per thread in flight):
+// higher-priority neighbours mark the vertex's first-fit bitmap, lower-priority
+// ones are released; then one warp per vertex picks the first free colour.
+constexpr int kSmallColourN = 12288;
+constexpr int kSmallColourThreads = 1024;
+constexpr int kSmallChunk = 64;
+constexpr double kSmallColourMinDeg = 64.0;   // sparse small levels: the grid kernel is faster
+__global__ void __launch_bounds__(kSmallColourThreads, 1) k_color_small(int n, const int *rp, const int *ci,
+                                                                          uint64_t salt, int *color,
+                                                                          int *rounds_out) {
+    extern __shared__ int sm_col[];
+    int *col = sm_col, *indeg = sm_col + n, *la = sm_col + 2 * n, *lb = sm_col + 3 * n;
+    __shared__ unsigned bm[kSmallChunk][kBmWords];
+    __shared__ int s_off[kSmallChunk + 1], s_b[kSmallChunk], s_v[kSmallChunk];
+    __shared__ unsigned long long s_pv[kSmallChunk];
+    __shared__ int s_cnt[2], s_err;
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    constexpr int nwarps = kSmallColourThreads / 32;
+    if (threadIdx.x == 0) { s_cnt[0] = 0; s_cnt[1] = 0; s_err = 0; }
+    __syncthreads();
+    // in-degrees in the priority DAG: warp per vertex, 8 entries per lane in flight
+    for (int v = warp; v < n; v += nwarps) {
+        const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+        const int b = rp[v], e = rp[v + 1];
+        int c = 0;
+        for (int k0 = b; k0 < e; k0 += 256) {
+            int u8[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) u8[i] = k0 + i * 32 + lane < e ? ci[k0 + i * 32 + lane] : -1;
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+                c += u8[i] >= 0 && higher_prio(splitmix64(salt ^ (uint64_t)u8[i]), u8[i], pv, v);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) {
+            indeg[v] = c;
+            col[v] = -1;
+            if (c == 0) la[atomicAdd(&s_cnt[0], 1)] = v;
+        }
+    }
+    __syncthreads();
+    int cur = 0, r = 0;
+    int cnt = s_cnt[0];
+    while (cnt > 0 && r + 1 < kMaxRounds) {
+        const int *in = cur ? lb : la;
+        int *out = cur ? la : lb;
+        int *ocnt = &s_cnt[cur ^ 1];
+        for (int c0 = 0; c0 < cnt; c0 += kSmallChunk) {
+            const int m = min(kSmallChunk, cnt - c0);
+            // chunk table: vertices, row starts, entry offsets (warp 0 scans)
+            if (warp == 0) {
+                int carry = 0;
+                for (int t0 = 0; t0 < m; t0 += 32) {
+                    const int t = t0 + lane;
+                    int d = 0;
+                    if (t < m) {
+                        const int v = in[c0 + t];
+                        const int b = rp[v];
+                        d = rp[v + 1] - b;
+                        s_v[t] = v;
+                        s_b[t] = b;
+                        s_pv[t] = splitmix64(salt ^ (uint64_t)v);
+                    }
+                    int x = d;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (t < m) s_off[t] = carry + x - d;
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (lane == 0) s_off[m] = carry;
+            }
+            for (int t = threadIdx.x; t < m * kBmWords; t += blockDim.x) bm[t / kBmWords][t % kBmWords] = 0u;
+            __syncthreads();
+            const int E = s_off[m];
+            for (int e0 = threadIdx.x; e0 < E; e0 += 8 * kSmallColourThreads) {
+                int idx[8], u8[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int e = e0 + i * kSmallColourThreads;
+                    int lo = 0, hi = m - 1;   // last t with s_off[t] <= e
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (s_off[mid] <= e) lo = mid; else hi = mid - 1;
+                    }
+                    idx[i] = e < E ? lo : -1;
+                    u8[i] = e < E ? ci[s_b[lo] + e - s_off[lo]] : 0;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    if (idx[i] < 0) continue;
+                    const int u = u8[i], t = idx[i];
+                    if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, s_pv[t], s_v[t])) {
+                        const int cu = col[u];
+                        if (cu < 0) s_err = 1;   // impossible: uncoloured predecessor
+                        else if (cu < 32 * kBmWords) atomicOr(&bm[t][cu >> 5], 1u << (cu & 31));
+                    } else if (atomicSub(&indeg[u], 1) == 1) {
+                        out[atomicAdd(ocnt, 1)] = u;
+                    }
+                }
+            }
+            __syncthreads();
+            for (int t = warp; t < m; t += nwarps) {
+                const int v = s_v[t];
+                int c = 0x7fffffff;
+                for (int q = lane; q < kBmWords; q += 32)
+                    if (~bm[t][q]) c = min(c, q * 32 + __ffs(~bm[t][q]) - 1);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) c = min(c, __shfl_xor_sync(0xffffffffu, c, o));
+                // rare: colours 0 .. 32 kBmWords - 1 all taken -> the warp rescans windows beyond
+                const int b = s_b[t], e = b + s_off[t + 1] - s_off[t];
+                for (int wb = 32 * kBmWords; c == 0x7fffffff; wb += 32) {
+                    unsigned used = 0u;
+                    for (int k = b + lane; k < e; k += 32) {
+                        const int u = ci[k];
+                        if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, s_pv[t], v)) continue;
+                        const int cu = col[u] - wb;
+                        if (cu >= 0 && cu < 32) used |= 1u << cu;
+                    }
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) used |= __shfl_xor_sync(0xffffffffu, used, o);
+                    if (~used) c = wb + __ffs(~used) - 1;
+                }
+                if (lane == 0) col[v] = c;
+            }
+            __syncthreads();
+        }
+        cnt = *ocnt;
+        r++;
+        __syncthreads();
+        if (threadIdx.x == 0) s_cnt[cur] = 0;   // the list just consumed is the next output
+        cur ^= 1;
+        __syncthreads();
+    }
+    for (int v = threadIdx.x; v < n; v += blockDim.x) color[v] = col[v];
+    if (threadIdx.x == 0) {
+        rounds_out[0] = cnt == 0 ? r : -1;
+        rounds_out[1] = s_err;
+    }
+}
+
 // The colouring of a level runs on the handle's second stream, overlapped with
 // the matching / Galerkin chain of the coarser levels on the main stream; its
 // colour count is read back only when the level's layout is built.
@@ -1962,11 +2111,22 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
         int *pcol = color.as<int>(), *pin = job.indeg.as<int>(), *pa = job.la.as<int>(), *pb = job.lb.as<int>(),
             *pc = job.counts.as<int>(), *pr = job.counts.as<int>() + kMaxRounds;
         void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr};
-        RoundTrace tr(st, "colour");
-        // half the co-resident grid: the other half stays free for the coarsening
-        // chain running concurrently on the main stream
-        DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridDiv));
-        tr.report(job.counts.as<int>());
+        if (n <= kSmallColourN && avg >= kSmallColourMinDeg) {
+            static bool attr = false;
+            if (!attr) {
+                FDL_CK(cudaFuncSetAttribute(k_color_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            16 * kSmallColourN));
+                attr = true;
+            }
+            k_color_small<<<1, kSmallColourThreads, (size_t)16 * n, st>>>(n, rp, ci, salt, pcol, pr);
+            FDL_LAUNCH_CK();
+        } else {
+            RoundTrace tr(st, "colour");
+            // half the co-resident grid: the other half stays free for the coarsening
+            // chain running concurrently on the main stream
+            DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridDiv));
+            tr.report(job.counts.as<int>());
+        }
     }
     job.mx.alloc(4, st);
     reduce_max_i32(color.as<int>(), n, job.mx.as<int>(), st);

@@ -64,6 +64,9 @@ SMALL = {
     "path100": lambda: gg.path(100),
     "star40": lambda: gg.star(40),
     "complete30": lambda: gg.complete(30),
+    # dense small levels (average degree >= 64): the single-CTA colouring
+    "complete100": lambda: gg.complete(100),
+    "dense1500_deg120": lambda: gg.random_connected(1500, 90000, 21),
     "hub3000_3hubs": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
     "clique70_tail2000": lambda: clique_with_tail(70, 2000),
     "tiny_p5": lambda: gg.path(5),
