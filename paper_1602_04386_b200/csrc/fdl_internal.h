@@ -83,6 +83,9 @@ struct Level {
     std::vector<int> seg;    // [ncolors + 1] GS row range of every colour
     DBuf seg_d;              // device copy of seg
     int gs_tail_c0 = 0;      // colours [gs_tail_c0, ncolors) run in one single-CTA launch
+    std::vector<int> gs_runs;  // GS schedule of one sweep: (c_begin, c_end, kind) triplets,
+                               // kind 0 = grid tile pass of one colour, 1 = cluster run,
+                               // 2 = single-CTA tail
     DistPlan dist;
     int ncolors = 0;
     int ntiles = 0;

@@ -2348,6 +2348,22 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
                (long long)segnnz[ncolors] - segnnz[c0 - 1] <= 16LL * kGsTailRows)
             c0--;
         L.gs_tail_c0 = c0;
+        // colours before the tail: a grid-wide tile pass each, except runs of
+        // small colours (<= kClusterColourRows rows), one cluster launch per run
+        constexpr int kClusterColourRows = 16384;
+        L.gs_runs.clear();
+        for (int c = 0; c < c0;) {
+            int e = c;
+            while (e < c0 && seg[e + 1] - seg[e] <= kClusterColourRows) e++;
+            if (e > c) {
+                L.gs_runs.insert(L.gs_runs.end(), {c, e, 1});
+                c = e;
+            } else {
+                L.gs_runs.insert(L.gs_runs.end(), {c, c + 1, 0});
+                c++;
+            }
+        }
+        if (c0 < ncolors) L.gs_runs.insert(L.gs_runs.end(), {c0, ncolors, 2});
     }
     L.ctile.assign(ncolors + 1, 0);
     int nt = 0;

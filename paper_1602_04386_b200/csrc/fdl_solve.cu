@@ -473,62 +473,127 @@ __device__ __forceinline__ void cta_sum2(double &a, double &b, double (*sm)[2]) 
     __syncthreads();
 }
 
-// GS colours [c0, ncolors) of `sweeps` sweeps (GS layout, x in place), one CTA:
-// short rows thread per row, long rows a warp each; a barrier between colours.
-// stat_mode as for the tile pass (statistics of the rows handled here).
-__global__ void __launch_bounds__(kCtaThreads) k_gs_tail(CsrView L, const int *__restrict__ seg, int c0,
-                                                         int ncolors, int sweeps, double *x, double *slot,
+// GS colours [c0, c1) of `sweeps` sweeps (GS layout, x in place) by ONE
+// thread-block cluster (CLUSTER) or ONE CTA: the many small colours of dense
+// levels and the small trailing colours, where a grid-wide launch per colour
+// would be launch-bound.  Row r of a colour belongs to CTA (r - a) mod |cluster|; rows
+// <= kShortMax entries a thread each, <= kGcLong a warp each, longer the CTA;
+// every row keeps 8 loads per thread in flight.  A cluster barrier (release /
+// acquire at cluster scope) separates the colours; x is read through L2
+// (__ldcg) because other CTAs of the cluster rewrite it.  Statistics of the
+// last sweep: one pass over the rows in a fixed order, reduced over the
+// cluster in rank order (deterministic).
+constexpr int kGcThreads = 512;
+constexpr int kGcWarps = kGcThreads / 32;
+constexpr int kGcLong = 2048;
+constexpr int kGcMaxCluster = 16;
+
+__device__ __forceinline__ void gc_row_part(const CsrView &L, const double *x, int kb, int ke, int step,
+                                            double &num, double &den) {
+    for (int k0 = kb; k0 < ke; k0 += 8 * step) {
+        int c8[8];
+        double w8[8], x8[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int k = k0 + i * step;
+            c8[i] = k < ke ? __ldg(L.ci + k) : -1;
+            w8[i] = k < ke ? __ldg(L.w + k) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) x8[i] = c8[i] >= 0 ? __ldcg(x + c8[i]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            num = fma(w8[i], x8[i], num);
+            den += w8[i];
+        }
+    }
+}
+
+template <bool CLUSTER>
+__global__ void __launch_bounds__(kGcThreads) k_gs_multi(CsrView L, const int *__restrict__ seg, int c0,
+                                                         int c1, int sweeps, double *x, double *slot,
                                                          int stat_mode, int n) {
-    __shared__ double sm[kCtaWarps][2];
+    const int cr = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
+    const int ncl = CLUSTER ? (int)cg::this_cluster().num_blocks() : 1;
     const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    constexpr int kMedCap = 1024, kLongCap = 64;
+    __shared__ double sm[kGcWarps][2];
+    __shared__ double s_part[kGcMaxCluster][2];
+    __shared__ int s_med[kMedCap], s_long[kLongCap];
+    __shared__ int s_nmed, s_nlong;
     double S = 0.0, Q = 0.0;
+    auto finish_row = [&](int r, double num, double den, bool) { x[r] = num / den; };
     for (int s = 0; s < sweeps; s++) {
         const bool last = s == sweeps - 1;
-        for (int c = c0; c < ncolors; c++) {
-            const int a = seg[c], b = seg[c + 1];
-            int has_long = 0;
-            for (int r = a + tid; r < b; r += kCtaThreads) {
+        for (int c = c0; c < c1; c++) {
+            const int a = seg[c] + cr, b = seg[c + 1];   // this CTA: rows a, a + ncl, ...
+            if (tid == 0) { s_nmed = 0; s_nlong = 0; }
+            __syncthreads();
+            // short rows here; longer ones listed for the warp / CTA passes
+            for (int r = a + tid * ncl; r < b; r += kGcThreads * ncl) {
                 const int kb = L.rp[r], ke = L.rp[r + 1];
-                if (ke - kb > kShortMax) { has_long = 1; continue; }
+                if (ke - kb > kGcLong) { const int i = atomicAdd(&s_nlong, 1); if (i < kLongCap) s_long[i] = r; continue; }
+                if (ke - kb > kShortMax) { const int i = atomicAdd(&s_nmed, 1); if (i < kMedCap) s_med[i] = r; continue; }
                 double num = 0.0, den = 0.0;
-                for (int k = kb; k < ke; k++) {
-                    const double wk = L.w[k];
-                    num = fma(wk, x[L.ci[k]], num);
-                    den += wk;
-                }
-                const double xn = num / den;
-                x[r] = xn;
-                if (last) { S += xn; Q = fma(xn, xn, Q); }
+                gc_row_part(L, x, kb, ke, 1, num, den);
+                finish_row(r, num, den, last);
             }
-            if (__syncthreads_or(has_long)) {
-                for (int r = a + warp; r < b; r += kCtaWarps) {
-                    const int kb = L.rp[r], ke = L.rp[r + 1];
-                    if (ke - kb <= kShortMax) continue;
-                    double num = 0.0, den = 0.0;
-                    for (int k = kb + lane; k < ke; k += 32) {
-                        const double wk = L.w[k];
-                        num = fma(wk, x[L.ci[k]], num);
-                        den += wk;
-                    }
+            __syncthreads();
+            const int nmed = s_nmed, nlong = s_nlong;
+            // warp rows (from the list; a full list: every row of the share rescanned)
+            const bool medlist = nmed <= kMedCap;
+            for (int i = warp; medlist ? i < nmed : a + i * ncl < b; i += kGcWarps) {
+                const int r = medlist ? s_med[i] : a + i * ncl;
+                const int kb = L.rp[r], ke = L.rp[r + 1];
+                if (ke - kb <= kShortMax || ke - kb > kGcLong) continue;
+                double num = 0.0, den = 0.0;
+                gc_row_part(L, x, kb + lane, ke, 32, num, den);
 #pragma unroll
-                    for (int o = 16; o; o >>= 1) {
-                        num += __shfl_xor_sync(0xffffffffu, num, o);
-                        den += __shfl_xor_sync(0xffffffffu, den, o);
-                    }
-                    const double xn = num / den;
-                    if (lane == 0) {
-                        x[r] = xn;
-                        if (last) { S += xn; Q = fma(xn, xn, Q); }
-                    }
+                for (int o = 16; o; o >>= 1) {
+                    num += __shfl_xor_sync(0xffffffffu, num, o);
+                    den += __shfl_xor_sync(0xffffffffu, den, o);
                 }
+                if (lane == 0) finish_row(r, num, den, last);
             }
-            __syncthreads();   // colour c complete before colour c+1 reads it
+            // CTA rows (uniform loop over the list, or over the share when it overflowed)
+            const bool longlist = nlong <= kLongCap;
+            for (int i = 0; longlist ? i < nlong : a + i * ncl < b; i++) {
+                const int r = longlist ? s_long[i] : a + i * ncl;
+                const int kb = L.rp[r], ke = L.rp[r + 1];
+                if (ke - kb <= kGcLong) continue;
+                double num = 0.0, den = 0.0;
+                gc_row_part(L, x, kb + tid, ke, kGcThreads, num, den);
+                cta_sum2(num, den, sm);
+                if (tid == 0) finish_row(r, num, den, last);
+            }
+            // colour c complete (cluster- / CTA-wide) before colour c+1 reads it
+            if (CLUSTER) cg::this_cluster().sync();
+            else __syncthreads();
         }
     }
     if (!(stat_mode & 4)) return;
+    // statistics of the rows of these colours, in a fixed row -> thread map (the
+    // lists above are filled in atomic order)
+    for (int r = seg[c0] + cr * kGcThreads + tid; r < seg[c1]; r += ncl * kGcThreads) {
+        const double xr = __ldcg(x + r);
+        S += xr;
+        Q = fma(xr, xr, Q);
+    }
     cta_sum2(S, Q, sm);
-    if (tid == 0) {
-        const double tot[kNumStats] = {S, Q, 0.0};
+    if (CLUSTER) {
+        if (tid == 0) {
+            double *dst = cg::this_cluster().map_shared_rank(&s_part[0][0], 0);
+            dst[2 * cr] = S;
+            dst[2 * cr + 1] = Q;
+        }
+        cg::this_cluster().sync();
+    } else if (tid == 0) {
+        s_part[0][0] = S;
+        s_part[0][1] = Q;
+    }
+    if (cr == 0 && tid == 0) {
+        double tot[kNumStats] = {0.0, 0.0, 0.0};
+        for (int i = 0; i < ncl; i++) { tot[0] += s_part[i][0]; tot[1] += s_part[i][1]; }
         finish_stats(tot, slot, stat_mode, n);
     }
 }
@@ -675,8 +740,46 @@ __global__ void k_normalise(int n, double *z, const double *slot) {
 constexpr size_t kPassSmemBytes = sizeof(PassSmem);
 
 constexpr int kSmallPiRows = 4096;   // levels this small run all power steps in one CTA
+constexpr int kSmallPiNnz = 1 << 18;  // ... unless dense: one CTA streams ~0.1 TB/s
 
 // CTAs of a pass: resident CTAs per SM x SMs (persistent tile loop), per OP
+// one cluster (16 CTAs where the device allows, else 8) for k_gs_multi<true>
+static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0, int c1, int sweeps, double *x,
+                              double *slot, int mode, int n) {
+    static int cl = 0;
+    if (!cl) {
+        cl = 8;
+        if (cudaFuncSetAttribute(k_gs_multi<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(kGcMaxCluster);
+            q.blockDim = dim3(kGcThreads);
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = kGcMaxCluster;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, k_gs_multi<true>, &q) == cudaSuccess && nclusters > 0)
+                cl = kGcMaxCluster;
+        }
+        (void)cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(kGcThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FDL_CK(cudaLaunchKernelEx(&cfg, k_gs_multi<true>, v, seg, c0, c1, sweeps, x, slot, mode, n));
+}
+
 static int g_pass_grid[4] = {0, 0, 0, 0};
 static int pass_grid(int op) { return g_pass_grid[op]; }
 
@@ -709,35 +812,42 @@ struct Enq {
     void pass(const Level &L, int tb, int te, PassArgs a) {
         pass_tiles<OP>(L, L.tiles.as<Tile>() + tb, te - tb, a);
     }
-    // Colours [0, c0) as grid-wide tile passes, the small trailing colours
-    // [c0, ncolors) (<= kTailRows rows together) in one single-CTA launch per sweep;
-    // a small level (c0 == 0) does all its sweeps in one launch.
-    void gs(const Level &L, double *x, int sweeps, double *out_slot) {
-        if (sweeps <= 0) return;
-        const int c0 = L.gs_tail_c0;
+    // One sweep = the level's GS schedule (L.gs_runs): grid-wide tile passes for
+    // big colours, one cluster launch per run of small colours, one single-CTA
+    // launch for the small trailing colours; a level that is one run does all
+    // its sweeps in one launch.  Statistics of the last sweep go to out_slot.
+    void gs_run(const Level &L, int cb, int ce, int kind, double *x, int sweeps, double *out_slot, int mode) {
         CsrView v{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()};
-        if (c0 == 0) {
-            k_gs_tail<<<1, kCtaThreads, 0, st>>>(v, L.seg_d.as<int>(), 0, L.ncolors, sweeps, x, out_slot,
-                                                 out_slot ? (4 | 1 | 2) : 0, L.n);
+        if (kind == 0) {
+            PassArgs a{};
+            a.x = x;
+            a.n = L.n;
+            a.out_stat = out_slot;
+            a.stat_mode = mode;
+            pass<OP_GS>(L, L.ctile[cb], L.ctile[cb + 1], a);
+        } else if (kind == 1) {
+            launch_gs_cluster(st, v, L.seg_d.as<int>(), cb, ce, sweeps, x, out_slot, mode, L.n);
+            launches++;
+        } else {
+            k_gs_multi<false><<<1, kGcThreads, 0, st>>>(v, L.seg_d.as<int>(), cb, ce, sweeps, x, out_slot, mode,
+                                                        L.n);
             FDL_LAUNCH_CK();
             launches++;
+        }
+    }
+    void gs(const Level &L, double *x, int sweeps, double *out_slot) {
+        if (sweeps <= 0) return;
+        const int nr = (int)L.gs_runs.size() / 3;
+        const int *R = L.gs_runs.data();
+        if (nr == 1 && R[2] != 0) {
+            gs_run(L, R[0], R[1], R[2], x, sweeps, out_slot, out_slot ? (4 | 1 | 2) : 0);
             return;
         }
         for (int s = 0; s < sweeps; s++) {
             const bool want = (s == sweeps - 1) && out_slot;
-            for (int c = 0; c < c0; c++) {
-                PassArgs a{};
-                a.x = x;
-                a.n = L.n;
-                a.out_stat = out_slot;
-                a.stat_mode = want ? (4 | (c == 0 ? 1 : 0) | (c0 == L.ncolors && c == c0 - 1 ? 2 : 0)) : 0;
-                pass<OP_GS>(L, L.ctile[c], L.ctile[c + 1], a);
-            }
-            if (c0 < L.ncolors) {
-                k_gs_tail<<<1, kCtaThreads, 0, st>>>(v, L.seg_d.as<int>(), c0, L.ncolors, 1, x, out_slot,
-                                                     want ? (4 | 2) : 0, L.n);
-                FDL_LAUNCH_CK();
-                launches++;
+            for (int i = 0; i < nr; i++) {
+                const int mode = want ? (4 | (i == 0 ? 1 : 0) | (i == nr - 1 ? 2 : 0)) : 0;
+                gs_run(L, R[3 * i], R[3 * i + 1], R[3 * i + 2], x, 1, out_slot, mode);
             }
         }
     }
@@ -745,7 +855,7 @@ struct Enq {
     void pi_iters(const Level &L, double *&cur, double *&oth, double *&cur_slot, int iters,
                   double *(*next_slot)(void *), void *ctx) {
         if (iters <= 0) return;
-        if (L.n <= kSmallPiRows) {
+        if (L.n <= kSmallPiRows && L.nnz <= kSmallPiNnz) {
             double *ns = next_slot(ctx);
             CsrView v{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
             k_pi_small<<<1, kCtaThreads, 0, st>>>(v, L.shift, iters, cur, oth, cur_slot, ns);
