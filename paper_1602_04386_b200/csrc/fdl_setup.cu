@@ -2261,6 +2261,24 @@ __global__ void k_make_tiles(const int *rp, int s0, int s1, int ntiles, Tile *ou
     }
 }
 
+// the GS tiles of every colour in one launch: tile t belongs to the colour c
+// with ctile[c] <= t < ctile[c + 1] (binary search), then as k_make_tiles
+__global__ void k_make_tiles_colours(const int *rp, const int *seg, const int *ctile, int ncolors, Tile *out) {
+    const int nt = ctile[ncolors];
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+        int lo = 0, hi = ncolors - 1;   // last c with ctile[c] <= t
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (ctile[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        const int c = lo, s0 = seg[c], s1 = seg[c + 1], tl = t - ctile[c], ntc = ctile[c + 1] - ctile[c];
+        const long long C0 = (long long)rp[s0] + s0;
+        const int a = tl == 0 ? s0 : lower_bound_coord(rp, s0, s1, C0 + (long long)tl * kTileT);
+        const int b = (tl + 1 == ntc) ? s1 : lower_bound_coord(rp, s0, s1, C0 + (long long)(tl + 1) * kTileT);
+        out[t] = make_int2(a, b);
+    }
+}
+
 static int tiles_for(long long coord_span) { return std::max(1, (int)((coord_span + kTileT - 1) / kTileT)); }
 
 static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &L,
@@ -2381,12 +2399,11 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     L.ctile_d.alloc((size_t)(ncolors + 1) * 4, st);
     FDL_CK(cudaMemcpyAsync(L.ctile_d.p, L.ctile.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
     L.tiles.alloc((size_t)nt * sizeof(Tile), st);
-    for (int c = 0; c < ncolors; c++)
-        if (cnt[c]) {
-            k_make_tiles<<<grid_for(cnt[c]), 256, 0, st>>>(L.rp.as<int>(), seg[c], seg[c + 1], cnt[c],
-                                                           L.tiles.as<Tile>() + L.ctile[c]);
-            FDL_LAUNCH_CK();
-        }
+    if (L.ctile[ncolors] > 0) {
+        k_make_tiles_colours<<<grid_for(L.ctile[ncolors]), 256, 0, st>>>(
+            L.rp.as<int>(), L.seg_d.as<int>(), L.ctile_d.as<int>(), ncolors, L.tiles.as<Tile>());
+        FDL_LAUNCH_CK();
+    }
     k_make_tiles<<<grid_for(cnt[ncolors]), 256, 0, st>>>(L.rpN.as<int>(), 0, n, cnt[ncolors],
                                                          L.tiles.as<Tile>() + L.ctile[ncolors]);
     FDL_LAUNCH_CK();
