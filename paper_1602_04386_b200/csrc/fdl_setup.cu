@@ -171,6 +171,12 @@ constexpr int kMaxRounds = 1 << 16;
 #define FDL_MATCH_UNROLL 4
 #endif
 constexpr int kMatchUnroll = FDL_MATCH_UNROLL;
+// the matching and the colouring (second stream) are both cooperative: each
+// takes part of the co-resident grid so that they can run side by side
+#ifndef FDL_MATCH_GRID_DIV
+#define FDL_MATCH_GRID_DIV 2
+#endif
+constexpr int kMatchGridDiv = FDL_MATCH_GRID_DIV;
 static_assert(kAppendCap >= 2 * kMatchUnroll * kCoopThreads, "append buffer too small");   // JP depth can reach thousands on dense cores
 
 // FIEDLER_TRACE: per-phase device timestamps of the cooperative kernels
@@ -575,7 +581,7 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
             *pr = counts.as<int>() + kMaxRounds;
         void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr};
         RoundTrace tr(st, "match");
-        DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st));
+        DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st, kMatchGridDiv));
         tr.report(counts.as<int>());
     }
     rounds = read_int(counts.as<int>() + kMaxRounds, st);
@@ -2088,7 +2094,7 @@ __global__ void __launch_bounds__(kSmallColourThreads, 1) k_color_small(int n, c
 // the matching / Galerkin chain of the coarser levels on the main stream; its
 // colour count is read back only when the level's layout is built.
 #ifndef FDL_COLOUR_GRID_DIV
-#define FDL_COLOUR_GRID_DIV 2
+#define FDL_COLOUR_GRID_DIV 3
 #endif
 constexpr int kColourGridDiv = FDL_COLOUR_GRID_DIV;
 
@@ -2122,8 +2128,10 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             FDL_LAUNCH_CK();
         } else {
             RoundTrace tr(st, "colour");
-            // half the co-resident grid: the other half stays free for the coarsening
-            // chain running concurrently on the main stream
+            // a third of the co-resident grid, the matching (main stream) half:
+            // both cooperative kernels fit side by side with room for the rest
+            // of the coarsening chain (a full-grid cooperative launch would wait
+            // for the other one to drain)
             DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridDiv));
             tr.report(job.counts.as<int>());
         }
