@@ -2090,6 +2090,170 @@ __global__ void __launch_bounds__(kSmallColourThreads, 1) k_color_small(int n, c
     }
 }
 
+// Mid-size dense levels (n <= kClusterColourN, average degree >= 64): the same
+// topological JP by ONE cluster of kColourCluster CTAs.  Vertex v lives in CTA
+// v mod C (local slot v / C): its colour, in-degree and list entries sit in that
+// CTA's shared memory and the other CTAs reach them through distributed shared
+// memory (loads, atomics on the in-degree and the owner's next-list counter).
+// Each CTA works its own list as k_color_small does; cluster barriers separate
+// the rounds.
+constexpr int kColourCluster = 16;
+constexpr int kClusterColourLocal = 12288;   // vertices per CTA (16 bytes each in smem)
+constexpr int kClusterColourN = kColourCluster * kClusterColourLocal;
+__global__ void __launch_bounds__(kSmallColourThreads, 1) k_color_cluster(int n, const int *rp, const int *ci,
+                                                                            uint64_t salt, int *color,
+                                                                            int *rounds_out) {
+    cg::cluster_group clu = cg::this_cluster();
+    const int cr = (int)clu.block_rank();
+    constexpr int C = kColourCluster;
+    const int nloc = (n + C - 1) / C;
+    extern __shared__ int sm_cc[];
+    int *col = sm_cc, *indeg = sm_cc + nloc, *la = sm_cc + 2 * nloc, *lb = sm_cc + 3 * nloc;
+    __shared__ unsigned bm[kSmallChunk][kBmWords];
+    __shared__ int s_off[kSmallChunk + 1], s_b[kSmallChunk], s_v[kSmallChunk];
+    __shared__ unsigned long long s_pv[kSmallChunk];
+    __shared__ int s_cnt[2], s_err, s_total;
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    constexpr int nwarps = kSmallColourThreads / 32;
+    if (threadIdx.x == 0) { s_cnt[0] = 0; s_cnt[1] = 0; s_err = 0; }
+    __syncthreads();
+    // in-degrees of the own vertices v = cr + C * i
+    for (int i = warp; i < nloc; i += nwarps) {
+        const int v = cr + C * i;
+        if (v >= n) break;
+        const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+        const int b = rp[v], e = rp[v + 1];
+        int c = 0;
+        for (int k0 = b; k0 < e; k0 += 256) {
+            int u8[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) u8[q] = k0 + q * 32 + lane < e ? ci[k0 + q * 32 + lane] : -1;
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                c += u8[q] >= 0 && higher_prio(splitmix64(salt ^ (uint64_t)u8[q]), u8[q], pv, v);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) {
+            indeg[i] = c;
+            col[i] = -1;
+            if (c == 0) la[atomicAdd(&s_cnt[0], 1)] = v;
+        }
+    }
+    clu.sync();
+    int cur = 0, r = 0;
+    int total = 0;
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int q = 0; q < C; q++) t += clu.map_shared_rank(&s_cnt[0], q)[0];
+        s_total = t;
+    }
+    __syncthreads();
+    total = s_total;
+    while (total > 0 && r + 1 < kMaxRounds) {
+        const int *in = cur ? lb : la;
+        const int cnt = s_cnt[cur];
+        for (int c0 = 0; c0 < cnt; c0 += kSmallChunk) {
+            const int m = min(kSmallChunk, cnt - c0);
+            if (warp == 0) {
+                int carry = 0;
+                for (int t0 = 0; t0 < m; t0 += 32) {
+                    const int t = t0 + lane;
+                    int d = 0;
+                    if (t < m) {
+                        const int v = in[c0 + t];
+                        const int b = rp[v];
+                        d = rp[v + 1] - b;
+                        s_v[t] = v;
+                        s_b[t] = b;
+                        s_pv[t] = splitmix64(salt ^ (uint64_t)v);
+                    }
+                    int x = d;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (t < m) s_off[t] = carry + x - d;
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (lane == 0) s_off[m] = carry;
+            }
+            for (int t = threadIdx.x; t < m * kBmWords; t += blockDim.x) bm[t / kBmWords][t % kBmWords] = 0u;
+            __syncthreads();
+            const int E = s_off[m];
+            for (int e0 = threadIdx.x; e0 < E; e0 += 8 * kSmallColourThreads) {
+                int idx[8], u8[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int e = e0 + q * kSmallColourThreads;
+                    int lo = 0, hi = m - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (s_off[mid] <= e) lo = mid; else hi = mid - 1;
+                    }
+                    idx[q] = e < E ? lo : -1;
+                    u8[q] = e < E ? ci[s_b[lo] + e - s_off[lo]] : 0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    if (idx[q] < 0) continue;
+                    const int u = u8[q], t = idx[q];
+                    const int ow = u % C, ul = u / C;
+                    if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, s_pv[t], s_v[t])) {
+                        const int cu = clu.map_shared_rank(col, ow)[ul];
+                        if (cu < 0) s_err = 1;   // impossible: uncoloured predecessor
+                        else if (cu < 32 * kBmWords) atomicOr(&bm[t][cu >> 5], 1u << (cu & 31));
+                    } else if (atomicSub(clu.map_shared_rank(indeg, ow) + ul, 1) == 1) {
+                        int *ocnt = clu.map_shared_rank(&s_cnt[cur ^ 1], ow);
+                        int *olist = clu.map_shared_rank(cur ? la : lb, ow);
+                        olist[atomicAdd(ocnt, 1)] = u;
+                    }
+                }
+            }
+            __syncthreads();
+            for (int t = warp; t < m; t += nwarps) {
+                const int v = s_v[t];
+                int c = 0x7fffffff;
+                for (int q = lane; q < kBmWords; q += 32)
+                    if (~bm[t][q]) c = min(c, q * 32 + __ffs(~bm[t][q]) - 1);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) c = min(c, __shfl_xor_sync(0xffffffffu, c, o));
+                const int b = s_b[t], e = b + s_off[t + 1] - s_off[t];
+                for (int wb = 32 * kBmWords; c == 0x7fffffff; wb += 32) {   // rare: > 2048 colours
+                    unsigned used = 0u;
+                    for (int k = b + lane; k < e; k += 32) {
+                        const int u = ci[k];
+                        if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, s_pv[t], v)) continue;
+                        const int cu = clu.map_shared_rank(col, u % C)[u / C] - wb;
+                        if (cu >= 0 && cu < 32) used |= 1u << cu;
+                    }
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) used |= __shfl_xor_sync(0xffffffffu, used, o);
+                    if (~used) c = wb + __ffs(~used) - 1;
+                }
+                if (lane == 0) col[v / C] = c;
+            }
+            __syncthreads();
+        }
+        clu.sync();   // every push of the round landed; colours of the round final
+        r++;
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int q = 0; q < C; q++) t += clu.map_shared_rank(&s_cnt[cur ^ 1], q)[0];
+            s_total = t;
+            s_cnt[cur] = 0;   // the list just consumed is the next round's output
+        }
+        clu.sync();   // counters reset everywhere before the next round pushes
+        total = s_total;
+        cur ^= 1;
+    }
+    for (int i = threadIdx.x; i < nloc; i += blockDim.x)
+        if (cr + C * i < n) color[cr + C * i] = col[i];
+    if (s_err) atomicOr(rounds_out + 1, 1);
+    if (cr == 0 && threadIdx.x == 0) rounds_out[0] = total == 0 ? r : -1;
+}
+
 // The colouring of a level runs on the handle's second stream, overlapped with
 // the matching / Galerkin chain of the coarser levels on the main stream; its
 // colour count is read back only when the level's layout is built.
@@ -2101,6 +2265,35 @@ constexpr int kColourGridDiv = FDL_COLOUR_GRID_DIV;
 struct ColourJob {
     DBuf la, lb, indeg, counts, mx;
 };
+
+// whether a 16-CTA cluster of k_color_cluster (1024 threads, ~210 KB shared
+// memory each) can be resident on this device
+static bool cluster_colour_ok() {
+    static int ok = -1;
+    if (ok < 0) {
+        ok = 0;
+        if (cudaFuncSetAttribute(k_color_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                cudaSuccess &&
+            cudaFuncSetAttribute(k_color_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 16 * kClusterColourLocal) == cudaSuccess) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(kColourCluster);
+            q.blockDim = dim3(kSmallColourThreads);
+            q.dynamicSmemBytes = (size_t)16 * kClusterColourLocal;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = kColourCluster;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nc = 0;
+            ok = cudaOccupancyMaxActiveClusters(&nc, k_color_cluster, &q) == cudaSuccess && nc > 0;
+        }
+        (void)cudaGetLastError();
+    }
+    return ok > 0;
+}
 
 static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJob &job, cudaStream_t st) {
     int n = g.n;
@@ -2126,6 +2319,21 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             }
             k_color_small<<<1, kSmallColourThreads, (size_t)16 * n, st>>>(n, rp, ci, salt, pcol, pr);
             FDL_LAUNCH_CK();
+        } else if (n <= kClusterColourN && avg >= kSmallColourMinDeg && cluster_colour_ok()) {
+            const int nloc = (n + kColourCluster - 1) / kColourCluster;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(kColourCluster);
+            cfg.blockDim = dim3(kSmallColourThreads);
+            cfg.dynamicSmemBytes = (size_t)16 * nloc;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = kColourCluster;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            FDL_CK(cudaLaunchKernelEx(&cfg, k_color_cluster, n, rp, ci, salt, pcol, pr));
         } else {
             RoundTrace tr(st, "colour");
             // a third of the co-resident grid, the matching (main stream) half:

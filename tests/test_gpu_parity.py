@@ -67,6 +67,8 @@ SMALL = {
     # dense small levels (average degree >= 64): the single-CTA colouring
     "complete100": lambda: gg.complete(100),
     "dense1500_deg120": lambda: gg.random_connected(1500, 90000, 21),
+    # mid-size dense level (n > 12288, average degree >= 64): the cluster colouring
+    "dense16k_deg70": lambda: gg.random_connected(16000, 560000, 22),
     "hub3000_3hubs": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
     "clique70_tail2000": lambda: clique_with_tail(70, 2000),
     "tiny_p5": lambda: gg.path(5),
