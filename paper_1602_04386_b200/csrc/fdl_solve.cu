@@ -258,6 +258,28 @@ __device__ __forceinline__ double ldx(const double *p) {
     return COHERENT ? __ldcg(p) : __ldg(p);
 }
 
+// entries kb, kb + step, ... < ke of a row (global memory) into acc, in that
+// order, 8 per thread with their loads and gathers in flight together
+template <int OP, bool COHERENT>
+__device__ __forceinline__ void acc_range(RowAcc<OP> &acc, const CsrView &L, const double *x, int kb, int ke,
+                                          int step) {
+    for (int k0 = kb; k0 < ke; k0 += 8 * step) {
+        int c8[8];
+        double w8[8], x8[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int k = k0 + i * step;
+            c8[i] = k < ke ? __ldcs(L.ci + k) : -1;
+            w8[i] = k < ke ? __ldcs(L.w + k) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) x8[i] = c8[i] >= 0 ? ldx<COHERENT>(x + c8[i]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (c8[i] >= 0) acc.add(w8[i], x8[i]);
+    }
+}
+
 // one thread stages the column/weight streams of tile t into stage b
 __device__ __forceinline__ void issue_tile(PassSmem &S, const CsrView &L, Tile t, int b,
                                            unsigned long long pol) {
@@ -275,12 +297,58 @@ __device__ __forceinline__ void issue_tile(PassSmem &S, const CsrView &L, Tile t
     }
 }
 
+// Short rows (<= kShortMax) of a tile with few rows: a sub-warp of W lanes per
+// row, lane l taking entries l, l + W, ... from shared memory (all its gathers
+// in flight), then a shuffle reduction; returns whether the tile has long rows.
+template <int OP, int W, bool COHERENT>
+__device__ __forceinline__ int subwarp_rows(const Tile t, const int *__restrict__ sci,
+                                            const double *__restrict__ sw, const CsrView &L,
+                                            const PassArgs &a, const Scal &sc, double st[kNumStats]) {
+    const int sl = threadIdx.x & (W - 1);
+    const double *__restrict__ x = a.x;
+    int has_long = 0;
+    for (int r = t.x + (int)threadIdx.x / W; r - (int)(threadIdx.x & 31) / W < t.y;
+         r += kPassThreads / W) {
+        // (loop bound per warp: all lanes of a warp iterate together for the shuffles)
+        const bool live = r < t.y;
+        int kb = 0, ke = 0;
+        if (live) { kb = L.rp[r]; ke = L.rp[r + 1]; }
+        const bool sh = live && ke - kb <= kShortMax;
+        if (live && !sh) has_long = 1;
+        RowAcc<OP> acc;
+        if (OP != OP_GS && sh) acc.own = own_of<OP>(r, a);
+        const int n = sh ? ke - kb : 0;
+        for (int j0 = 0; j0 < n; j0 += 4 * W) {   // 4 entries per lane per step
+            int c[4];
+            double wv[4], xv[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int j = j0 + sl + i * W;
+                c[i] = j < n ? sci[kb + j] : 0;
+                wv[i] = j < n ? sw[kb + j] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; i++) xv[i] = (j0 + sl + i * W < n) ? ldx<COHERENT>(x + c[i]) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                if (j0 + sl + i * W < n) acc.add(wv[i], xv[i]);
+        }
+#pragma unroll
+        for (int o = W / 2; o; o >>= 1) {
+            acc.a += __shfl_xor_sync(0xffffffffu, acc.a, o, W);
+            if (OP != OP_PI) acc.b += __shfl_xor_sync(0xffffffffu, acc.b, o, W);
+        }
+        if (sh && sl == 0) row_finish<OP>(r, acc, a, sc, st);
+    }
+    return has_long;
+}
+
 // Reduce the rows of tile t, whose streams land in stage b (mbarrier phase `phase`).
 // Rows <= 32 nonzeros: thread per row from shared memory, two rows per thread with
 // their gathers in flight together; longer rows: a warp each (round robin over the
 // warps) from global memory; a row longer than a tile (necessarily the tile's last)
 // gets the whole CTA.  Ends with a __syncthreads (stage b may then be refilled).
-template <int OP, int CH, bool COHERENT>
+template <int OP, int CH, bool COHERENT, int SW>
 __device__ __forceinline__ void tile_compute(const Tile t, PassSmem &S, int b, unsigned phase,
                                              RowAcc<OP> *s_red, const CsrView &L, const PassArgs &a,
                                              const Scal &sc, double st[kNumStats]) {
@@ -307,9 +375,16 @@ __device__ __forceinline__ void tile_compute(const Tile t, PassSmem &S, int b, u
             if (OP != OP_GS) own1 = own_of<OP>(rr1, a);
         }
     };
-    fetch(r0);   // the first pair's offsets / own values are in flight during the wait
-    mbar_wait(&S.bar[b], phase);
     int has_long = 0;
+    if constexpr (SW > 0) {
+        // dense level: a sub-warp of SW lanes per short row instead
+        mbar_wait(&S.bar[b], phase);
+        has_long = subwarp_rows<OP, SW, COHERENT>(t, sci, sw, L, a, sc, st);
+        r0 = t.y;   // the pair loop below has nothing left
+    } else {
+        fetch(r0);   // the first pair's offsets / own values are in flight during the wait
+        mbar_wait(&S.bar[b], phase);
+    }
     for (; r0 < t.y; r0 += 2 * kPassThreads) {
         if (r0 != t.x + tid) fetch(r0);
         const int r1 = r0 + kPassThreads;
@@ -358,8 +433,7 @@ __device__ __forceinline__ void tile_compute(const Tile t, PassSmem &S, int b, u
             if (ke - kb <= kShortMax || (cta_last && row == last)) continue;   // warp-uniform
             RowAcc<OP> acc;
             if (OP != OP_GS) acc.own = own_of<OP>(row, a);
-            for (int k = kb + lane; k < ke; k += 32)
-                acc.add(__ldcs(L.w + k), ldx<COHERENT>(x + __ldcs(L.ci + k)));
+            acc_range<OP, COHERENT>(acc, L, x, kb + lane, ke, 32);
             acc.warp_sum();
             if (lane == 0) row_finish<OP>(row, acc, a, sc, st);
         }
@@ -367,8 +441,7 @@ __device__ __forceinline__ void tile_compute(const Tile t, PassSmem &S, int b, u
             const int kb = L.rp[last], ke = L.rp[t.y];
             RowAcc<OP> acc;
             if (OP != OP_GS) acc.own = own_of<OP>(last, a);
-            for (int k = kb + tid; k < ke; k += kPassThreads)
-                acc.add(__ldcs(L.w + k), ldx<COHERENT>(x + __ldcs(L.ci + k)));
+            acc_range<OP, COHERENT>(acc, L, x, kb + tid, ke, kPassThreads);
             acc.warp_sum();
             if (lane == 0) s_red[warp] = acc;
             __syncthreads();
@@ -403,7 +476,7 @@ __device__ __forceinline__ Scal load_scal(const PassArgs &a) {
     return sc;
 }
 
-template <int OP, int CH = 0>
+template <int OP, int CH = 0, int SW = 0>
 __global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
                                                            CsrView L, PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -429,7 +502,7 @@ __global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_
             fence_proxy_async();   // generic reads of that stage (previous tile) before async writes
             issue_tile(S, L, tiles[ahead], (it + kStages - 1) % kStages, pol);
         }
-        tile_compute<OP, CH, false>(tiles[ti], S, b, (unsigned)(it / kStages) & 1u, s_red, L, a, sc, st);
+        tile_compute<OP, CH, false, SW>(tiles[ti], S, b, (unsigned)(it / kStages) & 1u, s_red, L, a, sc, st);
     }
     if (OP == OP_GS && !(a.stat_mode & 4)) return;   // uniform: statistics not wanted
     grid_reduce(st, a.partials, a.counter, [&](const double *tot) {
@@ -780,6 +853,7 @@ static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0
     FDL_CK(cudaLaunchKernelEx(&cfg, k_gs_multi<true>, v, seg, c0, c1, sweeps, x, slot, mode, n));
 }
 
+constexpr double kDenseRowDeg = 12.0;   // rows per tile few enough for sub-warp rows
 static int g_pass_grid[4] = {0, 0, 0, 0};
 static int pass_grid(int op) { return g_pass_grid[op]; }
 
@@ -798,10 +872,13 @@ struct Enq {
         a.counter = h.counter.as<unsigned>();
         CsrView v = OP == OP_GS ? CsrView{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()}
                                 : CsrView{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
-        // GS: the chunk of 4 suits <= 4.5 neighbours per row, 8 the denser coarse levels
+        // GS: the chunk of 4 suits <= 4.5 neighbours per row, 8 the denser coarse
+        // levels; dense levels (>= kDenseRowDeg per row): 4 lanes per short row
         if (OP == OP_GS && L.nnz <= 4.5 * L.n) {
             grid = std::min(nt, g_pass_grid[3]);
             k_tilepass<OP_GS, 4><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
+        } else if (L.nnz >= kDenseRowDeg * (double)L.n) {
+            k_tilepass<OP, 0, 4><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
         } else {
             k_tilepass<OP><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
         }
@@ -946,6 +1023,9 @@ int rowpass_grid() {
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_RQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_RQ, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 
     int b3 = 0;
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_tilepass<OP_GS, 4>, kPassThreads, smem));
