@@ -41,9 +41,6 @@ void set_error(const std::string &m) { g_last_error = m; }
 Handle::~Handle() {
     if (gexec) cudaGraphExecDestroy(gexec);
     gexec = nullptr;
-    // level buffers were allocated on the setup streams: the solve's last use (main
-    // stream) must be complete before they are freed
-    if (stream) cudaStreamSynchronize(stream);
     levels.clear();
     xa.release(); xb.release(); vnat.release(); scal.release();
     partials.release(); counter.release(); result.release();
@@ -51,10 +48,6 @@ Handle::~Handle() {
     if (stream2) {
         cudaStreamSynchronize(stream2);
         cudaStreamDestroy(stream2);
-    }
-    if (stream3) {
-        cudaStreamSynchronize(stream3);
-        cudaStreamDestroy(stream3);
     }
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
@@ -193,7 +186,6 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     }
     cudaStream_t st = h->stream;
     FDL_CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
-    FDL_CK(cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking));
     h->row_grid = rowpass_grid();
     EventTimer timer(st);
 

@@ -101,7 +101,6 @@ struct Handle {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaStream_t stream2 = nullptr;   // setup: colourings overlapped with the coarsening chain
-    cudaStream_t stream3 = nullptr;   // setup: solve layouts overlapped with both
     fiedler_opts opts{};
     std::vector<Level> levels;
     int n0 = 0;

@@ -20,11 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
-#include <condition_variable>
-#include <exception>
-#include <mutex>
 #include <queue>
-#include <thread>
 
 #include <cooperative_groups.h>
 
@@ -2654,57 +2650,14 @@ __global__ void k_compose_qg(int n, const int *perm, const int *q_nat, int *qg) 
 }
 
 void build_hierarchy(Handle &h, NatGraph &&g0) {
-    // Three streams: the coarsening chain (match -> Galerkin, level by level) on
-    // the main stream, each level's colouring on stream2 as soon as the level
-    // exists, and each level's solve layout on stream3 as soon as its colouring
-    // is done -- issued by a second host thread, because a layout needs the
-    // colour count on the host (a sync) while the chain keeps being issued.
-    cudaStream_t st = h.stream, sb = h.stream2, sl = h.stream3;
+    cudaStream_t st = h.stream, sb = h.stream2;
     const fiedler_opts &o = h.opts;
     NatGraph cur = std::move(g0);
     h.levels.clear();
-    const size_t cap = (size_t)std::max(1, o.max_levels) + 1;
-    h.levels.reserve(cap);   // no reallocation while the layout thread reads them
     std::vector<NatGraph> graphs;
-    graphs.reserve(cap);
     std::vector<std::unique_ptr<ColourJob>> jobs;
-    jobs.reserve(cap);
-    std::vector<cudaEvent_t> evc;   // colouring of level ell complete (stream2)
-    evc.reserve(cap);
     cudaEvent_t ev;
     FDL_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    std::mutex mu;
-    std::condition_variable cv;
-    int published = 0;
-    bool closed = false;
-    std::exception_ptr err;
-    const int dev = h.device;
-    std::thread layouts([&] {
-        try {
-            FDL_CK(cudaSetDevice(dev));
-            for (int ell = 0;; ell++) {
-                {
-                    std::unique_lock<std::mutex> lk(mu);
-                    cv.wait(lk, [&] { return published > ell || closed; });
-                    if (published <= ell) break;
-                }
-                Level &L = h.levels[ell];
-                FDL_CK(cudaStreamWaitEvent(sl, evc[ell], 0));
-                const int ncol = color_finish(*jobs[ell], L.color_rounds, sl);
-                build_layout(graphs[ell], L.color_nat.as<int>(), ncol, L, sl);
-            }
-        } catch (...) {
-            err = std::current_exception();
-        }
-    });
-    auto close_layouts = [&] {
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            closed = true;
-        }
-        cv.notify_all();
-        if (layouts.joinable()) layouts.join();
-    };
     try {
         for (int ell = 0;; ell++) {
             Level L;
@@ -2713,10 +2666,6 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
             FDL_CK(cudaStreamWaitEvent(sb, ev, 0));
             jobs.emplace_back(new ColourJob());
             color_launch(cur, salt_color(o.seed, ell), L.color_nat, *jobs.back(), sb);
-            cudaEvent_t e;
-            FDL_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            evc.push_back(e);
-            FDL_CK(cudaEventRecord(e, sb));
             bool coarsen = cur.n > o.coarsest_size && ell + 1 < o.max_levels;
             NatGraph next;
             if (coarsen) {
@@ -2732,31 +2681,26 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
                     trace_mark(st, ell == 0 ? "L0 galerkin" : "Lk galerkin");
                 }
             }
-            {
-                std::lock_guard<std::mutex> lk(mu);
-                h.levels.push_back(std::move(L));
-                graphs.push_back(std::move(cur));
-                published++;
-            }
-            cv.notify_all();
+            h.levels.push_back(std::move(L));
+            graphs.push_back(std::move(cur));
             if (!coarsen) break;
             cur = std::move(next);
         }
-        close_layouts();
-        if (err) std::rethrow_exception(err);
-        // the layouts (stream3) are complete before anything else uses the levels
-        FDL_CK(cudaEventRecord(ev, sl));
+        // layouts: the colourings must be complete (main stream waits for the second)
+        FDL_CK(cudaEventRecord(ev, sb));
         FDL_CK(cudaStreamWaitEvent(st, ev, 0));
+        trace_mark(sb, "colourings (second stream)");
+        for (size_t ell = 0; ell < h.levels.size(); ell++) {
+            Level &L = h.levels[ell];
+            const int ncol = color_finish(*jobs[ell], L.color_rounds, sb);
+            build_layout(graphs[ell], L.color_nat.as<int>(), ncol, L, st);
+        }
         trace_mark(st, "layouts");
     } catch (...) {
-        close_layouts();
         cudaStreamSynchronize(sb);
-        cudaStreamSynchronize(sl);
-        for (cudaEvent_t e : evc) cudaEventDestroy(e);
         cudaEventDestroy(ev);
         throw;
     }
-    for (cudaEvent_t e : evc) cudaEventDestroy(e);
     cudaEventDestroy(ev);
     const int J = (int)h.levels.size() - 1;
     for (int ell = 0; ell < J; ell++) {
