@@ -49,6 +49,7 @@ Handle::~Handle() {
         cudaStreamSynchronize(stream2);
         cudaStreamDestroy(stream2);
     }
+    if (ev_pattern) cudaEventDestroy(ev_pattern);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -205,6 +206,12 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
         g0.own_w.alloc(padded((size_t)std::max<int64_t>(nnz, 1) * 8), st);
         if (nnz) {
             FDL_CK(cudaMemcpyAsync(g0.own_ci.p, col_idx, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
+            // without validation the level-0 colouring (pattern only) may start
+            // while the weights are still being copied
+            if (!o.validate) {
+                FDL_CK(cudaEventCreateWithFlags(&h->ev_pattern, cudaEventDisableTiming));
+                FDL_CK(cudaEventRecord(h->ev_pattern, st));
+            }
             FDL_CK(cudaMemcpyAsync(g0.own_w.p, weights, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
         }
         g0.ci = g0.own_ci.as<int>();

@@ -101,6 +101,7 @@ struct Handle {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaStream_t stream2 = nullptr;   // setup: colourings overlapped with the coarsening chain
+    cudaEvent_t ev_pattern = nullptr; // host input: level-0 pattern (rp, ci) on the device
     fiedler_opts opts{};
     std::vector<Level> levels;
     int n0 = 0;

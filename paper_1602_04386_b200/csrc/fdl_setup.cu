@@ -2662,8 +2662,13 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
         for (int ell = 0;; ell++) {
             Level L;
             // colouring of level ell on the second stream, once the level exists
-            FDL_CK(cudaEventRecord(ev, st));
-            FDL_CK(cudaStreamWaitEvent(sb, ev, 0));
+            // (level 0 from host input: once its pattern is, weights may still be copying)
+            if (ell == 0 && h.ev_pattern) {
+                FDL_CK(cudaStreamWaitEvent(sb, h.ev_pattern, 0));
+            } else {
+                FDL_CK(cudaEventRecord(ev, st));
+                FDL_CK(cudaStreamWaitEvent(sb, ev, 0));
+            }
             jobs.emplace_back(new ColourJob());
             color_launch(cur, salt_color(o.seed, ell), L.color_nat, *jobs.back(), sb);
             bool coarsen = cur.n > o.coarsest_size && ell + 1 < o.max_levels;
