@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
                                                              const double *w, uint64_t salt, int *m,
                                                              int *ptr, int *mate, int *nbr, int *cursor,
                                                              int *la, int *lb, int *counts,
-                                                             int *rounds_out) {
+                                                             int *rounds_out, int *lm, int *mcount) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
@@ -427,37 +427,56 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
                 __syncthreads();
                 if (s_n > kAppendCap - kMatchUnroll * kCoopThreads) app.flush(out, gcount);
             }
-        } else
-        // sub-warp slot s of CTA b takes entry base + s * gridDim + b: a short
-        // list (deep rounds of dense levels) is spread over all CTAs
-        for (long long base = 0; base < cnt; base += (long long)gridDim.x * per_block) {
-            const long long idx = base + (long long)(threadIdx.x / W) * gridDim.x + blockIdx.x;
-            const int v = idx < cnt ? in[idx] : -1;
-            bool keep = false, moved = false;
-            int cur = -1;
-            if (v >= 0 && mate[v] < 0) {
-                if (mate[ptr[v]] < 0) keep = true;
-                else { moved = true; cur = cursor[v]; }
+        } else {
+            // (b1) thread per entry: matched vertices drop out, those whose target
+            //      is still free stay listed, the rest (the movers) are collected
+            int *mc = mcount + r;
+            for (long long base = (long long)blockIdx.x * kCoopThreads; base < cnt;
+                 base += (long long)gridDim.x * kCoopThreads) {
+                const long long idx = base + threadIdx.x;
+                const int v = idx < cnt ? in[idx] : -1;
+                bool keep = false, mv = false;
+                if (v >= 0 && mate[v] < 0) {
+                    if (mate[ptr[v]] < 0) keep = true;
+                    else mv = true;
+                }
+                if (keep) app.push(v);
+                const unsigned bal = __ballot_sync(0xffffffffu, mv);   // one atomic per warp
+                int wb = 0;
+                if (bal && lane_id() == 0) wb = atomicAdd(mc, __popc(bal));
+                wb = __shfl_sync(0xffffffffu, wb, 0);
+                if (mv) lm[wb + __popc(bal & ((1u << lane_id()) - 1u))] = v;
+                __syncthreads();
+                if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
             }
-            int bj = -1;
-            const bool rescan = moved && cur < 0;
-            if (moved && cur >= 0 && lane == 0) {
-                const int b = rp[v], deg = rp[v + 1] - b;
-                int c = cur + 1;
-                while (c < deg && mate[nbr[b + c]] >= 0) c++;
-                bj = c < deg ? nbr[b + c] : -1;
-                cursor[v] = c;
+            grid.sync();
+            // (b2) a sub-warp per mover re-points it at its heaviest FREE neighbour
+            //      (cursor advance, or a rescan of a long row); slot s of CTA b
+            //      takes mover base + s * gridDim + b, spread over all CTAs
+            const int mcnt = *(volatile int *)mc;
+            for (long long base = 0; base < mcnt; base += (long long)gridDim.x * per_block) {
+                const long long idx = base + (long long)(threadIdx.x / W) * gridDim.x + blockIdx.x;
+                const int v = idx < mcnt ? lm[idx] : -1;
+                const int cur = v >= 0 ? cursor[v] : -1;
+                int bj = -1;
+                const bool rescan = v >= 0 && cur < 0;
+                if (v >= 0 && cur >= 0 && lane == 0) {
+                    const int b = rp[v], deg = rp[v + 1] - b;
+                    int c = cur + 1;
+                    while (c < deg && mate[nbr[b + c]] >= 0) c++;
+                    bj = c < deg ? nbr[b + c] : -1;
+                    cursor[v] = c;
+                }
+                const int bs = heaviest<W>(rescan ? v : -1, rp, ci, w, salt, lane,
+                                           [&](int j) { return mate[j] >= 0; });
+                if (rescan) bj = bs;
+                if (v >= 0 && lane == 0) {
+                    ptr[v] = bj;
+                    if (bj >= 0) app.push(v);
+                }
+                __syncthreads();
+                if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
             }
-            const int bs = heaviest<W>(rescan ? v : -1, rp, ci, w, salt, lane,
-                                       [&](int j) { return mate[j] >= 0; });
-            if (rescan) bj = bs;
-            if (lane == 0 && moved) {
-                ptr[v] = bj;
-                keep = bj >= 0;
-            }
-            if (lane == 0 && keep) app.push(v);
-            __syncthreads();
-            if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
         }
         __syncthreads();
         app.flush(out, gcount);
@@ -566,6 +585,8 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
                         cudaStream_t st) {
     int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
+    DBuf lmv((size_t)n * 4, st), mcount((size_t)kMaxRounds * 4, st);
+    FDL_CK(cudaMemsetAsync(mcount.p, 0, (size_t)kMaxRounds * 4, st));
     DBuf m((size_t)n * 4, st), ptr((size_t)n * 4, st), la((size_t)n * 4, st), lb((size_t)n * 4, st),
         nbr((size_t)std::max(g.nnz, 1) * 4, st), cursor((size_t)n * 4, st),
         counts((size_t)(kMaxRounds + 1) * 4, st);
@@ -579,7 +600,8 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
         int *pm = m.as<int>(), *pp = ptr.as<int>(), *pmate = mate.as<int>(), *pn = nbr.as<int>(),
             *pcur = cursor.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(), *pc = counts.as<int>(),
             *pr = counts.as<int>() + kMaxRounds;
-        void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr};
+        int *plm = lmv.as<int>(), *pmc = mcount.as<int>();
+        void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr, &plm, &pmc};
         RoundTrace tr(st, "match");
         DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st, kMatchGridDiv));
         tr.report(counts.as<int>());
