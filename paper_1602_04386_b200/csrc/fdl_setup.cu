@@ -636,19 +636,19 @@ __global__ void k_seg_starts(int n, const unsigned *keys, int *segstart) {
 // ================================================================= Galerkin product
 // I L I^T with the R3 summation order, computed per COARSE ROW
 // from the aggregate members (no global sort of all contributions):
-//   1. members of every aggregate (counting sort by aggregate id; n elements);
-//   2. every member m emits, for each neighbour j in another aggregate B, the
-//      contribution (B, lo = min(m, j), hi = max(m, j), w_mj): the R3 order of
-//      the fine edges {i < j} is ascending (lo, hi);
-//   3. each coarse row A sorts its contributions by (B, lo, hi) (registers for <= 16,
-//      a warp in shared memory for <= 256, a global two-key radix sort for the
-//      rare longer rows) and left-folds every run of equal B in kpos order --
-//      the oracle's fold, computed independently and identically on both sides
-//      of the pair, so W_c is symmetric bit for bit;
+//   1. members of every aggregate (counting sort by aggregate id) and the slot
+//      count T_A = sum of the member degrees of every coarse row A;
+//   2. the contributions of row A are its members' fine entries (m, j) with
+//      B = q(j) != A: (B, lo = min(m, j), hi = max(m, j), w_mj); the R3 order
+//      of the fine edges {i < j} is ascending (lo, hi);
+//   3. each row sorts its contributions by (B, lo, hi) and left-folds every run
+//      of equal B in that order -- the oracle's fold, computed independently
+//      and identically on both sides of the pair, so W_c is symmetric bit for
+//      bit.  Rows by size: <= 16 slots in warp batches (k_gal_direct_batch,
+//      one 64-bit key per slot), <= 32 a warp with a slot per lane, <= 256 a
+//      warp in shared memory, bigger rows (hubs) by emitting their
+//      contributions and one global two-key radix sort (galerkin_big_rows);
 //   4. prefix scan of the row lengths and a compacting copy give the CSR.
-// Steps 2-3 have a direct form (no materialised contributions, see
-// k_gal_direct) taken whenever no coarse row exceeds kGalMid slots.
-constexpr int kGalSmall = 16;
 constexpr int kGalMid = 256;
 
 __global__ void k_member_fill(int n, const int *q, const int *mrp, int *fill, int *mem) {
@@ -734,177 +734,16 @@ __global__ void k_gal_member_emit(int n, const int *mem, const int *rp, const in
     }
 }
 
-// rows with <= CAP contributions: register bitonic sort + sequential fold.
-// The CAP = 8 pass runs over every row and sorts out the rest: rows with
-// 8 < s <= 16 (a CAP = 16 pass over that list), kGalSmall < s <= kGalMid (warp
-// path) and longer (global path).
-// bitonic sort of CAP register entries by (B, lo, hi) -- (B, lo) in k, hi in
-// k2; empty slots hold k = ~0 and sort last -- then a left fold of every run
-// of equal B in that order; the runs go to outB/outW[0 ..), their count to *deg_out
-template <int CAP>
-__device__ __forceinline__ void sort_fold_regs(unsigned long long (&k)[CAP], unsigned (&k2)[CAP],
-                                               double (&v)[CAP], int *outB, double *outW, int *deg_out) {
-#pragma unroll
-    for (int kk = 2; kk <= CAP; kk <<= 1)
-#pragma unroll
-        for (int jj = kk >> 1; jj > 0; jj >>= 1)
-#pragma unroll
-            for (int i = 0; i < CAP; i++) {
-                const int l = i ^ jj;
-                if (l > i) {
-                    const bool up = (i & kk) == 0;
-                    const bool gt = k[i] > k[l] || (k[i] == k[l] && k2[i] > k2[l]);
-                    if (gt == up) {
-                        unsigned long long tk = k[i]; k[i] = k[l]; k[l] = tk;
-                        unsigned t2 = k2[i]; k2[i] = k2[l]; k2[l] = t2;
-                        double tv = v[i]; v[i] = v[l]; v[l] = tv;
-                    }
-                }
-            }
-    int runs = 0;
-    unsigned curB = 0;
-    double acc = 0.0;
-#pragma unroll
-    for (int i = 0; i < CAP; i++) {
-        if (k[i] != ~0ull) {
-            const unsigned B = (unsigned)(k[i] >> 32);
-            if (i == 0) { curB = B; acc = v[i]; }
-            else if (B != curB) {
-                outB[runs] = (int)curB; outW[runs] = acc; runs++;
-                curB = B; acc = v[i];
-            } else {
-                acc += v[i];
-            }
-        }
-    }
-    if (k[0] != ~0ull) { outB[runs] = (int)curB; outW[runs] = acc; runs++; }
-    *deg_out = runs;
-}
-
-// rows with <= CAP contributions: register bitonic sort + sequential fold.
-// The CAP = 8 pass runs over every row and sorts out the rest: rows with
-// 8 < s <= 16 (a CAP = 16 pass over that list), kGalSmall < s <= kGalMid (warp
-// path) and longer (global path).
-template <int CAP>
-__device__ __forceinline__ void gal_row_sort_fold(int s, int sb, const unsigned long long *keys,
-                                                  const unsigned *keys2, const double *vals, int *outB,
-                                                  double *outW, int *deg_out) {
-    unsigned long long k[CAP];
-    unsigned k2[CAP];
-    double v[CAP];
-#pragma unroll
-    for (int i = 0; i < CAP; i++) {
-        k[i] = i < s ? keys[sb + i] : ~0ull;
-        k2[i] = i < s ? keys2[sb + i] : ~0u;
-        v[i] = i < s ? vals[sb + i] : 0.0;
-    }
-    sort_fold_regs<CAP>(k, k2, v, outB + sb, outW + sb, deg_out);
-}
-
-__global__ void __launch_bounds__(256) k_gal_rows_small(int c, const int *mrp, const int *coff,
-                                                        const unsigned long long *keys, const unsigned *keys2,
-                                                        const double *vals,
-                                                        int *outB, double *outW, int *deg, int *f16,
-                                                        int *midflag, int *bigflag) {
-    for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
-        const int sb = coff[mrp[A]], se = coff[mrp[A + 1]];
-        const int s = se - sb;
-        f16[A] = (s > 8 && s <= kGalSmall);
-        midflag[A] = (s > kGalSmall && s <= kGalMid);
-        bigflag[A] = (s > kGalMid);
-        if (s > 8) continue;
-        gal_row_sort_fold<8>(s, sb, keys, keys2, vals, outB, outW, &deg[A]);
-    }
-}
-
-__global__ void __launch_bounds__(256) k_gal_rows_16(const int *list, const int *count, const int *mrp,
-                                                     const int *coff, const unsigned long long *keys,
-                                                     const unsigned *keys2, const double *vals, int *outB, double *outW,
-                                                     int *deg) {
-    const int cnt = *count;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-        const int A = list[i];
-        const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb;
-        gal_row_sort_fold<kGalSmall>(s, sb, keys, keys2, vals, outB, outW, &deg[A]);
-    }
-}
-
-// rows with kGalSmall < s <= kGalMid contributions: one warp each, bitonic sort in shared memory
-constexpr int kGalMidWarps = 8;
-__global__ void __launch_bounds__(kGalMidWarps * 32) k_gal_rows_mid(const int *list, const int *count,
-                                                                    const int *mrp, const int *coff,
-                                                                    const unsigned long long *keys, const unsigned *keys2,
-                                                                    const double *vals, int *outB,
-                                                                    double *outW, int *deg) {
-    __shared__ unsigned long long sk[kGalMidWarps][kGalMid];
-    __shared__ unsigned sk2[kGalMidWarps][kGalMid];
-    __shared__ double sv[kGalMidWarps][kGalMid];
-    const int warp = threadIdx.x >> 5, lane = lane_id();
-    const int cnt = *count;
-    unsigned long long *K = sk[warp];
-    unsigned *K2 = sk2[warp];
-    double *V = sv[warp];
-    for (int idx = blockIdx.x * kGalMidWarps + warp; idx < cnt; idx += gridDim.x * kGalMidWarps) {
-        const int A = list[idx];
-        const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb;
-        int N = 32;
-        while (N < s) N <<= 1;
-        for (int i = lane; i < N; i += 32) {
-            K[i] = i < s ? keys[sb + i] : ~0ull;
-            K2[i] = i < s ? keys2[sb + i] : ~0u;
-            V[i] = i < s ? vals[sb + i] : 0.0;
-        }
-        __syncwarp();
-        for (int kk = 2; kk <= N; kk <<= 1)
-            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-                for (int i = lane; i < N; i += 32) {
-                    const int l = i ^ jj;
-                    if (l > i) {
-                        const bool up = (i & kk) == 0;
-                        const bool gt = K[i] > K[l] || (K[i] == K[l] && K2[i] > K2[l]);
-                        if (gt == up) {
-                            unsigned long long tk = K[i]; K[i] = K[l]; K[l] = tk;
-                            unsigned t2 = K2[i]; K2[i] = K2[l]; K2[l] = t2;
-                            double tv = V[i]; V[i] = V[l]; V[l] = tv;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-        // runs: heads in order, the head lane folds its run sequentially
-        int base = 0;
-        for (int c0 = 0; c0 < s; c0 += 32) {
-            const int i = c0 + lane;
-            const bool head = i < s && (i == 0 || (K[i] >> 32) != (K[i - 1] >> 32));
-            const unsigned hm = __ballot_sync(0xffffffffu, head);
-            if (head) {
-                const int r = base + __popc(hm & ((1u << lane) - 1u));
-                double acc = V[i];
-                for (int u = i + 1; u < s && (K[u] >> 32) == (K[i] >> 32); u++) acc += V[u];
-                outB[sb + r] = (int)(K[i] >> 32);
-                outW[sb + r] = acc;
-            }
-            base += __popc(hm);
-        }
-        if (lane == 0) deg[A] = base;
-        __syncwarp();
-    }
-}
-
-// ---- rows with more than kGalMid contributions: global two-key radix sort
-__global__ void k_big_sizes(int h, const int *list, const int *mrp, const int *coff, int *sz) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < h; r += gridDim.x * blockDim.x) {
-        const int A = list[r];
-        sz[r] = coff[mrp[A + 1]] - coff[mrp[A]];
-    }
+// ---- rows too big for the direct kernels: global two-key radix sort
+__global__ void k_big_sizes(int h, const int *lo, const int *hi, int *sz) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < h; r += gridDim.x * blockDim.x) sz[r] = hi[r] - lo[r];
 }
 
 // one CTA per big row: gather its segment into the concatenated arrays
-__global__ void k_big_gather(int h, const int *list, const int *mrp, const int *coff, const int *boff,
-                             const unsigned *keys2, unsigned *ck2, int *cidx, unsigned *crank, int *cdst) {
+__global__ void k_big_gather(int h, const int *lo, const int *hi, const int *boff, const unsigned *keys2,
+                             unsigned *ck2, int *cidx, unsigned *crank, int *cdst) {
     for (int r = blockIdx.x; r < h; r += gridDim.x) {
-        const int A = list[r];
-        const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb, o = boff[r];
+        const int sb = lo[r], s = hi[r] - sb, o = boff[r];
         for (int i = threadIdx.x; i < s; i += blockDim.x) {
             ck2[o + i] = keys2[sb + i];
             cidx[o + i] = o + i;
@@ -939,15 +778,15 @@ __global__ void k_big_place(int E, const int *idx, const int *cdst, const int *s
 }
 
 // one CTA per big row: heads, block scan for run indices, sequential fold per run
-__global__ void __launch_bounds__(256) k_big_fold(int h, const int *list, const int *mrp,
-                                                  const int *coff, const unsigned long long *keys,
+__global__ void __launch_bounds__(256) k_big_fold(int h, const int *list, const int *lo, const int *hi,
+                                                  const int *oo, const unsigned long long *keys,
                                                   const double *vals, int *outB, double *outW,
                                                   int *deg) {
     __shared__ int s_warp[8];
     __shared__ int s_base;
     for (int r = blockIdx.x; r < h; r += gridDim.x) {
         const int A = list[r];
-        const int sb = coff[mrp[A]], s = coff[mrp[A + 1]] - sb;
+        const int sb = lo[r], s = hi[r] - sb, ob = oo[r];
         if (threadIdx.x == 0) s_base = 0;
         __syncthreads();
         for (int c0 = 0; c0 < s; c0 += blockDim.x) {
@@ -964,8 +803,8 @@ __global__ void __launch_bounds__(256) k_big_fold(int h, const int *list, const 
                 const unsigned long long B = keys[sb + i] >> 32;
                 double acc = vals[sb + i];
                 for (int u = i + 1; u < s && (keys[sb + u] >> 32) == B; u++) acc += vals[sb + u];
-                outB[sb + ri] = (int)B;
-                outW[sb + ri] = acc;
+                outB[ob + ri] = (int)B;
+                outW[ob + ri] = acc;
             }
             __syncthreads();
             if (threadIdx.x == 0)
@@ -1436,9 +1275,105 @@ __global__ void __launch_bounds__(kGalDirectWarps * 32) k_gal_direct_warp(
     }
 }
 
-__global__ void k_row_base(int c, const int *mrp, const int *coff, int *rowoff) {
-    for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x)
-        rowoff[A] = coff[mrp[A]];
+
+__global__ void k_set_rows_zero(int h, const int *list, int *deg) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < h; r += gridDim.x * blockDim.x) deg[list[r]] = 0;
+}
+
+// big rows (class 3) of the direct path: their members, contribution ranges
+__global__ void k_big_member_counts(int h, const int *list, const int *mrp, int *nm) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < h; r += gridDim.x * blockDim.x)
+        nm[r] = mrp[list[r] + 1] - mrp[list[r]];
+}
+
+__global__ void k_big_members(int h, const int *list, const int *mrp, const int *mem, const int *moff,
+                              int *subm) {
+    for (int r = blockIdx.x; r < h; r += gridDim.x) {
+        const int mb = mrp[list[r]], nm = mrp[list[r] + 1] - mb;
+        for (int i = threadIdx.x; i < nm; i += blockDim.x) subm[moff[r] + i] = mem[mb + i];
+    }
+}
+
+__global__ void k_big_ranges(int h, const int *list, const int *moff, const int *coff, const int *rowoff,
+                             int *lo, int *hi, int *oo) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < h; r += gridDim.x * blockDim.x) {
+        lo[r] = coff[moff[r]];
+        hi[r] = coff[moff[r + 1]];
+        oo[r] = rowoff[list[r]];
+    }
+}
+
+// The big rows: every member emits its contributions (B, lo, hi, w), one global
+// two-key LSD radix sort orders each row's contributions by (B, lo, hi) (passes:
+// hi, then (B, lo), then the row rank), then a CTA per row folds its runs of B
+// into its reserved output slots (rowoff).
+static void galerkin_big_rows(const NatGraph &g, const int *q, int c, int h, const int *biglist,
+                              const int *mrp, const int *mem, const int *rowoff, int *outB, double *outW,
+                              int *deg, cudaStream_t st) {
+    const double avg = g.n ? (double)g.nnz / g.n : 0.0;
+    DBuf nm((size_t)h * 4, st), moff((size_t)(h + 1) * 4, st);
+    k_big_member_counts<<<grid_for(h), 256, 0, st>>>(h, biglist, mrp, nm.as<int>());
+    FDL_LAUNCH_CK();
+    scan_exclusive(nm.as<int>(), moff.as<int>(), h, moff.as<int>() + h, st);
+    const int M = read_int(moff.as<int>() + h, st);
+    DBuf subm((size_t)std::max(M, 1) * 4, st), cnt((size_t)std::max(M, 1) * 4, st),
+        coff((size_t)(M + 1) * 4, st);
+    k_big_members<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(h, biglist, mrp, mem, moff.as<int>(), subm.as<int>());
+    FDL_LAUNCH_CK();
+    DISPATCH_WC(avg, (k_gal_member_count<W><<<sub_grid(M, W), 256, 0, st>>>(
+                         M, subm.as<int>(), g.rp, g.ci, q, cnt.as<int>())));
+    FDL_LAUNCH_CK();
+    scan_exclusive(cnt.as<int>(), coff.as<int>(), M, coff.as<int>() + M, st);
+    const int E = read_int(coff.as<int>() + M, st);
+    DBuf keys((size_t)std::max(E, 1) * 8, st), keys2((size_t)std::max(E, 1) * 4, st),
+        vals((size_t)std::max(E, 1) * 8, st);
+    if (E > 0) {
+        DISPATCH_WC(avg, (k_gal_member_emit<W><<<sub_grid(M, W), 256, 0, st>>>(
+                             M, subm.as<int>(), g.rp, g.ci, g.w, q, coff.as<int>(),
+                             keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>())));
+        FDL_LAUNCH_CK();
+    }
+    DBuf lo((size_t)h * 4, st), hi((size_t)h * 4, st), oo((size_t)h * 4, st), sz((size_t)h * 4, st),
+        boff((size_t)(h + 1) * 4, st);
+    k_big_ranges<<<grid_for(h), 256, 0, st>>>(h, biglist, moff.as<int>(), coff.as<int>(), rowoff, lo.as<int>(),
+                                               hi.as<int>(), oo.as<int>());
+    FDL_LAUNCH_CK();
+    k_big_sizes<<<grid_for(h), 256, 0, st>>>(h, lo.as<int>(), hi.as<int>(), sz.as<int>());
+    FDL_LAUNCH_CK();
+    scan_exclusive(sz.as<int>(), boff.as<int>(), h, boff.as<int>() + h, st);
+    const int EB = E;   // every contribution here belongs to a big row
+    if (EB > 0) {
+        DBuf ckey((size_t)EB * 8, st), ck2((size_t)EB * 4, st), cidx((size_t)EB * 4, st),
+            crank((size_t)EB * 4, st), cdst((size_t)EB * 4, st), srcpos((size_t)EB * 4, st);
+        k_big_gather<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
+            h, lo.as<int>(), hi.as<int>(), boff.as<int>(), keys2.as<unsigned>(), ck2.as<unsigned>(),
+            cidx.as<int>(), crank.as<unsigned>(), cdst.as<int>());
+        FDL_LAUNCH_CK();
+        // srcpos[o] = original position of concatenated element o (= cdst before sorting)
+        FDL_CK(cudaMemcpyAsync(srcpos.p, cdst.p, (size_t)EB * 4, cudaMemcpyDeviceToDevice, st));
+        // LSD radix passes, least significant key first: hi, then (B, lo), then the row rank
+        radix_sort_u32_i32(ck2.as<unsigned>(), cidx.as<int>(), EB, 32, st);
+        k_big_key1_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), srcpos.as<int>(),
+                                                    keys.as<unsigned long long>(), ckey.as<unsigned long long>());
+        FDL_LAUNCH_CK();
+        radix_sort_u64_i32(ckey.as<unsigned long long>(), cidx.as<int>(), EB, 32 + bits_for(c - 1), st);
+        DBuf rank2((size_t)EB * 4, st);
+        k_big_rank_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), crank.as<unsigned>(), rank2.as<unsigned>());
+        FDL_LAUNCH_CK();
+        radix_sort_u32_i32(rank2.as<unsigned>(), cidx.as<int>(), EB, bits_for(h - 1), st);
+        DBuf keys_s((size_t)E * 8, st), vals_s((size_t)E * 8, st);
+        k_big_place<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), cdst.as<int>(), srcpos.as<int>(),
+                                                  keys.as<unsigned long long>(), vals.as<double>(),
+                                                  keys_s.as<unsigned long long>(), vals_s.as<double>());
+        FDL_LAUNCH_CK();
+        k_big_fold<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(h, biglist, lo.as<int>(), hi.as<int>(), oo.as<int>(),
+                                                            keys_s.as<unsigned long long>(), vals_s.as<double>(),
+                                                            outB, outW, deg);
+        FDL_LAUNCH_CK();
+    } else {
+        k_set_rows_zero<<<grid_for(h), 256, 0, st>>>(h, biglist, deg);
+        FDL_LAUNCH_CK();
+    }
 }
 
 static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st) {
@@ -1469,11 +1404,12 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
                                                                   mem.as<int>());
     FDL_LAUNCH_CK();
     mfill.release();
-    // rows by size class: the direct path takes the level when no row is too
-    // big for its warp kernel, the general path (steps 2-3) otherwise
-    DBuf deg((size_t)(c + 1) * 4, st), rowoff, outB, outW;
+    // rows by size class (gal_class): 0 in warp batches, 1 warp per row, 2 warp in
+    // shared memory, 3 (big) through the sort-based path
+    DBuf deg((size_t)(c + 1) * 4, st), rowoff((size_t)c * 4, st), outB((size_t)std::max(g.nnz, 1) * 4, st),
+        outW((size_t)std::max(g.nnz, 1) * 8, st);
     int dc[3] = {0, 0, 0};
-    DBuf dl((size_t)c * 4 * 2, st), dcnt(16, st);
+    DBuf dl((size_t)c * 4 * 3, st), dcnt(16, st);
     FDL_CK(cudaMemsetAsync(dcnt.p, 0, 16, st));
     {
         DBuf f32((size_t)c * 4, st), fmid((size_t)c * 4, st), fbig((size_t)c * 4, st);
@@ -1482,20 +1418,16 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
         FDL_LAUNCH_CK();
         compact_flagged(nullptr, f32.as<int>(), c, dl.as<int>(), dcnt.as<int>(), st);
         compact_flagged(nullptr, fmid.as<int>(), c, dl.as<int>() + c, dcnt.as<int>() + 1, st);
-        compact_flagged(nullptr, fbig.as<int>(), c, dl.as<int>() + c, dcnt.as<int>() + 2, st);   // count only
+        compact_flagged(nullptr, fbig.as<int>(), c, dl.as<int>() + 2 * c, dcnt.as<int>() + 2, st);
         FDL_CK(cudaMemcpyAsync(dc, dcnt.p, 12, cudaMemcpyDeviceToHost, st));
         FDL_CK(cudaStreamSynchronize(st));
     }
-    const bool direct = dc[2] == 0;
-    if (direct) {
-        outB.alloc((size_t)std::max(g.nnz, 1) * 4, st);
-        outW.alloc((size_t)std::max(g.nnz, 1) * 8, st);
+    {
         // rows ascend: input contract.  FIEDLER_TEST_FULL_SORT=1 (tests) forces
         // the fallback that very large levels take
         const char *fs = std::getenv("FIEDLER_TEST_FULL_SORT");
         const bool b64 = c < (1 << 27) && n < (1 << 29) && !(fs && fs[0] == '1');
         DBuf redo(b64 ? 0 : (size_t)c * 4, st);
-        rowoff.alloc((size_t)c * 4, st);
         k_gal_direct_batch<<<std::min(div_up(c, 32 * kGalBatchWarps), kNumSMs * 32), kGalBatchWarps * 32, 0,
                              st>>>(c, b64, mrp.as<int>(), mem.as<int>(), toff.as<int>(), g.rp, g.ci, g.w, q,
                                    outB.as<int>(), outW.as<double>(), deg.as<int>(), rowoff.as<int>(),
@@ -1522,96 +1454,11 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
                                          outW.as<double>(), deg.as<int>());
             FDL_LAUNCH_CK();
         }
+        if (dc[2] > 0)
+            galerkin_big_rows(g, q, c, dc[2], dl.as<int>() + 2 * c, mrp.as<int>(), mem.as<int>(),
+                              rowoff.as<int>(), outB.as<int>(), outW.as<double>(), deg.as<int>(), st);
         toff.release();
-    } else {
-        toff.release();
-        // 2. contributions in member order
-        DBuf cnt((size_t)n * 4, st), coff((size_t)(n + 1) * 4, st);
-        DISPATCH_WC(avg, (k_gal_member_count<W><<<sub_grid(n, W), 256, 0, st>>>(
-                             n, mem.as<int>(), g.rp, g.ci, q, cnt.as<int>())));
-        FDL_LAUNCH_CK();
-        scan_exclusive(cnt.as<int>(), coff.as<int>(), n, coff.as<int>() + n, st);
-        cnt.release();
-        const int E = read_int(coff.as<int>() + n, st);
-        DBuf keys((size_t)std::max(E, 1) * 8, st), keys2((size_t)std::max(E, 1) * 4, st),
-            vals((size_t)std::max(E, 1) * 8, st);
-        if (E > 0) {
-            DISPATCH_WC(avg, (k_gal_member_emit<W><<<sub_grid(n, W), 256, 0, st>>>(
-                                 n, mem.as<int>(), g.rp, g.ci, g.w, q, coff.as<int>(),
-                                 keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>())));
-            FDL_LAUNCH_CK();
-        }
         mem.release();
-        // 3. per-row sort + fold
-        outB.alloc((size_t)std::max(E, 1) * 4, st);
-        outW.alloc((size_t)std::max(E, 1) * 8, st);
-        DBuf f16((size_t)c * 4, st), midf((size_t)c * 4, st),
-            bigf((size_t)c * 4, st), lists((size_t)c * 4 * 3, st), lcnt(16, st);
-        k_gal_rows_small<<<grid_for(c, 256, kNumSMs * 8), 256, 0, st>>>(
-            c, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(), keys2.as<unsigned>(), vals.as<double>(),
-            outB.as<int>(), outW.as<double>(), deg.as<int>(), f16.as<int>(), midf.as<int>(), bigf.as<int>());
-        FDL_LAUNCH_CK();
-        int *midlist = lists.as<int>(), *biglist = lists.as<int>() + c, *list16 = lists.as<int>() + 2 * c;
-        compact_flagged(nullptr, midf.as<int>(), c, midlist, lcnt.as<int>(), st);
-        compact_flagged(nullptr, bigf.as<int>(), c, biglist, lcnt.as<int>() + 1, st);
-        compact_flagged(nullptr, f16.as<int>(), c, list16, lcnt.as<int>() + 2, st);
-        int hc[3];
-        FDL_CK(cudaMemcpyAsync(hc, lcnt.p, 12, cudaMemcpyDeviceToHost, st));
-        FDL_CK(cudaStreamSynchronize(st));
-        if (hc[2] > 0) {
-            k_gal_rows_16<<<grid_for(hc[2], 256, kNumSMs * 8), 256, 0, st>>>(
-                list16, lcnt.as<int>() + 2, mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
-                keys2.as<unsigned>(), vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
-            FDL_LAUNCH_CK();
-        }
-        if (hc[0] > 0) {
-            k_gal_rows_mid<<<std::min(div_up(hc[0], kGalMidWarps), kNumSMs * 8), kGalMidWarps * 32, 0, st>>>(
-                midlist, lcnt.as<int>(), mrp.as<int>(), coff.as<int>(), keys.as<unsigned long long>(),
-                keys2.as<unsigned>(), vals.as<double>(), outB.as<int>(), outW.as<double>(), deg.as<int>());
-            FDL_LAUNCH_CK();
-        }
-        const int h = hc[1];
-        if (h > 0) {
-            DBuf sz((size_t)h * 4, st), boff((size_t)(h + 1) * 4, st);
-            k_big_sizes<<<grid_for(h), 256, 0, st>>>(h, biglist, mrp.as<int>(), coff.as<int>(), sz.as<int>());
-            FDL_LAUNCH_CK();
-            scan_exclusive(sz.as<int>(), boff.as<int>(), h, boff.as<int>() + h, st);
-            const int EB = read_int(boff.as<int>() + h, st);
-            DBuf ckey((size_t)EB * 8, st), ck2((size_t)EB * 4, st), cidx((size_t)EB * 4, st),
-                crank((size_t)EB * 4, st), cdst((size_t)EB * 4, st), srcpos((size_t)EB * 4, st);
-            k_big_gather<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
-                h, biglist, mrp.as<int>(), coff.as<int>(), boff.as<int>(), keys2.as<unsigned>(),
-                ck2.as<unsigned>(), cidx.as<int>(), crank.as<unsigned>(), cdst.as<int>());
-            FDL_LAUNCH_CK();
-            // srcpos[o] = original position of concatenated element o (= cdst before sorting)
-            FDL_CK(cudaMemcpyAsync(srcpos.p, cdst.p, (size_t)EB * 4, cudaMemcpyDeviceToDevice, st));
-            // LSD radix passes, least significant key first: hi, then (B, lo), then the row rank
-            radix_sort_u32_i32(ck2.as<unsigned>(), cidx.as<int>(), EB, 32, st);
-            k_big_key1_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), srcpos.as<int>(),
-                                                        keys.as<unsigned long long>(), ckey.as<unsigned long long>());
-            FDL_LAUNCH_CK();
-            radix_sort_u64_i32(ckey.as<unsigned long long>(), cidx.as<int>(), EB, 32 + bits_for(c - 1), st);
-            DBuf rank2((size_t)EB * 4, st);
-            k_big_rank_of<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), crank.as<unsigned>(),
-                                                        rank2.as<unsigned>());
-            FDL_LAUNCH_CK();
-            radix_sort_u32_i32(rank2.as<unsigned>(), cidx.as<int>(), EB, bits_for(h - 1), st);
-            DBuf keys_s((size_t)E * 8, st), vals_s((size_t)E * 8, st);
-            k_big_place<<<grid_for(EB), 256, 0, st>>>(EB, cidx.as<int>(), cdst.as<int>(), srcpos.as<int>(),
-                                                      keys.as<unsigned long long>(), vals.as<double>(),
-                                                      keys_s.as<unsigned long long>(), vals_s.as<double>());
-            FDL_LAUNCH_CK();
-            k_big_fold<<<std::min(h, kNumSMs * 8), 256, 0, st>>>(
-                h, biglist, mrp.as<int>(), coff.as<int>(), keys_s.as<unsigned long long>(), vals_s.as<double>(),
-                outB.as<int>(), outW.as<double>(), deg.as<int>());
-            FDL_LAUNCH_CK();
-        }
-        keys.release();
-        keys2.release();
-        vals.release();
-        rowoff.alloc((size_t)c * 4, st);
-        k_row_base<<<grid_for(c), 256, 0, st>>>(c, mrp.as<int>(), coff.as<int>(), rowoff.as<int>());
-        FDL_LAUNCH_CK();
     }
     // 4. CSR assembly
     scan_exclusive(deg.as<int>(), out.own_rp.as<int>(), c, out.own_rp.as<int>() + c, st);
