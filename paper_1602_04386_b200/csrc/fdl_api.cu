@@ -103,6 +103,23 @@ static void check_device(int dev) {
     }
 }
 
+// Grow the stream-ordered pool once to `need` bytes in one piece (the pool
+// keeps freed memory: release threshold = max), so that later creates do not
+// map new physical memory piecemeal in the middle of the setup.
+static void reserve_pool(int dev, size_t need, cudaStream_t st) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t reserved = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) != cudaSuccess) return;
+    if (reserved >= need) return;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return;
+    need = std::min(need, (size_t)(fr * 0.6));
+    void *p = nullptr;
+    if (need > reserved && cudaMallocAsync(&p, need, st) == cudaSuccess) cudaFreeAsync(p, st);
+    (void)cudaGetLastError();
+}
+
 static SolveCfg cfg_of(const fiedler_opts &o) {
     SolveCfg c;
     c.gs = o.gs_sweeps;
@@ -190,6 +207,8 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     h->row_grid = rowpass_grid();
     EventTimer timer(st);
 
+    if (!std::getenv("FIEDLER_NO_POOL_RESERVE"))
+        reserve_pool(o.device, (size_t)(8.0 * ((double)n * 12.0 + (double)nnz * 12.0)), st);
     NatGraph g0;
     g0.n = (int)n;
     g0.nnz = (int)nnz;
