@@ -1,5 +1,5 @@
-// fdl_prims.cu -- hand-written device primitives: exclusive scan (reduce-then-
-// scan, 4096-element tiles, vectorised int4 traffic) and a stable LSD radix
+// fdl_prims.cu -- hand-written device primitives: exclusive scan (single pass,
+// decoupled look-back, 4096-element tiles, vectorised int4 traffic) and a stable LSD radix
 // sort (8-bit digits, 8192-element tiles, warp __match_any_sync ranking).
 // Used by the aggregate numbering (prefix scan of leader flags), work-list and
 // CSR offset scans everywhere, the Galerkin product's long-row path (two-key
@@ -57,49 +57,56 @@ __device__ __forceinline__ void load4(const int *in, int64_t n, int64_t i, int x
     }
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const int *in, int64_t n, int *bsums) {
-    int64_t i = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-    int x[4];
-    load4(in, n, i, x);
-    int s = x[0] + x[1] + x[2] + x[3];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    __shared__ int sw[32];
-    if (lane_id() == 0) sw[threadIdx.x >> 5] = s;
+// Single-pass scan with decoupled look-back: tiles take their index from a
+// counter (a tile's predecessors started earlier: no deadlock), publish their
+// aggregate at once (flag 1) and their inclusive prefix once known (flag 2);
+// warp 0 of a tile looks back 32 predecessors at a time.  status[t] =
+// flag << 32 | value, written atomically; read volatile.  Reads the input once.
+__global__ void __launch_bounds__(kScanThreads) k_scan_lb(const int *in, int *out, int64_t n, int ntiles,
+                                                          unsigned long long *status, int *tile_ctr,
+                                                          int *total) {
+    __shared__ int s_tile, s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1);
     __syncthreads();
-    if (threadIdx.x < 32) {
-        int t = sw[threadIdx.x];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (threadIdx.x == 0) bsums[blockIdx.x] = t;
-    }
-}
-
-// single block: exclusive scan of nb block sums in place; writes total
-__global__ void __launch_bounds__(kScanThreads) k_scan_bsums(int *bsums, int nb, int *total) {
-    int carry = 0;
-    for (int base = 0; base < nb; base += kScanThreads) {
-        int i = base + threadIdx.x;
-        int v = i < nb ? bsums[i] : 0;
-        int tot;
-        int ex = block_excl_scan(v, tot);
-        if (i < nb) bsums[i] = ex + carry;
-        carry += tot;
-    }
-    if (threadIdx.x == 0 && total) *total = carry;
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_final(const int *in, int *out, int64_t n,
-                                                             const int *bsums) {
-    int64_t i = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    const int t = s_tile;
+    const int64_t i = (int64_t)t * kScanTile + (int64_t)threadIdx.x * kScanItems;
     int x[4];
     load4(in, n, i, x);
-    int s = x[0] + x[1] + x[2] + x[3];
+    const int s = x[0] + x[1] + x[2] + x[3];
     int tot;
-    int ex = block_excl_scan(s, tot) + bsums[blockIdx.x];
+    const int ex = block_excl_scan(s, tot);
+    if (threadIdx.x == 0)
+        atomicExch(status + t, (t == 0 ? (2ull << 32) : (1ull << 32)) | (unsigned)tot);
+    if (threadIdx.x < 32) {
+        int prefix = 0;
+        for (int j = t - 1; j >= 0;) {
+            const int idx = j - (int)threadIdx.x;
+            const unsigned long long sv =
+                idx >= 0 ? *reinterpret_cast<volatile unsigned long long *>(status + idx) : (2ull << 32);
+            const unsigned flag = (unsigned)(sv >> 32);
+            const unsigned incl = __ballot_sync(0xffffffffu, flag == 2u);
+            const unsigned inv = __ballot_sync(0xffffffffu, flag == 0u);
+            const int fi = incl ? __ffs(incl) - 1 : 32;
+            const int fz = inv ? __ffs(inv) - 1 : 32;
+            if (fz < fi) continue;   // a nearer predecessor has not published yet: re-read
+            int v = ((int)threadIdx.x <= fi && idx >= 0) ? (int)(unsigned)(sv & 0xffffffffu) : 0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            prefix += v;
+            if (fi < 32) break;
+            j -= 32;
+        }
+        if (threadIdx.x == 0) {
+            s_prefix = prefix;
+            if (t > 0) atomicExch(status + t, (2ull << 32) | (unsigned)(prefix + tot));
+            if (t == ntiles - 1 && total) *total = prefix + tot;
+        }
+    }
+    __syncthreads();
+    const int base = ex + s_prefix;
     int y[4];
-    y[0] = ex;
-    y[1] = ex + x[0];
+    y[0] = base;
+    y[1] = base + x[0];
     y[2] = y[1] + x[1];
     y[3] = y[2] + x[2];
     if (i + 3 < n && ((reinterpret_cast<uintptr_t>(out + i) & 15) == 0)) {
@@ -116,13 +123,12 @@ void scan_exclusive(const int *in, int *out, int64_t n, int *total, cudaStream_t
         if (total) FDL_CK(cudaMemsetAsync(total, 0, sizeof(int), st));
         return;
     }
-    int nb = div_up(n, kScanTile);
-    DBuf bs((size_t)nb * sizeof(int), st);
-    k_scan_reduce<<<nb, kScanThreads, 0, st>>>(in, n, bs.as<int>());
-    FDL_LAUNCH_CK();
-    k_scan_bsums<<<1, kScanThreads, 0, st>>>(bs.as<int>(), nb, total);
-    FDL_LAUNCH_CK();
-    k_scan_final<<<nb, kScanThreads, 0, st>>>(in, out, n, bs.as<int>());
+    const int nb = div_up(n, kScanTile);
+    // status words (8 bytes per tile) followed by the tile counter
+    DBuf ws((size_t)nb * 8 + 16, st);
+    FDL_CK(cudaMemsetAsync(ws.p, 0, (size_t)nb * 8 + 16, st));
+    unsigned long long *status = ws.as<unsigned long long>();
+    k_scan_lb<<<nb, kScanThreads, 0, st>>>(in, out, n, nb, status, reinterpret_cast<int *>(status + nb), total);
     FDL_LAUNCH_CK();
 }
 
