@@ -128,6 +128,9 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 void scan_exclusive(const int *in, int *out, int64_t n, int *total, cudaStream_t st);
 // Stable LSD radix sort of (key, value) pairs on bits [0, bits); result in keys/vals.
 void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStream_t st);
+// stable sort of the vertices by colour (< 256 colours): perm, inv, degree in sorted order, segment starts
+void colour_sort(const int *color, int64_t n, int ncolors, const int *rp, int *perm, int *inv, int *degp,
+                 int *segstart, cudaStream_t st);
 void radix_sort_u64_i32(unsigned long long *keys, int *vals, int64_t n, int bits, cudaStream_t st);
 // Stream compaction: out[k] = (in ? in[i] : i) for the k-th i in [0, n) with
 // flags[i] != 0 (order kept); *d_count (device) = number kept.  flags are 0/1.

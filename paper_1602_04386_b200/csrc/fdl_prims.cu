@@ -202,6 +202,76 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const K *keys, const 
     }
 }
 
+// One stable counting-sort pass of the vertices by colour (colours < 256) that
+// also writes what the GS layout needs from it: perm[pos] = v, inv[v] = pos
+// (coalesced: v is read in order) and degp[pos] = degree of v.
+__global__ void __launch_bounds__(kRsThreads) k_colour_scatter(const unsigned *color, int64_t n, int nb,
+                                                               const int *offs, const int *rp, int *perm,
+                                                               int *inv, int *degp) {
+    __shared__ int s_run[256];
+    __shared__ int s_cnt[kRsWarps][256];
+    s_run[threadIdx.x] = offs[(int64_t)threadIdx.x * nb + blockIdx.x];
+#pragma unroll
+    for (int w = 0; w < kRsWarps; w++) s_cnt[w][threadIdx.x] = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    int64_t base = (int64_t)blockIdx.x * kRsTile;
+    for (int s = 0; s < kRsSub; s++) {
+        if (base + (int64_t)s * kRsThreads >= n) break;  // block-uniform
+        int64_t i = base + (int64_t)s * kRsThreads + threadIdx.x;
+        bool valid = i < n;
+        int d = valid ? (int)(color[i] & 255u) : 256;
+        int dg = valid ? rp[i + 1] - rp[i] : 0;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        int rank = __popc(peers & lt);
+        if (valid && rank == 0) s_cnt[warp][d] = __popc(peers);
+        __syncthreads();
+        {
+            int t = threadIdx.x;
+            int run = s_run[t];
+#pragma unroll
+            for (int w = 0; w < kRsWarps; w++) {
+                int c = s_cnt[w][t];
+                s_cnt[w][t] = run;
+                run += c;
+            }
+            s_run[t] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            int pos = s_cnt[warp][d] + rank;
+            perm[pos] = (int)i;
+            inv[i] = pos;
+            degp[pos] = dg;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < kRsWarps; w++) s_cnt[w][threadIdx.x] = 0;
+        __syncthreads();
+    }
+}
+
+__global__ void k_seg_from_hist(int ncolors, int nb, const int *offs, int *segstart) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncolors; c += gridDim.x * blockDim.x)
+        segstart[c] = offs[(int64_t)c * nb];
+}
+
+void colour_sort(const int *color, int64_t n, int ncolors, const int *rp, int *perm, int *inv, int *degp,
+                 int *segstart, cudaStream_t st) {
+    FDL_REQUIRE(ncolors <= 256 && n < (int64_t(1) << 31), FIEDLER_ERR_INTERNAL, "colour_sort: bad sizes");
+    const int nb = div_up(n, kRsTile);
+    DBuf hist((size_t)256 * nb * sizeof(int), st);
+    const unsigned *keys = reinterpret_cast<const unsigned *>(color);
+    k_rs_hist<unsigned><<<nb, kRsThreads, 0, st>>>(keys, n, 0, nb, hist.as<int>());
+    FDL_LAUNCH_CK();
+    scan_exclusive(hist.as<int>(), hist.as<int>(), (int64_t)256 * nb, nullptr, st);
+    k_colour_scatter<<<nb, kRsThreads, 0, st>>>(keys, n, nb, hist.as<int>(), rp, perm, inv, degp);
+    FDL_LAUNCH_CK();
+    k_seg_from_hist<<<1, 256, 0, st>>>(ncolors, nb, hist.as<int>(), segstart);
+    FDL_LAUNCH_CK();
+}
+
 template <class K, class V>
 static void radix_sort_impl(K *keys, V *vals, int64_t n, int bits, cudaStream_t st) {
     if (n <= 1 || bits <= 0) return;

@@ -2374,20 +2374,26 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     L.nnz = g.nnz;
     L.ncolors = ncolors;
     // ---- GS layout: rows sorted (stably) by colour
-    DBuf keys((size_t)n * 4, st);
     L.perm.alloc((size_t)n * 4, st);
-    k_color_keys<<<grid_for(n), 256, 0, st>>>(n, color_nat, keys.as<unsigned>(), L.perm.as<int>());
-    FDL_LAUNCH_CK();
-    radix_sort_u32_i32(keys.as<unsigned>(), L.perm.as<int>(), n, bits_for(ncolors - 1), st);
-    DBuf segstart((size_t)(ncolors + 1) * 4, st);
-    FDL_CK(cudaMemsetAsync(segstart.p, 0xff, (size_t)(ncolors + 1) * 4, st));
-    k_seg_starts<<<grid_for(n), 256, 0, st>>>(n, keys.as<unsigned>(), segstart.as<int>());
-    FDL_LAUNCH_CK();
-    keys.release();
     L.inv.alloc((size_t)n * 4, st);
     DBuf degp((size_t)n * 4, st);
-    k_inv_and_deg<<<grid_for(n), 256, 0, st>>>(n, L.perm.as<int>(), g.rp, L.inv.as<int>(), degp.as<int>());
-    FDL_LAUNCH_CK();
+    DBuf segstart((size_t)(ncolors + 1) * 4, st);
+    FDL_CK(cudaMemsetAsync(segstart.p, 0xff, (size_t)(ncolors + 1) * 4, st));
+    if (ncolors <= 256) {
+        // one counting-sort pass: perm, inv, degrees and segment starts together
+        colour_sort(color_nat, n, ncolors, g.rp, L.perm.as<int>(), L.inv.as<int>(), degp.as<int>(),
+                    segstart.as<int>(), st);
+    } else {
+        DBuf keys((size_t)n * 4, st);
+        k_color_keys<<<grid_for(n), 256, 0, st>>>(n, color_nat, keys.as<unsigned>(), L.perm.as<int>());
+        FDL_LAUNCH_CK();
+        radix_sort_u32_i32(keys.as<unsigned>(), L.perm.as<int>(), n, bits_for(ncolors - 1), st);
+        k_seg_starts<<<grid_for(n), 256, 0, st>>>(n, keys.as<unsigned>(), segstart.as<int>());
+        FDL_LAUNCH_CK();
+        keys.release();
+        k_inv_and_deg<<<grid_for(n), 256, 0, st>>>(n, L.perm.as<int>(), g.rp, L.inv.as<int>(), degp.as<int>());
+        FDL_LAUNCH_CK();
+    }
     L.rp.alloc((size_t)(n + 1) * 4 + kPadBytes, st);
     scan_exclusive(degp.as<int>(), L.rp.as<int>(), n, L.rp.as<int>() + n, st);
     degp.release();
