@@ -876,13 +876,22 @@ __device__ __forceinline__ int gal_class(int nm, int T) {
     return 3;
 }
 
-__global__ void k_gal_classify(int c, const int *mrp, const int *toff, int *f32, int *fmid, int *fbig) {
-    for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
-        const int nm = mrp[A + 1] - mrp[A], T = toff[A + 1] - toff[A];
-        const int k = gal_class(nm, T);
-        f32[A] = k == 1;
-        fmid[A] = k == 2;
-        fbig[A] = k == 3;
+// lists of the rows of classes 1, 2, 3 (warp-aggregated appends; the list
+// order is irrelevant: every row's result and place are its own)
+__global__ void k_gal_classify(int c, const int *mrp, const int *toff, int *l1, int *l2, int *l3, int *cnt) {
+    for (int A0 = blockIdx.x * blockDim.x; A0 < c; A0 += gridDim.x * blockDim.x) {   // warp-uniform
+        const int A = A0 + threadIdx.x;
+        int k = 0;
+        if (A < c) k = gal_class(mrp[A + 1] - mrp[A], toff[A + 1] - toff[A]);
+#pragma unroll
+        for (int q = 1; q <= 3; q++) {
+            const unsigned bal = __ballot_sync(0xffffffffu, k == q);
+            if (!bal) continue;
+            int base = 0;
+            if (lane_id() == 0) base = atomicAdd(cnt + q - 1, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (k == q) (q == 1 ? l1 : q == 2 ? l2 : l3)[base + __popc(bal & ((1u << lane_id()) - 1u))] = A;
+        }
     }
 }
 
@@ -1411,17 +1420,11 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     int dc[3] = {0, 0, 0};
     DBuf dl((size_t)c * 4 * 3, st), dcnt(16, st);
     FDL_CK(cudaMemsetAsync(dcnt.p, 0, 16, st));
-    {
-        DBuf f32((size_t)c * 4, st), fmid((size_t)c * 4, st), fbig((size_t)c * 4, st);
-        k_gal_classify<<<grid_for(c), 256, 0, st>>>(c, mrp.as<int>(), toff.as<int>(), f32.as<int>(),
-                                                    fmid.as<int>(), fbig.as<int>());
-        FDL_LAUNCH_CK();
-        compact_flagged(nullptr, f32.as<int>(), c, dl.as<int>(), dcnt.as<int>(), st);
-        compact_flagged(nullptr, fmid.as<int>(), c, dl.as<int>() + c, dcnt.as<int>() + 1, st);
-        compact_flagged(nullptr, fbig.as<int>(), c, dl.as<int>() + 2 * c, dcnt.as<int>() + 2, st);
-        FDL_CK(cudaMemcpyAsync(dc, dcnt.p, 12, cudaMemcpyDeviceToHost, st));
-        FDL_CK(cudaStreamSynchronize(st));
-    }
+    k_gal_classify<<<grid_for(c), 256, 0, st>>>(c, mrp.as<int>(), toff.as<int>(), dl.as<int>(),
+                                                dl.as<int>() + c, dl.as<int>() + 2 * c, dcnt.as<int>());
+    FDL_LAUNCH_CK();
+    FDL_CK(cudaMemcpyAsync(dc, dcnt.p, 12, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaStreamSynchronize(st));
     {
         // rows ascend: input contract.  FIEDLER_TEST_FULL_SORT=1 (tests) forces
         // the fallback that very large levels take
