@@ -244,6 +244,15 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     build_hierarchy(*h, std::move(g0));
     prepare_solve(*h, cfg_of(o));
     trace_mark(st, "create: prepare_solve");
+    if (trace_enabled()) {
+        cudaMemPool_t pool;
+        uint64_t hi = 0, res = 0;
+        if (cudaDeviceGetDefaultMemPool(&pool, o.device) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &hi) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res) == cudaSuccess)
+            std::fprintf(stderr, "[fiedler trace] pool: used high %.2f GB, reserved %.2f GB, input %.2f GB\n",
+                         hi * 1e-9, res * 1e-9, ((double)n * 12.0 + (double)nnz * 12.0) * 1e-9);
+    }
     h->setup_launches = (int)(g_launch_count - l0);
     h->setup_ms = timer.stop_ms();
     *out = reinterpret_cast<fiedler_handle>(h.release());
