@@ -876,22 +876,24 @@ __device__ __forceinline__ int gal_class(int nm, int T) {
     return 3;
 }
 
-// lists of the rows of classes 1, 2, 3 (warp-aggregated appends; the list
-// order is irrelevant: every row's result and place are its own)
-__global__ void k_gal_classify(int c, const int *mrp, const int *toff, int *l1, int *l2, int *l3, int *cnt) {
-    for (int A0 = blockIdx.x * blockDim.x; A0 < c; A0 += gridDim.x * blockDim.x) {   // warp-uniform
+// lists of the rows of classes 1, 2, 3 (CTA-aggregated appends: shared-memory
+// counters, one global atomic per class and block; the list order is
+// irrelevant: every row's result and place are its own)
+__global__ void __launch_bounds__(256) k_gal_classify(int c, const int *mrp, const int *toff, int *l1, int *l2,
+                                                      int *l3, int *cnt) {
+    __shared__ int s_cnt[3], s_base[3];
+    for (int A0 = blockIdx.x * blockDim.x; A0 < c; A0 += gridDim.x * blockDim.x) {   // block-uniform
+        if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+        __syncthreads();
         const int A = A0 + threadIdx.x;
-        int k = 0;
+        int k = 0, li = 0;
         if (A < c) k = gal_class(mrp[A + 1] - mrp[A], toff[A + 1] - toff[A]);
-#pragma unroll
-        for (int q = 1; q <= 3; q++) {
-            const unsigned bal = __ballot_sync(0xffffffffu, k == q);
-            if (!bal) continue;
-            int base = 0;
-            if (lane_id() == 0) base = atomicAdd(cnt + q - 1, __popc(bal));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (k == q) (q == 1 ? l1 : q == 2 ? l2 : l3)[base + __popc(bal & ((1u << lane_id()) - 1u))] = A;
-        }
+        if (k > 0) li = atomicAdd(&s_cnt[k - 1], 1);
+        __syncthreads();
+        if (threadIdx.x < 3 && s_cnt[threadIdx.x]) s_base[threadIdx.x] = atomicAdd(cnt + threadIdx.x, s_cnt[threadIdx.x]);
+        __syncthreads();
+        if (k > 0) (k == 1 ? l1 : k == 2 ? l2 : l3)[s_base[k - 1] + li] = A;
+        __syncthreads();
     }
 }
 
