@@ -740,11 +740,22 @@ __global__ void __launch_bounds__(256) k_prolong(int n, const int *__restrict__ 
                                                  const double *__restrict__ xc, double *__restrict__ y,
                                                  double *slot, double *partials, unsigned *counter) {
     double st[kNumStats] = {0.0, 0.0, 0.0};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        double v = __ldg(xc + __ldcs(qp + i));
-        y[i] = v;
-        st[0] += v;
-        st[1] = fma(v, v, st[1]);
+    const int stride = gridDim.x * blockDim.x;
+    // 4 entries per thread in flight; statistics still summed in i order per thread
+    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+        int q[4];
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) q[u] = i0 + u * stride < n ? __ldcs(qp + i0 + u * stride) : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = q[u] >= 0 ? __ldg(xc + q[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (q[u] >= 0) {
+                y[i0 + u * stride] = v[u];
+                st[0] += v[u];
+                st[1] = fma(v[u], v[u], st[1]);
+            }
     }
     grid_reduce(st, partials, counter, [&](const double *tot) { finish_stats(tot, slot, 3, n); });
 }
@@ -784,8 +795,18 @@ __global__ void k_sign(int n, const double *__restrict__ z, const double *slot, 
 // GS numbering -> natural numbering: dst[v] = src[inv[v]] (coalesced writes)
 __global__ void __launch_bounds__(256) k_gs_to_nat(int n, const int *__restrict__ inv,
                                                    const double *__restrict__ src, double *__restrict__ dst) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        dst[v] = __ldg(src + __ldcs(inv + v));
+    const int stride = gridDim.x * blockDim.x;
+    for (int v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < n; v0 += 4 * stride) {   // 4 gathers in flight
+        int p[4];
+        double x[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) p[u] = v0 + u * stride < n ? __ldcs(inv + v0 + u * stride) : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++) x[u] = p[u] >= 0 ? __ldg(src + p[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (p[u] >= 0) dst[v0 + u * stride] = x[u];
+    }
 }
 
 __global__ void k_set_slot(double *slot, double mu, double sigma) {
