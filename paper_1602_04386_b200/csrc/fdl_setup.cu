@@ -489,25 +489,48 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
     if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
 }
 
+// leader of v's aggregate (4 vertices per thread with their loads in flight)
 __global__ void k_leaders(int n, const int *m, const int *mate, int *leader, int *flag, int *err) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        int L;
-        int mv = mate[v];
-        if (mv >= 0) L = min(v, mv);
-        else if (m[v] >= 0) {
-            int u = m[v];
-            int mu = mate[u];
-            if (mu < 0) { atomicOr(err, 1); mu = u; }   // impossible for a maximal matching
-            L = min(u, mu);
-        } else L = v;
-        leader[v] = L;
-        flag[v] = (L == v);
+    const int stride = gridDim.x * blockDim.x;
+    for (int v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < n; v0 += 4 * stride) {
+        int mv[4], mm[4], mu[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int v = v0 + u * stride;
+            mv[u] = v < n ? mate[v] : 0;
+            mm[u] = v < n ? m[v] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) mu[u] = (mv[u] < 0 && mm[u] >= 0) ? mate[mm[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int v = v0 + u * stride;
+            if (v >= n) continue;
+            int L;
+            if (mv[u] >= 0) L = min(v, mv[u]);
+            else if (mm[u] >= 0) {
+                int x = mu[u];
+                if (x < 0) { atomicOr(err, 1); x = mm[u]; }   // impossible for a maximal matching
+                L = min(mm[u], x);
+            } else L = v;
+            leader[v] = L;
+            flag[v] = (L == v);
+        }
     }
 }
 
 __global__ void k_assign(int n, const int *leader, const int *id, int *q) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-        q[v] = id[leader[v]];
+    const int stride = gridDim.x * blockDim.x;
+    for (int v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < n; v0 += 4 * stride) {
+        int L[4], r[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) L[u] = v0 + u * stride < n ? leader[v0 + u * stride] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++) r[u] = L[u] >= 0 ? id[L[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (L[u] >= 0) q[v0 + u * stride] = r[u];
+    }
 }
 
 static int read_int(const int *dptr, cudaStream_t st) {
@@ -2525,8 +2548,17 @@ static bool coarsest_connected(const Level &L, cudaStream_t st) {
 }
 
 __global__ void k_compose_qg(int n, const int *perm, const int *q_nat, int *qg) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-        qg[t] = q_nat[perm[t]];
+    const int stride = gridDim.x * blockDim.x;
+    for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < n; t0 += 4 * stride) {   // 4 gathers in flight
+        int p[4], r[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) p[u] = t0 + u * stride < n ? perm[t0 + u * stride] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; u++) r[u] = p[u] >= 0 ? q_nat[p[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (p[u] >= 0) qg[t0 + u * stride] = r[u];
+    }
 }
 
 void build_hierarchy(Handle &h, NatGraph &&g0) {
