@@ -106,6 +106,10 @@ static void check_device(int dev) {
 // Grow the stream-ordered pool once to `need` bytes in one piece (the pool
 // keeps freed memory: release threshold = max), so that later creates do not
 // map new physical memory piecemeal in the middle of the setup.
+#ifndef FDL_POOL_FACTOR
+#define FDL_POOL_FACTOR 8.0
+#endif
+constexpr double kPoolFactor = FDL_POOL_FACTOR;
 static void reserve_pool(int dev, size_t need, cudaStream_t st) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
@@ -208,7 +212,7 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     EventTimer timer(st);
 
     if (!std::getenv("FIEDLER_NO_POOL_RESERVE"))
-        reserve_pool(o.device, (size_t)(8.0 * ((double)n * 12.0 + (double)nnz * 12.0)), st);
+        reserve_pool(o.device, (size_t)(kPoolFactor * ((double)n * 12.0 + (double)nnz * 12.0)), st);
     NatGraph g0;
     g0.n = (int)n;
     g0.nnz = (int)nnz;

@@ -12,5 +12,5 @@ os.makedirs(out, exist_ok=True)
 for v in VARIANTS:
     tag = "_".join("%s%d" % (k.replace("FDL_", ""), x) for k, x in v.items())
     name = os.path.join(out, "libfiedler_%s.so" % tag)
-    b.build(defines=tuple("%s=%d" % (k, x) for k, x in v.items()), out=name)
+    b.build(defines=tuple("%s=%s" % (k, x) for k, x in v.items()), out=name)
     print(name)
