@@ -110,6 +110,9 @@ static void check_device(int dev) {
 #define FDL_POOL_FACTOR 8.0
 #endif
 constexpr double kPoolFactor = FDL_POOL_FACTOR;
+#ifndef FDL_STREAM2_PRIO
+#define FDL_STREAM2_PRIO 0
+#endif
 static void reserve_pool(int dev, size_t need, cudaStream_t st) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
@@ -207,7 +210,12 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
         h->own_stream = true;
     }
     cudaStream_t st = h->stream;
-    FDL_CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+    {   // stream2 priority (build knob FDL_STREAM2_PRIO: 0 default, 1 highest, -1 lowest)
+        int lo = 0, hi = 0;
+        FDL_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const int pr = FDL_STREAM2_PRIO > 0 ? hi : FDL_STREAM2_PRIO < 0 ? lo : 0;
+        FDL_CK(cudaStreamCreateWithPriority(&h->stream2, cudaStreamNonBlocking, pr));
+    }
     h->row_grid = rowpass_grid();
     EventTimer timer(st);
 

@@ -173,10 +173,10 @@ constexpr int kMaxRounds = 1 << 16;
 constexpr int kMatchUnroll = FDL_MATCH_UNROLL;
 // the matching and the colouring (second stream) are both cooperative: each
 // takes part of the co-resident grid so that they can run side by side
-#ifndef FDL_MATCH_GRID_DIV
-#define FDL_MATCH_GRID_DIV 2
+#ifndef FDL_MATCH_GRID_FRAC
+#define FDL_MATCH_GRID_FRAC 0.5
 #endif
-constexpr int kMatchGridDiv = FDL_MATCH_GRID_DIV;
+constexpr double kMatchGridFrac = FDL_MATCH_GRID_FRAC;
 static_assert(kAppendCap >= 2 * kMatchUnroll * kCoopThreads, "append buffer too small");   // JP depth can reach thousands on dense cores
 
 // FIEDLER_TRACE: per-phase device timestamps of the cooperative kernels
@@ -575,7 +575,7 @@ struct RoundTrace {
 
 // cooperative launch with every CTA co-resident (grid = SMs x resident CTAs)
 template <class K>
-static void coop_launch(K kernel, void **args, cudaStream_t st, int grid_div = 1) {
+static void coop_launch(K kernel, void **args, cudaStream_t st, double grid_frac = 1.0) {
     static int grid = 0;   // one cache per kernel instantiation
     if (!grid) {
         int per_sm = 0, dev = 0, sms = kNumSMs;
@@ -590,7 +590,7 @@ static void coop_launch(K kernel, void **args, cudaStream_t st, int grid_div = 1
     // the kernels are grid-size agnostic: if the driver finds fewer co-resident
     // CTAs than the occupancy query promised, retry with a smaller grid
     for (;;) {
-        cudaError_t e = cudaLaunchCooperativeKernel((const void *)kernel, dim3(std::max(1, grid / grid_div)),
+        cudaError_t e = cudaLaunchCooperativeKernel((const void *)kernel, dim3(std::max(1, (int)(grid * grid_frac))),
                                                     dim3(kCoopThreads), args, 0, st);
         if (e == cudaErrorCooperativeLaunchTooLarge && grid > kNumSMs) {
             (void)cudaGetLastError();
@@ -626,7 +626,7 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
         int *plm = lmv.as<int>(), *pmc = mcount.as<int>();
         void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr, &plm, &pmc};
         RoundTrace tr(st, "match");
-        DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st, kMatchGridDiv));
+        DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st, kMatchGridFrac));
         tr.report(counts.as<int>());
     }
     rounds = read_int(counts.as<int>() + kMaxRounds, st);
@@ -2154,10 +2154,10 @@ __global__ void __launch_bounds__(kSmallColourThreads, 1) k_color_cluster(int n,
 // The colouring of a level runs on the handle's second stream, overlapped with
 // the matching / Galerkin chain of the coarser levels on the main stream; its
 // colour count is read back only when the level's layout is built.
-#ifndef FDL_COLOUR_GRID_DIV
-#define FDL_COLOUR_GRID_DIV 3
+#ifndef FDL_COLOUR_GRID_FRAC
+#define FDL_COLOUR_GRID_FRAC 0.3333
 #endif
-constexpr int kColourGridDiv = FDL_COLOUR_GRID_DIV;
+constexpr double kColourGridFrac = FDL_COLOUR_GRID_FRAC;
 
 struct ColourJob {
     DBuf la, lb, indeg, counts, mx;
@@ -2237,7 +2237,7 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             // both cooperative kernels fit side by side with room for the rest
             // of the coarsening chain (a full-grid cooperative launch would wait
             // for the other one to drain)
-            DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridDiv));
+            DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridFrac));
             tr.report(job.counts.as<int>());
         }
     }
@@ -2563,6 +2563,10 @@ __global__ void k_compose_qg(int n, const int *perm, const int *q_nat, int *qg) 
 
 void build_hierarchy(Handle &h, NatGraph &&g0) {
     cudaStream_t st = h.stream, sb = h.stream2;
+    {   // FIEDLER_SERIAL_COLOUR=1 (diagnostics): colourings on the main stream
+        const char *e = std::getenv("FIEDLER_SERIAL_COLOUR");
+        if (e && e[0] == '1') sb = st;
+    }
     const fiedler_opts &o = h.opts;
     NatGraph cur = std::move(g0);
     h.levels.clear();

@@ -10,7 +10,7 @@ VARIANTS = eval(sys.argv[1]) if len(sys.argv) > 1 else [dict(FDL_HEAVY_DEG=64), 
 out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build_variants")
 os.makedirs(out, exist_ok=True)
 for v in VARIANTS:
-    tag = "_".join("%s%d" % (k.replace("FDL_", ""), x) for k, x in v.items())
+    tag = "_".join("%s%s" % (k.replace("FDL_", ""), x) for k, x in v.items())
     name = os.path.join(out, "libfiedler_%s.so" % tag)
     b.build(defines=tuple("%s=%s" % (k, x) for k, x in v.items()), out=name)
     print(name)
