@@ -28,6 +28,12 @@
  *     L = D - W (Definition 2.1).  nnz counts both directions.
  *   - `mem` arguments say where a pointer lives: FIEDLER_MEM_HOST (pageable or
  *     pinned host memory) or FIEDLER_MEM_DEVICE (memory of opts->device).
+ *   - Device memory comes from the device's default stream-ordered pool; the
+ *     library sets its release threshold to "keep everything" and grows it once
+ *     per fiedler_create to ~8x the input size (FIEDLER_NO_POOL_RESERVE=1 skips
+ *     that).  Environment, diagnostics only: FIEDLER_TRACE=1 (phase times on
+ *     stderr), FIEDLER_SERIAL_COLOUR=1 (colourings on the main stream),
+ *     FIEDLER_TEST_FULL_SORT=1 (the Galerkin fallback of very large levels).
  *     Input buffers are only read and never retained after the call returns
  *     (fiedler_create copies what it needs); output buffers are caller-owned.
  *   - Every call returns FIEDLER_OK (0) or a negative FIEDLER_ERR_* code and
