@@ -874,7 +874,10 @@ static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0
     FDL_CK(cudaLaunchKernelEx(&cfg, k_gs_multi<true>, v, seg, c0, c1, sweeps, x, slot, mode, n));
 }
 
-constexpr double kDenseRowDeg = 12.0;   // rows per tile few enough for sub-warp rows
+#ifndef FDL_DENSE_ROW_DEG
+#define FDL_DENSE_ROW_DEG 7.0
+#endif
+constexpr double kDenseRowDeg = FDL_DENSE_ROW_DEG;   // rows per tile few enough for sub-warp rows
 static int g_pass_grid[4] = {0, 0, 0, 0};
 static int pass_grid(int op) { return g_pass_grid[op]; }
 
