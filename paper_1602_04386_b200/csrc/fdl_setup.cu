@@ -2487,7 +2487,10 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
         L.gs_tail_c0 = c0;
         // colours before the tail: a grid-wide tile pass each, except runs of
         // small colours (<= kClusterColourRows rows), one cluster launch per run
-        constexpr int kClusterColourRows = 16384;
+#ifndef FDL_CLUSTER_COLOUR_ROWS
+#define FDL_CLUSTER_COLOUR_ROWS 4096
+#endif
+        constexpr int kClusterColourRows = FDL_CLUSTER_COLOUR_ROWS;
         L.gs_runs.clear();
         for (int c = 0; c < c0;) {
             int e = c;
