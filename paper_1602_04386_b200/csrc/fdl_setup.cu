@@ -2479,7 +2479,10 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     // trailing colours small enough for the single-CTA GS kernel (<= kGsTailRows rows
     // and nonzeros small enough together); a whole small level qualifies
     {
-        constexpr int kGsTailRows = 16384;
+#ifndef FDL_GS_TAIL_ROWS
+#define FDL_GS_TAIL_ROWS 1024
+#endif
+        constexpr int kGsTailRows = FDL_GS_TAIL_ROWS;
         int c0 = ncolors;
         while (c0 > 0 && seg[ncolors] - seg[c0 - 1] <= kGsTailRows &&
                (long long)segnnz[ncolors] - segnnz[c0 - 1] <= 16LL * kGsTailRows)

@@ -833,7 +833,10 @@ __global__ void k_normalise(int n, double *z, const double *slot) {
 // ----------------------------------------------------------------- host-side schedule
 constexpr size_t kPassSmemBytes = sizeof(PassSmem);
 
-constexpr int kSmallPiRows = 4096;   // levels this small run all power steps in one CTA
+#ifndef FDL_SMALL_PI_ROWS
+#define FDL_SMALL_PI_ROWS 1024
+#endif
+constexpr int kSmallPiRows = FDL_SMALL_PI_ROWS;   // levels this small run all power steps in one CTA
 constexpr int kSmallPiNnz = 1 << 18;  // ... unless dense: one CTA streams ~0.1 TB/s
 
 // CTAs of a pass: resident CTAs per SM x SMs (persistent tile loop), per OP
