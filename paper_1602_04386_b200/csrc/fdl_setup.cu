@@ -1849,7 +1849,10 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
 constexpr int kSmallColourN = 12288;
 constexpr int kSmallColourThreads = 1024;
 constexpr int kSmallChunk = 64;
-constexpr double kSmallColourMinDeg = 64.0;   // sparse small levels: the grid kernel is faster
+#ifndef FDL_SMALL_COLOUR_MINDEG
+#define FDL_SMALL_COLOUR_MINDEG 64.0
+#endif
+constexpr double kSmallColourMinDeg = FDL_SMALL_COLOUR_MINDEG;   // sparse small levels: the grid kernel is faster
 __global__ void __launch_bounds__(kSmallColourThreads, 1) k_color_small(int n, const int *rp, const int *ci,
                                                                           uint64_t salt, int *color,
                                                                           int *rounds_out) {
