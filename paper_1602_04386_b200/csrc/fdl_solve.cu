@@ -556,7 +556,10 @@ __device__ __forceinline__ void cta_sum2(double &a, double &b, double (*sm)[2]) 
 // (__ldcg) because other CTAs of the cluster rewrite it.  Statistics of the
 // last sweep: one pass over the rows in a fixed order, reduced over the
 // cluster in rank order (deterministic).
-constexpr int kGcThreads = 512;
+#ifndef FDL_GC_THREADS
+#define FDL_GC_THREADS 512
+#endif
+constexpr int kGcThreads = FDL_GC_THREADS;
 constexpr int kGcWarps = kGcThreads / 32;
 constexpr int kGcLong = 2048;
 constexpr int kGcMaxCluster = 16;
