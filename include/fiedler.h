@@ -40,9 +40,18 @@
  *     leaves a human-readable message for fiedler_last_error() (thread-local).
  *     No call falls back to a CPU path: without a usable sm_100 device every
  *     call that needs one fails with FIEDLER_ERR_CUDA.
- *   - Work is issued on opts->stream (a cudaStream_t; NULL = a stream owned by
- *     the handle) and the calls return after that stream has finished the
- *     call's work (results are ready on return).
+ *   - Every handle issues its work on a stream it owns (created by
+ *     fiedler_create, destroyed by fiedler_destroy; all of the handle's device
+ *     buffers are allocated and freed in that stream's order).  A caller's
+ *     stream in opts->stream (a cudaStream_t, may differ between calls) is
+ *     joined with events: the call's work starts after the work already
+ *     enqueued on it and later work on it runs after the call's.  Calls other
+ *     than fiedler_dist_op return after the call's work has finished
+ *     (results are ready on return).
+ *   - A handle is not thread-safe: calls on one handle must not overlap in
+ *     time (one host thread at a time), and the fiedler_dist_op work of one
+ *     handle must be serialised on one stream -- every call shares the
+ *     handle's partial-sum scratch and its last-CTA counter.
  */
 #ifndef FIEDLER_H
 #define FIEDLER_H
@@ -250,7 +259,11 @@ FIEDLER_API int fiedler_dist_plan(fiedler_handle h, int32_t level, int32_t nrank
 #define FIEDLER_DOP_HALO_UNPACK 12  /* y at the ghost rows = x (recv buffer); arg 0: y natural, 1: GS    */
 
 /* Enqueue one operation of the partitioned solve on `stream` (NULL = the
- * handle's stream) for the plan last built on `level`.  Never synchronises.
+ * handle's stream) for the plan last built on `level`.  Never synchronises
+ * `stream` (the first call may wait for the handle's own stream while it
+ * allocates the handle's scratch).  All fiedler_dist_op calls of a handle,
+ * and its fiedler_solve / fiedler_level_* calls, must be serialised on one
+ * stream: they share the handle's reduction scratch (see the notes above).
  * x / y / stat / stat_in / sign_slot: device pointers (unused ones may be
  * NULL).  Errors: ARG (no plan on level, bad op), CUDA. */
 FIEDLER_API int fiedler_dist_op(fiedler_handle h, int32_t level, int32_t op, int64_t arg,

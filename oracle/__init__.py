@@ -255,8 +255,13 @@ def prolongate(q: np.ndarray, yc: np.ndarray) -> np.ndarray:
 
 
 def shift_of(d: np.ndarray) -> float:
-    """Shift c of c I - L: Gershgorin bound 2 max_i d_i >= lambda_max (reading R8)."""
-    return 2.0 * float(d.max()) if d.size else 0.0
+    """Shift c of c I - L: Gershgorin bound 2 max_i d_i >= lambda_max (reading R8).
+    On a 2-vertex level (K2) the bound is attained, 2 max d = lambda_max, and
+    c I - L would map the only non-constant direction -- the Fiedler vector --
+    to zero; there c = 3 max d (R8)."""
+    if not d.size:
+        return 0.0
+    return (3.0 if d.size == 2 else 2.0) * float(d.max())
 
 
 def sign_fix(v: np.ndarray) -> np.ndarray:

@@ -27,18 +27,23 @@ def build(force=False, verbose=False, defines=(), out=None):
     lib = out or LIB
     if not force and not defines and not _stale():
         return LIB
-    objs = []
-    logs = []
-    for src in SOURCES:
-        tag = "" if not defines else "_" + "_".join(d.replace("=", "") for d in defines)
+    from concurrent.futures import ThreadPoolExecutor
+    tag = "" if not defines else "_" + "_".join(d.replace("=", "") for d in defines)
+
+    def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", tag + ".o"))
         cmd = [NVCC] + FLAGS + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("nvcc failed on %s" % src)
-        objs.append(obj)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    logs = []
+    with ThreadPoolExecutor(len(SOURCES)) as ex:     # one nvcc per translation unit
+        for src, obj, r in ex.map(compile_one, SOURCES):
+            logs.append(r.stdout + r.stderr)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError("nvcc failed on %s" % src)
+            objs.append(obj)
     tmp = lib + ".tmp%d" % os.getpid()
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-o", tmp] + objs

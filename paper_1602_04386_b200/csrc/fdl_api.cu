@@ -50,11 +50,29 @@ Handle::~Handle() {
         cudaStreamDestroy(stream2);
     }
     if (ev_pattern) cudaEventDestroy(ev_pattern);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
 void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32, cudaStream_t st);
 int rowpass_grid();
+
+// Orders the handle's own stream after the caller's stream on entry (the
+// caller's inputs) and the caller's stream after the handle's on exit (the
+// results): the work of one call looks stream-ordered on the caller's stream.
+struct StreamJoin {
+    cudaEvent_t ev;
+    cudaStream_t user, own;
+    StreamJoin(cudaEvent_t e, cudaStream_t u, cudaStream_t o) : ev(e), user(u && u != o ? u : nullptr), own(o) {
+        if (!user) return;
+        FDL_CK(cudaEventRecord(ev, user));
+        FDL_CK(cudaStreamWaitEvent(own, ev, 0));
+    }
+    ~StreamJoin() {
+        if (!user) return;
+        if (cudaEventRecord(ev, own) == cudaSuccess) cudaStreamWaitEvent(user, ev, 0);
+    }
+};
 
 struct EventTimer {
     cudaEvent_t a = nullptr, b = nullptr;
@@ -79,7 +97,7 @@ struct EventTimer {
 
 static void check_device(int dev) {
     // the capability check runs once per device (cudaGetDeviceProperties costs ~10 ms)
-    static int checked[64] = {0};
+    static DeviceCache checked{};
     int count = 0;
     FDL_CK(cudaGetDeviceCount(&count));
     FDL_REQUIRE(dev >= 0 && dev < count && dev < 64, FIEDLER_ERR_CUDA, "no such CUDA device");
@@ -91,16 +109,13 @@ static void check_device(int dev) {
     FDL_REQUIRE(major == 10, FIEDLER_ERR_CUDA,
                 "libfiedler is built for sm_100a (B200); device is sm_" + std::to_string(major) +
                     std::to_string(minor));
-    checked[dev] = 1;
-    static bool pool_done = false;
-    if (!pool_done) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        pool_done = true;
+    // this device's default pool keeps freed memory (release threshold = max)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    checked[dev].store(1);
 }
 
 // Grow the stream-ordered pool once to `need` bytes in one piece (the pool
@@ -202,14 +217,14 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     std::unique_ptr<Handle> h(new Handle());
     h->device = o.device;
     h->opts = o;
-    if (o.stream) {
-        h->stream = (cudaStream_t)o.stream;
-        h->own_stream = false;
-    } else {
-        FDL_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-        h->own_stream = true;
-    }
+    // The handle always works on a stream of its own: every device buffer it
+    // allocates is freed on that stream, which lives until fiedler_destroy.  A
+    // caller's stream (opts->stream) is joined with events (StreamJoin).
+    FDL_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+    FDL_CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     cudaStream_t st = h->stream;
+    StreamJoin join(h->ev_join, (cudaStream_t)o.stream, st);
     {   // stream2 priority (build knob FDL_STREAM2_PRIO: 0 default, 1 highest, -1 lowest)
         int lo = 0, hi = 0;
         FDL_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -283,14 +298,8 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
     fiedler_opts o = opts ? *opts : h.opts;
     FDL_REQUIRE(o.gs_sweeps >= 0 && o.power_iters >= 0, FIEDLER_ERR_ARG, "invalid options");
     FDL_CK(cudaSetDevice(h.device));
-    if (opts && opts->stream && (cudaStream_t)opts->stream != h.stream) {
-        FDL_CK(cudaStreamSynchronize(h.stream));
-        if (h.own_stream) FDL_CK(cudaStreamDestroy(h.stream));
-        h.stream = (cudaStream_t)opts->stream;
-        h.own_stream = false;
-        if (h.gexec) { cudaGraphExecDestroy(h.gexec); h.gexec = nullptr; }
-    }
     cudaStream_t st = h.stream;
+    StreamJoin join(h.ev_join, opts ? (cudaStream_t)opts->stream : nullptr, st);
     SolveCfg cfg = cfg_of(o);
     prepare_solve(h, cfg);
     trace_mark(st, "solve: enter");
@@ -360,9 +369,8 @@ int fiedler_destroy(fiedler_handle hh) {
     Handle *h = reinterpret_cast<Handle *>(hh);
     cudaSetDevice(h->device);
     trace_mark(nullptr, "destroy: enter");
-    cudaStream_t st = h->own_stream ? nullptr : h->stream;
     delete h;
-    trace_mark(st, "destroy: done");
+    trace_mark(nullptr, "destroy: done");
     return FIEDLER_OK;
     API_END
 }

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -112,6 +113,17 @@ __device__ __forceinline__ uint64_t edge_hash(uint64_t salt, int a, int b) {
 
 // ----------------------------------------------------------------- launch helpers
 constexpr int kNumSMs = 148;
+
+// Per-device caches of launch configurations and function attributes (each
+// device needs its own cudaFuncSetAttribute calls).  Lock-free: racing threads
+// compute the same value.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+    return d;
+}
+using DeviceCache = std::atomic<int>[kMaxDevices];
 inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 inline int grid_for(int64_t threads, int block = 256, int cap = kNumSMs * 32) {
     int64_t g = (threads + block - 1) / block;

@@ -89,7 +89,7 @@ struct Level {
     DistPlan dist;
     int ncolors = 0;
     int ntiles = 0;
-    double shift = 0.0;      // c of c I - L: 2 max_i d_i (R8)
+    double shift = 0.0;      // c of c I - L: 2 max_i d_i, 3 max_i d_i when n == 2 (R8)
     int match_rounds = 0;
     int color_rounds = 0;
     int gs_tile_begin(int c) const { return ctile[c]; }
@@ -99,9 +99,10 @@ struct Level {
 struct Handle {
     int device = 0;
     cudaStream_t stream = nullptr;
-    bool own_stream = false;
+    bool own_stream = false;          // always true: the handle owns `stream` (fdl_api.cu)
     cudaStream_t stream2 = nullptr;   // setup: colourings overlapped with the coarsening chain
     cudaEvent_t ev_pattern = nullptr; // host input: level-0 pattern (rp, ci) on the device
+    cudaEvent_t ev_join = nullptr;    // joins a caller's stream with `stream` (fdl_api.cu StreamJoin)
     fiedler_opts opts{};
     std::vector<Level> levels;
     int n0 = 0;

@@ -212,6 +212,15 @@ struct CtaAppend {
         if (p < kAppendCap) buf[p] = v;
         else out[atomicAdd(gcount, 1)] = v;
     }
+    // all threads, after a __syncthreads(): whether more than thr entries are
+    // buffered.  Every thread reads the count before the barrier inside, so a
+    // fast warp's next push cannot make the threads disagree (the decision
+    // guards barriers).
+    __device__ __forceinline__ bool due(int thr) {
+        const int x = *n;
+        __syncthreads();
+        return x > thr;
+    }
     // all threads; call after __syncthreads()
     __device__ __forceinline__ void flush(int *out, int *gcount) {
         const int cnt = min(*n, kAppendCap);
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
             if (bj >= 0) app.push(v);
         }
         __syncthreads();
-        if (s_n > kAppendCap - kCoopThreads) app.flush(la, counts);
+        if (app.due(kAppendCap - kCoopThreads)) app.flush(la, counts);
     }
     __syncthreads();
     app.flush(la, counts);
@@ -425,7 +434,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
                     if (keep) app.push(v[u]);
                 }
                 __syncthreads();
-                if (s_n > kAppendCap - kMatchUnroll * kCoopThreads) app.flush(out, gcount);
+                if (app.due(kAppendCap - kMatchUnroll * kCoopThreads)) app.flush(out, gcount);
             }
         } else {
             // (b1) thread per entry: matched vertices drop out, those whose target
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
                 wb = __shfl_sync(0xffffffffu, wb, 0);
                 if (mv) lm[wb + __popc(bal & ((1u << lane_id()) - 1u))] = v;
                 __syncthreads();
-                if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
+                if (app.due(kAppendCap - kCoopThreads)) app.flush(out, gcount);
             }
             grid.sync();
             // (b2) a sub-warp per mover re-points it at its heaviest FREE neighbour
@@ -475,7 +484,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
                     if (bj >= 0) app.push(v);
                 }
                 __syncthreads();
-                if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
+                if (app.due(kAppendCap - kCoopThreads)) app.flush(out, gcount);
             }
         }
         __syncthreads();
@@ -576,7 +585,9 @@ struct RoundTrace {
 // cooperative launch with every CTA co-resident (grid = SMs x resident CTAs)
 template <class K>
 static void coop_launch(K kernel, void **args, cudaStream_t st, double grid_frac = 1.0) {
-    static int grid = 0;   // one cache per kernel instantiation
+    static DeviceCache grid_cache{};   // one cache per kernel instantiation and device
+    std::atomic<int> &grid_slot = grid_cache[current_device()];
+    int grid = grid_slot.load();
     if (!grid) {
         int per_sm = 0, dev = 0, sms = kNumSMs;
         // a small shared-memory carveout: these kernels live on L1-cached gathers
@@ -586,6 +597,7 @@ static void coop_launch(K kernel, void **args, cudaStream_t st, double grid_frac
         FDL_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         FDL_REQUIRE(per_sm > 0, FIEDLER_ERR_CUDA, "cooperative kernel cannot be resident");
         grid = per_sm * sms;
+        grid_slot.store(grid);
     }
     // the kernels are grid-size agnostic: if the driver finds fewer co-resident
     // CTAs than the occupancy query promised, retry with a smaller grid
@@ -595,6 +607,7 @@ static void coop_launch(K kernel, void **args, cudaStream_t st, double grid_frac
         if (e == cudaErrorCooperativeLaunchTooLarge && grid > kNumSMs) {
             (void)cudaGetLastError();
             grid = grid * 3 / 4;
+            grid_slot.store(grid);
             continue;
         }
         FDL_CK(e);
@@ -1692,23 +1705,26 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
             if (c == 0) app.push(v);
         }
         __syncthreads();
-        if (W > 1 && s_nh > kHeavyCap - per_block) {
-            for (int i = 0; i < s_nh; i++) {
+        const int nh0 = s_nh;   // read by every thread before the next barrier
+        __syncthreads();
+        if (W > 1 && nh0 > kHeavyCap - per_block) {
+            for (int i = 0; i < nh0; i++) {
                 const int hv = s_heavy[i];
                 const int hc = cta_indeg(hv, rp, ci, salt, s_red);
-                if (threadIdx.x == 0) { indeg[hv] = hc; if (hc == 0) app.push(hv); }
+                if (threadIdx.x == 0) { indeg[hv] = hc; if (hc == 0) app.push_safe(hv, la, counts); }
             }
             __syncthreads();
             if (threadIdx.x == 0) s_nh = 0;
             __syncthreads();
         }
-        if (s_n > kAppendCap - kCoopThreads) app.flush(la, counts);
+        if (app.due(kAppendCap - kCoopThreads)) app.flush(la, counts);
     }
     if (W > 1) {
-        for (int i = 0; i < s_nh; i++) {
+        const int nh0 = s_nh;   // after the loop's last barrier; no push follows
+        for (int i = 0; i < nh0; i++) {
             const int hv = s_heavy[i];
             const int hc = cta_indeg(hv, rp, ci, salt, s_red);
-            if (threadIdx.x == 0) { indeg[hv] = hc; if (hc == 0) app.push(hv); }
+            if (threadIdx.x == 0) { indeg[hv] = hc; if (hc == 0) app.push_safe(hv, la, counts); }
         }
         __syncthreads();
         if (threadIdx.x == 0) s_nh = 0;
@@ -1820,11 +1836,13 @@ __global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *r
                 }
             }
             __syncthreads();
-            if (W > 1 && s_nh > kHeavyCap - per_block) {
+            const int nh1 = s_nh;   // read by every thread before the next barrier
+            __syncthreads();
+            if (W > 1 && nh1 > kHeavyCap - per_block) {
                 heavy_round(out, gcount);
                 __syncthreads();
             }
-            if (s_n > kAppendCap - kCoopThreads) app.flush(out, gcount);
+            if (app.due(kAppendCap - kCoopThreads)) app.flush(out, gcount);
         }
         if (W > 1) heavy_round(out, gcount);
         __syncthreads();
@@ -2169,9 +2187,10 @@ struct ColourJob {
 // whether a 16-CTA cluster of k_color_cluster (1024 threads, ~210 KB shared
 // memory each) can be resident on this device
 static bool cluster_colour_ok() {
-    static int ok = -1;
-    if (ok < 0) {
-        ok = 0;
+    static DeviceCache cache{};   // 0 unknown, 1 no, 2 yes
+    std::atomic<int> &slot = cache[current_device()];
+    if (slot.load() == 0) {
+        int ok = 0;
         if (cudaFuncSetAttribute(k_color_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                 cudaSuccess &&
             cudaFuncSetAttribute(k_color_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2191,8 +2210,9 @@ static bool cluster_colour_ok() {
             ok = cudaOccupancyMaxActiveClusters(&nc, k_color_cluster, &q) == cudaSuccess && nc > 0;
         }
         (void)cudaGetLastError();
+        slot.store(ok ? 2 : 1);
     }
-    return ok > 0;
+    return slot.load() == 2;
 }
 
 static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJob &job, cudaStream_t st) {
@@ -2211,11 +2231,12 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             *pc = job.counts.as<int>(), *pr = job.counts.as<int>() + kMaxRounds;
         void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr};
         if (n <= kSmallColourN && avg >= kSmallColourMinDeg) {
-            static bool attr = false;
-            if (!attr) {
+            static DeviceCache attr{};
+            std::atomic<int> &attr_slot = attr[current_device()];
+            if (!attr_slot.load()) {
                 FDL_CK(cudaFuncSetAttribute(k_color_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             16 * kSmallColourN));
-                attr = true;
+                attr_slot.store(1);
             }
             k_color_small<<<1, kSmallColourThreads, (size_t)16 * n, st>>>(n, rp, ci, salt, pcol, pr);
             FDL_LAUNCH_CK();
@@ -2447,7 +2468,9 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     double dm = 0.0;
     FDL_CK(cudaMemcpyAsync(&dm, dmax.p, 8, cudaMemcpyDeviceToHost, st));
     FDL_CK(cudaStreamSynchronize(st));
-    L.shift = 2.0 * dm;
+    // R8: c = 2 max_i d_i (Gershgorin); on a 2-vertex level 2 max d = lambda_max
+    // exactly and c I - L would annihilate the only non-constant direction
+    L.shift = (n == 2 ? 3.0 : 2.0) * dm;
     seg[ncolors] = n;
     for (int k = ncolors - 1; k >= 0; k--)
         if (seg[k] < 0) seg[k] = seg[k + 1];

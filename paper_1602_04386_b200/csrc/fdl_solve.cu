@@ -846,7 +846,9 @@ constexpr int kSmallPiNnz = 1 << 18;  // ... unless dense: one CTA streams ~0.1 
 // one cluster (16 CTAs where the device allows, else 8) for k_gs_multi<true>
 static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0, int c1, int sweeps, double *x,
                               double *slot, int mode, int n) {
-    static int cl = 0;
+    static DeviceCache cl_cache{};
+    std::atomic<int> &cl_slot = cl_cache[current_device()];
+    int cl = cl_slot.load();
     if (!cl) {
         cl = 8;
         if (cudaFuncSetAttribute(k_gs_multi<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
@@ -865,6 +867,7 @@ static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0
                 cl = kGcMaxCluster;
         }
         (void)cudaGetLastError();
+        cl_slot.store(cl);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl);
@@ -884,8 +887,8 @@ static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0
 #define FDL_DENSE_ROW_DEG 7.0
 #endif
 constexpr double kDenseRowDeg = FDL_DENSE_ROW_DEG;   // rows per tile few enough for sub-warp rows
-static int g_pass_grid[4] = {0, 0, 0, 0};
-static int pass_grid(int op) { return g_pass_grid[op]; }
+static DeviceCache g_pass_grid[4] = {};   // per OP (3: the 4-lane dense variant), per device
+static int pass_grid(int op) { return g_pass_grid[op][current_device()].load(); }
 
 struct Enq {
     Handle &h;
@@ -905,7 +908,7 @@ struct Enq {
         // GS: the chunk of 4 suits <= 4.5 neighbours per row, 8 the denser coarse
         // levels; dense levels (>= kDenseRowDeg per row): 4 lanes per short row
         if (OP == OP_GS && L.nnz <= 4.5 * L.n) {
-            grid = std::min(nt, g_pass_grid[3]);
+            grid = std::min(nt, pass_grid(3));
             k_tilepass<OP_GS, 4><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
         } else if (L.nnz >= kDenseRowDeg * (double)L.n) {
             k_tilepass<OP, 0, 4><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
@@ -1013,9 +1016,12 @@ struct Enq {
     }
 };
 
-static void ensure_solve_buffers(Handle &h, int nslots) {
+// returns true when it allocated (on h.stream)
+static bool ensure_solve_buffers(Handle &h, int nslots) {
     cudaStream_t st = h.stream;
+    bool grew = false;
     if (!h.xa.p) {
+        grew = true;
         h.xa.alloc((size_t)h.n0 * 8, st);
         h.xb.alloc((size_t)h.n0 * 8, st);
         h.vnat.alloc((size_t)h.n0 * 8, st);
@@ -1029,7 +1035,9 @@ static void ensure_solve_buffers(Handle &h, int nslots) {
         h.scal.alloc((size_t)nslots * 4 * 8, st);
         FDL_CK(cudaMemsetAsync(h.scal.p, 0, (size_t)nslots * 4 * 8, st));
         h.nslots = nslots;
+        grew = true;
     }
+    return grew;
 }
 
 static int slots_needed(const Handle &h, const SolveCfg &cfg) {
@@ -1046,8 +1054,9 @@ int prepare_solve(Handle &h, const SolveCfg &cfg) {
 
 // returns the largest pass grid (sizes the partial-sum buffer)
 int rowpass_grid() {
-    static int cached = 0;
-    if (cached) return cached;
+    static DeviceCache cache{};
+    const int cdev = current_device();
+    if (int c = cache[cdev].load()) return c;
     const int smem = (int)kPassSmemBytes;
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1066,12 +1075,13 @@ int rowpass_grid() {
     int dev = 0, sms = kNumSMs;
     FDL_CK(cudaGetDevice(&dev));
     FDL_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    g_pass_grid[OP_GS] = sms * std::max(1, b0);
-    g_pass_grid[OP_PI] = sms * std::max(1, b1);
-    g_pass_grid[OP_RQ] = sms * std::max(1, b2);
-    g_pass_grid[3] = sms * std::max(1, b3);
-    cached = sms * std::max(std::max(1, b3), std::max(b0, std::max(b1, b2)));
-    return cached;
+    g_pass_grid[OP_GS][cdev].store(sms * std::max(1, b0));
+    g_pass_grid[OP_PI][cdev].store(sms * std::max(1, b1));
+    g_pass_grid[OP_RQ][cdev].store(sms * std::max(1, b2));
+    g_pass_grid[3][cdev].store(sms * std::max(1, b3));
+    const int all = sms * std::max(std::max(1, b3), std::max(b0, std::max(b1, b2)));
+    cache[cdev].store(all);
+    return all;
 }
 
 int enqueue_solve(Handle &h, const SolveCfg &cfg) {
@@ -1561,7 +1571,8 @@ void dist_op(Handle &h, int level, int op, int64_t arg, const double *x, double 
     const Level &L = h.levels[level];
     const DistPlan &P = L.dist;
     FDL_REQUIRE(P.valid, FIEDLER_ERR_ARG, "fiedler_dist_op: no plan on this level (call fiedler_dist_plan)");
-    ensure_solve_buffers(h, 8);
+    // scratch allocated on the handle's stream must exist before `st` uses it
+    if (ensure_solve_buffers(h, 8) && st != h.stream) FDL_CK(cudaStreamSynchronize(h.stream));
     Enq e{h, st};
     double *partials = h.partials.as<double>();
     unsigned *counter = h.counter.as<unsigned>();

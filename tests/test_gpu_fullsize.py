@@ -1,10 +1,14 @@
 """Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py
 times (one fiedler_create + fiedler_solve through the C ABI, device input).
 
-* config 2 (R-MAT 2^20): the oracle solves it in tens of seconds, so the whole
-  result is compared (north-star bars) and the first coarse level bit-exactly.
-* configs 3 and 4 (16.7 M and 67 M vertices): outputs the oracle can compute
-  one by one and properties that characterise the method at any size:
+* configs 2, 3 and 4 (R-MAT 2^20, the 256^3 grid, the 8192^2 grid the bench
+  line is quoted on) are compared with oracle.solve at full size: lambda_2 and
+  the vector within the north-star bars, and EVERY level's hierarchy (CSR
+  pattern and values, matching, aggregate ids, colours) bit-exact -- through
+  SHA-256 digests of the arrays for configs 3 and 4 (tests/oracle_fullsize.py
+  runs the oracle in a background process, ~2.5 and ~6 min, while the GPU
+  tests of this module run);
+* config 3 in addition: properties that characterise the method at any size:
     - the returned vector: unit norm, orthogonal to 1, sign convention (R10),
       and its Rayleigh quotient / residual recomputed by the oracle's C code;
     - level 0 -> 1: the matching IS the greedy heaviest-first matching in the
@@ -16,10 +20,14 @@ times (one fiedler_create + fiedler_solve through the C ABI, device input).
     - the coarse operator on sampled coarse rows: the R3 left fold of the fine
       weights between the aggregates, bit for bit.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
 import graphgen as gg
+from oracle_fullsize import level_digests
 
 pytestmark = pytest.mark.gpu
 
@@ -33,6 +41,35 @@ def splitmix64(x):
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
     return z ^ (z >> np.uint64(31))
+
+
+@pytest.fixture(scope="module")
+def oracle_jobs(tmp_path_factory):
+    """Start the full-size oracle runs of configs 3 and 4 at once (background
+    processes, oracle/ only); tests wait for their results."""
+    import subprocess
+    import sys
+    d = tmp_path_factory.mktemp("oracle_fullsize")
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle_fullsize.py")
+    jobs = {}
+    for cfg in (3, 4):
+        prefix = str(d / ("config%d" % cfg))
+        log = open(prefix + ".log", "w")
+        jobs[cfg] = (subprocess.Popen([sys.executable, script, str(cfg), prefix], stdout=log,
+                                      stderr=subprocess.STDOUT), prefix)
+    yield jobs
+    for p, _ in jobs.values():
+        if p.poll() is None:
+            p.kill()
+
+
+def oracle_result(jobs, cfg, timeout=1800):
+    p, prefix = jobs[cfg]
+    rc = p.wait(timeout=timeout)
+    assert rc == 0, open(prefix + ".log").read()[-2000:]
+    with open(prefix + ".json") as f:
+        res = json.load(f)
+    return res, np.load(prefix + ".vec.npy")
 
 
 @pytest.fixture(scope="module")
@@ -189,7 +226,19 @@ def check_galerkin_sample(rp, ci, w, q, ex1, nsample=4000, seed=0):
         assert np.array_equal(ex1["w"][b:e].view(np.uint64), np.array(vals).view(np.uint64))
 
 
-def test_config2_full_parity(fd, orc):
+def gpu_level_digests(fd, h):
+    out = []
+    nl = fd.fiedler_num_levels(h)
+    for ell in range(nl):
+        ex = fd.fiedler_level_export(h, ell)
+        last = ell == nl - 1
+        out.append(level_digests(ex["rp"], ex["ci"], ex["w"], ex["color"], None if last else ex["agg"],
+                                 None if last else ex["mate"]))
+        del ex
+    return out
+
+
+def test_config2_full_parity(fd, orc, oracle_jobs):
     g = gg.config(2)
     v, lam, info, ex0, ex1 = run_gpu(fd, g)
     ref = orc.solve(orc.Graph.from_csr(g.n, g.rp, g.ci, g.w), orc.Config())
@@ -205,6 +254,39 @@ def test_config2_full_parity(fd, orc):
 
 
 @pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_oracle_parity(fd, oracle_jobs, cfg):
+    """BASELINE configs 3 and 4 at full size against oracle.solve: every
+    level bit-exact (digests), lambda_2 rel <= 1e-10, 1 - |cos| <= 1e-10."""
+    import torch
+    g = gg.config(cfg)
+    args = [torch.from_numpy(a).cuda() for a in (g.rp, g.ci, g.w)]
+    n = g.n
+    del g
+    vec = torch.empty(n, dtype=torch.float64, device="cuda")
+    info = fd.fiedler_info()
+    h = fd.fiedler_create(n, int(args[0][-1]), *args, fd.fiedler_default_opts(validate=0))
+    try:
+        lam = fd.fiedler_solve(h, vec, None, info)
+        del args
+        dig = gpu_level_digests(fd, h)
+    finally:
+        fd.fiedler_destroy(h)
+    v = vec.cpu().numpy()
+    del vec
+    torch.cuda.empty_cache()
+    ref, vref = oracle_result(oracle_jobs, cfg)
+    assert info.num_levels == ref["num_levels"] == len(dig)
+    for ell, (a, b) in enumerate(zip(dig, ref["levels"])):
+        assert a == b, (cfg, ell, {k: (a[k], b.get(k)) for k in a if a[k] != b.get(k)})
+    assert abs(lam - ref["lambda2"]) / ref["lambda2"] <= 1e-10, (lam, ref["lambda2"])
+    cos = abs(float(v @ vref)) / (np.linalg.norm(v) * np.linalg.norm(vref))
+    assert 1 - cos <= 1e-10, 1 - cos
+    nz = np.flatnonzero(v)
+    assert v[nz[0]] > 0
+    assert info.residual_norm == pytest.approx(ref["residual_norm"], rel=1e-6, abs=1e-7 * ref["lambda2"])
+
+
+@pytest.mark.parametrize("cfg", [3])
 def test_full_size_properties(fd, orc, cfg):
     g = gg.config(cfg)
     v, lam, info, ex0, ex1 = run_gpu(fd, g)

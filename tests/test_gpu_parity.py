@@ -72,7 +72,9 @@ SMALL = {
     "hub3000_3hubs": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
     "clique70_tail2000": lambda: clique_with_tail(70, 2000),
     "tiny_p5": lambda: gg.path(5),
-    "tiny_p3": lambda: gg.path(3),   # (P2 is degenerate for the Gershgorin shift: c = lambda_2)
+    "tiny_p3": lambda: gg.path(3),
+    # K2: the Gershgorin shift 2 max d equals lambda_max = lambda_2 (R8: 3 max d there)
+    "tiny_p2": lambda: gg.path(2, weights=[0.75]),
 }
 
 
@@ -180,7 +182,8 @@ def test_solve_parity_small(fd, orc, name):
 def test_solve_parity_iteration_variants(fd, orc):
     g = gg.grid2d(40, "uniform", seed=2)
     for kw in ({"gs_sweeps": 0}, {"power_iters": 0}, {"gs_sweeps": 3, "power_iters": 25},
-               {"seed": 12345}, {"coarsest_size": 100}):
+               {"seed": 12345}, {"coarsest_size": 100},
+               {"coarsest_size": 2}):          # hierarchy down to a 2-vertex level (R8)
         compare_solve(fd, orc, g, kw)
 
 

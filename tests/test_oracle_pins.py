@@ -80,6 +80,31 @@ def test_randperm_is_permutation(orc):
         assert np.array_equal(np.sort(p), np.arange(n))
 
 
+def test_randperm_hand_trace(orc):
+    """Fisher-Yates traced by hand from SplitMix64 draws (golden/randperm_trace.json)."""
+    gv = gold("randperm_trace.json")
+    s0 = py_splitmix64(gv["seed"] ^ 0x7065726D00000000 ^ gv["level"])
+    assert s0 == int(gv["s0"], 16)
+    for st in gv["steps"]:
+        r = py_splitmix64((s0 + st["i"]) & M64)
+        assert r == int(st["r"], 16) and r % (st["i"] + 1) == st["j"]
+    assert list(orc.randperm(gv["n"], gv["seed"], gv["level"])) == gv["perm"]
+
+
+def test_randperm_is_uniform(orc):
+    """Fisher-Yates draws every permutation of 4 items with probability 1/24.
+    Sattolo's variant (j < i, the '% i' slip) draws only the 6 cyclic ones and
+    an off-by-one range skews the counts: a chi-square test over 24000 seeds
+    (23 degrees of freedom; 99.99 % quantile ~ 59) rejects both."""
+    import itertools
+    idx = {p: k for k, p in enumerate(itertools.permutations(range(4)))}
+    counts = np.zeros(24)
+    for seed in range(24000):
+        counts[idx[tuple(int(x) for x in orc.randperm(4, seed, 0))]] += 1
+    chi2 = float(((counts - 1000.0) ** 2 / 1000.0).sum())
+    assert counts.min() > 0 and chi2 < 59.0, (chi2, counts)
+
+
 # ------------------------------------------------------------ Definition 2.1
 
 def test_laplacian_p3_and_k3(orc):
@@ -221,6 +246,48 @@ def test_hec_parallel_matching_equals_handshake(orc, n, extra, seed):
             best = max(range(nb.size), key=lambda t: keys[t])
             assert q[x] == q[nb[best]]
         assert c <= n // 2 + (n % 2)
+
+
+def handshake_rounds(g, key):
+    """Synchronous rounds of the locally-dominant handshake for edge order `key`."""
+    mate = [-1] * g.n
+    rounds = 0
+    while True:
+        ptr = [-1] * g.n
+        for v in range(g.n):
+            if mate[v] != -1:
+                continue
+            best = None
+            for k in range(g.rp[v], g.rp[v + 1]):
+                u = int(g.ci[k])
+                if mate[u] == -1 and (best is None or key(v, u, g.w[k]) > best[0]):
+                    best = (key(v, u, g.w[k]), u)
+            if best is not None:
+                ptr[v] = best[1]
+        pairs = [v for v in range(g.n) if ptr[v] != -1 and ptr[ptr[v]] == v]
+        if not pairs:
+            return rounds
+        for v in pairs:
+            mate[v] = ptr[v]
+        rounds += 1
+
+
+def test_tie_rule_r2_depth(orc):
+    """Why R2 breaks weight ties by splitmix64 of the index pair rather than by
+    the plain index (R2): on unit-weight graphs (BASELINE config 0)
+    an index order makes the greedy matching a chain -- the handshake needs
+    ~1.5 m rounds on an m x m grid and n/2 on a path, i.e. no parallelism --
+    whereas the hashed order (a fixed permutation of the index pairs, since
+    splitmix64 is a bijection) needs a handful."""
+    salt = orc.salt_match(0, 0)
+    by_hash = lambda v, u, w: (w, py_splitmix64(salt ^ ((min(v, u) << 32) | max(v, u))))
+    by_index = lambda v, u, w: (w, -min(v, u), -max(v, u))
+    for m in (16, 32):
+        g = gg.grid2d(m)
+        assert handshake_rounds(g, by_index) >= 1.4 * m
+        assert handshake_rounds(g, by_hash) <= 6
+    p = gg.path(200)
+    assert handshake_rounds(p, by_index) == 100 and handshake_rounds(p, by_hash) <= 6
 
 
 def test_hec_parallel_p4(orc):
