@@ -179,6 +179,56 @@ def traffic_from_profiles():
     return None
 
 
+def phase_bytes(n, nnz, nc, nnzc):
+    """Algorithmic bytes of the setup phases of one level:
+    what a perfect kernel must move -- int32 CSR offsets / columns, f64 weights,
+    int32 per-vertex outputs."""
+    graph = 4 * (n + 1) + 12 * nnz          # rp, ci, w of the level
+    pattern = 4 * (n + 1) + 4 * nnz         # rp, ci
+    return {
+        # read the graph; write mate, m (first pointer), aggregate id
+        "match": graph + 12 * n,
+        # read the fine graph and the aggregate ids; write the coarse CSR
+        "galerkin": graph + 4 * n + (4 * (nc + 1) + 12 * nnzc if nc else 0),
+        # read the pattern; write the colours
+        "colour": pattern + 4 * n,
+        # read the natural CSR and the colours; write the colour-permuted CSR, perm, inv
+        "layout": 2 * graph + 12 * n,
+    }
+
+
+def setup_phase_rooflines(fd, n, nnz, rp, ci, w, opts, vec, peak):
+    os.environ["FIEDLER_PHASE_TIMES"] = "1"
+    try:
+        info = fd.fiedler_info()
+        hh = fd.fiedler_create(n, nnz, rp, ci, w, opts)
+        fd.fiedler_solve(hh, vec, None, info)
+        fd.fiedler_destroy(hh)
+    finally:
+        del os.environ["FIEDLER_PHASE_TIMES"]
+    lv = info.levels()
+    out = {"note": "device ms between CUDA events around each setup phase (one extra create with "
+                   "FIEDLER_PHASE_TIMES=1, outside the timed region); the colouring runs on a second "
+                   "stream, concurrently with the matching / Galerkin chain; algorithmic bytes: "
+                   "DESIGN.md section 7", "setup_ms_this_create": info.setup_ms}
+    tot = {k: 0.0 for k in ("match", "galerkin", "colour", "layout")}
+    for i, L in enumerate(lv):
+        for k in tot:
+            tot[k] += L[k + "_ms"]
+    out["all_levels_ms"] = tot
+    L0 = lv[0]
+    nc, nnzc = (lv[1]["n"], lv[1]["nnz"]) if len(lv) > 1 else (0, 0)
+    by = phase_bytes(L0["n"], L0["nnz"], nc, nnzc)
+    lvl0 = {}
+    for k in tot:
+        ms = L0[k + "_ms"]
+        gbs = by[k] / (ms / 1e3) / 1e9 if ms > 0 else None
+        lvl0[k] = {"ms": ms, "algorithmic_bytes": by[k], "GB/s": gbs,
+                   "frac": (gbs / peak) if gbs else None}
+    out["level0"] = lvl0
+    return out
+
+
 def partitioned_solve_timing(fd, g, rp, ci, w, dev, local, args, lam_single):
     """Time the row-partitioned solve (paper_1602_04386_b200.dist) of the graph on
     all ranks: device time of `steps` solves, max over ranks."""
@@ -294,8 +344,10 @@ def main():
     achieved = k_bytes / (k_ms / 1e3) / 1e9
     tr = traffic_from_profiles()
     traffic = None
+    traffic_source = None
     if tr and tr.get("config") == args.config and tr.get("kernel_bytes_per_launch"):
         traffic = tr["kernel_bytes_per_launch"]
+        traffic_source = tr.get("source")
 
     # algorithmic GB/s (the bytes a perfect kernel moves, per the DESIGN.md
     # formulas) and, where the committed ncu capture matches the config, the
@@ -311,6 +363,11 @@ def main():
                 kernels[key]["dram_GB/s"] = tr[tkey] / (ms / 1e3) / 1e9
                 kernels[key]["dram_frac"] = tr[tkey] / (ms / 1e3) / 1e9 / peak
                 kernels[key]["dram_bytes_source"] = tr.get("gs_rq_source")
+
+    # ---- setup phases on the roofline: one extra create outside the timed
+    # region with FIEDLER_PHASE_TIMES=1 (CUDA events around every phase of
+    # every level, include/fiedler.h); algorithmic bytes per DESIGN.md section 7
+    setup_kernels = setup_phase_rooflines(fd, n, nnz, rp, ci, w, opts, vec, peak)
 
     # ---- end to end through the public API with HOST buffers (pinned)
     prp = torch.from_numpy(g.rp).pin_memory()
@@ -366,11 +423,12 @@ def main():
             "solve_time_ms": tot_ms / args.steps, "setup_ms": setup_ms, "solve_ms": solve_ms,
             "lambda2": lam,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_source,
                          "kernel": "k_tilepass<OP_PI> level 0 (one power-iteration step)",
                          "algorithmic_bytes_per_launch": k_bytes, "launch_ms": k_ms,
                          "peak_source": peak_src},
             "kernels": kernels,
+            "setup_kernels": setup_kernels,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,

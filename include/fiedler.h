@@ -32,7 +32,8 @@
  *     library sets its release threshold to "keep everything" and grows it once
  *     per fiedler_create to ~8x the input size (FIEDLER_NO_POOL_RESERVE=1 skips
  *     that).  Environment, diagnostics only: FIEDLER_TRACE=1 (phase times on
- *     stderr), FIEDLER_SERIAL_COLOUR=1 (colourings on the main stream),
+ *     stderr), FIEDLER_PHASE_TIMES=1 (device times of the setup phases in
+ *     fiedler_info), FIEDLER_SERIAL_COLOUR=1 (colourings on the main stream),
  *     FIEDLER_TEST_FULL_SORT=1 (the Galerkin fallback of very large levels).
  *     Input buffers are only read and never retained after the call returns
  *     (fiedler_create copies what it needs); output buffers are caller-owned.
@@ -110,6 +111,14 @@ typedef struct fiedler_info {
     int32_t level_colors[FIEDLER_MAX_LEVELS]; /* colours of the multicolour ordering     */
     int32_t level_match_rounds[FIEDLER_MAX_LEVELS]; /* handshake rounds of the matching  */
     double level_shift[FIEDLER_MAX_LEVELS]; /* c of c I - L (R8)                          */
+    /* Device time of the setup phases of every level (CUDA events; filled only
+     * when the handle was created with FIEDLER_PHASE_TIMES=1 in the
+     * environment, else 0).  The colouring runs on a second stream, overlapped
+     * with the matching / Galerkin chain, so the phases may overlap in time. */
+    double level_match_ms[FIEDLER_MAX_LEVELS];    /* heavy-edge matching + aggregate numbering */
+    double level_galerkin_ms[FIEDLER_MAX_LEVELS]; /* Galerkin product to the next level        */
+    double level_colour_ms[FIEDLER_MAX_LEVELS];   /* multicolour ordering                       */
+    double level_layout_ms[FIEDLER_MAX_LEVELS];   /* GS / natural solve layouts, tiles, shift   */
 } fiedler_info;
 
 typedef struct fiedler_handle_s *fiedler_handle;

@@ -73,11 +73,17 @@ class fiedler_info(ctypes.Structure):
                 ("level_nnz", ctypes.c_int64 * FIEDLER_MAX_LEVELS),
                 ("level_colors", ctypes.c_int32 * FIEDLER_MAX_LEVELS),
                 ("level_match_rounds", ctypes.c_int32 * FIEDLER_MAX_LEVELS),
-                ("level_shift", ctypes.c_double * FIEDLER_MAX_LEVELS)]
+                ("level_shift", ctypes.c_double * FIEDLER_MAX_LEVELS),
+                ("level_match_ms", ctypes.c_double * FIEDLER_MAX_LEVELS),
+                ("level_galerkin_ms", ctypes.c_double * FIEDLER_MAX_LEVELS),
+                ("level_colour_ms", ctypes.c_double * FIEDLER_MAX_LEVELS),
+                ("level_layout_ms", ctypes.c_double * FIEDLER_MAX_LEVELS)]
 
     def levels(self):
         return [dict(n=self.level_n[i], nnz=self.level_nnz[i], colors=self.level_colors[i],
-                     match_rounds=self.level_match_rounds[i], shift=self.level_shift[i])
+                     match_rounds=self.level_match_rounds[i], shift=self.level_shift[i],
+                     match_ms=self.level_match_ms[i], galerkin_ms=self.level_galerkin_ms[i],
+                     colour_ms=self.level_colour_ms[i], layout_ms=self.level_layout_ms[i])
                 for i in range(self.num_levels)]
 
 

@@ -357,6 +357,10 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
             info->level_colors[l] = h.levels[l].ncolors;
             info->level_match_rounds[l] = h.levels[l].match_rounds;
             info->level_shift[l] = h.levels[l].shift;
+            info->level_match_ms[l] = h.levels[l].phase_ms[0];
+            info->level_galerkin_ms[l] = h.levels[l].phase_ms[1];
+            info->level_colour_ms[l] = h.levels[l].phase_ms[2];
+            info->level_layout_ms[l] = h.levels[l].phase_ms[3];
         }
     }
     return FIEDLER_OK;

@@ -92,6 +92,8 @@ struct Level {
     double shift = 0.0;      // c of c I - L: 2 max_i d_i, 3 max_i d_i when n == 2 (R8)
     int match_rounds = 0;
     int color_rounds = 0;
+    // FIEDLER_PHASE_TIMES=1: device ms of the setup phases (match, Galerkin, colour, layout)
+    double phase_ms[4] = {0.0, 0.0, 0.0, 0.0};
     int gs_tile_begin(int c) const { return ctile[c]; }
     int nat_tile_begin() const { return ctile[ncolors]; }
 };

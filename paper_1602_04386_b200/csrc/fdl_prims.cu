@@ -1,5 +1,5 @@
 // fdl_prims.cu -- hand-written device primitives: exclusive scan (single pass,
-// decoupled look-back, 4096-element tiles, vectorised int4 traffic) and a stable LSD radix
+// decoupled look-back, 16384-element tiles, vectorised int4 traffic) and a stable LSD radix
 // sort (8-bit digits, 8192-element tiles, warp __match_any_sync ranking).
 // Used by the aggregate numbering (prefix scan of leader flags), work-list and
 // CSR offset scans everywhere, the Galerkin product's long-row path (two-key
@@ -11,8 +11,15 @@
 namespace fdl {
 
 // =============================================================== scan
+// 16 items per thread (4 x int4): 16384-element tiles keep the look-back chain
+// short (one inclusive-prefix hop covers up to 32 tiles = 512 K elements);
+// with 4096-element tiles the chain of hops, not bandwidth, bounded the scan
 constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 4;
+#ifndef FDL_SCAN_ITEMS
+#define FDL_SCAN_ITEMS 16
+#endif
+constexpr int kScanItems = FDL_SCAN_ITEMS;
+static_assert(kScanItems % 4 == 0, "scan items come in int4 groups");
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -70,9 +77,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const int *in, int *ou
     __syncthreads();
     const int t = s_tile;
     const int64_t i = (int64_t)t * kScanTile + (int64_t)threadIdx.x * kScanItems;
-    int x[4];
-    load4(in, n, i, x);
-    const int s = x[0] + x[1] + x[2] + x[3];
+    int x[kScanItems];
+#pragma unroll
+    for (int g = 0; g < kScanItems / 4; g++) load4(in, n, i + 4 * g, x + 4 * g);
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) s += x[k];
     int tot;
     const int ex = block_excl_scan(s, tot);
     if (threadIdx.x == 0)
@@ -103,18 +113,23 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const int *in, int *ou
         }
     }
     __syncthreads();
-    const int base = ex + s_prefix;
-    int y[4];
-    y[0] = base;
-    y[1] = base + x[0];
-    y[2] = y[1] + x[1];
-    y[3] = y[2] + x[2];
-    if (i + 3 < n && ((reinterpret_cast<uintptr_t>(out + i) & 15) == 0)) {
-        *reinterpret_cast<int4 *>(out + i) = make_int4(y[0], y[1], y[2], y[3]);
-    } else {
+    int run = ex + s_prefix;
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-            if (i + k < n) out[i + k] = y[k];
+    for (int g = 0; g < kScanItems / 4; g++) {
+        int y[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            y[k] = run;
+            run += x[4 * g + k];
+        }
+        const int64_t j = i + 4 * g;
+        if (j + 3 < n && ((reinterpret_cast<uintptr_t>(out + j) & 15) == 0)) {
+            *reinterpret_cast<int4 *>(out + j) = make_int4(y[0], y[1], y[2], y[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                if (j + k < n) out[j + k] = y[k];
+        }
     }
 }
 

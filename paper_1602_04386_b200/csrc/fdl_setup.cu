@@ -165,6 +165,14 @@ void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32,
 // deterministic.
 namespace cg = cooperative_groups;
 constexpr int kCoopThreads = 256;
+#ifndef FDL_COOP_MINB
+#define FDL_COOP_MINB 6
+#endif
+constexpr int kCoopMinBlocks = FDL_COOP_MINB;   // resident CTAs per SM the register budget must allow
+#ifndef FDL_MATCH_MINB
+#define FDL_MATCH_MINB 5
+#endif
+constexpr int kMatchMinBlocks = FDL_MATCH_MINB;   // ... for the matching (more live state per thread)
 constexpr int kAppendCap = 2048;
 constexpr int kMaxRounds = 1 << 16;
 #ifndef FDL_MATCH_UNROLL
@@ -218,7 +226,9 @@ struct CtaAppend {
     // guards barriers).
     __device__ __forceinline__ bool due(int thr) {
         const int x = *n;
+#ifndef FDL_RACY_FLUSH
         __syncthreads();
+#endif
         return x > thr;
     }
     // all threads; call after __syncthreads()
@@ -266,10 +276,43 @@ __device__ __forceinline__ bool edge_greater(double wa, unsigned long long ha, d
 // heaviest FREE neighbour is then a cursor advance.  Longer rows are rescanned.
 template <int W> struct SortSlots { static constexpr int value = W == 1 ? 8 : 4; };
 
+// One thread ranks the <= S entries of row v in the strict edge order
+// (nbr[b + rank] = neighbour); returns the heaviest neighbour (-1: none).
+template <int S>
+__device__ __forceinline__ int rank_row(int v, int b, int deg, const int *ci, const double *w, uint64_t salt,
+                                        int *nbr) {
+    double wv[S];
+    unsigned long long hv[S];
+    int cv[S];
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        const bool on = v >= 0 && i < deg;
+        cv[i] = on ? ci[b + i] : -1;
+        wv[i] = on ? w[b + i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < S; i++) hv[i] = cv[i] >= 0 ? edge_hash(salt, v, cv[i]) : 0ull;
+    int top = -1;
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        int rank = 0;
+#pragma unroll
+        for (int j = 0; j < S; j++)
+            if (j != i) rank += cv[j] >= 0 && edge_greater(wv[j], hv[j], wv[i], hv[i]);
+        if (cv[i] >= 0) {
+            nbr[b + rank] = cv[i];
+            if (rank == 0) top = cv[i];
+        }
+    }
+    return top;
+}
+
 // counts[r] = length of the work list of round r (zeroed by the host); the
 // lists ping-pong between la and lb.  rounds_out[0] = handshake rounds.
+// W == 1 (low-degree levels): round 0 takes two rows per thread and the first
+// handshake list is implicit (every vertex; isolated ones have no pointer).
 template <int W>
-__global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *rp, const int *ci,
+__global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(int n, const int *rp, const int *ci,
                                                              const double *w, uint64_t salt, int *m,
                                                              int *ptr, int *mate, int *nbr, int *cursor,
                                                              int *la, int *lb, int *counts,
@@ -286,7 +329,46 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
     const int per_block = kCoopThreads / W;
     // round 0: rank every short row's neighbours; m(v) = heaviest neighbour =
     // the first handshake pointer; vertices with a neighbour enter the list
-    for (long long base = (long long)blockIdx.x * per_block; base < n;
+    if (W == 1) {
+        for (long long base = (long long)blockIdx.x * 2 * kCoopThreads; base < n;
+             base += (long long)gridDim.x * 2 * kCoopThreads) {
+            int v[2], b[2], deg[2];
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                const long long idx = base + u * kCoopThreads + threadIdx.x;
+                v[u] = idx < n ? (int)idx : -1;
+                b[u] = v[u] >= 0 ? rp[v[u]] : 0;
+                deg[u] = v[u] >= 0 ? rp[v[u] + 1] - b[u] : 0;
+            }
+            // warp-uniform slot count: 4 (grids), 8, or a rescan of long rows
+            const int dmax = max(deg[0], deg[1]);
+            const bool four = __all_sync(0xffffffffu, dmax <= 4);
+            const bool ranked = __all_sync(0xffffffffu, dmax <= 8);
+            auto store = [&](int vv, int top) {
+                if (vv < 0) return;
+                m[vv] = top;
+                ptr[vv] = top;
+                cursor[vv] = ranked ? 0 : -1;
+            };
+            if (four) {
+                const int t0 = rank_row<4>(v[0], b[0], deg[0], ci, w, salt, nbr);
+                const int t1 = rank_row<4>(v[1], b[1], deg[1], ci, w, salt, nbr);
+                store(v[0], t0);
+                store(v[1], t1);
+            } else {
+#pragma unroll 1
+                for (int u = 0; u < 2; u++) {
+                    const int vv = u ? v[1] : v[0], bb = u ? b[1] : b[0], dd = u ? deg[1] : deg[0];
+                    int t;
+                    if (ranked) t = rank_row<8>(vv, bb, dd, ci, w, salt, nbr);
+                    else t = vv >= 0 ? heaviest<1>(vv, rp, ci, w, salt, 0, [](int) { return false; }) : -1;
+                    store(vv, t);
+                }
+            }
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = n;   // implicit list: every vertex
+    }
+    for (long long base = (long long)blockIdx.x * per_block; W > 1 && base < n;
          base += (long long)gridDim.x * per_block) {
         const long long idx = base + threadIdx.x / W;
         const int v = idx < n ? (int)idx : -1;
@@ -354,6 +436,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
     grid.sync();
     round_stamp(stamp++);
     int *in = la, *out = lb;
+    bool implicit = W == 1;   // the first list of W == 1 is every vertex, in order
     int r = 0;
     int cnt = *(volatile int *)&counts[0];
     while (cnt > 0 && r + 1 < kMaxRounds) {
@@ -365,7 +448,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
 #pragma unroll
                 for (int u = 0; u < kMatchUnroll; u++) {
                     const int i = i0 + u * stride;
-                    v[u] = i < cnt ? in[i] : -1;
+                    v[u] = i < cnt ? (implicit ? i : in[i]) : -1;
                 }
 #pragma unroll
                 for (int u = 0; u < kMatchUnroll; u++) p[u] = v[u] >= 0 ? ptr[v[u]] : -1;
@@ -389,7 +472,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
 #pragma unroll
                 for (int u = 0; u < kMatchUnroll; u++) {
                     const long long idx = base + u * kCoopThreads + threadIdx.x;
-                    v[u] = idx < cnt ? in[idx] : -1;
+                    v[u] = idx < cnt ? (implicit ? (int)idx : in[idx]) : -1;
                 }
 #pragma unroll
                 for (int u = 0; u < kMatchUnroll; u++) {
@@ -401,7 +484,8 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
                     e[u] = ok ? rp[v[u] + 1] : 0;
                 }
 #pragma unroll
-                for (int u = 0; u < kMatchUnroll; u++) mp[u] = (v[u] >= 0 && mv[u] < 0) ? mate[p[u]] : -1;
+                for (int u = 0; u < kMatchUnroll; u++)
+                    mp[u] = (v[u] >= 0 && mv[u] < 0 && p[u] >= 0) ? mate[p[u]] : -1;
 #pragma unroll
                 for (int u = 0; u < kMatchUnroll; u++) {
                     const bool adv = v[u] >= 0 && mv[u] < 0 && mp[u] >= 0 && cur[u] >= 0;
@@ -412,7 +496,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
                 for (int u = 0; u < kMatchUnroll; u++) mc[u] = cand[u] >= 0 ? mate[cand[u]] : -1;
 #pragma unroll
                 for (int u = 0; u < kMatchUnroll; u++) {
-                    if (v[u] < 0 || mv[u] >= 0) continue;
+                    if (v[u] < 0 || mv[u] >= 0 || p[u] < 0) continue;   // matched, or no neighbour
                     bool keep = mp[u] < 0;
                     if (!keep) {   // the target got matched: re-point
                         int bj;
@@ -494,6 +578,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_match_coop(int n, const int *r
         r++;
         cnt = *(volatile int *)gcount;
         int *t = in; in = out; out = t;
+        implicit = false;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
 }
@@ -582,9 +667,14 @@ struct RoundTrace {
     }
 };
 
-// cooperative launch with every CTA co-resident (grid = SMs x resident CTAs)
+// cooperative launch with every CTA co-resident (grid = SMs x resident CTAs);
+// `work` = vertices x lanes per vertex: small levels take only as many CTAs as
+// they can use (8 work items per thread), which keeps their grid barriers cheap
+#ifndef FDL_COOP_ITEMS_PER_THREAD
+#define FDL_COOP_ITEMS_PER_THREAD 8
+#endif
 template <class K>
-static void coop_launch(K kernel, void **args, cudaStream_t st, double grid_frac = 1.0) {
+static void coop_launch(K kernel, void **args, cudaStream_t st, double grid_frac, int64_t work) {
     static DeviceCache grid_cache{};   // one cache per kernel instantiation and device
     std::atomic<int> &grid_slot = grid_cache[current_device()];
     int grid = grid_slot.load();
@@ -602,8 +692,10 @@ static void coop_launch(K kernel, void **args, cudaStream_t st, double grid_frac
     // the kernels are grid-size agnostic: if the driver finds fewer co-resident
     // CTAs than the occupancy query promised, retry with a smaller grid
     for (;;) {
-        cudaError_t e = cudaLaunchCooperativeKernel((const void *)kernel, dim3(std::max(1, (int)(grid * grid_frac))),
-                                                    dim3(kCoopThreads), args, 0, st);
+        const int64_t useful = (work + (int64_t)kCoopThreads * FDL_COOP_ITEMS_PER_THREAD - 1) /
+                               ((int64_t)kCoopThreads * FDL_COOP_ITEMS_PER_THREAD);
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)(grid * grid_frac), useful));
+        cudaError_t e = cudaLaunchCooperativeKernel((const void *)kernel, dim3(g), dim3(kCoopThreads), args, 0, st);
         if (e == cudaErrorCooperativeLaunchTooLarge && grid > kNumSMs) {
             (void)cudaGetLastError();
             grid = grid * 3 / 4;
@@ -625,11 +717,11 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
     FDL_CK(cudaMemsetAsync(mcount.p, 0, (size_t)kMaxRounds * 4, st));
     DBuf m((size_t)n * 4, st), ptr((size_t)n * 4, st), la((size_t)n * 4, st), lb((size_t)n * 4, st),
         nbr((size_t)std::max(g.nnz, 1) * 4, st), cursor((size_t)n * 4, st),
-        counts((size_t)(kMaxRounds + 1) * 4, st);
+        counts((size_t)(kMaxRounds + 2) * 4, st);
     q.alloc((size_t)n * 4, st);
     mate.alloc((size_t)n * 4, st);
     FDL_CK(cudaMemsetAsync(mate.p, 0xff, (size_t)n * 4, st));
-    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 1) * 4, st));
+    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 2) * 4, st));
     {
         const int *rp = g.rp, *ci = g.ci;
         const double *w = g.w;
@@ -639,11 +731,14 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
         int *plm = lmv.as<int>(), *pmc = mcount.as<int>();
         void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr, &plm, &pmc};
         RoundTrace tr(st, "match");
-        DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st, kMatchGridFrac));
+        DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st, kMatchGridFrac, (int64_t)n * W));
         tr.report(counts.as<int>());
     }
-    rounds = read_int(counts.as<int>() + kMaxRounds, st);
-    FDL_REQUIRE(rounds >= 0, FIEDLER_ERR_INTERNAL, "matching did not terminate");
+    int rr[2];
+    FDL_CK(cudaMemcpyAsync(rr, counts.as<int>() + kMaxRounds, 8, cudaMemcpyDeviceToHost, st));
+    FDL_CK(cudaStreamSynchronize(st));
+    rounds = rr[0];
+    FDL_REQUIRE(rounds >= 0 && rr[1] == 0, FIEDLER_ERR_INTERNAL, "matching did not terminate");
     la.release();
     lb.release();
     nbr.release();
@@ -1664,7 +1759,7 @@ __device__ __forceinline__ void cta_first_fit(int v, const int *rp, const int *c
 // it releases its lower-priority neighbours.  Every vertex and edge is handled
 // a constant number of times (the round-based JP rescans waiting vertices).
 template <int W>
-__global__ void __launch_bounds__(kCoopThreads) k_color_coop(int n, const int *rp, const int *ci,
+__global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int n, const int *rp, const int *ci,
                                                              uint64_t salt, int *color, int *indeg,
                                                              int *la, int *lb, int *counts,
                                                              int *rounds_out) {
@@ -2261,7 +2356,7 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             // both cooperative kernels fit side by side with room for the rest
             // of the coarsening chain (a full-grid cooperative launch would wait
             // for the other one to drain)
-            DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridFrac));
+            DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridFrac, (int64_t)n * W));
             tr.report(job.counts.as<int>());
         }
     }
@@ -2593,8 +2688,48 @@ __global__ void k_compose_qg(int n, const int *perm, const int *q_nat, int *qg) 
     }
 }
 
+// FIEDLER_PHASE_TIMES=1: CUDA events around the setup phases of every level
+// (read once the setup is complete; off by default: no events in the timed
+// creates of the bench)
+struct PhaseTimes {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;   // per level and phase: begin, end
+    PhaseTimes() {
+        const char *e = std::getenv("FIEDLER_PHASE_TIMES");
+        on = e && e[0] == '1';
+    }
+    ~PhaseTimes() {
+        for (cudaEvent_t x : ev)
+            if (x) cudaEventDestroy(x);
+    }
+    cudaEvent_t &at(int level, int phase, int end) {
+        const size_t i = ((size_t)level * 4 + phase) * 2 + end;
+        if (ev.size() <= i) ev.resize(i + 1, nullptr);
+        return ev[i];
+    }
+    void mark(int level, int phase, int end, cudaStream_t s) {
+        if (!on) return;
+        cudaEvent_t &x = at(level, phase, end);
+        if (!x) FDL_CK(cudaEventCreate(&x));
+        FDL_CK(cudaEventRecord(x, s));
+    }
+    void collect(std::vector<Level> &levels) {
+        if (!on) return;
+        for (size_t l = 0; l < levels.size(); l++)
+            for (int p = 0; p < 4; p++) {
+                const size_t i = (l * 4 + p) * 2;
+                if (i + 1 >= ev.size() || !ev[i] || !ev[i + 1]) continue;
+                float ms = 0.f;
+                FDL_CK(cudaEventSynchronize(ev[i + 1]));
+                FDL_CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+                levels[l].phase_ms[p] = ms;
+            }
+    }
+};
+
 void build_hierarchy(Handle &h, NatGraph &&g0) {
     cudaStream_t st = h.stream, sb = h.stream2;
+    PhaseTimes pt;
     {   // FIEDLER_SERIAL_COLOUR=1 (diagnostics): colourings on the main stream
         const char *e = std::getenv("FIEDLER_SERIAL_COLOUR");
         if (e && e[0] == '1') sb = st;
@@ -2618,11 +2753,15 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
                 FDL_CK(cudaStreamWaitEvent(sb, ev, 0));
             }
             jobs.emplace_back(new ColourJob());
+            pt.mark(ell, 2, 0, sb);
             color_launch(cur, salt_color(o.seed, ell), L.color_nat, *jobs.back(), sb);
+            pt.mark(ell, 2, 1, sb);
             bool coarsen = cur.n > o.coarsest_size && ell + 1 < o.max_levels;
             NatGraph next;
             if (coarsen) {
+                pt.mark(ell, 0, 0, st);
                 int c = hec_parallel(cur, salt_match(o.seed, ell), L.q_nat, L.mate_nat, L.match_rounds, st);
+                pt.mark(ell, 0, 1, st);
                 trace_mark(st, ell == 0 ? "L0 matching" : "Lk matching");
                 // stall guard (R9): stop when HEC no longer shrinks the graph
                 if ((double)c > 0.95 * (double)cur.n || c < 2) {
@@ -2630,7 +2769,9 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
                     L.q_nat.release();
                     L.mate_nat.release();
                 } else {
+                    pt.mark(ell, 1, 0, st);
                     next = galerkin(cur, L.q_nat.as<int>(), c, st);
+                    pt.mark(ell, 1, 1, st);
                     trace_mark(st, ell == 0 ? "L0 galerkin" : "Lk galerkin");
                 }
             }
@@ -2646,7 +2787,9 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
         for (size_t ell = 0; ell < h.levels.size(); ell++) {
             Level &L = h.levels[ell];
             const int ncol = color_finish(*jobs[ell], L.color_rounds, sb);
+            pt.mark((int)ell, 3, 0, st);
             build_layout(graphs[ell], L.color_nat.as<int>(), ncol, L, st);
+            pt.mark((int)ell, 3, 1, st);
         }
         trace_mark(st, "layouts");
     } catch (...) {
@@ -2664,6 +2807,7 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
         FDL_LAUNCH_CK();
     }
     FDL_CK(cudaStreamSynchronize(st));
+    pt.collect(h.levels);
     trace_mark(st, "compose qp");
     if (!coarsest_connected(h.levels[J], st))
         throw Error(FIEDLER_ERR_DISCONNECTED,

@@ -1,11 +1,11 @@
 #!/bin/bash
-# ncu --set full of selected setup kernels of one create() on config CFG.  KRE=<kernel regex>
+# ncu --set full of the level-0 setup kernels of config CFG (one create + solve)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 CFG=${CFG:-4}
-KRE=${KRE:-"k_heavy_init|k_color_round|k_permute_rows|k_rs_scatter|k_repoint"}
-timeout 600 python tools/profile_step.py $CFG 1 > gpurun_out/step_plain.log 2>&1 && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:$KRE" -c ${NK:-6} \
-   -o gpurun_out/prof_setup -f python tools/profile_step.py $CFG 1 > gpurun_out/ncu_setup.log 2>&1
-echo "ncu exit $?" >> gpurun_out/ncu_setup.log
-tail -n 3 gpurun_out/ncu_setup.log
+TAG=${TAG:-setup}
+timeout 300 python tools/profile_step.py $CFG 1 > gpurun_out/ncu_${TAG}_plain.log 2>&1 || exit 1
+timeout 1500 ncu --set full --clock-control none --import-source on \
+  -k regex:"${KREGEX:-k_match_coop|k_color_coop|k_gal_direct_batch|k_permute_rows|k_gal_write}" -c ${COUNT:-5} \
+  -o gpurun_out/prof_${TAG} -f python tools/profile_step.py $CFG 1 > gpurun_out/ncu_${TAG}.log 2>&1
+echo "ncu exit $?" >> gpurun_out/ncu_${TAG}.log
