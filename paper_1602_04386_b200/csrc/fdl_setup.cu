@@ -1754,6 +1754,108 @@ __device__ __forceinline__ void cta_first_fit(int v, const int *rp, const int *c
     __syncthreads();
 }
 
+// W == 1 round work: colour a released vertex from its higher-priority
+// neighbours' colours (all final) and release its lower-priority neighbours
+// (they read colour(v) only after the round's grid barrier).  The row is taken
+// 8 entries at a time with every load and atomic of a chunk in flight; two
+// rows of <= 4 entries share one chunk (colour_pair_w1).
+// slot i of a chunk: vertex vs[i], neighbour u[i] (-1: empty slot)
+__device__ __forceinline__ void colour_chunk(const int (&vs)[8], const int (&u8)[8], const uint64_t (&pvs)[8],
+                                             uint64_t salt, const int *color, int *indeg,
+                                             unsigned long long &mask0, unsigned long long &mask1,
+                                             CtaAppend &app, int *out, int *gcount, int *rounds_out) {
+    int r8[8];
+    bool hi8[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+        hi8[i] = u8[i] >= 0 && higher_prio(splitmix64(salt ^ (uint64_t)u8[i]), u8[i], pvs[i], vs[i]);
+#pragma unroll
+    for (int i = 0; i < 8; i++) r8[i] = hi8[i] ? color[u8[i]] : 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const bool lo = u8[i] >= 0 && !hi8[i];
+        const int o = atom_dec_if(&indeg[lo ? u8[i] : 0], lo);
+        if (lo) r8[i] = o;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        if (u8[i] < 0) continue;
+        if (hi8[i]) {
+            unsigned long long &mk = i < 4 ? mask0 : mask1;
+            if (r8[i] < 0) rounds_out[1] = 1;   // impossible: uncoloured predecessor
+            else if (r8[i] < 64) mk |= 1ull << r8[i];
+        } else if (r8[i] == 1) {
+            app.push_safe(u8[i], out, gcount);
+        }
+    }
+}
+
+// first free colour of v given the colours < 64 of its higher-priority
+// neighbours (mask); rare: all of 0..63 taken -> windows of 64 beyond
+__device__ __forceinline__ int first_fit_w1(int v, unsigned long long mask, const int *rp, const int *ci,
+                                            uint64_t salt, const int *color) {
+    if (~mask) return __ffsll((long long)~mask) - 1;
+    const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+    const int b = rp[v], e = rp[v + 1];
+    for (int wb = 64;; wb += 64) {
+        unsigned long long m2 = 0ull;
+        for (int k = b; k < e; k++) {
+            const int u = ci[k];
+            if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+            const int cu = color[u];
+            if (cu >= wb && cu < wb + 64) m2 |= 1ull << (cu - wb);
+        }
+        if (~m2) return wb + __ffsll((long long)~m2) - 1;
+    }
+}
+
+__device__ __forceinline__ void colour_pair_w1(int v0, int v1, const int *rp, const int *ci, uint64_t salt,
+                                               int *color, int *indeg, CtaAppend &app, int *out, int *gcount,
+                                               int *rounds_out) {
+    const int b0 = v0 >= 0 ? rp[v0] : 0, e0 = v0 >= 0 ? rp[v0 + 1] : 0;
+    const int b1 = v1 >= 0 ? rp[v1] : 0, e1 = v1 >= 0 ? rp[v1 + 1] : 0;
+    const uint64_t p0 = v0 >= 0 ? splitmix64(salt ^ (uint64_t)v0) : 0, p1 = v1 >= 0 ? splitmix64(salt ^ (uint64_t)v1) : 0;
+    if (__all_sync(0xffffffffu, e0 - b0 <= 4 && e1 - b1 <= 4)) {   // warp-uniform: one chunk, both rows
+        int vs[8], u8[8];
+        uint64_t pvs[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const bool first = i < 4;
+            const int k = (first ? b0 : b1) + (i & 3);
+            vs[i] = first ? v0 : v1;
+            pvs[i] = first ? p0 : p1;
+            u8[i] = k < (first ? e0 : e1) ? ci[k] : -1;
+        }
+        unsigned long long m0 = 0ull, m1 = 0ull;
+        colour_chunk(vs, u8, pvs, salt, color, indeg, m0, m1, app, out, gcount, rounds_out);
+        if (v0 >= 0) color[v0] = first_fit_w1(v0, m0, rp, ci, salt, color);
+        if (v1 >= 0) color[v1] = first_fit_w1(v1, m1, rp, ci, salt, color);
+        return;
+    }
+#pragma unroll 1
+    for (int s = 0; s < 2; s++) {
+        const int v = s ? v1 : v0, b = s ? b1 : b0, e = s ? e1 : e0;
+        const uint64_t pv = s ? p1 : p0;
+        if (v < 0) continue;
+        unsigned long long mask = 0ull, dummy = 0ull;
+        for (int k = b; k < e; k += 8) {
+            int vs[8], u8[8];
+            uint64_t pvs[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                vs[i] = v;
+                pvs[i] = pv;
+                u8[i] = k + i < e ? ci[k + i] : -1;
+            }
+            unsigned long long m0 = 0ull, m1 = 0ull;
+            colour_chunk(vs, u8, pvs, salt, color, indeg, m0, m1, app, out, gcount, rounds_out);
+            mask |= m0 | m1;
+        }
+        (void)dummy;
+        color[v] = first_fit_w1(v, mask, rp, ci, salt, color);
+    }
+}
+
 // Topological (DAG) form of the same greedy colouring: indeg[v] = number of
 // higher-priority neighbours; a vertex is coloured once all of them are, then
 // it releases its lower-priority neighbours.  Every vertex and edge is handled
@@ -1853,8 +1955,9 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
         // W == 1: contiguous entries per CTA; W > 1: sub-warp slot s of CTA b
         // takes entry base + s * gridDim + b, so a short list (the deep rounds
         // of dense levels) is spread over all CTAs, at most one heavy vertex each
-        for (long long base = W == 1 ? (long long)blockIdx.x * per_block : 0; base < cnt;
-             base += (long long)gridDim.x * per_block) {
+        // (W == 1 takes two entries per thread: idx and idx + kCoopThreads)
+        for (long long base = W == 1 ? (long long)blockIdx.x * 2 * kCoopThreads : 0; base < cnt;
+             base += (long long)gridDim.x * (W == 1 ? 2 * kCoopThreads : per_block)) {
             const long long idx = W == 1 ? base + threadIdx.x
                                          : base + (long long)(threadIdx.x / W) * gridDim.x + blockIdx.x;
             int v = idx < cnt ? in[idx] : -1;
@@ -1863,60 +1966,9 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
                 v = -1;
             }
             if (W == 1) {
-                // one pass over the row, 8 entries at a time with every load and
-                // atomic of the chunk in flight: the colours of the higher-priority
-                // neighbours (all final) and the release of the lower-priority ones
-                // (they read colour(v) only after the round's grid barrier)
-                if (v >= 0) {
-                    const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
-                    const int b = rp[v], e = rp[v + 1];
-                    unsigned long long mask = 0ull;
-                    int big = 0;
-                    for (int k = b; k < e; k += 8) {
-                        int u8[8], r8[8];
-                        bool hi8[8];
-#pragma unroll
-                        for (int i = 0; i < 8; i++) u8[i] = k + i < e ? ci[k + i] : -1;
-#pragma unroll
-                        for (int i = 0; i < 8; i++)
-                            hi8[i] = u8[i] >= 0 &&
-                                     higher_prio(splitmix64(salt ^ (uint64_t)u8[i]), u8[i], pv, v);
-#pragma unroll
-                        for (int i = 0; i < 8; i++) r8[i] = hi8[i] ? color[u8[i]] : 0;
-#pragma unroll
-                        for (int i = 0; i < 8; i++) {
-                            const bool lo = u8[i] >= 0 && !hi8[i];
-                            const int o = atom_dec_if(&indeg[lo ? u8[i] : 0], lo);
-                            if (lo) r8[i] = o;
-                        }
-#pragma unroll
-                        for (int i = 0; i < 8; i++) {
-                            if (u8[i] < 0) continue;
-                            if (hi8[i]) {
-                                if (r8[i] < 0) rounds_out[1] = 1;   // impossible: uncoloured predecessor
-                                else if (r8[i] < 64) mask |= 1ull << r8[i];
-                                else big = 1;
-                            } else if (r8[i] == 1) {
-                                app.push_safe(u8[i], out, gcount);
-                            }
-                        }
-                    }
-                    int col = ~mask ? __ffsll((long long)~mask) - 1 : -1;
-                    (void)big;
-                    if (col < 0) {   // rare: colours 0..63 all taken by higher neighbours
-                        for (int wb = 64;; wb += 64) {
-                            unsigned long long m2 = 0ull;
-                            for (int k = b; k < e; k++) {
-                                const int u = ci[k];
-                                if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
-                                const int cu = color[u];
-                                if (cu >= wb && cu < wb + 64) m2 |= 1ull << (cu - wb);
-                            }
-                            if (~m2) { col = wb + __ffsll((long long)~m2) - 1; break; }
-                        }
-                    }
-                    color[v] = col;
-                }
+                const long long idx1 = idx + kCoopThreads;   // the thread's second entry
+                const int v1 = idx1 < cnt ? in[idx1] : -1;
+                colour_pair_w1(v, v1, rp, ci, salt, color, indeg, app, out, gcount, rounds_out);
             } else {
                 // all higher-priority neighbours are coloured: first fit
                 color_first_fit<W>(v, rp, ci, salt, color, lane, s_bm[threadIdx.x / W]);
@@ -1937,7 +1989,7 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
                 heavy_round(out, gcount);
                 __syncthreads();
             }
-            if (app.due(kAppendCap - kCoopThreads)) app.flush(out, gcount);
+            if (app.due(kAppendCap - 2 * kCoopThreads)) app.flush(out, gcount);
         }
         if (W > 1) heavy_round(out, gcount);
         __syncthreads();
