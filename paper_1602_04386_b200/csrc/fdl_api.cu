@@ -84,7 +84,10 @@ struct EventTimer {
     }
     double stop_ms() {
         FDL_CK(cudaEventRecord(b, s));
-        FDL_CK(cudaEventSynchronize(b));
+        cudaError_t e;
+        while ((e = cudaEventQuery(b)) == cudaErrorNotReady) {   // poll: no sleeping host wake-up
+        }
+        FDL_CK(e);
         float ms = 0.f;
         FDL_CK(cudaEventElapsedTime(&ms, a, b));
         return ms;
@@ -337,9 +340,8 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
                                                            : cudaMemcpyDeviceToDevice, st));
     }
     double res[3] = {0, 0, 0};
-    FDL_CK(cudaMemcpyAsync(res, h.result.p, sizeof(res), cudaMemcpyDeviceToHost, st));
     double ms = timer.stop_ms();
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{res, h.result.p, sizeof(res)}});
     trace_mark(st, "solve: run+copy");
     if (lambda2) *lambda2 = res[0];
     if (info) {

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <initializer_list>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -138,6 +139,19 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 // ----------------------------------------------------------------- primitives (fdl_prims.cu)
 // Exclusive prefix sum of int32; `total` (device, may be null) receives the sum.
 void scan_exclusive(const int *in, int *out, int64_t n, int *total, cudaStream_t st);
+
+// Small device -> host readbacks (counts, sizes, flags) of the setup: the
+// pieces are copied into pinned host memory and the host polls an event, so a
+// round trip costs a few microseconds of device idle time (a pageable copy +
+// cudaStreamSynchronize cost ~40 us each).  Waits for all prior work on st.
+struct ReadPiece {
+    void *dst;
+    const void *src;
+    size_t bytes;
+};
+void readback(cudaStream_t st, std::initializer_list<ReadPiece> pieces);
+// the same wait without copies
+void host_wait(cudaStream_t st);
 // Stable LSD radix sort of (key, value) pairs on bits [0, bits); result in keys/vals.
 void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStream_t st);
 // stable sort of the vertices by colour (< 256 colours): perm, inv, degree in sorted order, segment starts

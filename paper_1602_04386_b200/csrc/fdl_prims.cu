@@ -4,7 +4,9 @@
 // Used by the aggregate numbering (prefix scan of leader flags), work-list and
 // CSR offset scans everywhere, the Galerkin product's long-row path (two-key
 // radix sort) and the multicolour layout (sort by colour).
+#include <algorithm>
 #include <climits>
+#include <cstring>
 
 #include "fdl_common.cuh"
 
@@ -130,6 +132,58 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const int *in, int *ou
             for (int k = 0; k < 4; k++)
                 if (j + k < n) out[j + k] = y[k];
         }
+    }
+}
+
+// ---------------------------------------------------------------- readbacks
+namespace {
+struct PinnedScratch {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev[kMaxDevices] = {};
+    ~PinnedScratch() {
+        if (p) cudaFreeHost(p);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+thread_local PinnedScratch tl_pin;
+
+void poll(cudaStream_t st) {
+    cudaEvent_t &ev = tl_pin.ev[current_device()];
+    if (!ev) FDL_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    FDL_CK(cudaEventRecord(ev, st));
+    cudaError_t e;
+    while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+    }
+    FDL_CK(e);
+}
+}  // namespace
+
+void host_wait(cudaStream_t st) { poll(st); }
+
+void readback(cudaStream_t st, std::initializer_list<ReadPiece> pieces) {
+    size_t total = 0;
+    for (const ReadPiece &r : pieces) total += (r.bytes + 15) & ~(size_t)15;
+    if (total > tl_pin.cap) {
+        if (tl_pin.p) FDL_CK(cudaFreeHost(tl_pin.p));
+        tl_pin.p = nullptr;
+        tl_pin.cap = 0;
+        const size_t cap = std::max<size_t>(total, 1 << 16);
+        FDL_CK(cudaMallocHost(&tl_pin.p, cap));
+        tl_pin.cap = cap;
+    }
+    char *buf = static_cast<char *>(tl_pin.p);
+    size_t off = 0;
+    for (const ReadPiece &r : pieces) {
+        if (r.bytes) FDL_CK(cudaMemcpyAsync(buf + off, r.src, r.bytes, cudaMemcpyDeviceToHost, st));
+        off += (r.bytes + 15) & ~(size_t)15;
+    }
+    poll(st);
+    off = 0;
+    for (const ReadPiece &r : pieces) {
+        if (r.bytes) std::memcpy(r.dst, buf + off, r.bytes);
+        off += (r.bytes + 15) & ~(size_t)15;
     }
 }
 

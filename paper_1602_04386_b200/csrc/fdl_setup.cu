@@ -128,13 +128,11 @@ void validate_input(int64_t n, int64_t nnz, const int *rp32, const int *ci, cons
     k_rp_check32<<<grid_for(n + 1), 256, 0, st>>>(rp32, (int)n, (int)nnz, fl.as<int>());
     FDL_LAUNCH_CK();
     int h = 0;
-    FDL_CK(cudaMemcpyAsync(&h, fl.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{&h, fl.p, sizeof(int)}});
     FDL_REQUIRE(h == 0, FIEDLER_ERR_GRAPH, "row_ptr is not a valid CSR offset array");
     k_validate<<<grid_for(n), 256, 0, st>>>((int)n, rp32, ci, w, fl.as<int>());
     FDL_LAUNCH_CK();
-    FDL_CK(cudaMemcpyAsync(&h, fl.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{&h, fl.p, sizeof(int)}});
     if (h) {
         std::string m = "invalid graph CSR:";
         if (h & 2) m += " column index out of range;";
@@ -152,8 +150,7 @@ void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32,
     k_rp64_to_32<<<grid_for(n + 1), 256, 0, st>>>(rp64_dev, n, nnz, rp32, fl.as<int>());
     FDL_LAUNCH_CK();
     int h = 0;
-    FDL_CK(cudaMemcpyAsync(&h, fl.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{&h, fl.p, sizeof(int)}});
     FDL_REQUIRE(h == 0, FIEDLER_ERR_GRAPH, "row_ptr is not a valid CSR offset array");
 }
 
@@ -629,8 +626,7 @@ __global__ void k_assign(int n, const int *leader, const int *id, int *q) {
 
 static int read_int(const int *dptr, cudaStream_t st) {
     int h;
-    FDL_CK(cudaMemcpyAsync(&h, dptr, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{&h, dptr, sizeof(int)}});
     return h;
 }
 
@@ -735,8 +731,7 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
         tr.report(counts.as<int>());
     }
     int rr[2];
-    FDL_CK(cudaMemcpyAsync(rr, counts.as<int>() + kMaxRounds, 8, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{rr, counts.as<int>() + kMaxRounds, 8}});
     rounds = rr[0];
     FDL_REQUIRE(rounds >= 0 && rr[1] == 0, FIEDLER_ERR_INTERNAL, "matching did not terminate");
     la.release();
@@ -753,8 +748,7 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
     k_assign<<<grid_for(n), 256, 0, st>>>(n, leader.as<int>(), id.as<int>(), q.as<int>());
     FDL_LAUNCH_CK();
     int th[2];
-    FDL_CK(cudaMemcpyAsync(th, tot.p, 8, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{th, tot.p, 8}});
     FDL_REQUIRE(th[1] == 0, FIEDLER_ERR_INTERNAL, "heavy-edge matching is not maximal");
     return th[0];
 }
@@ -1556,8 +1550,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     k_gal_classify<<<grid_for(c), 256, 0, st>>>(c, mrp.as<int>(), toff.as<int>(), dl.as<int>(),
                                                 dl.as<int>() + c, dl.as<int>() + 2 * c, dcnt.as<int>());
     FDL_LAUNCH_CK();
-    FDL_CK(cudaMemcpyAsync(dc, dcnt.p, 12, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{dc, dcnt.p, 12}});
     {
         // rows ascend: input contract.  FIEDLER_TEST_FULL_SORT=1 (tests) forces
         // the fallback that very large levels take
@@ -2421,9 +2414,7 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
 
 static int color_finish(ColourJob &job, int &rounds, cudaStream_t st) {
     int h[3];
-    FDL_CK(cudaMemcpyAsync(&h[0], job.counts.as<int>() + kMaxRounds, 8, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaMemcpyAsync(&h[2], job.mx.p, 4, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{&h[0], job.counts.as<int>() + kMaxRounds, 8}, {&h[2], job.mx.p, 4}});
     rounds = h[0];
     FDL_REQUIRE(rounds >= 0 && h[1] == 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
     job.counts.release();
@@ -2525,6 +2516,21 @@ __global__ void k_gather_i32(int k, const int *src, const int *idx, int *out) {
         out[i] = src[idx[i]];
 }
 
+// colour segment starts of the GS layout (segstart[c] = first row of colour c,
+// -1 when empty) -> seg[c] with empty colours taking the next start,
+// seg[ncolors] = n, and their nonzero offsets segnnz[c] = rp[seg[c]]
+__global__ void k_seg_fix(int ncolors, int n, const int *segstart, const int *rp, int *seg, int *segnnz) {
+    int next = n;
+    seg[ncolors] = n;
+    segnnz[ncolors] = rp[n];
+    for (int k = ncolors - 1; k >= 0; k--) {
+        const int s = segstart[k];
+        next = s < 0 ? next : s;
+        seg[k] = next;
+        segnnz[k] = rp[next];
+    }
+}
+
 // Tiles of the row range [s0, s1): tile t holds the rows whose coordinate
 // rp[r] + r lies in [C0 + t*kTileT, C0 + (t+1)*kTileT), C0 = rp[s0] + s0.
 // The coordinate is strictly increasing in r, so the bounds are binary searches.
@@ -2610,24 +2616,19 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     // owns padded storage, copied otherwise) -- see take_natural() below
 
     // colour segment boundaries and their nonzero offsets -> host
-    std::vector<int> seg(ncolors + 1);
-    FDL_CK(cudaMemcpyAsync(seg.data(), segstart.p, (size_t)(ncolors + 1) * 4, cudaMemcpyDeviceToHost, st));
+    // (empty colours take the next colour's start; one round trip for all)
+    std::vector<int> seg(ncolors + 1), segnnz(ncolors + 1);
+    DBuf sfix((size_t)(ncolors + 1) * 8, st);
+    k_seg_fix<<<1, 1, 0, st>>>(ncolors, n, segstart.as<int>(), L.rp.as<int>(), sfix.as<int>(),
+                               sfix.as<int>() + ncolors + 1);
+    FDL_LAUNCH_CK();
     double dm = 0.0;
-    FDL_CK(cudaMemcpyAsync(&dm, dmax.p, 8, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{seg.data(), sfix.p, (size_t)(ncolors + 1) * 4},
+                  {segnnz.data(), sfix.as<int>() + ncolors + 1, (size_t)(ncolors + 1) * 4},
+                  {&dm, dmax.p, 8}});
     // R8: c = 2 max_i d_i (Gershgorin); on a 2-vertex level 2 max d = lambda_max
     // exactly and c I - L would annihilate the only non-constant direction
     L.shift = (n == 2 ? 3.0 : 2.0) * dm;
-    seg[ncolors] = n;
-    for (int k = ncolors - 1; k >= 0; k--)
-        if (seg[k] < 0) seg[k] = seg[k + 1];
-    DBuf sidx((size_t)(ncolors + 1) * 4, st), sval((size_t)(ncolors + 1) * 4, st);
-    FDL_CK(cudaMemcpyAsync(sidx.p, seg.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
-    k_gather_i32<<<1, 256, 0, st>>>(ncolors + 1, L.rp.as<int>(), sidx.as<int>(), sval.as<int>());
-    FDL_LAUNCH_CK();
-    std::vector<int> segnnz(ncolors + 1);
-    FDL_CK(cudaMemcpyAsync(segnnz.data(), sval.p, (size_t)(ncolors + 1) * 4, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
 
     // natural CSR for the PI / RQ passes
     auto take = [&](DBuf &own, const void *ptr, size_t bytes, DBuf &dst) {
@@ -2710,9 +2711,7 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
 // ================================================================= connectivity (coarsest level)
 static bool coarsest_connected(const Level &L, cudaStream_t st) {
     std::vector<int> rp(L.n + 1), ci(std::max(L.nnz, 1));
-    FDL_CK(cudaMemcpyAsync(rp.data(), L.rp.p, (size_t)(L.n + 1) * 4, cudaMemcpyDeviceToHost, st));
-    if (L.nnz) FDL_CK(cudaMemcpyAsync(ci.data(), L.ci.p, (size_t)L.nnz * 4, cudaMemcpyDeviceToHost, st));
-    FDL_CK(cudaStreamSynchronize(st));
+    readback(st, {{rp.data(), L.rp.p, (size_t)(L.n + 1) * 4}, {ci.data(), L.ci.p, (size_t)L.nnz * 4}});
     std::vector<char> seen(L.n, 0);
     std::vector<int> stack{0};
     seen[0] = 1;
@@ -2858,7 +2857,7 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
                                                     L.qg.as<int>());
         FDL_LAUNCH_CK();
     }
-    FDL_CK(cudaStreamSynchronize(st));
+    host_wait(st);
     pt.collect(h.levels);
     trace_mark(st, "compose qp");
     if (!coarsest_connected(h.levels[J], st))
