@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--kernel-reps", type=int, default=20)
-    ap.add_argument("--no-partitioned", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="headline = the row-sharded step of one graph (default when --gpus > 1)")
     ap.add_argument("--partition-min-rows", type=int, default=1 << 20)
     return ap.parse_args()
 
@@ -229,35 +230,56 @@ def setup_phase_rooflines(fd, n, nnz, rp, ci, w, opts, vec, peak):
     return out
 
 
-def partitioned_solve_timing(fd, g, rp, ci, w, dev, local, args, lam_single):
-    """Time the row-partitioned solve (paper_1602_04386_b200.dist) of the graph on
-    all ranks: device time of `steps` solves, max over ranks."""
+def sharded_step_timing(fd, g, rp, ci, w, dev, local, args, comm, dist):
+    """The row-sharded step: fiedler_create (the setup,
+    replicated on every rank) + the row-partitioned solve of ONE graph
+    (paper_1602_04386_b200.dist, fine levels >= min_rows split across the
+    ranks, NCCL halo exchange / all-reduce / all-gather).  Device time of every
+    step between CUDA events on the stream everything runs on, max over ranks."""
     import torch
-    import torch.distributed as dist
-    from paper_1602_04386_b200.dist import LibOps, PartitionedSolver, TorchComm
-    h = fd.fiedler_create(g.n, g.nnz, rp, ci, w, fd.fiedler_default_opts(device=local, validate=0))
-    try:
-        ops = LibOps(h, dev)
-        solver = PartitionedSolver(ops, TorchComm(), min_rows=args.partition_min_rows)
-        _, lam, _ = solver.solve()           # warm-up
+    from paper_1602_04386_b200.dist import LibOps, PartitionedSolver
+    stream = torch.cuda.current_stream(dev)
+    opts = fd.fiedler_default_opts(device=local, validate=0, stream=stream.cuda_stream)
+    info = {}
+
+    def step():
+        h = fd.fiedler_create(g.n, g.nnz, rp, ci, w, opts)
+        try:
+            solver = PartitionedSolver(LibOps(h, dev, stream=stream.cuda_stream), comm,
+                                       min_rows=args.partition_min_rows)
+            _, lam, _ = solver.solve()
+            info.update(lam=lam, levels_partitioned=int(sum(solver.part)),
+                        halo_bytes=solver.halo_bytes_per_solve())
+        finally:
+            fd.fiedler_destroy(h)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize()
-        dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(ops.torch_stream)
-        for _ in range(args.steps):
-            _, lam, _ = solver.solve()
-        e1.record(ops.torch_stream)
+        e0.record(stream)
+        step()
+        e1.record(stream)
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.steps
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        times.append(e0.elapsed_time(e1))
+    tot = sum(times)
+    hb = float(info.get("halo_bytes", 0))
+    if dist:
+        t = torch.tensor([tot, hb], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return {"solve_ms": float(t.item()), "levels_partitioned": int(sum(solver.part)),
-                "min_rows": args.partition_min_rows,
-                "lambda2": lam, "lambda2_rel_diff_vs_1gpu": abs(lam - lam_single) / lam_single,
-                "note": "setup replicated on every rank; solve of one graph row-partitioned"}
-    finally:
-        fd.fiedler_destroy(h)
+        tot, hb = float(t[0].item()), float(t[1].item())
+    ms = tot / args.steps
+    return {"ms_per_step": ms, "lambda2": info.get("lam"), "levels_partitioned": info.get("levels_partitioned"),
+            "min_rows": args.partition_min_rows, "halo_bytes_per_step": hb,
+            "halo_GBps_effective": hb / (ms / 1e3) / 1e9 if ms > 0 else None,
+            "note": "setup replicated on every rank; solve of one graph row-partitioned; "
+                    "halo bytes = the most any rank sends per step (NCCL all-to-all over NVLink); "
+                    "GB/s = those bytes / the whole step time (a lower bound on the link rate)"}
 
 
 def main():
@@ -396,16 +418,41 @@ def main():
     h2d = 8 * (n + 1) + 4 * nnz + 8 * nnz
     d2h = 8 * n + 8
 
-    # ---- N > 1: the row-partitioned solve of ONE graph across the ranks
-    # (setup replicated, fine levels partitioned, NCCL
-    # halo exchange / all-reduce / all-gather).  Reported beside the replica
-    # throughput; any failure is reported, not hidden.
-    partitioned = None
-    if dist and not args.no_partitioned:
-        try:
-            partitioned = partitioned_solve_timing(fd, g, rp, ci, w, dev, local, args, lam)
-        except Exception as exc:  # reported in the JSON line
-            partitioned = {"error": "%s: %s" % (type(exc).__name__, exc)}
+    # ---- N > 1 (or --sharded): the headline is the row-sharded step of ONE
+    # graph across the ranks (strong scaling); the
+    # per-rank replica throughput measured above becomes a side field
+    sharded = None
+    if dist or args.sharded:
+        from paper_1602_04386_b200.dist import LocalComm, TorchComm
+        comm = TorchComm() if dist else LocalComm()
+        sharded = sharded_step_timing(fd, g, rp, ci, w, dev, local, args, comm, dist)
+        # end to end: pinned host CSR in, Fiedler vector back to the host, wall clock, max over ranks
+        from paper_1602_04386_b200.dist import LibOps, PartitionedSolver
+
+        def e2e_sharded():
+            hh2 = fd.fiedler_create(n, nnz, prp, pci, pw, eo)
+            try:
+                sv = PartitionedSolver(LibOps(hh2, dev, stream=stream.cuda_stream), comm,
+                                       min_rows=args.partition_min_rows)
+                vv, _, _ = sv.solve()
+                pvec.copy_(vv)
+            finally:
+                fd.fiedler_destroy(hh2)
+        e2e_sharded()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_sharded()
+        torch.cuda.synchronize()
+        es = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([es], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            es = float(t.item())
+        sharded["e2e"] = {"value": nnz_L * args.e2e_steps / es, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                          "d2h_bytes_per_step": 8 * n}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -434,8 +481,17 @@ def main():
             "gpu_launches": launches,
             "clocks": ck,
         }
-        if partitioned is not None:
-            line["partitioned"] = partitioned
+        if sharded is not None:
+            line["replicas"] = {"value": value, "ms_per_step": tot_ms / args.steps, "scaling": "weak",
+                                "e2e": line["e2e"],
+                                "note": "every rank solves its own copy of the graph (no communication)"}
+            line["value"] = nnz_L * 1.0 / (sharded["ms_per_step"] / 1e3)
+            line["ms_per_step"] = sharded["ms_per_step"]
+            line["solve_time_ms"] = sharded["ms_per_step"]
+            line["scaling"] = "strong"
+            line["config"]["parallelism"] = "row-sharded fine levels over %d GPU(s), setup replicated" % world
+            line["sharded"] = sharded
+            line["e2e"] = sharded.pop("e2e")
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -153,10 +153,44 @@ class PartitionedSolver:
         self.part = [nr > 1 and l < J and ops.sizes[l] >= min_rows for l in range(ops.num_levels)]
         self.plans = [ops.plan(l, nr if self.part[l] else 1, rk if self.part[l] else 0)
                       for l in range(ops.num_levels)]
+        # every buffer of a solve is allocated once, here: per level the
+        # prolongation target, two power-iteration vectors, the halo send /
+        # receive buffers and the all-gather buffers; statistic slots from one
+        # pool (each op writes what it later reads, so reuse across solves is safe)
+        L = ops.num_levels
+        self.ybuf = [ops.vec(ops.sizes[l]) for l in range(L)]
+        self.pbuf = [(ops.vec(ops.sizes[l]), ops.vec(ops.sizes[l])) for l in range(L)]
+        self.send = [ops.vec(self.plans[l].send_total) if self.part[l] else None for l in range(L)]
+        self.recv = [ops.vec(self.plans[l].recv_total) if self.part[l] else None for l in range(L)]
+        self.ag_out = [ops.vec(ops.sizes[l]) if self.part[l] else None for l in range(L)]
+        self.ag_in = [ops.vec((self.plans[l].row_end - self.plans[l].row_begin) * nr) if self.part[l] else None
+                      for l in range(L)]
+        self.vnat = ops.vec(ops.sizes[0])
+        self._slots = ops.vec(4 * (4 * L + 8)).view(-1, 4)
+        self._next_slot = 0
 
     # ---------------------------------------------------------------- helpers
     def _slot(self):
-        return self.ops.vec(4)
+        s = self._slots[self._next_slot % self._slots.shape[0]]
+        self._next_slot += 1
+        return s
+
+    def halo_bytes_per_solve(self, gs_sweeps=2, power_iters=10):
+        """Bytes this rank sends per solve: halo exchanges (one per GS colour
+        pass, per power step and after the return to natural order) and the
+        all-gathers of partitioned levels' vectors (statistics all-reduces are
+        a few doubles and not counted)."""
+        tot = 0
+        J = self.ops.num_levels - 1
+        for l in range(self.ops.num_levels):
+            if not self.part[l]:
+                continue
+            p = self.plans[l]
+            passes = power_iters + (gs_sweeps * p.colors + 1 if gs_sweeps > 0 else 0)
+            tot += 8 * p.send_total * passes
+            if l < J:   # all-gather of the level's vector (every level but the finest's RQ output)
+                tot += 8 * (p.row_end - p.row_begin) * p.nranks
+        return tot
 
     def _reduce_finalise(self, level, slot):
         if self.part[level]:
@@ -168,8 +202,7 @@ class PartitionedSolver:
         if not self.part[level]:
             return
         p = self.plans[level]
-        send = self.ops.vec(p.send_total)
-        recv = self.ops.vec(p.recv_total)
+        send, recv = self.send[level], self.recv[level]
         self.ops.op(level, FIEDLER_DOP_HALO_PACK, numbering, x=v, y=send)
         self.comm.all_to_all(recv[:p.recv_total], send[:p.send_total], p.recv_count, p.send_count)
         self.ops.op(level, FIEDLER_DOP_HALO_UNPACK, numbering, x=recv, y=v)
@@ -180,16 +213,18 @@ class PartitionedSolver:
             return v
         p = self.plans[level]
         own = p.row_end - p.row_begin
-        chunk = v[p.row_begin:p.row_end]
-        inp = chunk.repeat(p.nranks) if own else self.ops.vec(0)[:0]
+        inp = self.ag_in[level][:own * p.nranks]
+        if own:
+            inp.view(p.nranks, own).copy_(v[p.row_begin:p.row_end].unsqueeze(0).expand(p.nranks, own))
         sizes = [p.bounds[k + 1] - p.bounds[k] for k in range(p.nranks)]
-        out = self.ops.vec(p.n)
+        out = self.ag_out[level]
         self.comm.all_to_all(out[:p.n], inp, sizes, [own] * p.nranks)
         return out
 
     def _power(self, level, cur, slot, iters):
+        a, b = self.pbuf[level]
         for _ in range(iters):
-            nxt = self.ops.vec(self.ops.sizes[level])
+            nxt = b if cur is a else a
             s2 = self._slot()
             self.ops.op(level, FIEDLER_DOP_POWER, x=cur, y=nxt, stat=s2, stat_in=slot)
             self._reduce_finalise(level, s2)
@@ -210,8 +245,9 @@ class PartitionedSolver:
         ops = self.ops
         J = ops.num_levels - 1
         kJ = power_iters if coarsest_power_iters is None else coarsest_power_iters
+        self._next_slot = 0
         # Step 2: rand(n_J) (R6) and power iteration on c I - L^J
-        cur = ops.vec(ops.sizes[J])
+        cur = self.pbuf[J][0]
         slot = self._slot()
         ops.op(J, FIEDLER_DOP_RAND, seed, y=cur, stat=slot)
         ops.op(J, FIEDLER_DOP_FINALISE, stat=slot)
@@ -219,16 +255,15 @@ class PartitionedSolver:
         full = self._allgather(J, cur)
         # Step 3: cascadic refinement
         for l in range(J - 1, -1, -1):
-            n = ops.sizes[l]
             ps = self._slot()
-            y = ops.vec(n)
+            y = self.ybuf[l]
             if gs_sweeps > 0:
                 ops.op(l, FIEDLER_DOP_PROLONG, GS, x=full, y=y, stat=ps)
                 for _ in range(gs_sweeps):
                     for c in range(self.plans[l].colors):
                         ops.op(l, FIEDLER_DOP_GS_COLOUR, c, x=y)
                         self._halo(l, y, GS)
-                z = ops.vec(n)
+                z = self.pbuf[l][0]
                 ops.op(l, FIEDLER_DOP_TO_NAT, x=y, y=z, stat=ps)
                 self._reduce_finalise(l, ps)
                 self._halo(l, z, NATURAL)
@@ -246,7 +281,7 @@ class PartitionedSolver:
         if self.part[0]:
             self.comm.allreduce_min(key[:1])
         ops.op(0, FIEDLER_DOP_SIGN, stat=key)
-        vnat = ops.vec(ops.sizes[0])
+        vnat = self.vnat
         rq = self._slot()
         ops.op(0, FIEDLER_DOP_RAYLEIGH, x=cur, y=vnat, stat=rq, stat_in=slot, sign_slot=key)
         if self.part[0]:
@@ -254,4 +289,4 @@ class PartitionedSolver:
         ops.op(0, FIEDLER_DOP_FINALISE_RQ, stat=rq, stat_in=slot)
         v = self._allgather(0, vnat)
         res = rq.cpu()
-        return v[:ops.sizes[0]], float(res[0]), float(res[1])
+        return v[:ops.sizes[0]].clone(), float(res[0]), float(res[1])
