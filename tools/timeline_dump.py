@@ -14,7 +14,8 @@ import graphgen as gg  # noqa: E402
 import paper_1602_04386_b200 as fd  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/timeline_c%d.json" % cfg
+what = sys.argv[2] if len(sys.argv) > 2 else "create"          # create | solve
+out = sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/timeline_%s_c%d.json" % (what, cfg)
 g = gg.config(cfg)
 dev = torch.device("cuda", 0)
 rp, ci, w = (torch.from_numpy(a).to(dev) for a in (g.rp, g.ci, g.w))
@@ -22,9 +23,18 @@ opts = fd.fiedler_default_opts(validate=0, use_graph=0)
 for _ in range(2):
     fd.fiedler_destroy(fd.fiedler_create(g.n, g.nnz, rp, ci, w, opts))
 torch.cuda.synchronize()
-with profile(activities=[ProfilerActivity.CUDA]) as prof:
+if what == "solve":
     h = fd.fiedler_create(g.n, g.nnz, rp, ci, w, opts)
+    vec = torch.empty(g.n, dtype=torch.float64, device=dev)
+    fd.fiedler_solve(h, vec, opts, None)
     torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fd.fiedler_solve(h, vec, opts, None)
+        torch.cuda.synchronize()
+else:
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        h = fd.fiedler_create(g.n, g.nnz, rp, ci, w, opts)
+        torch.cuda.synchronize()
 fd.fiedler_destroy(h)
 path = os.path.join(tempfile.mkdtemp(), "trace.json")
 prof.export_chrome_trace(path)
