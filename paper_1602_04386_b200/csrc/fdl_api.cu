@@ -51,11 +51,23 @@ Handle::~Handle() {
     }
     if (ev_pattern) cudaEventDestroy(ev_pattern);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (arena.base) {   // every arena buffer is gone (their frees were no-ops)
+        cudaFreeAsync(arena.base, stream);
+        cudaStreamSynchronize(stream);
+    }
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
 void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32, cudaStream_t st);
 int rowpass_grid();
+
+thread_local SmallArena *tl_arena = nullptr;
+
+// routes the small allocations of the enclosing scope (one fiedler_create) to an arena
+struct ArenaScope {
+    explicit ArenaScope(SmallArena *a) { tl_arena = a; }
+    ~ArenaScope() { tl_arena = nullptr; }
+};
 
 // Orders the handle's own stream after the caller's stream on entry (the
 // caller's inputs) and the caller's stream after the handle's on exit (the
@@ -239,6 +251,10 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
 
     if (!std::getenv("FIEDLER_NO_POOL_RESERVE"))
         reserve_pool(o.device, (size_t)(kPoolFactor * ((double)n * 12.0 + (double)nnz * 12.0)), st);
+    // small-buffer arena of the setup: 4 MB + 128 B per vertex, at most 64 MB
+    h->arena.cap = std::min<size_t>((size_t)64 << 20, ((size_t)4 << 20) + (size_t)n * 128);
+    FDL_CK(cudaMallocAsync((void **)&h->arena.base, h->arena.cap, st));
+    ArenaScope arena_scope(&h->arena);
     NatGraph g0;
     g0.n = (int)n;
     g0.nnz = (int)nnz;

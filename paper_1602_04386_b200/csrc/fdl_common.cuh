@@ -55,12 +55,33 @@ bool trace_enabled();
 void trace_mark(cudaStream_t st, const char *what);
 
 // ----------------------------------------------------------------- memory
+// Small-buffer arena of one fiedler_create: while a create runs, buffers of at
+// most kArenaMaxBytes are carved from one slab by a bump pointer and never
+// reused; their frees are no-ops and the slab goes with the handle.  The setup
+// makes ~40 small allocations per level (counts, flags, the arrays of the
+// small levels); as pool calls they cost host time that left the device idle
+// between the small levels' kernels.
+constexpr size_t kArenaMaxBytes = (size_t)1 << 20;
+struct SmallArena {
+    char *base = nullptr;
+    size_t cap = 0, off = 0;
+    void *take(size_t b) {
+        const size_t r = (b + 255) & ~(size_t)255;
+        if (!base || off + r > cap) return nullptr;
+        void *p = base + off;
+        off += r;
+        return p;
+    }
+};
+extern thread_local SmallArena *tl_arena;   // set by fiedler_create for its duration
+
 // Stream-ordered device buffer (cudaMallocAsync pool; capture-safe frees are
-// never issued inside a captured region).
+// never issued inside a captured region), or a piece of the create's arena.
 struct DBuf {
     void *p = nullptr;
     size_t bytes = 0;
     cudaStream_t s = nullptr;
+    bool in_arena = false;
     DBuf() = default;
     DBuf(size_t b, cudaStream_t st) { alloc(b, st); }
     DBuf(const DBuf &) = delete;
@@ -69,8 +90,8 @@ struct DBuf {
     DBuf &operator=(DBuf &&o) noexcept {
         if (this != &o) {
             release();
-            p = o.p; bytes = o.bytes; s = o.s;
-            o.p = nullptr; o.bytes = 0;
+            p = o.p; bytes = o.bytes; s = o.s; in_arena = o.in_arena;
+            o.p = nullptr; o.bytes = 0; o.in_arena = false;
         }
         return *this;
     }
@@ -79,12 +100,18 @@ struct DBuf {
         release();
         s = st;
         bytes = b;
-        if (b) FDL_CK(cudaMallocAsync(&p, b, st));
+        if (!b) return;
+        if (tl_arena && b <= kArenaMaxBytes && (p = tl_arena->take(b))) {
+            in_arena = true;
+            return;
+        }
+        FDL_CK(cudaMallocAsync(&p, b, st));
     }
     void release() noexcept {
-        if (p) cudaFreeAsync(p, s);
+        if (p && !in_arena) cudaFreeAsync(p, s);
         p = nullptr;
         bytes = 0;
+        in_arena = false;
     }
     template <class T> T *as() const { return static_cast<T *>(p); }
 };

@@ -105,6 +105,7 @@ struct Handle {
     cudaStream_t stream2 = nullptr;   // setup: colourings overlapped with the coarsening chain
     cudaEvent_t ev_pattern = nullptr; // host input: level-0 pattern (rp, ci) on the device
     cudaEvent_t ev_join = nullptr;    // joins a caller's stream with `stream` (fdl_api.cu StreamJoin)
+    SmallArena arena;                 // small buffers of the create (fdl_common.cuh); freed last
     fiedler_opts opts{};
     std::vector<Level> levels;
     int n0 = 0;
