@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <memory>
 #include <string>
 
@@ -38,24 +39,55 @@ thread_local long long g_launch_count = 0;
 
 void set_error(const std::string &m) { g_last_error = m; }
 
+#ifndef FDL_STREAM2_PRIO
+#define FDL_STREAM2_PRIO 0
+#endif
+
+// ---- per-device pool of stream sets (include: fdl_internal.h StreamSet)
+namespace {
+std::mutex g_pool_mu;
+std::vector<StreamSet> g_pool[kMaxDevices];
+}  // namespace
+
+static StreamSet take_stream_set(int dev) {
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_pool[dev].empty()) {
+            StreamSet s = g_pool[dev].back();
+            g_pool[dev].pop_back();
+            return s;
+        }
+    }
+    StreamSet s;
+    FDL_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    {   // stream2 priority (build knob FDL_STREAM2_PRIO: 0 default, 1 highest, -1 lowest)
+        int lo = 0, hi = 0;
+        FDL_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const int pr = FDL_STREAM2_PRIO > 0 ? hi : FDL_STREAM2_PRIO < 0 ? lo : 0;
+        FDL_CK(cudaStreamCreateWithPriority(&s.stream2, cudaStreamNonBlocking, pr));
+    }
+    for (cudaEvent_t &e : s.ev) FDL_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (cudaEvent_t &e : s.tev) FDL_CK(cudaEventCreate(&e));
+    return s;
+}
+
+static void give_stream_set(int dev, const StreamSet &s) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool[dev].push_back(s);
+}
+
 Handle::~Handle() {
     if (gexec) cudaGraphExecDestroy(gexec);
     gexec = nullptr;
     levels.clear();
     xa.release(); xb.release(); vnat.release(); scal.release();
     partials.release(); counter.release(); result.release();
-    if (stream) cudaStreamSynchronize(stream);
-    if (stream2) {
-        cudaStreamSynchronize(stream2);
-        cudaStreamDestroy(stream2);
-    }
-    if (ev_pattern) cudaEventDestroy(ev_pattern);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (arena.base) {   // every arena buffer is gone (their frees were no-ops)
-        cudaFreeAsync(arena.base, stream);
-        cudaStreamSynchronize(stream);
-    }
-    if (own_stream && stream) cudaStreamDestroy(stream);
+    if (arena.base) cudaFreeAsync(arena.base, stream);   // every arena buffer is gone (no-op frees)
+    arena.base = nullptr;
+    // idle streams go back to the pool (nothing of this handle is left on them)
+    const bool ok = (!stream || cudaStreamSynchronize(stream) == cudaSuccess) &&
+                    (!stream2 || cudaStreamSynchronize(stream2) == cudaSuccess);
+    if (set.stream && ok) give_stream_set(device, set);
 }
 
 void convert_row_ptr(const int64_t *rp64_dev, int64_t n, int64_t nnz, int *rp32, cudaStream_t st);
@@ -86,12 +118,11 @@ struct StreamJoin {
     }
 };
 
+// device time of one call between two timing events of the handle's set
 struct EventTimer {
     cudaEvent_t a = nullptr, b = nullptr;
     cudaStream_t s;
-    explicit EventTimer(cudaStream_t st) : s(st) {
-        FDL_CK(cudaEventCreate(&a));
-        FDL_CK(cudaEventCreate(&b));
+    EventTimer(cudaStream_t st, const StreamSet &set) : a(set.tev[0]), b(set.tev[1]), s(st) {
         FDL_CK(cudaEventRecord(a, s));
     }
     double stop_ms() {
@@ -103,10 +134,6 @@ struct EventTimer {
         float ms = 0.f;
         FDL_CK(cudaEventElapsedTime(&ms, a, b));
         return ms;
-    }
-    ~EventTimer() {
-        if (a) cudaEventDestroy(a);
-        if (b) cudaEventDestroy(b);
     }
 };
 
@@ -140,9 +167,6 @@ static void check_device(int dev) {
 #define FDL_POOL_FACTOR 8.0
 #endif
 constexpr double kPoolFactor = FDL_POOL_FACTOR;
-#ifndef FDL_STREAM2_PRIO
-#define FDL_STREAM2_PRIO 0
-#endif
 static void reserve_pool(int dev, size_t need, cudaStream_t st) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
@@ -235,19 +259,15 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     // The handle always works on a stream of its own: every device buffer it
     // allocates is freed on that stream, which lives until fiedler_destroy.  A
     // caller's stream (opts->stream) is joined with events (StreamJoin).
-    FDL_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->set = take_stream_set(o.device);
+    h->stream = h->set.stream;
+    h->stream2 = h->set.stream2;
+    h->ev_join = h->set.ev[0];
     h->own_stream = true;
-    FDL_CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     cudaStream_t st = h->stream;
     StreamJoin join(h->ev_join, (cudaStream_t)o.stream, st);
-    {   // stream2 priority (build knob FDL_STREAM2_PRIO: 0 default, 1 highest, -1 lowest)
-        int lo = 0, hi = 0;
-        FDL_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        const int pr = FDL_STREAM2_PRIO > 0 ? hi : FDL_STREAM2_PRIO < 0 ? lo : 0;
-        FDL_CK(cudaStreamCreateWithPriority(&h->stream2, cudaStreamNonBlocking, pr));
-    }
     h->row_grid = rowpass_grid();
-    EventTimer timer(st);
+    EventTimer timer(st, h->set);
 
     if (!std::getenv("FIEDLER_NO_POOL_RESERVE"))
         reserve_pool(o.device, (size_t)(kPoolFactor * ((double)n * 12.0 + (double)nnz * 12.0)), st);
@@ -274,7 +294,7 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
             // without validation the level-0 colouring (pattern only) may start
             // while the weights are still being copied
             if (!o.validate) {
-                FDL_CK(cudaEventCreateWithFlags(&h->ev_pattern, cudaEventDisableTiming));
+                h->ev_pattern = h->set.ev[1];
                 FDL_CK(cudaEventRecord(h->ev_pattern, st));
             }
             FDL_CK(cudaMemcpyAsync(g0.own_w.p, weights, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
@@ -322,7 +342,7 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
     SolveCfg cfg = cfg_of(o);
     prepare_solve(h, cfg);
     trace_mark(st, "solve: enter");
-    EventTimer timer(st);
+    EventTimer timer(st, h.set);
     int launches = 0;
     if (o.use_graph) {
         if (!h.gexec || h.g_gs != cfg.gs || h.g_pi != cfg.pi || h.g_piJ != cfg.piJ ||

@@ -98,8 +98,19 @@ struct Level {
     int nat_tile_begin() const { return ctile[ncolors]; }
 };
 
+// The streams and events of a handle come from a per-device pool and go back
+// to it at fiedler_destroy (fdl_api.cu): creating and destroying them for
+// every handle cost up to tens of milliseconds now and then (driver work).
+struct StreamSet {
+    cudaStream_t stream = nullptr;    // the handle's stream
+    cudaStream_t stream2 = nullptr;   // setup: colourings beside the coarsening chain
+    cudaEvent_t ev[4] = {};           // 0: join, 1: pattern, 2: setup scratch, 3: spare (no timing)
+    cudaEvent_t tev[2] = {};          // timing events of create / solve
+};
+
 struct Handle {
     int device = 0;
+    StreamSet set;                    // from the pool, returned by ~Handle
     cudaStream_t stream = nullptr;
     bool own_stream = false;          // always true: the handle owns `stream` (fdl_api.cu)
     cudaStream_t stream2 = nullptr;   // setup: colourings overlapped with the coarsening chain

@@ -2790,8 +2790,7 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
     h.levels.clear();
     std::vector<NatGraph> graphs;
     std::vector<std::unique_ptr<ColourJob>> jobs;
-    cudaEvent_t ev;
-    FDL_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaEvent_t ev = h.set.ev[2];
     try {
         for (int ell = 0;; ell++) {
             Level L;
@@ -2845,10 +2844,8 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
         trace_mark(st, "layouts");
     } catch (...) {
         cudaStreamSynchronize(sb);
-        cudaEventDestroy(ev);
         throw;
     }
-    cudaEventDestroy(ev);
     const int J = (int)h.levels.size() - 1;
     for (int ell = 0; ell < J; ell++) {
         Level &L = h.levels[ell];
