@@ -77,7 +77,8 @@ struct PassArgs {
     double *y;              // output (PI)
     const double *in_stat;  // slot of the input vector: [2]=mu, [3]=sigma
     double *out_stat;       // slot receiving S, Q, mu, sigma
-    int stat_mode;          // bit0: first contribution (assign), bit1: last (finalise), bit2: wanted
+    int stat_mode;          // bit0: first contribution (assign), bit1: last (finalise), bit2: wanted,
+                            // bit3: sums shifted by the slot's previous mean (see finish_stats)
     int n;                  // level size (mean)
     double shift;           // c
     double *partials;       // [grid][kNumStats]
@@ -168,8 +169,9 @@ __device__ __forceinline__ void row_finish(int r, const RowAcc<OP> &acc, const P
     if (OP == OP_GS) {
         double xn = acc.a / acc.b;
         const_cast<double *>(a.x)[r] = xn;
-        st[0] += xn;
-        st[1] = fma(xn, xn, st[1]);
+        const double xs = xn - sc.mu;   // shift K (finish_stats), 0 without bit 3
+        st[0] += xs;
+        st[1] = fma(xs, xs, st[1]);
     } else if (OP == OP_PI) {
         double z = (a.shift * (acc.own - sc.mu) + acc.a) * sc.inv_sigma;
         a.y[r] = z;
@@ -238,14 +240,20 @@ __device__ __forceinline__ void grid_reduce(double st[kNumStats], double *partia
     }
 }
 
+// slot = {S, Q, mean, deflated norm}.  With bit 3 of mode the sums are of
+// x - K, K = slot[2] on entry (the Gauss-Seidel passes shift by the mean of
+// their input, which their output stays close to): then Q - S^2/n does not
+// cancel even when |mean| >> the deflated norm.  Without it K = 0 (the
+// power-step / prolongation / random outputs have means ~ 0 or ~ the norm).
 __device__ __forceinline__ void finish_stats(const double tot[kNumStats], double *slot, int mode,
                                              int n) {
     if (mode & 1) { slot[0] = tot[0]; slot[1] = tot[1]; }
     else { slot[0] += tot[0]; slot[1] += tot[1]; }
     if (mode & 2) {
-        double mu = slot[0] / (double)n;
-        double var = slot[1] - (double)n * mu * mu;   // sum (x - mu)^2
-        slot[2] = mu;
+        const double K = (mode & 8) ? slot[2] : 0.0;
+        const double m = slot[0] / (double)n;          // mean of x - K
+        const double var = slot[1] - slot[0] * m;      // sum (x - mean)^2
+        slot[2] = K + m;
         slot[3] = sqrt(fmax(var, 0.0));
     }
 }
@@ -467,6 +475,7 @@ __device__ __forceinline__ void init_stages(PassSmem &S) {
 template <int OP>
 __device__ __forceinline__ Scal load_scal(const PassArgs &a) {
     Scal sc{0.0, 1.0, 1.0, 1.0};
+    if (OP == OP_GS && (a.stat_mode & 12) == 12) sc.mu = a.out_stat[2];   // shift of the statistics
     if (OP != OP_GS) {
         sc.mu = a.in_stat[2];
         sc.sigma = a.in_stat[3];
@@ -649,9 +658,10 @@ __global__ void __launch_bounds__(kGcThreads) k_gs_multi(CsrView L, const int *_
     }
     if (!(stat_mode & 4)) return;
     // statistics of the rows of these colours, in a fixed row -> thread map (the
-    // lists above are filled in atomic order)
+    // lists above are filled in atomic order), shifted by K (finish_stats)
+    const double K = (stat_mode & 8) ? slot[2] : 0.0;
     for (int r = seg[c0] + cr * kGcThreads + tid; r < seg[c1]; r += ncl * kGcThreads) {
-        const double xr = __ldcg(x + r);
+        const double xr = __ldcg(x + r) - K;
         S += xr;
         Q = fma(xr, xr, Q);
     }
@@ -949,14 +959,15 @@ struct Enq {
         if (sweeps <= 0) return;
         const int nr = (int)L.gs_runs.size() / 3;
         const int *R = L.gs_runs.data();
+        // statistics shifted by the input's mean, slot[2] of out_slot (bit 3)
         if (nr == 1 && R[2] != 0) {
-            gs_run(L, R[0], R[1], R[2], x, sweeps, out_slot, out_slot ? (4 | 1 | 2) : 0);
+            gs_run(L, R[0], R[1], R[2], x, sweeps, out_slot, out_slot ? (8 | 4 | 1 | 2) : 0);
             return;
         }
         for (int s = 0; s < sweeps; s++) {
             const bool want = (s == sweeps - 1) && out_slot;
             for (int i = 0; i < nr; i++) {
-                const int mode = want ? (4 | (i == 0 ? 1 : 0) | (i == nr - 1 ? 2 : 0)) : 0;
+                const int mode = want ? (8 | 4 | (i == 0 ? 1 : 0) | (i == nr - 1 ? 2 : 0)) : 0;
                 gs_run(L, R[3 * i], R[3 * i + 1], R[3 * i + 2], x, 1, out_slot, mode);
             }
         }
@@ -1114,6 +1125,8 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
             e.prolong(L, L.qg.as<int>(), cur, oth, ps);
             std::swap(cur, oth);
             double *gsl = e.slot(sl++);
+            // the GS statistics are shifted by the mean of the GS input (finish_stats)
+            FDL_CK(cudaMemcpyAsync(gsl + 2, ps + 2, 8, cudaMemcpyDeviceToDevice, h.stream));
             e.gs(L, cur, cfg.gs, gsl);
             e.to_nat(L, cur, oth);
             std::swap(cur, oth);
@@ -1161,6 +1174,10 @@ void apply_level_op(Handle &h, int level, int op, int count, const double *x_in,
             FDL_CK(cudaMemcpyAsync(xa, x_in, (size_t)L.n * 8, cudaMemcpyDeviceToDevice, st));
         }
         if (op == FIEDLER_OP_GS_SWEEPS) {
+            // statistics shifted by K = the first input entry (finish_stats): any
+            // value near the data keeps Q - S^2/n free of cancellation
+            FDL_CK(cudaMemsetAsync(s0, 0, 32, st));
+            FDL_CK(cudaMemcpyAsync(s0 + 2, xa, 8, cudaMemcpyDeviceToDevice, st));
             e.gs(L, xa, count, s0);
             k_scatter_f64<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), xa, x_out);
             FDL_LAUNCH_CK();

@@ -141,6 +141,25 @@ def test_single_ops_vs_oracle(fd, orc, name):
         fd.fiedler_destroy(h)
 
 
+def test_gs_statistics_without_cancellation(fd):
+    """The mean / deflated norm a GS pass reports (the lazy deflation and
+    normalisation of R5) stay accurate when the vector is nearly constant,
+    |mean| >> deflated norm: the sums are shifted (finish_stats), so
+    Q - S^2/n does not cancel.  Reference: numpy two-pass on the returned vector."""
+    g = gg.grid2d(64, "uniform", seed=4)
+    h = fd.fiedler_create(g.n, g.nnz, g.rp, g.ci, g.w)
+    try:
+        x = 1.0e6 + 1.0e-3 * np.random.default_rng(3).standard_normal(g.n)
+        out = np.empty_like(x)
+        mu, sig = fd.fiedler_level_apply(h, 0, fd.FIEDLER_OP_GS_SWEEPS, x, out, 2)
+    finally:
+        fd.fiedler_destroy(h)
+    ref_mu = out.mean()
+    ref_sig = np.sqrt(((out - ref_mu) ** 2).sum())
+    assert mu == pytest.approx(ref_mu, rel=1e-14)
+    assert sig == pytest.approx(ref_sig, rel=1e-9)
+
+
 def compare_solve(fd, orc, g, cfg_kw=None, device_input=False):
     cfg_kw = cfg_kw or {}
     ref = orc.solve(orc_graph(orc, g), orc.Config(**cfg_kw))
