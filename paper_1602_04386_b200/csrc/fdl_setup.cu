@@ -341,25 +341,28 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
             const int dmax = max(deg[0], deg[1]);
             const bool four = __all_sync(0xffffffffu, dmax <= 4);
             const bool ranked = __all_sync(0xffffffffu, dmax <= 8);
-            auto store = [&](int vv, int top) {
+            auto store = [&](int vv, int top, bool rk) {
                 if (vv < 0) return;
                 m[vv] = top;
                 ptr[vv] = top;
-                cursor[vv] = ranked ? 0 : -1;
+                cursor[vv] = rk ? 0 : -1;
             };
             if (four) {
                 const int t0 = rank_row<4>(v[0], b[0], deg[0], ci, w, salt, nbr);
                 const int t1 = rank_row<4>(v[1], b[1], deg[1], ci, w, salt, nbr);
-                store(v[0], t0);
-                store(v[1], t1);
+                store(v[0], t0, true);
+                store(v[1], t1, true);
             } else {
 #pragma unroll 1
                 for (int u = 0; u < 2; u++) {
                     const int vv = u ? v[1] : v[0], bb = u ? b[1] : b[0], dd = u ? deg[1] : deg[0];
+                    // rows of <= 8 entries are ranked even in a warp with longer
+                    // rows (only those are rescanned when they re-point)
+                    const bool rk = ranked || dd <= 8;
                     int t;
-                    if (ranked) t = rank_row<8>(vv, bb, dd, ci, w, salt, nbr);
+                    if (rk) t = rank_row<8>(vv, bb, dd, ci, w, salt, nbr);
                     else t = vv >= 0 ? heaviest<1>(vv, rp, ci, w, salt, 0, [](int) { return false; }) : -1;
-                    store(vv, t);
+                    store(vv, t, rk);
                 }
             }
         }
@@ -500,9 +503,19 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
                         if (cur[u] > 0) {   // ranked row: cursor advance from cur + 1
                             int c = cur[u], j = cand[u], mj = mc[u];
                             while (j >= 0 && mj >= 0) {
-                                c++;
-                                j = b[u] + c < e[u] ? nbr[b[u] + c] : -1;
-                                mj = j >= 0 ? mate[j] : -1;
+                                // the next four candidates, their mate loads in flight together
+                                int jj[4], mm[4];
+#pragma unroll
+                                for (int k = 0; k < 4; k++)
+                                    jj[k] = b[u] + c + 1 + k < e[u] ? nbr[b[u] + c + 1 + k] : -1;
+#pragma unroll
+                                for (int k = 0; k < 4; k++) mm[k] = jj[k] >= 0 ? mate[jj[k]] : -1;
+                                int fk = 4, fj = -1, fm = -1;   // first free candidate or the row end
+#pragma unroll
+                                for (int k = 0; k < 4; k++)
+                                    if (fk == 4 && !(jj[k] >= 0 && mm[k] >= 0)) { fk = k; fj = jj[k]; fm = mm[k]; }
+                                if (fk < 4) { c += 1 + fk; j = fj; mj = fm; }
+                                else { c += 4; j = jj[3]; mj = mm[3]; }
                             }
                             bj = j;
                             cursor[v[u]] = c;
