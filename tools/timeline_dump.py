@@ -23,10 +23,11 @@ opts = fd.fiedler_default_opts(validate=0, use_graph=0)
 for _ in range(2):
     fd.fiedler_destroy(fd.fiedler_create(g.n, g.nnz, rp, ci, w, opts))
 torch.cuda.synchronize()
-if what == "solve":
+if what in ("solve", "first_solve"):
     h = fd.fiedler_create(g.n, g.nnz, rp, ci, w, opts)
     vec = torch.empty(g.n, dtype=torch.float64, device=dev)
-    fd.fiedler_solve(h, vec, opts, None)
+    if what == "solve":     # a repeated solve (the first one also finishes the deferred level 0)
+        fd.fiedler_solve(h, vec, opts, None)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         fd.fiedler_solve(h, vec, opts, None)
