@@ -268,7 +268,9 @@ FIEDLER_API int fiedler_dist_plan(fiedler_handle h, int32_t level, int32_t nrank
 #define FIEDLER_DOP_HALO_UNPACK 12  /* y at the ghost rows = x (recv buffer); arg 0: y natural, 1: GS    */
 
 /* Enqueue one operation of the partitioned solve on `stream` (NULL = the
- * handle's stream) for the plan last built on `level`.  Never synchronises
+ * handle's own stream, which is non-blocking: device inputs written on other
+ * streams must be complete, or pass their stream) for the plan last built on
+ * `level`.  Never synchronises
  * `stream` (the first call may wait for the handle's own stream while it
  * allocates the handle's scratch).  All fiedler_dist_op calls of a handle,
  * and its fiedler_solve / fiedler_level_* calls, must be serialised on one

@@ -177,6 +177,7 @@ struct ReadPiece {
     size_t bytes;
 };
 void readback(cudaStream_t st, std::initializer_list<ReadPiece> pieces);
+void readback(cudaStream_t st, const std::vector<ReadPiece> &pieces);
 // the same wait without copies
 void host_wait(cudaStream_t st);
 // Stable LSD radix sort of (key, value) pairs on bits [0, bits); result in keys/vals.

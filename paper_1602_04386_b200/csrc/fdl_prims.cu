@@ -163,6 +163,10 @@ void poll(cudaStream_t st) {
 void host_wait(cudaStream_t st) { poll(st); }
 
 void readback(cudaStream_t st, std::initializer_list<ReadPiece> pieces) {
+    readback(st, std::vector<ReadPiece>(pieces));
+}
+
+void readback(cudaStream_t st, const std::vector<ReadPiece> &pieces) {
     size_t total = 0;
     for (const ReadPiece &r : pieces) total += (r.bytes + 15) & ~(size_t)15;
     if (total > tl_pin.cap) {

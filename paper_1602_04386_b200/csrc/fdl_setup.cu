@@ -744,9 +744,6 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
         tr.report(counts.as<int>());
     }
     int rr[2];
-    readback(st, {{rr, counts.as<int>() + kMaxRounds, 8}});
-    rounds = rr[0];
-    FDL_REQUIRE(rounds >= 0 && rr[1] == 0, FIEDLER_ERR_INTERNAL, "matching did not terminate");
     la.release();
     lb.release();
     nbr.release();
@@ -760,8 +757,11 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
     scan_exclusive(flag.as<int>(), id.as<int>(), n, tot.as<int>(), st);
     k_assign<<<grid_for(n), 256, 0, st>>>(n, leader.as<int>(), id.as<int>(), q.as<int>());
     FDL_LAUNCH_CK();
+    // one round trip for the round count / termination flag and the aggregate count
     int th[2];
-    readback(st, {{th, tot.p, 8}});
+    readback(st, {{rr, counts.as<int>() + kMaxRounds, 8}, {th, tot.p, 8}});
+    rounds = rr[0];
+    FDL_REQUIRE(rounds >= 0 && rr[1] == 0, FIEDLER_ERR_INTERNAL, "matching did not terminate");
     FDL_REQUIRE(th[1] == 0, FIEDLER_ERR_INTERNAL, "heavy-edge matching is not maximal");
     return th[0];
 }
@@ -2425,14 +2425,26 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
     job.indeg.release();
 }
 
-static int color_finish(ColourJob &job, int &rounds, cudaStream_t st) {
-    int h[3];
-    readback(st, {{&h[0], job.counts.as<int>() + kMaxRounds, 8}, {&h[2], job.mx.p, 4}});
-    rounds = h[0];
-    FDL_REQUIRE(rounds >= 0 && h[1] == 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
-    job.counts.release();
-    job.mx.release();
-    return h[2] + 1;
+// the colour counts of all levels in one round trip: ncol[l], rounds[l]
+static void color_finish_all(std::vector<std::unique_ptr<ColourJob>> &jobs, std::vector<int> &ncol,
+                             std::vector<int> &rounds, cudaStream_t st) {
+    const size_t L = jobs.size();
+    std::vector<int> h(3 * L);
+    std::vector<ReadPiece> pieces;
+    for (size_t l = 0; l < L; l++) {
+        pieces.push_back({&h[3 * l], jobs[l]->counts.as<int>() + kMaxRounds, 8});
+        pieces.push_back({&h[3 * l + 2], jobs[l]->mx.p, 4});
+    }
+    readback(st, pieces);
+    ncol.resize(L);
+    rounds.resize(L);
+    for (size_t l = 0; l < L; l++) {
+        rounds[l] = h[3 * l];
+        FDL_REQUIRE(rounds[l] >= 0 && h[3 * l + 1] == 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
+        ncol[l] = h[3 * l + 2] + 1;
+        jobs[l]->counts.release();
+        jobs[l]->mx.release();
+    }
 }
 
 // ================================================================= solve layout
@@ -2847,9 +2859,12 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
         FDL_CK(cudaEventRecord(ev, sb));
         FDL_CK(cudaStreamWaitEvent(st, ev, 0));
         trace_mark(sb, "colourings (second stream)");
+        std::vector<int> ncols, crounds;
+        color_finish_all(jobs, ncols, crounds, sb);
         for (size_t ell = 0; ell < h.levels.size(); ell++) {
             Level &L = h.levels[ell];
-            const int ncol = color_finish(*jobs[ell], L.color_rounds, sb);
+            L.color_rounds = crounds[ell];
+            const int ncol = ncols[ell];
             pt.mark((int)ell, 3, 0, st);
             build_layout(graphs[ell], L.color_nat.as<int>(), ncol, L, st);
             pt.mark((int)ell, 3, 1, st);

@@ -56,11 +56,15 @@ def test_plans_match_reference(fd, orc, name):
                     assert [info.recv_count[k] for k in range(world)] == ref.recv_count
                     x = torch.arange(L.g.n, dtype=torch.float64, device="cuda")
                     sb = torch.zeros(max(ref.send_total, 1), dtype=torch.float64, device="cuda")
+                    # the op runs on the handle's (non-blocking) stream: inputs made
+                    # on torch's stream must be complete first
+                    torch.cuda.synchronize()
                     fd.fiedler_dist_op(h, lev, fd.FIEDLER_DOP_HALO_PACK, 0, x=x, y=sb)
                     torch.cuda.synchronize()
                     assert np.array_equal(sb[:ref.send_total].cpu().numpy().astype(np.int64), sidx)
                     rb = torch.arange(max(ref.recv_total, 1), dtype=torch.float64, device="cuda")
                     y = torch.full((L.g.n,), -1.0, dtype=torch.float64, device="cuda")
+                    torch.cuda.synchronize()
                     fd.fiedler_dist_op(h, lev, fd.FIEDLER_DOP_HALO_UNPACK, 0, x=rb, y=y)
                     torch.cuda.synchronize()
                     got = y.cpu().numpy()
