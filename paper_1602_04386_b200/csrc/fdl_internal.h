@@ -21,13 +21,13 @@ namespace fdl {
 // first nonzero: that range is staged into shared memory by bulk copies.
 constexpr int kShortMax = 32;    // longer rows are reduced by a warp from global memory
 #ifndef FDL_TILE_T
-#define FDL_TILE_T 2048
+#define FDL_TILE_T 1024
 #endif
 #ifndef FDL_STAGES
 #define FDL_STAGES 2
 #endif
 #ifndef FDL_PASS_MINB
-#define FDL_PASS_MINB 4
+#define FDL_PASS_MINB 8
 #endif
 constexpr int kTileT = FDL_TILE_T;    // coordinate window per tile
 constexpr int kStages = FDL_STAGES;   // depth of the bulk-copy pipeline of a row pass

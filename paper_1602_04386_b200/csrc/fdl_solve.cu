@@ -40,7 +40,7 @@ namespace cg = cooperative_groups;
 
 enum { OP_GS = 0, OP_PI = 1, OP_RQ = 2 };
 #ifndef FDL_PASS_THREADS
-#define FDL_PASS_THREADS 256
+#define FDL_PASS_THREADS 128
 #endif
 constexpr int kPassThreads = FDL_PASS_THREADS;
 constexpr int kPassWarps = kPassThreads / 32;
@@ -49,7 +49,7 @@ constexpr int kPassWarps = kPassThreads / 32;
 // value and a sparse colour sub-range, prefer a deeper chunk)
 template <int OP, int CH> struct PassTune {
     static constexpr int chunk = CH ? CH : (OP == 0 ? 8 : 4);
-    static constexpr int min_blocks = (chunk == 4 && OP != 2) ? 4 : 3;
+    static constexpr int min_blocks = ((chunk == 4 && OP != 2) ? 4 : 3) * FDL_PASS_MINB / 4;
 };
 constexpr int kNumStats = 3;
 constexpr int kCiBuf = kStageCap + 8;   // + start alignment (<= 3) + 16-byte round-up (<= 3)
