@@ -1211,7 +1211,10 @@ __device__ __forceinline__ int batch_sort_fold(const int *KB, const int *LO, con
 // output block of the batch (rowoff[A] = its offset; the other classes' rows
 // keep T_A entries reserved there).  Without the b64 premises (`b64` false)
 // every class-0 row is appended to `redo` for the warp-per-row kernel.
-constexpr int kGalBatchWarps = 4;
+#ifndef FDL_GAL_BATCH_WARPS
+#define FDL_GAL_BATCH_WARPS 4
+#endif
+constexpr int kGalBatchWarps = FDL_GAL_BATCH_WARPS;   // warps (32-row batches) per CTA
 constexpr int kGalBatchSlots = 32 * 16;
 #ifndef FDL_GAL_UNROLL
 #define FDL_GAL_UNROLL 8
@@ -1570,7 +1573,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
         const char *fs = std::getenv("FIEDLER_TEST_FULL_SORT");
         const bool b64 = c < (1 << 27) && n < (1 << 29) && !(fs && fs[0] == '1');
         DBuf redo(b64 ? 0 : (size_t)c * 4, st);
-        k_gal_direct_batch<<<std::min(div_up(c, 32 * kGalBatchWarps), kNumSMs * 32), kGalBatchWarps * 32, 0,
+        k_gal_direct_batch<<<std::min(div_up(c, 32 * kGalBatchWarps), kNumSMs * 128 / kGalBatchWarps), kGalBatchWarps * 32, 0,
                              st>>>(c, b64, mrp.as<int>(), mem.as<int>(), toff.as<int>(), g.rp, g.ci, g.w, q,
                                    outB.as<int>(), outW.as<double>(), deg.as<int>(), rowoff.as<int>(),
                                    redo.as<int>(), dcnt.as<int>() + 3);
