@@ -90,7 +90,9 @@ typedef struct fiedler_opts {
     int32_t power_iters;          /* power iterations per level (default 10)                */
     int32_t coarsest_power_iters; /* power iterations on level J; -1 = power_iters          */
     int32_t validate;             /* 1 = check the CSR conventions on the device (default 1) */
-    int32_t use_graph;            /* 1 = replay the solve as one CUDA graph (default 1)     */
+    int32_t use_graph;            /* 1 = repeated solves with the same configuration are
+                                     captured once and replayed as one CUDA graph (the
+                                     first runs eagerly); 0 = always eager (default 1)     */
     uint64_t seed;                /* counter-based generator seed (R6), default 0           */
     void *stream;                 /* cudaStream_t to use; NULL = handle-owned stream        */
 } fiedler_opts;

@@ -344,10 +344,21 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
     trace_mark(st, "solve: enter");
     EventTimer timer(st, h.set);
     int launches = 0;
-    if (o.use_graph) {
-        if (!h.gexec || h.g_gs != cfg.gs || h.g_pi != cfg.pi || h.g_piJ != cfg.piJ ||
-            h.g_seed != cfg.seed) {
-            if (h.gexec) { cudaGraphExecDestroy(h.gexec); h.gexec = nullptr; }
+    // The first solve of a handle (and of every new configuration) runs eagerly:
+    // capturing and instantiating a graph costs more host time than it saves
+    // once, and eager launches keep the tile passes' programmatic dependent
+    // launches (measured: config 4 solve 30.7 ms via a fresh graph, 29.8 eager).
+    // A repeated solve with the same configuration is captured and replayed.
+    const bool same_cfg = h.g_gs == cfg.gs && h.g_pi == cfg.pi && h.g_piJ == cfg.piJ && h.g_seed == cfg.seed;
+    const bool replay = o.use_graph && same_cfg && h.solves_same > 0;
+    if (!same_cfg) {
+        h.solves_same = 0;
+        if (h.gexec) { cudaGraphExecDestroy(h.gexec); h.gexec = nullptr; }
+    }
+    h.g_gs = cfg.gs; h.g_pi = cfg.pi; h.g_piJ = cfg.piJ; h.g_seed = cfg.seed;
+    h.solves_same++;
+    if (replay) {
+        if (!h.gexec) {
             cudaGraph_t g = nullptr;
             FDL_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
             try {
@@ -361,7 +372,6 @@ int fiedler_solve(fiedler_handle hh, const fiedler_opts *opts, double *vec, int3
             cudaError_t e = cudaGraphInstantiate(&h.gexec, g, 0);
             cudaGraphDestroy(g);
             FDL_CK(e);
-            h.g_gs = cfg.gs; h.g_pi = cfg.pi; h.g_piJ = cfg.piJ; h.g_seed = cfg.seed;
             h.g_launches = launches;
         }
         trace_mark(st, "solve: capture+instantiate");

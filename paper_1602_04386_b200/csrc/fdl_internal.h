@@ -136,6 +136,7 @@ struct Handle {
     int g_gs = -1, g_pi = -1, g_piJ = -1;
     uint64_t g_seed = 0;
     int g_launches = 0;
+    int solves_same = 0;      // solves so far with the configuration in g_* (the first runs eagerly)
     ~Handle();
 };
 

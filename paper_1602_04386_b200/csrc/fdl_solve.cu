@@ -492,7 +492,6 @@ __global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_
     PassSmem &S = *reinterpret_cast<PassSmem *>(smem_raw);
     __shared__ RowAcc<OP> s_red[kPassWarps];
     init_stages(S);
-    const Scal sc = load_scal<OP>(a);
     double st[kNumStats] = {0.0, 0.0, 0.0};
     unsigned long long pol = 0;
     if (threadIdx.x == 0) pol = evict_first_policy();
@@ -503,6 +502,12 @@ __global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_
             const int tk = blockIdx.x + k * gridDim.x;
             if (tk < ntiles) issue_tile(S, L, tiles[tk], k, pol);
         }
+    // programmatic dependent launch: everything above (mbarriers, the first
+    // tile's column / weight streams -- the matrix, never written by the
+    // solve) overlaps the previous kernel's tail; the vectors and statistics
+    // it wrote are read only after this wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const Scal sc = load_scal<OP>(a);
     int it = 0;
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, it++) {
         const int b = it % kStages;
@@ -900,6 +905,27 @@ constexpr double kDenseRowDeg = FDL_DENSE_ROW_DEG;   // rows per tile few enough
 static DeviceCache g_pass_grid[4] = {};   // per OP (3: the 4-lane dense variant), per device
 static int pass_grid(int op) { return g_pass_grid[op][current_device()].load(); }
 
+// A tile pass as a programmatic dependent launch (FDL_PDL): its CTAs may start
+// while the previous kernel on the stream drains, up to griddepcontrol.wait
+#ifndef FDL_PDL
+#define FDL_PDL 1
+#endif
+template <class K>
+static void launch_pass(K kernel, int grid, cudaStream_t st, const Tile *tiles, int nt, CsrView v, PassArgs a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kPassThreads);
+    cfg.dynamicSmemBytes = kPassSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = FDL_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FDL_CK(cudaLaunchKernelEx(&cfg, kernel, tiles, nt, v, a));
+    FDL_LAUNCH_CK();
+}
+
 struct Enq {
     Handle &h;
     cudaStream_t st;
@@ -919,13 +945,12 @@ struct Enq {
         // levels; dense levels (>= kDenseRowDeg per row): 4 lanes per short row
         if (OP == OP_GS && L.nnz <= 4.5 * L.n) {
             grid = std::min(nt, pass_grid(3));
-            k_tilepass<OP_GS, 4><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
+            launch_pass(k_tilepass<OP_GS, 4>, grid, st, tiles, nt, v, a);
         } else if (L.nnz >= kDenseRowDeg * (double)L.n) {
-            k_tilepass<OP, 0, 4><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
+            launch_pass(k_tilepass<OP, 0, 4>, grid, st, tiles, nt, v, a);
         } else {
-            k_tilepass<OP><<<grid, kPassThreads, kPassSmemBytes, st>>>(tiles, nt, v, a);
+            launch_pass(k_tilepass<OP>, grid, st, tiles, nt, v, a);
         }
-        FDL_LAUNCH_CK();
         launches++;
     }
     template <int OP>
