@@ -39,6 +39,10 @@ namespace fdl {
 namespace cg = cooperative_groups;
 
 enum { OP_GS = 0, OP_PI = 1, OP_RQ = 2 };
+// solve-path kernels are programmatic dependent launches (pdl_wait, launch_pdl)
+#ifndef FDL_PDL
+#define FDL_PDL 1
+#endif
 #ifndef FDL_PASS_THREADS
 #define FDL_PASS_THREADS 128
 #endif
@@ -257,6 +261,10 @@ __device__ __forceinline__ void finish_stats(const double tot[kNumStats], double
         slot[3] = sqrt(fmax(var, 0.0));
     }
 }
+
+// programmatic dependent launch (launch_pdl): wait for the previous kernel on
+// the stream -- its writes visible -- before reading what it produced
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ----------------------------------------------------------------- the tile pass
 // x gathers: through the read-only path, or L2-coherent (__ldcg) when x is
@@ -506,7 +514,7 @@ __global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_
     // tile's column / weight streams -- the matrix, never written by the
     // solve) overlaps the previous kernel's tail; the vectors and statistics
     // it wrote are read only after this wait
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    pdl_wait();
     const Scal sc = load_scal<OP>(a);
     int it = 0;
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, it++) {
@@ -603,6 +611,7 @@ template <bool CLUSTER>
 __global__ void __launch_bounds__(kGcThreads) k_gs_multi(CsrView L, const int *__restrict__ seg, int c0,
                                                          int c1, int sweeps, double *x, double *slot,
                                                          int stat_mode, int n) {
+    pdl_wait();
     const int cr = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
     const int ncl = CLUSTER ? (int)cg::this_cluster().num_blocks() : 1;
     const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
@@ -695,6 +704,7 @@ __global__ void __launch_bounds__(kGcThreads) k_gs_multi(CsrView L, const int *_
 // in_slot = (mu, sigma) of y0 on entry, out_slot = statistics of the result.
 __global__ void __launch_bounds__(kCtaThreads) k_pi_small(CsrView L, double shift, int iters, double *y0,
                                                           double *y1, const double *in_slot, double *out_slot) {
+    pdl_wait();
     __shared__ double sm[kCtaWarps][2];
     __shared__ double s_mu, s_isig;
     const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
@@ -756,7 +766,9 @@ __global__ void __launch_bounds__(kCtaThreads) k_pi_small(CsrView L, double shif
 // coarse level's natural numbering; map = q (natural output) or q o perm (GS output)
 __global__ void __launch_bounds__(256) k_prolong(int n, const int *__restrict__ qp,
                                                  const double *__restrict__ xc, double *__restrict__ y,
-                                                 double *slot, double *partials, unsigned *counter) {
+                                                 double *slot, double *partials, unsigned *counter,
+                                                 double *mean_copy) {
+    pdl_wait();
     double st[kNumStats] = {0.0, 0.0, 0.0};
     const int stride = gridDim.x * blockDim.x;
     // 4 entries per thread in flight; statistics still summed in i order per thread
@@ -775,13 +787,17 @@ __global__ void __launch_bounds__(256) k_prolong(int n, const int *__restrict__ 
                 st[1] = fma(v[u], v[u], st[1]);
             }
     }
-    grid_reduce(st, partials, counter, [&](const double *tot) { finish_stats(tot, slot, 3, n); });
+    grid_reduce(st, partials, counter, [&](const double *tot) {
+        finish_stats(tot, slot, 3, n);
+        if (mean_copy) *mean_copy = slot[2];   // the GS statistics' shift (finish_stats)
+    });
 }
 
 // rand(n_J) in natural order, counter-based (R6)
 __global__ void __launch_bounds__(256) k_rand(int n, uint64_t seed,
                                               double *__restrict__ y, double *slot, double *partials,
                                               unsigned *counter) {
+    pdl_wait();
     const uint64_t s0 = splitmix64(seed ^ kTagRand);
     double st[kNumStats] = {0.0, 0.0, 0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -795,6 +811,7 @@ __global__ void __launch_bounds__(256) k_rand(int n, uint64_t seed,
 
 // sign convention: first nonzero entry (natural order) of v = (z - mu)/sigma positive
 __global__ void k_sign(int n, const double *__restrict__ z, const double *slot, double *sign) {
+    pdl_wait();
     const double mu = slot[2];
     for (int base = 0; base < n; base += 32) {
         int i = base + lane_id();
@@ -813,6 +830,7 @@ __global__ void k_sign(int n, const double *__restrict__ z, const double *slot, 
 // GS numbering -> natural numbering: dst[v] = src[inv[v]] (coalesced writes)
 __global__ void __launch_bounds__(256) k_gs_to_nat(int n, const int *__restrict__ inv,
                                                    const double *__restrict__ src, double *__restrict__ dst) {
+    pdl_wait();
     const int stride = gridDim.x * blockDim.x;
     for (int v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < n; v0 += 4 * stride) {   // 4 gathers in flight
         int p[4];
@@ -888,13 +906,15 @@ static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0
     cfg.gridDim = dim3(cl);
     cfg.blockDim = dim3(kGcThreads);
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = cl;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = FDL_PDL;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     FDL_CK(cudaLaunchKernelEx(&cfg, k_gs_multi<true>, v, seg, c0, c1, sweeps, x, slot, mode, n));
 }
 
@@ -907,9 +927,6 @@ static int pass_grid(int op) { return g_pass_grid[op][current_device()].load(); 
 
 // A tile pass as a programmatic dependent launch (FDL_PDL): its CTAs may start
 // while the previous kernel on the stream drains, up to griddepcontrol.wait
-#ifndef FDL_PDL
-#define FDL_PDL 1
-#endif
 template <class K>
 static void launch_pass(K kernel, int grid, cudaStream_t st, const Tile *tiles, int nt, CsrView v, PassArgs a) {
     cudaLaunchConfig_t cfg = {};
@@ -923,6 +940,22 @@ static void launch_pass(K kernel, int grid, cudaStream_t st, const Tile *tiles, 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     FDL_CK(cudaLaunchKernelEx(&cfg, kernel, tiles, nt, v, a));
+    FDL_LAUNCH_CK();
+}
+
+// any solve-path kernel as a programmatic dependent launch
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = FDL_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FDL_CK(cudaLaunchKernelEx(&cfg, kernel, args...));
     FDL_LAUNCH_CK();
 }
 
@@ -974,9 +1007,8 @@ struct Enq {
             launch_gs_cluster(st, v, L.seg_d.as<int>(), cb, ce, sweeps, x, out_slot, mode, L.n);
             launches++;
         } else {
-            k_gs_multi<false><<<1, kGcThreads, 0, st>>>(v, L.seg_d.as<int>(), cb, ce, sweeps, x, out_slot, mode,
-                                                        L.n);
-            FDL_LAUNCH_CK();
+            launch_pdl(k_gs_multi<false>, dim3(1), dim3(kGcThreads), st, v, (const int *)L.seg_d.as<int>(), cb, ce,
+                       sweeps, x, out_slot, mode, (int)L.n);
             launches++;
         }
     }
@@ -1004,8 +1036,8 @@ struct Enq {
         if (L.n <= kSmallPiRows && L.nnz <= kSmallPiNnz) {
             double *ns = next_slot(ctx);
             CsrView v{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
-            k_pi_small<<<1, kCtaThreads, 0, st>>>(v, L.shift, iters, cur, oth, cur_slot, ns);
-            FDL_LAUNCH_CK();
+            launch_pdl(k_pi_small, dim3(1), dim3(kCtaThreads), st, v, (double)L.shift, iters, cur, oth,
+                       (const double *)cur_slot, ns);
             launches++;
             if (iters & 1) std::swap(cur, oth);
             cur_slot = ns;
@@ -1039,15 +1071,15 @@ struct Enq {
         a.result = h.result.as<double>();
         pass<OP_RQ>(L, L.nat_tile_begin(), L.ntiles, a);
     }
-    void prolong(const Level &L, const int *map, const double *xc, double *y, double *out_slot) {
-        k_prolong<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(
-            L.n, map, xc, y, out_slot, h.partials.as<double>(), h.counter.as<unsigned>());
-        FDL_LAUNCH_CK();
+    void prolong(const Level &L, const int *map, const double *xc, double *y, double *out_slot,
+                 double *mean_copy = nullptr) {
+        launch_pdl(k_prolong, dim3(grid_for(L.n, 256, h.row_grid)), dim3(256), st, (int)L.n, map, xc, y, out_slot,
+                   h.partials.as<double>(), h.counter.as<unsigned>(), mean_copy);
         launches++;
     }
     void to_nat(const Level &L, const double *xg, double *xn) {
-        k_gs_to_nat<<<grid_for(L.n, 256, h.row_grid), 256, 0, st>>>(L.n, L.inv.as<int>(), xg, xn);
-        FDL_LAUNCH_CK();
+        launch_pdl(k_gs_to_nat, dim3(grid_for(L.n, 256, h.row_grid)), dim3(256), st, (int)L.n,
+                   (const int *)L.inv.as<int>(), xg, xn);
         launches++;
     }
 };
@@ -1130,9 +1162,8 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
     // ---- coarsest level: rand(n_J), deflate + normalise (lazily), power iteration
     const Level &LJ = h.levels[J];
     double *cur_slot = e.slot(sl++);
-    k_rand<<<grid_for(LJ.n, 256, h.row_grid), 256, 0, h.stream>>>(
-        LJ.n, cfg.seed, xa, cur_slot, h.partials.as<double>(), h.counter.as<unsigned>());
-    FDL_LAUNCH_CK();
+    launch_pdl(k_rand, dim3(grid_for(LJ.n, 256, h.row_grid)), dim3(256), h.stream, (int)LJ.n, (uint64_t)cfg.seed, xa,
+               cur_slot, h.partials.as<double>(), h.counter.as<unsigned>());
     e.launches++;
     double *cur = xa, *oth = xb;
     struct SlotCtx { Enq *e; int *sl; } sctx{&e, &sl};
@@ -1147,11 +1178,11 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
         double *ps = e.slot(sl++);
         if (cfg.gs > 0) {
             // prolong straight into GS numbering, sweep, return to natural numbering
-            e.prolong(L, L.qg.as<int>(), cur, oth, ps);
-            std::swap(cur, oth);
+            // (the GS statistics are shifted by the mean of the GS input: the
+            // prolongation copies it into the GS slot, finish_stats)
             double *gsl = e.slot(sl++);
-            // the GS statistics are shifted by the mean of the GS input (finish_stats)
-            FDL_CK(cudaMemcpyAsync(gsl + 2, ps + 2, 8, cudaMemcpyDeviceToDevice, h.stream));
+            e.prolong(L, L.qg.as<int>(), cur, oth, ps, gsl + 2);
+            std::swap(cur, oth);
             e.gs(L, cur, cfg.gs, gsl);
             e.to_nat(L, cur, oth);
             std::swap(cur, oth);
@@ -1166,8 +1197,7 @@ int enqueue_solve(Handle &h, const SolveCfg &cfg) {
     // ---- Rayleigh quotient on level 0 (+ vector in natural order)
     const Level &L0 = h.levels[0];
     double *sgn = e.slot(sl++);
-    k_sign<<<1, 32, 0, h.stream>>>(L0.n, cur, cur_slot, sgn);
-    FDL_LAUNCH_CK();
+    launch_pdl(k_sign, dim3(1), dim3(32), h.stream, (int)L0.n, (const double *)cur, (const double *)cur_slot, sgn);
     e.launches++;
     e.rq(L0, cur, cur_slot, h.vnat.as<double>(), sgn);
     FDL_REQUIRE(sl <= nslots, FIEDLER_ERR_INTERNAL, "slot overflow");
