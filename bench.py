@@ -361,6 +361,9 @@ def main():
     gs_ms, gs_bytes = fd.fiedler_level_time(hh, 0, fd.FIEDLER_OP_GS_SWEEPS, args.kernel_reps)
     rq_ms, rq_bytes = fd.fiedler_level_time(hh, 0, fd.FIEDLER_OP_RAYLEIGH, args.kernel_reps)
     nlev = fd.fiedler_num_levels(hh)
+    # the power step on the next levels (vectors and CSR smaller, still > L2 on config 4)
+    pi_lv = {ell: fd.fiedler_level_time(hh, ell, fd.FIEDLER_OP_POWER, args.kernel_reps)
+             for ell in (1, 2, 3) if ell < nlev - 1}
     fd.fiedler_destroy(hh)
     peak, peak_src = load_peaks()
     achieved = k_bytes / (k_ms / 1e3) / 1e9
@@ -378,6 +381,9 @@ def main():
                                    "frac": gs_bytes / (gs_ms / 1e3) / 1e9 / peak},
                "rayleigh_level0": {"ms": rq_ms, "GB/s": rq_bytes / (rq_ms / 1e3) / 1e9,
                                    "frac": rq_bytes / (rq_ms / 1e3) / 1e9 / peak}}
+    for ell, (ms, by) in pi_lv.items():
+        kernels["power_level%d" % ell] = {"ms": ms, "GB/s": by / (ms / 1e3) / 1e9,
+                                          "frac": by / (ms / 1e3) / 1e9 / peak}
     if tr and tr.get("config") == args.config:
         for key, tkey, ms in (("gs_sweep_level0", "gs_sweep_dram_bytes", gs_ms),
                               ("rayleigh_level0", "rayleigh_dram_bytes", rq_ms)):

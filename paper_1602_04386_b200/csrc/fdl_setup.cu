@@ -1799,10 +1799,52 @@ __device__ __forceinline__ void colour_chunk(const int (&vs)[8], const int (&u8)
     }
 }
 
+// Colouring state of the W == 1 rounds.  IntColourState: colour and in-degree
+// in two int arrays.  ByteColourState: ONE byte per vertex -- the in-degree
+// while uncoloured (bit 7 clear), 0x80 | colour once coloured -- for levels
+// whose degrees are all <= kByteMaxDeg (so every colour is < 127): a quarter
+// of one int array, which keeps the random accesses of the rounds in L2 (the
+// int arrays of level 0 of config 4 are 2 x 268 MB; the byte state 67 MB).
+struct IntColourState {
+    int *color, *indeg;
+    __device__ __forceinline__ int colour_of(int u) const { return color[u]; }   // < 0: uncoloured
+    // predicated release of u: old in-degree (0 when pred is false)
+    __device__ __forceinline__ int release(int u, bool pred) const { return atom_dec_if(&indeg[pred ? u : 0], pred); }
+    __device__ __forceinline__ void set_colour(int v, int c) const { color[v] = c; }
+};
+constexpr int kByteMaxDeg = 126;
+struct ByteColourState {
+    unsigned char *s;
+    __device__ __forceinline__ int colour_of(int u) const {
+        const int b = s[u];
+        return (b & 0x80) ? (b & 0x7f) : -1;
+    }
+    // the in-degree is a byte of an aligned word: subtracting 1 << shift never
+    // borrows across bytes (a vertex is released exactly in-degree times)
+    __device__ __forceinline__ int release(int u, bool pred) const {
+        const int uu = pred ? u : 0;
+        unsigned *wp = reinterpret_cast<unsigned *>(s + (uu & ~3));
+        const unsigned d = 0u - (1u << (8 * (uu & 3)));   // add of -(1 << shift) mod 2^32
+        unsigned old = 0u;
+        asm volatile(
+            "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q atom.global.add.u32 %0, [%1], %2;\n}\n"
+            : "+r"(old)
+            : "l"(wp), "r"(d), "r"((int)pred)
+            : "memory");
+        return (int)((old >> (8 * (uu & 3))) & 0xffu);
+    }
+    // v's byte is 0 (in-degree reached 0): OR in the colour; the neighbouring
+    // bytes of the word may be released concurrently, hence the atomic
+    __device__ __forceinline__ void set_colour(int v, int c) const {
+        atomicOr(reinterpret_cast<unsigned *>(s + (v & ~3)), (0x80u | (unsigned)c) << (8 * (v & 3)));
+    }
+};
+
 // first free colour of v given the colours < 64 of its higher-priority
 // neighbours (mask); rare: all of 0..63 taken -> windows of 64 beyond
+template <class State>
 __device__ __forceinline__ int first_fit_w1(int v, unsigned long long mask, const int *rp, const int *ci,
-                                            uint64_t salt, const int *color) {
+                                            uint64_t salt, const State &cs) {
     if (~mask) return __ffsll((long long)~mask) - 1;
     const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
     const int b = rp[v], e = rp[v + 1];
@@ -1811,15 +1853,53 @@ __device__ __forceinline__ int first_fit_w1(int v, unsigned long long mask, cons
         for (int k = b; k < e; k++) {
             const int u = ci[k];
             if (!higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
-            const int cu = color[u];
+            const int cu = cs.colour_of(u);
             if (cu >= wb && cu < wb + 64) m2 |= 1ull << (cu - wb);
         }
         if (~m2) return wb + __ffsll((long long)~m2) - 1;
     }
 }
 
+// W == 1 round work: colour a released vertex from its higher-priority
+// neighbours' colours (all final) and release its lower-priority neighbours
+// (they read colour(v) only after the round's grid barrier).  The row is taken
+// 8 entries at a time with every load and atomic of a chunk in flight; two
+// rows of <= 4 entries share one chunk (colour_pair_w1).
+// slot i of a chunk: vertex vs[i], neighbour u[i] (-1: empty slot)
+template <class State>
+__device__ __forceinline__ void colour_chunk(const int (&vs)[8], const int (&u8)[8], const uint64_t (&pvs)[8],
+                                             uint64_t salt, const State &cs,
+                                             unsigned long long &mask0, unsigned long long &mask1,
+                                             CtaAppend &app, int *out, int *gcount, int *rounds_out) {
+    int r8[8];
+    bool hi8[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+        hi8[i] = u8[i] >= 0 && higher_prio(splitmix64(salt ^ (uint64_t)u8[i]), u8[i], pvs[i], vs[i]);
+#pragma unroll
+    for (int i = 0; i < 8; i++) r8[i] = hi8[i] ? cs.colour_of(u8[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const bool lo = u8[i] >= 0 && !hi8[i];
+        const int o = cs.release(u8[i], lo);
+        if (lo) r8[i] = o;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        if (u8[i] < 0) continue;
+        if (hi8[i]) {
+            unsigned long long &mk = i < 4 ? mask0 : mask1;
+            if (r8[i] < 0) rounds_out[1] = 1;   // impossible: uncoloured predecessor
+            else if (r8[i] < 64) mk |= 1ull << r8[i];
+        } else if (r8[i] == 1) {
+            app.push_safe(u8[i], out, gcount);
+        }
+    }
+}
+
+template <class State>
 __device__ __forceinline__ void colour_pair_w1(int v0, int v1, const int *rp, const int *ci, uint64_t salt,
-                                               int *color, int *indeg, CtaAppend &app, int *out, int *gcount,
+                                               const State &cs, CtaAppend &app, int *out, int *gcount,
                                                int *rounds_out) {
     const int b0 = v0 >= 0 ? rp[v0] : 0, e0 = v0 >= 0 ? rp[v0 + 1] : 0;
     const int b1 = v1 >= 0 ? rp[v1] : 0, e1 = v1 >= 0 ? rp[v1 + 1] : 0;
@@ -1836,9 +1916,9 @@ __device__ __forceinline__ void colour_pair_w1(int v0, int v1, const int *rp, co
             u8[i] = k < (first ? e0 : e1) ? ci[k] : -1;
         }
         unsigned long long m0 = 0ull, m1 = 0ull;
-        colour_chunk(vs, u8, pvs, salt, color, indeg, m0, m1, app, out, gcount, rounds_out);
-        if (v0 >= 0) color[v0] = first_fit_w1(v0, m0, rp, ci, salt, color);
-        if (v1 >= 0) color[v1] = first_fit_w1(v1, m1, rp, ci, salt, color);
+        colour_chunk(vs, u8, pvs, salt, cs, m0, m1, app, out, gcount, rounds_out);
+        if (v0 >= 0) cs.set_colour(v0, first_fit_w1(v0, m0, rp, ci, salt, cs));
+        if (v1 >= 0) cs.set_colour(v1, first_fit_w1(v1, m1, rp, ci, salt, cs));
         return;
     }
 #pragma unroll 1
@@ -1846,7 +1926,7 @@ __device__ __forceinline__ void colour_pair_w1(int v0, int v1, const int *rp, co
         const int v = s ? v1 : v0, b = s ? b1 : b0, e = s ? e1 : e0;
         const uint64_t pv = s ? p1 : p0;
         if (v < 0) continue;
-        unsigned long long mask = 0ull, dummy = 0ull;
+        unsigned long long mask = 0ull;
         for (int k = b; k < e; k += 8) {
             int vs[8], u8[8];
             uint64_t pvs[8];
@@ -1857,12 +1937,86 @@ __device__ __forceinline__ void colour_pair_w1(int v0, int v1, const int *rp, co
                 u8[i] = k + i < e ? ci[k + i] : -1;
             }
             unsigned long long m0 = 0ull, m1 = 0ull;
-            colour_chunk(vs, u8, pvs, salt, color, indeg, m0, m1, app, out, gcount, rounds_out);
+            colour_chunk(vs, u8, pvs, salt, cs, m0, m1, app, out, gcount, rounds_out);
             mask |= m0 | m1;
         }
-        (void)dummy;
-        color[v] = first_fit_w1(v, mask, rp, ci, salt, color);
+        cs.set_colour(v, first_fit_w1(v, mask, rp, ci, salt, cs));
     }
+}
+
+// The W == 1 colouring with the byte state (ByteColourState).  Round 0 also
+// checks the degree bound; a level that breaks it leaves counts[0] = 0 and
+// flag[0] = 1, and k_color_coop<1> (launched after it, gated on the flag)
+// colours it with the int state instead.  The rounds are those of
+// k_color_coop<1>; a last pass writes the int colours.
+__global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks)
+    k_color_byte(int n, const int *rp, const int *ci, uint64_t salt, int *color, unsigned char *st8,
+                 int *la, int *lb, int *counts, int *rounds_out, int *flag) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int s_buf[kAppendCap];
+    __shared__ int s_n, s_base, s_big;
+    if (threadIdx.x == 0) { s_n = 0; s_big = 0; }
+    __syncthreads();
+    CtaAppend app{s_buf, &s_n, &s_base};
+    int stamp = 0;
+    round_stamp(stamp++);
+    for (long long base = (long long)blockIdx.x * kCoopThreads; base < n; base += (long long)gridDim.x * kCoopThreads) {
+        const long long idx = base + threadIdx.x;
+        const int v = idx < n ? (int)idx : -1;
+        int c = 0;
+        if (v >= 0) {
+            const int b = rp[v], e = rp[v + 1];
+            if (e - b > kByteMaxDeg) {
+                s_big = 1;
+            } else {
+                const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+                for (int k = b; k < e; k++) {
+                    const int u = ci[k];
+                    c += higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v);
+                }
+                st8[v] = (unsigned char)c;
+                if (c == 0) app.push(v);
+            }
+        }
+        __syncthreads();
+        if (app.due(kAppendCap - kCoopThreads)) app.flush(la, counts);
+    }
+    __syncthreads();
+    app.flush(la, counts);
+    if (threadIdx.x == 0 && s_big) atomicOr(flag, 1);
+    grid.sync();
+    round_stamp(stamp++);
+    if (*(volatile int *)flag) {   // grid-uniform: the int-state kernel takes over
+        if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = 0;
+        return;
+    }
+    const ByteColourState cs{st8};
+    int *in = la, *out = lb;
+    int r = 0;
+    int cnt = *(volatile int *)&counts[0];
+    while (cnt > 0 && r + 1 < kMaxRounds) {
+        int *gcount = counts + r + 1;
+        for (long long base = (long long)blockIdx.x * 2 * kCoopThreads; base < cnt;
+             base += (long long)gridDim.x * 2 * kCoopThreads) {
+            const long long idx = base + threadIdx.x, idx1 = idx + kCoopThreads;
+            const int v = idx < cnt ? in[idx] : -1;
+            const int v1 = idx1 < cnt ? in[idx1] : -1;
+            colour_pair_w1(v, v1, rp, ci, salt, cs, app, out, gcount, rounds_out);
+            __syncthreads();
+            if (app.due(kAppendCap - 2 * kCoopThreads)) app.flush(out, gcount);
+        }
+        __syncthreads();
+        app.flush(out, gcount);
+        grid.sync();
+        round_stamp(stamp++);
+        r++;
+        cnt = *(volatile int *)gcount;
+        int *t = in; in = out; out = t;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
+    for (long long v = (long long)blockIdx.x * kCoopThreads + threadIdx.x; v < n;
+         v += (long long)gridDim.x * kCoopThreads)
+        color[v] = cs.colour_of((int)v);
 }
 
 // Topological (DAG) form of the same greedy colouring: indeg[v] = number of
@@ -1873,7 +2027,9 @@ template <int W>
 __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int n, const int *rp, const int *ci,
                                                              uint64_t salt, int *color, int *indeg,
                                                              int *la, int *lb, int *counts,
-                                                             int *rounds_out) {
+                                                             int *rounds_out, const int *gate) {
+    // gated (after k_color_byte): runs only when the byte state could not be used
+    if (gate && *(volatile const int *)gate == 0) return;
     cg::grid_group grid = cg::this_grid();
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
@@ -1977,7 +2133,7 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
             if (W == 1) {
                 const long long idx1 = idx + kCoopThreads;   // the thread's second entry
                 const int v1 = idx1 < cnt ? in[idx1] : -1;
-                colour_pair_w1(v, v1, rp, ci, salt, color, indeg, app, out, gcount, rounds_out);
+                colour_pair_w1(v, v1, rp, ci, salt, IntColourState{color, indeg}, app, out, gcount, rounds_out);
             } else {
                 // all higher-priority neighbours are coloured: first fit
                 color_first_fit<W>(v, rp, ci, salt, color, lane, s_bm[threadIdx.x / W]);
@@ -2337,8 +2493,12 @@ __global__ void __launch_bounds__(kSmallColourThreads, 1) k_color_cluster(int n,
 constexpr double kColourGridFrac = FDL_COLOUR_GRID_FRAC;
 
 struct ColourJob {
-    DBuf la, lb, indeg, counts, mx;
+    DBuf la, lb, indeg, counts, mx, st8;
 };
+#ifndef FDL_BYTE_COLOUR
+#define FDL_BYTE_COLOUR 1
+#endif
+constexpr bool kByteColour = FDL_BYTE_COLOUR;
 
 // whether a 16-CTA cluster of k_color_cluster (1024 threads, ~210 KB shared
 // memory each) can be resident on this device
@@ -2379,13 +2539,14 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
     job.la.alloc((size_t)n * 4, st);
     job.lb.alloc((size_t)n * 4, st);
     job.indeg.alloc((size_t)n * 4, st);
-    job.counts.alloc((size_t)(kMaxRounds + 2) * 4, st);
-    FDL_CK(cudaMemsetAsync(job.counts.p, 0, (size_t)(kMaxRounds + 2) * 4, st));
+    job.counts.alloc((size_t)(kMaxRounds + 4) * 4, st);
+    FDL_CK(cudaMemsetAsync(job.counts.p, 0, (size_t)(kMaxRounds + 4) * 4, st));
     {
         const int *rp = g.rp, *ci = g.ci;
         int *pcol = color.as<int>(), *pin = job.indeg.as<int>(), *pa = job.la.as<int>(), *pb = job.lb.as<int>(),
             *pc = job.counts.as<int>(), *pr = job.counts.as<int>() + kMaxRounds;
-        void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr};
+        const int *gate = nullptr;
+        void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr, &gate};
         if (n <= kSmallColourN && avg >= kSmallColourMinDeg) {
             static DeviceCache attr{};
             std::atomic<int> &attr_slot = attr[current_device()];
@@ -2413,6 +2574,15 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             FDL_CK(cudaLaunchKernelEx(&cfg, k_color_cluster, n, rp, ci, salt, pcol, pr));
         } else {
             RoundTrace tr(st, "colour");
+            if (avg <= 8.5 && kByteColour) {
+                // byte state (the int-state kernel below runs only if a degree is too big)
+                job.st8.alloc(padded((size_t)n), st);
+                unsigned char *p8 = job.st8.as<unsigned char>();
+                int *flag = pc + kMaxRounds + 2;
+                void *bargs[] = {&n, &rp, &ci, &salt, &pcol, &p8, &pa, &pb, &pc, &pr, &flag};
+                coop_launch(k_color_byte, bargs, st, kColourGridFrac, (int64_t)n);
+                gate = flag;
+            }
             // a third of the co-resident grid, the matching (main stream) half:
             // both cooperative kernels fit side by side with room for the rest
             // of the coarsening chain (a full-grid cooperative launch would wait
@@ -2426,6 +2596,7 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
     job.la.release();
     job.lb.release();
     job.indeg.release();
+    job.st8.release();
 }
 
 // the colour counts of all levels in one round trip: ncol[l], rounds[l]

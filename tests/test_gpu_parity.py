@@ -63,6 +63,9 @@ SMALL = {
     "rand300": lambda: gg.random_connected(300, 1500, 12),
     "path100": lambda: gg.path(100),
     "star40": lambda: gg.star(40),
+    # the byte colouring state holds degrees <= 126: the boundary and the int fallback
+    "star127_deg126": lambda: gg.star(127),
+    "star128_deg127": lambda: gg.star(128),
     "complete30": lambda: gg.complete(30),
     # dense small levels (average degree >= 64): the single-CTA colouring
     "complete100": lambda: gg.complete(100),
