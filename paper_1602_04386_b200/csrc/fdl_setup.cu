@@ -958,17 +958,44 @@ template <int W>
 __global__ void k_gal_write(int c, const int *rowoff, const int *crp, const int *outB,
                             const double *outW, int *cci, double *cw) {
     if (W == 1) {
-        for (int A = blockIdx.x * blockDim.x + threadIdx.x; A < c; A += gridDim.x * blockDim.x) {
-            const int sb = rowoff[A], o = crp[A], d = crp[A + 1] - o;
-            for (int i = 0; i < d; i += 8) {   // 8 entries in flight per step
-                int b8[8];
-                double w8[8];
+        // a warp per 32 consecutive rows: their output is one contiguous range,
+        // which the lanes write at consecutive positions (entry t of the range
+        // comes from the row whose prefix start is the last one <= t)
+        const int lane = lane_id();
+        const int nwarps = gridDim.x * (blockDim.x >> 5);
+        for (int A0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; A0 < c; A0 += nwarps * 32) {
+            const int A = A0 + lane;
+            const int o = A < c ? crp[A] : 0;
+            const int sb = A < c ? rowoff[A] : 0;
+            const int last = min(A0 + 32, c);
+            const int o0 = __shfl_sync(0xffffffffu, o, 0);
+            const int T = crp[last] - o0;
+            const int rel = A < c ? o - o0 : 0x7fffffff;   // prefix start of lane's row
+            for (int t0 = 0; t0 < T; t0 += 4 * 32) {
+                int b4[4];
+                double w4[4];
+                int src[4];
 #pragma unroll
-                for (int k = 0; k < 8; k++)
-                    if (i + k < d) { b8[k] = outB[sb + i + k]; w8[k] = outW[sb + i + k]; }
+                for (int u = 0; u < 4; u++) {
+                    const int t = t0 + u * 32 + lane;
+                    // row of entry t: the number of lanes with rel <= t, minus one
+                    // (rel ascends with the lane; a binary search over the shuffles)
+                    int r = 0;
 #pragma unroll
-                for (int k = 0; k < 8; k++)
-                    if (i + k < d) { cci[o + i + k] = b8[k]; cw[o + i + k] = w8[k]; }
+                    for (int step = 16; step; step >>= 1) {
+                        const int rr = __shfl_sync(0xffffffffu, rel, r + step);
+                        if (rr <= t) r += step;
+                    }
+                    const int rs = __shfl_sync(0xffffffffu, rel, r);
+                    const int sr = __shfl_sync(0xffffffffu, sb, r);
+                    src[u] = t < T ? sr + (t - rs) : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (src[u] >= 0) { b4[u] = outB[src[u]]; w4[u] = outW[src[u]]; }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (src[u] >= 0) { cci[o0 + t0 + u * 32 + lane] = b4[u]; cw[o0 + t0 + u * 32 + lane] = w4[u]; }
             }
         }
         return;
@@ -1611,7 +1638,7 @@ static NatGraph galerkin(const NatGraph &g, const int *q, int c, cudaStream_t st
     out.own_ci.alloc(padded((size_t)std::max(out.nnz, 1) * 4), st);
     out.own_w.alloc(padded((size_t)std::max(out.nnz, 1) * 8), st);
     const double cavg = c ? (double)out.nnz / c : 0.0;
-    DISPATCH_WC(cavg, (k_gal_write<W><<<sub_grid(c, W), 256, 0, st>>>(
+    DISPATCH_WC(cavg, (k_gal_write<W><<<W == 1 ? grid_for((int64_t)div_up(c, 32) * 32, 256, kNumSMs * 16) : sub_grid(c, W), 256, 0, st>>>(
                           c, rowoff.as<int>(), out.own_rp.as<int>(), outB.as<int>(),
                           outW.as<double>(), out.own_ci.as<int>(), out.own_w.as<double>())));
     FDL_LAUNCH_CK();

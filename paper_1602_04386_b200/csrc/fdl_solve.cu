@@ -922,7 +922,7 @@ static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0
 #define FDL_DENSE_ROW_DEG 7.0
 #endif
 constexpr double kDenseRowDeg = FDL_DENSE_ROW_DEG;   // rows per tile few enough for sub-warp rows
-static DeviceCache g_pass_grid[4] = {};   // per OP (3: the 4-lane dense variant), per device
+static DeviceCache g_pass_grid[4] = {};   // per OP (3: the GS chunk-4 variant), per device
 static int pass_grid(int op) { return g_pass_grid[op][current_device()].load(); }
 
 // A tile pass as a programmatic dependent launch (FDL_PDL): its CTAs may start
