@@ -1137,17 +1137,23 @@ __global__ void __launch_bounds__(256) k_gal_direct_sw(int c, const int *list, c
         const unsigned Bm = (unsigned)(key >> 32);
         const unsigned Bprev = __shfl_up_sync(0xffffffffu, Bm, 1, W);
         const bool head = key != ~0ull && (lane == 0 || Bprev != Bm);
-        // left fold of the run starting at a head, in order
-        double acc = v;
-        bool run = head;
-#pragma unroll
-        for (int u = 1; u < W; u++) {
-            const double x = __shfl_down_sync(0xffffffffu, v, u, W);
-            const unsigned bx = __shfl_down_sync(0xffffffffu, Bm, u, W);
-            run = run && lane + u < W && bx == Bm;
-            if (run) acc += x;
-        }
+        // left fold of the run starting at a head, in order; the loop runs to
+        // the longest run of the warp (runs end at the next head or the first
+        // empty slot -- the empty slots sort last)
         const unsigned hm = __ballot_sync(0xffffffffu, head) & sub;
+        const unsigned fm = __ballot_sync(0xffffffffu, key != ~0ull) & sub;
+        int runlen = 0;
+        if (head) {
+            const unsigned after = (hm | ~fm) & sub & ~((2u << wl) - 1u);   // later heads / empty slots
+            const int nxt = after ? __ffs(after) - 1 : (wl | (W - 1)) + 1;
+            runlen = nxt - wl;
+        }
+        const int maxrun = __reduce_max_sync(0xffffffffu, (unsigned)runlen);
+        double acc = v;
+        for (int u = 1; u < maxrun; u++) {
+            const double x = __shfl_down_sync(0xffffffffu, v, u, W);
+            if (u < runlen) acc += x;
+        }
         if (head) {
             const int r = __popc(hm & ((1u << wl) - 1u));
             outB[tb + r] = (int)Bm;
