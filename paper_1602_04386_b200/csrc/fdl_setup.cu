@@ -20,7 +20,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
 #include <queue>
+#include <thread>
 
 #include <cooperative_groups.h>
 
@@ -2632,28 +2636,6 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
     job.st8.release();
 }
 
-// the colour counts of all levels in one round trip: ncol[l], rounds[l]
-static void color_finish_all(std::vector<std::unique_ptr<ColourJob>> &jobs, std::vector<int> &ncol,
-                             std::vector<int> &rounds, cudaStream_t st) {
-    const size_t L = jobs.size();
-    std::vector<int> h(3 * L);
-    std::vector<ReadPiece> pieces;
-    for (size_t l = 0; l < L; l++) {
-        pieces.push_back({&h[3 * l], jobs[l]->counts.as<int>() + kMaxRounds, 8});
-        pieces.push_back({&h[3 * l + 2], jobs[l]->mx.p, 4});
-    }
-    readback(st, pieces);
-    ncol.resize(L);
-    rounds.resize(L);
-    for (size_t l = 0; l < L; l++) {
-        rounds[l] = h[3 * l];
-        FDL_REQUIRE(rounds[l] >= 0 && h[3 * l + 1] == 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
-        ncol[l] = h[3 * l + 2] + 1;
-        jobs[l]->counts.release();
-        jobs[l]->mx.release();
-    }
-}
-
 // ================================================================= solve layout
 __global__ void k_color_keys(int n, const int *color, unsigned *keys, int *vals) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
@@ -2844,8 +2826,7 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
                          n, L.inv.as<int>(), g.rp, g.ci, g.w, L.rp.as<int>(),
                          L.ci.as<int>(), L.w.as<double>(), dmax.as<unsigned long long>())));
     FDL_LAUNCH_CK();
-    // ---- PI/RQ layout: the natural CSR (taken over from the setup graph when it
-    // owns padded storage, copied otherwise) -- see take_natural() below
+    // ---- PI/RQ layout: the natural CSR, take_natural() once the setup is complete
 
     // colour segment boundaries and their nonzero offsets -> host
     // (empty colours take the next colour's start; one round trip for all)
@@ -2861,22 +2842,6 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     // R8: c = 2 max_i d_i (Gershgorin); on a 2-vertex level 2 max d = lambda_max
     // exactly and c I - L would annihilate the only non-constant direction
     L.shift = (n == 2 ? 3.0 : 2.0) * dm;
-
-    // natural CSR for the PI / RQ passes
-    auto take = [&](DBuf &own, const void *ptr, size_t bytes, DBuf &dst) {
-        if (own.p && own.p == ptr && own.bytes >= padded(bytes)) {
-            dst = std::move(own);
-        } else {
-            dst.alloc(padded(bytes), st);
-            if (bytes) FDL_CK(cudaMemcpyAsync(dst.p, ptr, bytes, cudaMemcpyDeviceToDevice, st));
-        }
-    };
-    take(g.own_rp, g.rp, (size_t)(n + 1) * 4, L.rpN);
-    take(g.own_ci, g.ci, (size_t)g.nnz * 4, L.ciN);
-    take(g.own_w, g.w, (size_t)g.nnz * 8, L.wN);
-    g.rp = L.rpN.as<int>();
-    g.ci = L.ciN.as<int>();
-    g.w = L.wN.as<double>();
 
     // tiles: GS colours, then the natural-order pass
     L.seg = seg;
@@ -2935,9 +2900,28 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
             L.rp.as<int>(), L.seg_d.as<int>(), L.ctile_d.as<int>(), ncolors, L.tiles.as<Tile>());
         FDL_LAUNCH_CK();
     }
-    k_make_tiles<<<grid_for(cnt[ncolors]), 256, 0, st>>>(L.rpN.as<int>(), 0, n, cnt[ncolors],
+    k_make_tiles<<<grid_for(cnt[ncolors]), 256, 0, st>>>(g.rp, 0, n, cnt[ncolors],
                                                          L.tiles.as<Tile>() + L.ctile[ncolors]);
     FDL_LAUNCH_CK();
+}
+
+// the natural CSR of a level for the PI / RQ passes: taken over from the setup
+// graph when it owns padded storage, copied otherwise (the caller's level 0)
+static void take_natural(NatGraph &g, Level &L, cudaStream_t st) {
+    auto take = [&](DBuf &own, const void *ptr, size_t bytes, DBuf &dst) {
+        if (own.p && own.p == ptr && own.bytes >= padded(bytes)) {
+            dst = std::move(own);
+        } else {
+            dst.alloc(padded(bytes), st);
+            if (bytes) FDL_CK(cudaMemcpyAsync(dst.p, ptr, bytes, cudaMemcpyDeviceToDevice, st));
+        }
+    };
+    take(g.own_rp, g.rp, (size_t)(g.n + 1) * 4, L.rpN);
+    take(g.own_ci, g.ci, (size_t)g.nnz * 4, L.ciN);
+    take(g.own_w, g.w, (size_t)g.nnz * 8, L.wN);
+    g.rp = L.rpN.as<int>();
+    g.ci = L.ciN.as<int>();
+    g.w = L.wN.as<double>();
 }
 
 // ================================================================= connectivity (coarsest level)
@@ -2977,9 +2961,10 @@ __global__ void k_compose_qg(int n, const int *perm, const int *q_nat, int *qg) 
 struct PhaseTimes {
     bool on = false;
     std::vector<cudaEvent_t> ev;   // per level and phase: begin, end
-    PhaseTimes() {
+    explicit PhaseTimes(int max_levels) {
         const char *e = std::getenv("FIEDLER_PHASE_TIMES");
         on = e && e[0] == '1';
+        ev.assign((size_t)(max_levels + 1) * 8, nullptr);   // sized once: two threads mark
     }
     ~PhaseTimes() {
         for (cudaEvent_t x : ev)
@@ -3010,36 +2995,99 @@ struct PhaseTimes {
     }
 };
 
+// Two host threads: this one drives the coarsening chain (matching, Galerkin)
+// on the main stream; a helper drives, on the second stream, the colouring and
+// the GS layout of every level as soon as the level exists.  Each blocks only
+// on its own stream's readbacks, so the layouts overlap the coarsening of the
+// coarser levels instead of following it.  Levels and graphs live in vectors
+// reserved up front (no reallocation while the helper holds references); the
+// helper touches only the colouring / layout members of a Level.
+struct LevelFeed {
+    std::mutex mu;
+    std::condition_variable cv;
+    int ready = 0;      // levels whose graph is enqueued (event recorded)
+    bool done = false;  // no more levels
+    void publish(int r) {
+        { std::lock_guard<std::mutex> lk(mu); ready = r; }
+        cv.notify_all();
+    }
+    void finish() {
+        { std::lock_guard<std::mutex> lk(mu); done = true; }
+        cv.notify_all();
+    }
+    bool wait_for(int ell) {   // true: level ell exists; false: no such level
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return ready > ell || done; });
+        return ready > ell;
+    }
+};
+
+static void colour_and_layout(Handle &h, std::vector<NatGraph> &graphs, std::vector<cudaEvent_t> &lev_ev,
+                              LevelFeed &feed, PhaseTimes &pt, cudaStream_t sb) {
+    for (int ell = 0; feed.wait_for(ell); ell++) {
+        Level &L = h.levels[ell];
+        NatGraph &g = graphs[ell];
+        // the colouring needs the pattern (level 0 from host input: its event,
+        // the weights may still be copying), the layout the whole level
+        FDL_CK(cudaStreamWaitEvent(sb, ell == 0 && h.ev_pattern ? h.ev_pattern : lev_ev[ell], 0));
+        ColourJob job;
+        pt.mark(ell, 2, 0, sb);
+        color_launch(g, salt_color(h.opts.seed, ell), L.color_nat, job, sb);
+        pt.mark(ell, 2, 1, sb);
+        int cr[3];
+        readback(sb, {{cr, job.counts.as<int>() + kMaxRounds, 8}, {cr + 2, job.mx.p, 4}});
+        FDL_REQUIRE(cr[0] >= 0 && cr[1] == 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
+        L.color_rounds = cr[0];
+        if (ell == 0 && h.ev_pattern) FDL_CK(cudaStreamWaitEvent(sb, lev_ev[0], 0));
+        pt.mark(ell, 3, 0, sb);
+        build_layout(g, L.color_nat.as<int>(), cr[2] + 1, L, sb);
+        pt.mark(ell, 3, 1, sb);
+        trace_mark(sb, ell == 0 ? "L0 colour+layout (second stream)" : "Lk colour+layout (second stream)");
+    }
+}
+
 void build_hierarchy(Handle &h, NatGraph &&g0) {
     cudaStream_t st = h.stream, sb = h.stream2;
-    PhaseTimes pt;
-    {   // FIEDLER_SERIAL_COLOUR=1 (diagnostics): colourings on the main stream
-        const char *e = std::getenv("FIEDLER_SERIAL_COLOUR");
-        if (e && e[0] == '1') sb = st;
-    }
     const fiedler_opts &o = h.opts;
-    NatGraph cur = std::move(g0);
+    const int maxl = std::max(1, o.max_levels);
+    PhaseTimes pt(maxl);
+    bool serial = false;
+    {   // FIEDLER_SERIAL_COLOUR=1 (diagnostics): colourings and layouts on the
+        // main stream, after the coarsening chain, one host thread
+        const char *e = std::getenv("FIEDLER_SERIAL_COLOUR");
+        serial = e && e[0] == '1';
+    }
+    if (serial) sb = st;
     h.levels.clear();
+    h.levels.reserve((size_t)maxl + 1);
     std::vector<NatGraph> graphs;
-    std::vector<std::unique_ptr<ColourJob>> jobs;
-    cudaEvent_t ev = h.set.ev[2];
+    graphs.reserve((size_t)maxl + 1);
+    std::vector<cudaEvent_t> lev_ev((size_t)maxl + 1, nullptr);
+    LevelFeed feed;
+    std::exception_ptr side_err;
+    long long side_launches = 0;
+    std::thread side;
+    auto run_side = [&] {
+        const long long l0 = g_launch_count;
+        try {
+            FDL_CK(cudaSetDevice(h.device));
+            colour_and_layout(h, graphs, lev_ev, feed, pt, sb);
+        } catch (...) {
+            side_err = std::current_exception();
+        }
+        side_launches = g_launch_count - l0;
+    };
+    if (!serial) side = std::thread(run_side);
     try {
+        graphs.emplace_back(std::move(g0));
         for (int ell = 0;; ell++) {
-            Level L;
-            // colouring of level ell on the second stream, once the level exists
-            // (level 0 from host input: once its pattern is, weights may still be copying)
-            if (ell == 0 && h.ev_pattern) {
-                FDL_CK(cudaStreamWaitEvent(sb, h.ev_pattern, 0));
-            } else {
-                FDL_CK(cudaEventRecord(ev, st));
-                FDL_CK(cudaStreamWaitEvent(sb, ev, 0));
-            }
-            jobs.emplace_back(new ColourJob());
-            pt.mark(ell, 2, 0, sb);
-            color_launch(cur, salt_color(o.seed, ell), L.color_nat, *jobs.back(), sb);
-            pt.mark(ell, 2, 1, sb);
-            bool coarsen = cur.n > o.coarsest_size && ell + 1 < o.max_levels;
-            NatGraph next;
+            h.levels.emplace_back();
+            Level &L = h.levels.back();
+            NatGraph &cur = graphs.back();
+            FDL_CK(cudaEventCreateWithFlags(&lev_ev[ell], cudaEventDisableTiming));
+            FDL_CK(cudaEventRecord(lev_ev[ell], st));
+            feed.publish(ell + 1);
+            bool coarsen = cur.n > o.coarsest_size && ell + 1 < maxl;
             if (coarsen) {
                 pt.mark(ell, 0, 0, st);
                 int c = hec_parallel(cur, salt_match(o.seed, ell), L.q_nat, L.mate_nat, L.match_rounds, st);
@@ -3052,36 +3100,39 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
                     L.mate_nat.release();
                 } else {
                     pt.mark(ell, 1, 0, st);
-                    next = galerkin(cur, L.q_nat.as<int>(), c, st);
+                    NatGraph next = galerkin(cur, L.q_nat.as<int>(), c, st);
                     pt.mark(ell, 1, 1, st);
                     trace_mark(st, ell == 0 ? "L0 galerkin" : "Lk galerkin");
+                    graphs.emplace_back(std::move(next));
                 }
             }
-            h.levels.push_back(std::move(L));
-            graphs.push_back(std::move(cur));
             if (!coarsen) break;
-            cur = std::move(next);
         }
-        // layouts: the colourings must be complete (main stream waits for the second)
-        FDL_CK(cudaEventRecord(ev, sb));
-        FDL_CK(cudaStreamWaitEvent(st, ev, 0));
-        trace_mark(sb, "colourings (second stream)");
-        std::vector<int> ncols, crounds;
-        color_finish_all(jobs, ncols, crounds, sb);
-        for (size_t ell = 0; ell < h.levels.size(); ell++) {
-            Level &L = h.levels[ell];
-            L.color_rounds = crounds[ell];
-            const int ncol = ncols[ell];
-            pt.mark((int)ell, 3, 0, st);
-            build_layout(graphs[ell], L.color_nat.as<int>(), ncol, L, st);
-            pt.mark((int)ell, 3, 1, st);
-        }
-        trace_mark(st, "layouts");
     } catch (...) {
+        feed.finish();
+        if (side.joinable()) side.join();
         cudaStreamSynchronize(sb);
+        for (cudaEvent_t e : lev_ev)
+            if (e) cudaEventDestroy(e);
         throw;
     }
+    feed.finish();
+    if (serial) run_side();
+    else side.join();
+    g_launch_count += serial ? 0 : side_launches;
+    for (cudaEvent_t e : lev_ev)
+        if (e) cudaEventDestroy(e);
+    if (side_err) {
+        cudaStreamSynchronize(sb);
+        std::rethrow_exception(side_err);
+    }
+    // the main stream continues after the colourings and layouts
+    cudaEvent_t ev = h.set.ev[2];
+    FDL_CK(cudaEventRecord(ev, sb));
+    FDL_CK(cudaStreamWaitEvent(st, ev, 0));
+    trace_mark(st, "colourings and layouts joined");
     const int J = (int)h.levels.size() - 1;
+    for (int ell = 0; ell <= J; ell++) take_natural(graphs[ell], h.levels[ell], st);
     for (int ell = 0; ell < J; ell++) {
         Level &L = h.levels[ell];
         L.qg.alloc((size_t)L.n * 4, st);
