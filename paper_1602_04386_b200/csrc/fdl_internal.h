@@ -85,7 +85,9 @@ struct Level {
     int gs_tail_c0 = 0;      // colours [gs_tail_c0, ncolors) run in one single-CTA launch
     std::vector<int> gs_runs;  // GS schedule of one sweep: (c_begin, c_end, kind) triplets,
                                // kind 0 = grid tile pass of one colour, 1 = cluster run,
-                               // 2 = single-CTA tail
+                               // 2 = single-CTA run (k_gs_pieces; FDL_GS_PIECES=0: k_gs_multi)
+    DBuf gd_pieces;          // int4 pieces of the GS rows (build_gs_pieces), when a run uses them
+    DBuf gd_parts;           // [ncolors][kGdParts + 1] piece index bounds
     DistPlan dist;
     int ncolors = 0;
     int ntiles = 0;
@@ -148,6 +150,19 @@ void build_hierarchy(Handle &h, NatGraph &&g0);
 inline size_t padded(size_t bytes) { return bytes + kPadBytes; }
 
 // fdl_solve.cu
+// piece lists of the small-colour GS kernel (fdl_solve.cu k_gs_pieces)
+#ifndef FDL_GS_PIECES
+#define FDL_GS_PIECES 1
+#endif
+constexpr int kGdPiece = 256;    // entries of one warp-strided piece (8 per lane)
+constexpr int kGdGroup = 32;     // consecutive rows of one colour packed lane per row ...
+constexpr int kGdShort = 32;     // ... when none has more entries than this
+constexpr int kGdParts = 16;     // parts per colour (CTA shares of a 16-CTA cluster)
+constexpr int kGdSlotCapHost = 2048;
+constexpr int kGdMaxRunColours = 1024;   // colours of one k_gs_pieces launch
+// pieces and parts of the colours with use[c] != 0 (the others get empty part ranges)
+void build_gs_pieces(Level &L, const std::vector<int> &seg, const std::vector<int> &segnnz,
+                     const std::vector<char> &use, cudaStream_t st);
 struct SolveCfg {
     int gs, pi, piJ;
     uint64_t seed;

@@ -2866,6 +2866,58 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
 #endif
         constexpr int kClusterColourRows = FDL_CLUSTER_COLOUR_ROWS;
         L.gs_runs.clear();
+#if FDL_GS_PIECES
+        // k_gs_pieces runs (fdl_solve.cu): colours of <= kClusterColourRows rows,
+        // or dense colours (>= kGdDenseDeg entries per row) of <= kGdMaxEntries
+        // entries; the trailing colours of a run with <= kGdSingleEntries entries
+        // each go to one CTA (no cluster barrier)
+#ifndef FDL_GD_MAX_ENTRIES
+#define FDL_GD_MAX_ENTRIES 262144
+#endif
+#ifndef FDL_GD_SINGLE_ENTRIES
+#define FDL_GD_SINGLE_ENTRIES 8192
+#endif
+        constexpr long long kGdMaxEntries = FDL_GD_MAX_ENTRIES, kGdSingleEntries = FDL_GD_SINGLE_ENTRIES;
+        constexpr long long kGdDenseDeg = 16;
+        constexpr int kGdSinglePieces = 16;   // k_gs_pieces warps per CTA
+        (void)c0;
+        // eligibility and the one-CTA choice from bounds on the piece counts
+        // (no readback): pieces(c) <= rows + entries / kGdPiece + 1, and a part
+        // pair (two parts per CTA of an 8-CTA cluster) holds at most an eighth
+        // of them plus the pieces of the row its cut extends over
+        auto rows_of = [&](int c) { return (long long)seg[c + 1] - seg[c]; };
+        auto ent_of = [&](int c) { return (long long)segnnz[c + 1] - segnnz[c]; };
+        auto pbound = [&](int c) { return rows_of(c) + ent_of(c) / kGdPiece + 1; };
+        auto elig = [&](int c) {
+            const long long rows = rows_of(c), ent = ent_of(c);
+            if (rows == 0) return true;
+            if (!(rows <= kClusterColourRows || (ent <= kGdMaxEntries && ent >= kGdDenseDeg * rows)))
+                return false;
+            return pbound(c) / 8 + ent / kGdPiece + 2 <= kGdSlotCapHost;
+        };
+        auto single = [&](int c) { return ent_of(c) <= kGdSingleEntries && pbound(c) <= kGdSinglePieces; };
+        std::vector<char> use(ncolors, 0);
+        bool any = false;
+        for (int c = 0; c < ncolors; c++) {
+            use[c] = rows_of(c) > 0 && elig(c);
+            any |= use[c] != 0;
+        }
+        if (any) build_gs_pieces(L, seg, segnnz, use, st);
+        for (int c = 0; c < ncolors;) {
+            if (!any || !elig(c)) {
+                L.gs_runs.insert(L.gs_runs.end(), {c, c + 1, 0});
+                c++;
+                continue;
+            }
+            int e = c;
+            while (e < ncolors && elig(e) && e - c < kGdMaxRunColours) e++;
+            int t = e;
+            while (t > c && single(t - 1)) t--;
+            if (t > c) L.gs_runs.insert(L.gs_runs.end(), {c, t, 1});
+            if (e > t) L.gs_runs.insert(L.gs_runs.end(), {t, e, 2});
+            c = e;
+        }
+#else
         for (int c = 0; c < c0;) {
             int e = c;
             while (e < c0 && seg[e + 1] - seg[e] <= kClusterColourRows) e++;
@@ -2878,6 +2930,7 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
             }
         }
         if (c0 < ncolors) L.gs_runs.insert(L.gs_runs.end(), {c0, ncolors, 2});
+#endif
     }
     L.ctile.assign(ncolors + 1, 0);
     int nt = 0;

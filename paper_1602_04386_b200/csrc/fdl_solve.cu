@@ -698,6 +698,381 @@ __global__ void __launch_bounds__(kGcThreads) k_gs_multi(CsrView L, const int *_
     }
 }
 
+// ----------------------------------------------------------------- piece-list GS (small colours)
+// Runs of colours too small for a grid-wide tile pass each (the coarse levels
+// of every graph; all the dense coarse levels of a power-law graph, 150-500
+// colours per level) are latency-bound: one colour is one dependent step.
+// This kernel keeps each step to one barrier and one round trip of gathers:
+//  * the colour's rows are cut at setup into PIECES of <= kGdPiece entries
+//    (int4 {row, kind, kb, ke}: 32 consecutive short rows, lane per row; one
+//    whole row, warp-strided; or one piece of a longer row, warp-strided,
+//    combined in the CTA in piece order), and the pieces of every colour into
+//    kGdParts parts cut at row boundaries (build_gs_pieces);
+//  * a CTA of the cluster owns parts cr * 16/ncl ...; warp w takes pieces
+//    P0 + w, P0 + w + 16, ...;
+//  * the column / weight streams of a warp's first piece of the NEXT colour
+//    are loaded (and, for lane-per-row pieces, the row offsets before them)
+//    between the barrier's arrive and its wait: they never depend on x, so
+//    after the barrier only the x gathers remain (one round trip);
+//  * levels of <= kGdXsmemN vertices keep x in shared memory, replicated in
+//    every CTA of the cluster: a new value is stored to every replica through
+//    distributed shared memory (and to global memory for the result), so the
+//    gathers after the barrier are shared-memory loads.
+// The barrier between colours is barrier.cluster.arrive.release /
+// wait.acquire (split) for a cluster, __syncthreads for a single CTA.
+// Piece kinds (int4.y): >= 0: rows [x, y) one per lane; -1: row x whole;
+// -2: continuation piece of row x; <= -3: first of -(y) - 1 pieces of row x.
+constexpr int kGdThreads = 512;
+constexpr int kGdWarps = kGdThreads / 32;
+constexpr int kGdSlotCap = kGdSlotCapHost;   // pieces of one CTA's share of a colour (partial-sum slots)
+constexpr int kGdXsmemN = 20480;     // x replicated in shared memory up to this level size
+constexpr size_t kGdSmemBase = (size_t)kGdSlotCap * 16;   // then kGdMaxRunColours ranges, then x
+
+
+struct GdArgs {
+    CsrView L;                  // GS layout
+    const int4 *pieces;
+    const int *parts;           // [ncolors][kGdParts + 1] piece indices
+    const int *seg;             // [ncolors + 1] GS row range of every colour
+    int c0, c1, sweeps;
+    double *x;                  // GS numbering, in place
+    double *slot;
+    int stat_mode, n;
+};
+
+struct GdPiece {
+    int4 d;
+    int kb, ke;
+    int c[8];
+    double w[8];
+};
+
+// the three dependent steps of a piece's loads, software-pipelined over the
+// items (k_gs_pieces): descriptor; row offsets (lane-per-row pieces);
+// column / weight streams
+__device__ __forceinline__ int4 gd_desc(const int4 *__restrict__ pieces, int pi, int P1) {
+    return pi < P1 ? __ldg(pieces + pi) : make_int4(0, 0, 0, 0);   // {0,0,..}: no rows
+}
+__device__ __forceinline__ int2 gd_offs(const int4 d, const CsrView &L, int lane) {
+    if (d.y < 0) return make_int2(d.z + lane, d.w);
+    const int r = d.x + lane;
+    return r < d.y ? make_int2(__ldg(L.rp + r), __ldg(L.rp + r + 1)) : make_int2(0, 0);
+}
+__device__ __forceinline__ void gd_data(GdPiece &p, const int4 d, const int2 o, const CsrView &L) {
+    p.d = d;
+    p.kb = o.x;
+    p.ke = o.y;
+    const int step = d.y >= 0 ? 1 : 32;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const int k = p.kb + i * step;
+        p.c[i] = k < p.ke ? __ldg(L.ci + k) : -1;
+        p.w[i] = k < p.ke ? __ldg(L.w + k) : 0.0;
+    }
+}
+__device__ __forceinline__ void gd_load(GdPiece &p, const int4 *__restrict__ pieces, int pi, int P1,
+                                        const CsrView &L, int lane) {
+    const int4 d = gd_desc(pieces, pi, P1);
+    gd_data(p, d, gd_offs(d, L, lane), L);
+}
+
+template <bool XS>
+__device__ __forceinline__ double gd_xv(const double *xg, const double *xs, int j) {
+    return XS ? xs[j] : __ldcg(xg + j);
+}
+
+// new value v of row r: global x, and every replica of the cluster (XS)
+template <bool CLUSTER, bool XS>
+__device__ __forceinline__ void gd_store_lane(double *xg, double *xs, int r, double v, int ncl) {
+    xg[r] = v;
+    if (XS) {
+        if (CLUSTER) {
+            for (int j = 0; j < ncl; j++) cg::this_cluster().map_shared_rank(xs, j)[r] = v;
+        } else {
+            xs[r] = v;
+        }
+    }
+}
+// the same by a warp whose lanes all hold v: lane j stores replica j
+template <bool CLUSTER, bool XS>
+__device__ __forceinline__ void gd_store_warp(double *xg, double *xs, int r, double v, int ncl, int lane) {
+    if (lane == 0) xg[r] = v;
+    if (XS) {
+        if (CLUSTER) {
+            if (lane < ncl) cg::this_cluster().map_shared_rank(xs, lane)[r] = v;
+        } else if (lane == 0) {
+            xs[r] = v;
+        }
+    }
+}
+
+// one piece: gathers of the staged entries, then the row epilogue; returns
+// 1 if the piece is the first of a split row (combined after the CTA barrier)
+template <bool CLUSTER, bool XS>
+__device__ __forceinline__ int gd_piece(GdPiece &p, int slot_idx, double2 *slots, const CsrView &L,
+                                        double *xg, double *xs, int ncl, int lane) {
+    double xv[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) xv[i] = p.c[i] >= 0 ? gd_xv<XS>(xg, xs, p.c[i]) : 0.0;
+    double num = 0.0, den = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+        if (p.c[i] >= 0) { num = fma(p.w[i], xv[i], num); den += p.w[i]; }
+    if (p.d.y >= 0) {
+        // lane per row: entries past the first 8 (rows of 9..32 entries)
+        for (int k0 = p.kb + 8; k0 < p.ke; k0 += 8) {
+            int c[8];
+            double w[8], v[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                c[i] = k0 + i < p.ke ? __ldg(L.ci + k0 + i) : -1;
+                w[i] = k0 + i < p.ke ? __ldg(L.w + k0 + i) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; i++) v[i] = c[i] >= 0 ? gd_xv<XS>(xg, xs, c[i]) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+                if (c[i] >= 0) { num = fma(w[i], v[i], num); den += w[i]; }
+        }
+        const int r = p.d.x + lane;
+        if (r < p.d.y) gd_store_lane<CLUSTER, XS>(xg, xs, r, num / den, ncl);
+        return 0;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    if (p.d.y == -1) {
+        gd_store_warp<CLUSTER, XS>(xg, xs, p.d.x, num / den, ncl, lane);
+        return 0;
+    }
+    if (lane == 0) slots[slot_idx] = make_double2(num, den);
+    return p.d.y <= -3 ? 1 : 0;
+}
+
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <bool CLUSTER, bool XS>
+__global__ void __launch_bounds__(kGdThreads, 1) k_gs_pieces(GdArgs a) {
+    extern __shared__ __align__(16) unsigned char gd_smem[];
+    double2 *slots = reinterpret_cast<double2 *>(gd_smem);
+    double *xs = reinterpret_cast<double *>(gd_smem + kGdSmemBase + (size_t)kGdMaxRunColours * 8);
+    __shared__ double sm[kGdWarps][2];
+    __shared__ double s_part[kGcMaxCluster][2];
+    const int cr = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
+    const int ncl = CLUSTER ? (int)cg::this_cluster().num_blocks() : 1;
+    const int per = kGdParts / ncl;
+    const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    const CsrView L = a.L;
+    double *xg = a.x;
+    // this CTA's piece range of every colour of the run, in shared memory
+    int2 *rng = reinterpret_cast<int2 *>(gd_smem + kGdSmemBase);
+    const int ncol = a.c1 - a.c0;
+    for (int c = tid; c < ncol; c += kGdThreads)
+        rng[c] = make_int2(__ldg(a.parts + (a.c0 + c) * (kGdParts + 1) + cr * per),
+                           __ldg(a.parts + (a.c0 + c) * (kGdParts + 1) + (cr + 1) * per));
+    __syncthreads();
+    const int items = a.sweeps * ncol;
+    auto item_rng = [&](int it) {   // colour of item it (it / ncol <= sweeps: a few subtractions)
+        int c = it;
+        while (c >= ncol) c -= ncol;
+        return it < items ? rng[c] : make_int2(0, 0);
+    };
+    // pipeline of this warp's first piece (the matrix is never written by the
+    // solve): item it+1 fully loaded, it+2 up to its row offsets, it+3 its descriptor
+    GdPiece cur;
+    int4 d2, d3;
+    int2 o2;
+    {
+        const int2 r0 = item_rng(0), r1 = item_rng(1), r2 = item_rng(2);
+        const int4 d0 = gd_desc(a.pieces, r0.x + warp, r0.y);
+        d2 = gd_desc(a.pieces, r1.x + warp, r1.y);
+        d3 = gd_desc(a.pieces, r2.x + warp, r2.y);
+        const int2 o0 = gd_offs(d0, L, lane);
+        o2 = gd_offs(d2, L, lane);
+        gd_data(cur, d0, o0, L);
+    }
+    pdl_wait();
+    if (XS) {
+        for (int i = tid; i < a.n; i += kGdThreads) xs[i] = __ldcg(xg + i);
+        if (CLUSTER) cg::this_cluster().sync();   // no replica written before its owner filled it
+        else __syncthreads();
+    }
+    for (int it = 0; it < items; it++) {
+        if (it > 0) {
+            if (CLUSTER) cluster_wait();
+            else __syncthreads();
+        }
+        const int2 R = item_rng(it);
+        const int P0 = R.x, P1 = R.y;
+        int has_split = gd_piece<CLUSTER, XS>(cur, warp, slots, L, xg, xs, ncl, lane);
+        for (int pi = P0 + warp + kGdWarps; pi < P1; pi += kGdWarps) {
+            GdPiece q;
+            gd_load(q, a.pieces, pi, P1, L, lane);
+            has_split |= gd_piece<CLUSTER, XS>(q, pi - P0, slots, L, xg, xs, ncl, lane);
+        }
+        if (__syncthreads_or(has_split)) {
+            // rows split into pieces: the warp of the first piece folds the
+            // partial sums in piece order
+            for (int pi = P0 + warp; pi < P1; pi += kGdWarps) {
+                const int4 d = __ldg(a.pieces + pi);
+                if (d.y > -3) continue;
+                const int np = -d.y - 1;
+                double num = 0.0, den = 0.0;
+                for (int k = lane; k < np; k += 32) {
+                    const double2 sv = slots[pi - P0 + k];
+                    num += sv.x;
+                    den += sv.y;
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    num += __shfl_xor_sync(0xffffffffu, num, o);
+                    den += __shfl_xor_sync(0xffffffffu, den, o);
+                }
+                gd_store_warp<CLUSTER, XS>(xg, xs, d.x, num / den, ncl, lane);
+            }
+        }
+        if (it + 1 < items) {
+            if (CLUSTER) cluster_arrive();
+            gd_data(cur, d2, o2, L);
+            o2 = gd_offs(d3, L, lane);
+            d2 = d3;
+            const int2 r3 = item_rng(it + 3);
+            d3 = gd_desc(a.pieces, r3.x + warp, r3.y);
+        }
+    }
+    // every replica write done before any CTA reads the statistics or exits
+    if (CLUSTER) cg::this_cluster().sync();
+    else __syncthreads();
+    if (!(a.stat_mode & 4)) return;
+    // statistics of the rows of these colours in a fixed row -> thread map,
+    // shifted by K (finish_stats), reduced over the cluster in rank order
+    const double K = (a.stat_mode & 8) ? a.slot[2] : 0.0;
+    double S = 0.0, Q = 0.0;
+    const int rb = __ldg(a.seg + a.c0), re = __ldg(a.seg + a.c1);
+    for (int r = rb + cr * kGdThreads + tid; r < re; r += ncl * kGdThreads) {
+        const double xr = (XS ? xs[r] : __ldcg(xg + r)) - K;
+        S += xr;
+        Q = fma(xr, xr, Q);
+    }
+    cta_sum2(S, Q, sm);
+    if (CLUSTER) {
+        if (tid == 0) {
+            double *dst = cg::this_cluster().map_shared_rank(&s_part[0][0], 0);
+            dst[2 * cr] = S;
+            dst[2 * cr + 1] = Q;
+        }
+        cg::this_cluster().sync();
+    } else if (tid == 0) {
+        s_part[0][0] = S;
+        s_part[0][1] = Q;
+    }
+    if (cr == 0 && tid == 0) {
+        double tot[kNumStats] = {0.0, 0.0, 0.0};
+        for (int i = 0; i < ncl; i++) { tot[0] += s_part[i][0]; tot[1] += s_part[i][1]; }
+        finish_stats(tot, a.slot, a.stat_mode, a.n);
+    }
+}
+
+// ---- setup side: pieces and parts of a level (called by build_layout)
+// groups of 32 consecutive rows of one colour; gstart[c] = first group of colour c
+__device__ __forceinline__ int gd_group_colour(const int *gstart, int ncolors, int g) {
+    int lo = 0, hi = ncolors;   // largest c with gstart[c] <= g
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(gstart + mid) <= g) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+__global__ void k_gd_count(const int *rp, const int *seg, const int *gstart, int ncolors, int ngroups,
+                           int *gcnt) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+        const int c = gd_group_colour(gstart, ncolors, g);
+        const int r0 = seg[c] + (g - gstart[c]) * kGdGroup, r1 = min(r0 + kGdGroup, seg[c + 1]);
+        int cnt = 0, maxlen = 0;
+        for (int r = r0; r < r1; r++) {
+            const int len = rp[r + 1] - rp[r];
+            maxlen = max(maxlen, len);
+            cnt += len > kGdPiece ? (len + kGdPiece - 1) / kGdPiece : 1;
+        }
+        gcnt[g] = maxlen <= kGdShort ? 1 : cnt;
+    }
+}
+__global__ void k_gd_write(const int *rp, const int *seg, const int *gstart, int ncolors, int ngroups,
+                           const int *goff, int4 *pieces) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+        const int c = gd_group_colour(gstart, ncolors, g);
+        const int r0 = seg[c] + (g - gstart[c]) * kGdGroup, r1 = min(r0 + kGdGroup, seg[c + 1]);
+        int p = goff[g];
+        int maxlen = 0;
+        for (int r = r0; r < r1; r++) maxlen = max(maxlen, rp[r + 1] - rp[r]);
+        if (maxlen <= kGdShort) {
+            pieces[p] = make_int4(r0, r1, rp[r0], rp[r1]);
+            continue;
+        }
+        for (int r = r0; r < r1; r++) {
+            const int kb = rp[r], ke = rp[r + 1], len = ke - kb;
+            if (len <= kGdPiece) {
+                pieces[p++] = make_int4(r, -1, kb, ke);
+                continue;
+            }
+            const int np = (len + kGdPiece - 1) / kGdPiece;
+            for (int i = 0; i < np; i++)
+                pieces[p++] = make_int4(r, i == 0 ? -(np + 1) : -2, kb + i * kGdPiece, min(kb + (i + 1) * kGdPiece, ke));
+        }
+    }
+}
+// parts: kGdParts + 1 piece indices per colour, cut at the first piece of a row
+__global__ void k_gd_parts(const int *gstart, const int *goff, const int4 *pieces, int ncolors, int *parts) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncolors * (kGdParts + 1)) return;
+    const int c = t / (kGdParts + 1), k = t % (kGdParts + 1);
+    const int p0 = goff[gstart[c]], p1 = goff[gstart[c + 1]];
+    int p = p0 + (int)((long long)k * (p1 - p0) / kGdParts);
+    while (p < p1 && pieces[p].y == -2) p++;
+    parts[t] = p;
+}
+
+void build_gs_pieces(Level &L, const std::vector<int> &seg, const std::vector<int> &segnnz,
+                     const std::vector<char> &use, cudaStream_t st) {
+    const int ncolors = L.ncolors;
+    std::vector<int> gstart(ncolors + 1, 0);
+    long long bound = 1;
+    for (int c = 0; c < ncolors; c++) {
+        const int rows = seg[c + 1] - seg[c];
+        gstart[c + 1] = gstart[c] + (use[c] ? div_up(rows, kGdGroup) : 0);
+        if (use[c]) bound += rows + (segnnz[c + 1] - segnnz[c]) / kGdPiece + 1;   // >= pieces of colour c
+    }
+    const int ngroups = gstart[ncolors];
+    DBuf gs_d((size_t)(ncolors + 1) * 4, st);
+    FDL_CK(cudaMemcpyAsync(gs_d.p, gstart.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
+    DBuf gcnt((size_t)(ngroups + 1) * 4, st), goff((size_t)(ngroups + 1) * 4, st);
+    L.gd_pieces.alloc((size_t)bound * sizeof(int4), st);
+    if (ngroups > 0) {
+        k_gd_count<<<grid_for(ngroups), 256, 0, st>>>(L.rp.as<int>(), L.seg_d.as<int>(), gs_d.as<int>(), ncolors,
+                                                       ngroups, gcnt.as<int>());
+        FDL_LAUNCH_CK();
+    }
+    scan_exclusive(gcnt.as<int>(), goff.as<int>(), ngroups, goff.as<int>() + ngroups, st);
+    if (ngroups > 0) {
+        k_gd_write<<<grid_for(ngroups), 256, 0, st>>>(L.rp.as<int>(), L.seg_d.as<int>(), gs_d.as<int>(), ncolors,
+                                                       ngroups, goff.as<int>(), L.gd_pieces.as<int4>());
+        FDL_LAUNCH_CK();
+    }
+    const int np = ncolors * (kGdParts + 1);
+    L.gd_parts.alloc((size_t)np * 4, st);
+    k_gd_parts<<<grid_for(np), 256, 0, st>>>(gs_d.as<int>(), goff.as<int>(), L.gd_pieces.as<int4>(), ncolors,
+                                             L.gd_parts.as<int>());
+    FDL_LAUNCH_CK();
+}
+
 // `iters` power steps on c I - L of a small level (natural CSR), one CTA:
 // z = (c (y - mu) + sum w (y_j - y_i)) / sigma with (mu, sigma) of the previous
 // vector, ping-pong between y0 and y1 (the result ends in y0 if iters is even);
@@ -918,6 +1293,90 @@ static void launch_gs_cluster(cudaStream_t st, CsrView v, const int *seg, int c0
     FDL_CK(cudaLaunchKernelEx(&cfg, k_gs_multi<true>, v, seg, c0, c1, sweeps, x, slot, mode, n));
 }
 
+// k_gs_pieces: a cluster of 16 CTAs where the device allows (else 8), or one CTA
+template <bool CLUSTER, bool XS>
+static int gd_prepare() {
+    static DeviceCache cache{};
+    std::atomic<int> &slot = cache[current_device()];
+    int cl = slot.load();
+    if (cl) return cl;
+    const int smem = (int)(kGdSmemBase + (size_t)kGdMaxRunColours * 8 + (XS ? (size_t)kGdXsmemN * 8 : 0));
+    FDL_CK(cudaFuncSetAttribute(k_gs_pieces<CLUSTER, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cl = 1;
+    if (CLUSTER) {
+        cl = 8;
+        if (cudaFuncSetAttribute(k_gs_pieces<CLUSTER, XS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+            cudaSuccess) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(kGcMaxCluster);
+            q.blockDim = dim3(kGdThreads);
+            q.dynamicSmemBytes = smem;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = kGcMaxCluster;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, k_gs_pieces<CLUSTER, XS>, &q) == cudaSuccess &&
+                nclusters > 0)
+                cl = kGcMaxCluster;
+        }
+        (void)cudaGetLastError();
+    }
+    slot.store(cl);
+    return cl;
+}
+
+template <bool CLUSTER, bool XS>
+static void launch_gs_pieces_t(cudaStream_t st, const GdArgs &a) {
+    const int cl = gd_prepare<CLUSTER, XS>();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(kGdThreads);
+    cfg.dynamicSmemBytes = kGdSmemBase + (size_t)kGdMaxRunColours * 8 + (XS ? (size_t)a.n * 8 : 0);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = FDL_PDL;
+    if (CLUSTER) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = cl;
+        at[na].val.clusterDim.y = 1;
+        at[na++].val.clusterDim.z = 1;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    FDL_CK(cudaLaunchKernelEx(&cfg, k_gs_pieces<CLUSTER, XS>, a));
+    FDL_LAUNCH_CK();
+}
+
+static void launch_gs_pieces(cudaStream_t st, const Level &L, int c0, int c1, int sweeps, double *x, double *slot,
+                             int mode, bool cluster) {
+    GdArgs a{};
+    a.L = CsrView{L.n, L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>()};
+    a.pieces = L.gd_pieces.as<int4>();
+    a.parts = L.gd_parts.as<int>();
+    a.seg = L.seg_d.as<int>();
+    a.c0 = c0;
+    a.c1 = c1;
+    a.sweeps = sweeps;
+    a.x = x;
+    a.slot = slot;
+    a.stat_mode = mode;
+    a.n = L.n;
+    const bool xs = L.n <= kGdXsmemN;
+    if (cluster) {
+        if (xs) launch_gs_pieces_t<true, true>(st, a);
+        else launch_gs_pieces_t<true, false>(st, a);
+    } else {
+        if (xs) launch_gs_pieces_t<false, true>(st, a);
+        else launch_gs_pieces_t<false, false>(st, a);
+    }
+}
+
 #ifndef FDL_DENSE_ROW_DEG
 #define FDL_DENSE_ROW_DEG 7.0
 #endif
@@ -1003,6 +1462,9 @@ struct Enq {
             a.out_stat = out_slot;
             a.stat_mode = mode;
             pass<OP_GS>(L, L.ctile[cb], L.ctile[cb + 1], a);
+        } else if (FDL_GS_PIECES) {
+            launch_gs_pieces(st, L, cb, ce, sweeps, x, out_slot, mode, kind == 1);
+            launches++;
         } else if (kind == 1) {
             launch_gs_cluster(st, v, L.seg_d.as<int>(), cb, ce, sweeps, x, out_slot, mode, L.n);
             launches++;
