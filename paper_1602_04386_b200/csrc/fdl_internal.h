@@ -86,6 +86,12 @@ struct Level {
     std::vector<int> gs_runs;  // GS schedule of one sweep: (c_begin, c_end, kind) triplets,
                                // kind 0 = grid tile pass of one colour, 1 = cluster run,
                                // 2 = single-CTA run (k_gs_pieces; FDL_GS_PIECES=0: k_gs_multi)
+    // hub rows (> kTileT entries): piece tiles at the end of their pass's tile
+    // range; hubs of colour c at [hoff[c], hoff[c+1]), of the natural pass at
+    // [hoff[ncolors], hoff[ncolors+1]) (empty hoff: no hubs)
+    DBuf hubs;               // int4 {row, first piece tile (pass-relative), pieces, 0}
+    std::vector<int> hoff;
+    DBuf hub_part;           // double2 per tile of the largest pass
     DBuf gd_pieces;          // int4 pieces of the GS rows (build_gs_pieces), when a run uses them
     DBuf gd_parts;           // [ncolors][kGdParts + 1] piece index bounds
     DistPlan dist;

@@ -2767,7 +2767,9 @@ __global__ void k_make_tiles(const int *rp, int s0, int s1, int ntiles, Tile *ou
 
 // the GS tiles of every colour in one launch: tile t belongs to the colour c
 // with ctile[c] <= t < ctile[c + 1] (binary search), then as k_make_tiles
-__global__ void k_make_tiles_colours(const int *rp, const int *seg, const int *ctile, int ncolors, Tile *out) {
+// (cwin[c]: window tiles of colour c; the slots after them hold hub piece tiles)
+__global__ void k_make_tiles_colours(const int *rp, const int *seg, const int *ctile, const int *cwin, int ncolors,
+                                     Tile *out) {
     const int nt = ctile[ncolors];
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
         int lo = 0, hi = ncolors - 1;   // last c with ctile[c] <= t
@@ -2775,12 +2777,28 @@ __global__ void k_make_tiles_colours(const int *rp, const int *seg, const int *c
             const int mid = (lo + hi + 1) >> 1;
             if (ctile[mid] <= t) lo = mid; else hi = mid - 1;
         }
-        const int c = lo, s0 = seg[c], s1 = seg[c + 1], tl = t - ctile[c], ntc = ctile[c + 1] - ctile[c];
+        const int c = lo, s0 = seg[c], s1 = seg[c + 1], tl = t - ctile[c], ntc = cwin[c];
+        if (tl >= ntc) continue;
         const long long C0 = (long long)rp[s0] + s0;
         const int a = tl == 0 ? s0 : lower_bound_coord(rp, s0, s1, C0 + (long long)tl * kTileT);
         const int b = (tl + 1 == ntc) ? s1 : lower_bound_coord(rp, s0, s1, C0 + (long long)(tl + 1) * kTileT);
         out[t] = make_int2(a, b);
     }
+}
+
+// rows longer than a tile (hubs of power-law levels): {GS row, natural id, length}
+constexpr int kMaxHubs = 1 << 16;
+__global__ void k_hub_find(int n, const int *rp, const int *perm, int *count, int4 *list) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int len = rp[r + 1] - rp[r];
+        if (len > kTileT) {
+            const int i = atomicAdd(count, 1);
+            if (i < kMaxHubs) list[i] = make_int4(r, perm[r], len, 0);
+        }
+    }
+}
+__global__ void k_scatter_tiles(int k, const int *dst, const Tile *src, Tile *tiles) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) tiles[dst[i]] = src[i];
 }
 
 static int tiles_for(long long coord_span) { return std::max(1, (int)((coord_span + kTileT - 1) / kTileT)); }
@@ -2835,10 +2853,25 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     k_seg_fix<<<1, 1, 0, st>>>(ncolors, n, segstart.as<int>(), L.rp.as<int>(), sfix.as<int>(),
                                sfix.as<int>() + ncolors + 1);
     FDL_LAUNCH_CK();
+    // hub rows (> kTileT entries), found with the same round trip
+    DBuf hubd(16 + (size_t)std::min(n, kMaxHubs) * 16, st);
+    FDL_CK(cudaMemsetAsync(hubd.p, 0, 16, st));
+    k_hub_find<<<grid_for(n), 256, 0, st>>>(n, L.rp.as<int>(), L.perm.as<int>(), hubd.as<int>(),
+                                            reinterpret_cast<int4 *>(hubd.as<char>() + 16));
+    FDL_LAUNCH_CK();
     double dm = 0.0;
+    int nhub = 0;
     readback(st, {{seg.data(), sfix.p, (size_t)(ncolors + 1) * 4},
                   {segnnz.data(), sfix.as<int>() + ncolors + 1, (size_t)(ncolors + 1) * 4},
-                  {&dm, dmax.p, 8}});
+                  {&dm, dmax.p, 8},
+                  {&nhub, hubd.p, 4}});
+    std::vector<int4> hub;   // {GS row, natural id, length, colour}
+    if (nhub > 0 && nhub <= kMaxHubs) {
+        hub.resize(nhub);
+        readback(st, {{hub.data(), hubd.as<char>() + 16, (size_t)nhub * 16}});
+        std::sort(hub.begin(), hub.end(), [](const int4 &p, const int4 &q) { return p.x < q.x; });
+        for (auto &hb : hub) hb.w = (int)(std::upper_bound(seg.begin(), seg.end(), hb.x) - seg.begin()) - 1;
+    }
     // R8: c = 2 max_i d_i (Gershgorin); on a 2-vertex level 2 max d = lambda_max
     // exactly and c I - L would annihilate the only non-constant direction
     L.shift = (n == 2 ? 3.0 : 2.0) * dm;
@@ -2932,6 +2965,14 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
         if (c0 < ncolors) L.gs_runs.insert(L.gs_runs.end(), {c0, ncolors, 2});
 #endif
     }
+    // tiles of every pass: colour c's window tiles then its hub piece tiles,
+    // the natural pass likewise (hub rows: pieces of kTileT entries, a tile each)
+    std::vector<int> hpieces(ncolors + 1, 0);
+    for (const auto &hb : hub) {
+        const int np = div_up(hb.z, kTileT);
+        hpieces[hb.w] += np;
+        hpieces[ncolors] += np;
+    }
     L.ctile.assign(ncolors + 1, 0);
     int nt = 0;
     std::vector<int> cnt(ncolors + 1);
@@ -2939,23 +2980,64 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
         L.ctile[c] = nt;
         long long span = (long long)(segnnz[c + 1] + seg[c + 1]) - (segnnz[c] + seg[c]);
         cnt[c] = seg[c + 1] > seg[c] ? tiles_for(span) : 0;
-        nt += cnt[c];
+        nt += cnt[c] + hpieces[c];
     }
     L.ctile[ncolors] = nt;
     cnt[ncolors] = tiles_for((long long)g.nnz + n);
-    nt += cnt[ncolors];
+    nt += cnt[ncolors] + hpieces[ncolors];
     L.ntiles = nt;
     L.ctile_d.alloc((size_t)(ncolors + 1) * 4, st);
     FDL_CK(cudaMemcpyAsync(L.ctile_d.p, L.ctile.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
     L.tiles.alloc((size_t)nt * sizeof(Tile), st);
     if (L.ctile[ncolors] > 0) {
+        DBuf cwin((size_t)ncolors * 4, st);
+        FDL_CK(cudaMemcpyAsync(cwin.p, cnt.data(), (size_t)ncolors * 4, cudaMemcpyHostToDevice, st));
         k_make_tiles_colours<<<grid_for(L.ctile[ncolors]), 256, 0, st>>>(
-            L.rp.as<int>(), L.seg_d.as<int>(), L.ctile_d.as<int>(), ncolors, L.tiles.as<Tile>());
+            L.rp.as<int>(), L.seg_d.as<int>(), L.ctile_d.as<int>(), cwin.as<int>(), ncolors, L.tiles.as<Tile>());
         FDL_LAUNCH_CK();
     }
     k_make_tiles<<<grid_for(cnt[ncolors]), 256, 0, st>>>(g.rp, 0, n, cnt[ncolors],
                                                          L.tiles.as<Tile>() + L.ctile[ncolors]);
     FDL_LAUNCH_CK();
+    if (!hub.empty()) {
+        // hub lists {row, first piece tile (pass-relative), pieces, 0} per pass
+        // (rows ascending), and the piece tiles {row, -(1 + piece)}
+        std::vector<std::vector<int4>> per(ncolors + 1);
+        std::vector<int> used(ncolors + 1, 0);
+        std::vector<int> pdst;
+        std::vector<Tile> ptile;
+        auto add = [&](int pass, int row, int len) {
+            const int np = div_up(len, kTileT), first = cnt[pass] + used[pass];
+            per[pass].push_back(make_int4(row, first, np, 0));
+            for (int i = 0; i < np; i++) {
+                pdst.push_back(L.ctile[pass] + first + i);
+                ptile.push_back(make_int2(row, -(1 + i)));
+            }
+            used[pass] += np;
+        };
+        for (const auto &hb : hub) add(hb.w, hb.x, hb.z);
+        std::vector<int4> hn(hub);
+        std::sort(hn.begin(), hn.end(), [](const int4 &p, const int4 &q) { return p.y < q.y; });
+        for (const auto &hb : hn) add(ncolors, hb.y, hb.z);
+        std::vector<int4> all;
+        L.hoff.assign(ncolors + 2, 0);
+        int maxpass = 0;
+        for (int c = 0; c <= ncolors; c++) {
+            L.hoff[c] = (int)all.size();
+            all.insert(all.end(), per[c].begin(), per[c].end());
+            maxpass = std::max(maxpass, (c < ncolors ? L.ctile[c + 1] : nt) - L.ctile[c]);
+        }
+        L.hoff[ncolors + 1] = (int)all.size();
+        L.hubs.alloc(all.size() * sizeof(int4), st);
+        FDL_CK(cudaMemcpyAsync(L.hubs.p, all.data(), all.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+        L.hub_part.alloc((size_t)maxpass * 16, st);
+        const int k = (int)pdst.size();
+        DBuf pd((size_t)k * 4, st), pt((size_t)k * sizeof(Tile), st);
+        FDL_CK(cudaMemcpyAsync(pd.p, pdst.data(), (size_t)k * 4, cudaMemcpyHostToDevice, st));
+        FDL_CK(cudaMemcpyAsync(pt.p, ptile.data(), (size_t)k * sizeof(Tile), cudaMemcpyHostToDevice, st));
+        k_scatter_tiles<<<grid_for(k), 256, 0, st>>>(k, pd.as<int>(), pt.as<Tile>(), L.tiles.as<Tile>());
+        FDL_LAUNCH_CK();   // (pageable sources: staged by the time the copies return)
+    }
 }
 
 // the natural CSR of a level for the PI / RQ passes: taken over from the setup

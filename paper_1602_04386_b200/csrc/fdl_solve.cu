@@ -28,6 +28,7 @@
 // reduced by one thread from shared memory; longer rows by a warp (or, for a
 // row longer than a tile, the whole CTA) straight from global memory.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 
@@ -91,6 +92,12 @@ struct PassArgs {
     const double *sign;     // RQ: +-1
     double *result;         // RQ: {lambda2, residual, ||v||}, or the raw sums if rq_raw
     int rq_raw;             // RQ: write the raw partial sums (partitioned solve)
+    // rows longer than a tile ("hubs", power-law levels): reduced in pieces of
+    // kTileT entries by the piece tiles {row, -(1 + piece)} of the pass, partial
+    // sums in hub_part[tile], folded in piece order by the last CTA
+    const int4 *hubs;       // {row, first piece tile (pass-relative), pieces, 0}; null: no piece tiles
+    int nhub;
+    double2 *hub_part;
 };
 
 // ----------------------------------------------------------------- PTX helpers
@@ -217,9 +224,16 @@ __device__ __forceinline__ void block_sum(double v[N], double (*sm)[N]) {
 
 // Per-CTA partials -> last CTA folds all partials in a fixed order and runs
 // `fin(total)` on thread 0.  Deterministic for a fixed grid.
+struct NoHubs {
+    __device__ void operator()(double *) const {}
+};
 template <class Fin>
+__device__ __forceinline__ void grid_reduce(double st[kNumStats], double *partials, unsigned *counter, Fin fin);
+// Hub(hs): run by every thread of the last CTA before the totals; its
+// statistics hs are block-summed and added to them (fixed order)
+template <class Hub, class Fin>
 __device__ __forceinline__ void grid_reduce(double st[kNumStats], double *partials,
-                                            unsigned *counter, Fin fin) {
+                                            unsigned *counter, Hub hub, Fin fin) {
     __shared__ double sm[32][kNumStats];
     __shared__ bool s_last;
     block_sum<kNumStats>(st, sm);
@@ -233,15 +247,26 @@ __device__ __forceinline__ void grid_reduce(double st[kNumStats], double *partia
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    double hs[kNumStats] = {0.0, 0.0, 0.0};
+    hub(hs);
     double v[kNumStats] = {0.0, 0.0, 0.0};
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
 #pragma unroll
         for (int k = 0; k < kNumStats; k++) v[k] += __ldcg(&partials[b * kNumStats + k]);
     block_sum<kNumStats>(v, sm);
+    if (!std::is_same<Hub, NoHubs>::value) {
+        block_sum<kNumStats>(hs, sm);
+#pragma unroll
+        for (int k = 0; k < kNumStats; k++) v[k] += hs[k];
+    }
     if (threadIdx.x == 0) {
         fin(v);
         *counter = 0u;
     }
+}
+template <class Fin>
+__device__ __forceinline__ void grid_reduce(double st[kNumStats], double *partials, unsigned *counter, Fin fin) {
+    grid_reduce(st, partials, counter, NoHubs{}, fin);
 }
 
 // slot = {S, Q, mean, deflated norm}.  With bit 3 of mode the sums are of
@@ -296,11 +321,42 @@ __device__ __forceinline__ void acc_range(RowAcc<OP> &acc, const CsrView &L, con
     }
 }
 
+// entries kb, kb + 32, ... < ke of a row from the stage (sci / sw indexed by
+// the global entry number), 8 per lane with their gathers in flight
+template <int OP, bool COHERENT>
+__device__ __forceinline__ void acc_smem(RowAcc<OP> &acc, const int *__restrict__ sci,
+                                         const double *__restrict__ sw, const double *x, int kb, int ke) {
+    for (int k0 = kb; k0 < ke; k0 += 8 * 32) {
+        int c8[8];
+        double w8[8], x8[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int k = k0 + i * 32;
+            c8[i] = k < ke ? sci[k] : -1;
+            w8[i] = k < ke ? sw[k] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) x8[i] = c8[i] >= 0 ? ldx<COHERENT>(x + c8[i]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (c8[i] >= 0) acc.add(w8[i], x8[i]);
+    }
+}
+
 // one thread stages the column/weight streams of tile t into stage b
+// first entry / entry count of a tile (a piece tile: its kTileT-entry slice of the row)
+__device__ __forceinline__ int2 tile_entries(const CsrView &L, Tile t) {
+    if (t.y < 0) {
+        const int e0 = L.rp[t.x] + (-t.y - 1) * kTileT;
+        return make_int2(e0, min(kTileT, L.rp[t.x + 1] - e0));
+    }
+    const int e0 = L.rp[t.x];
+    return make_int2(e0, min(L.rp[t.y] - e0, kStageCap));
+}
 __device__ __forceinline__ void issue_tile(PassSmem &S, const CsrView &L, Tile t, int b,
                                            unsigned long long pol) {
-    const int e0 = L.rp[t.x], e1 = L.rp[t.y];
-    const int cnt = min(e1 - e0, kStageCap);
+    const int2 te = tile_entries(L, t);
+    const int e0 = te.x, cnt = te.y;
     if (cnt > 0) {
         const int a4 = e0 & ~3, a2 = e0 & ~1;
         const unsigned bci = round16((unsigned)(e0 + cnt - a4) * 4u);
@@ -364,12 +420,48 @@ __device__ __forceinline__ int subwarp_rows(const Tile t, const int *__restrict_
 // their gathers in flight together; longer rows: a warp each (round robin over the
 // warps) from global memory; a row longer than a tile (necessarily the tile's last)
 // gets the whole CTA.  Ends with a __syncthreads (stage b may then be refilled).
-template <int OP, int CH, bool COHERENT, int SW>
-__device__ __forceinline__ void tile_compute(const Tile t, PassSmem &S, int b, unsigned phase,
+template <int OP, int CH, bool COHERENT, int SW, bool HUB>
+__device__ __forceinline__ void tile_compute(const Tile t, int ti, PassSmem &S, int b, unsigned phase,
                                              RowAcc<OP> *s_red, const CsrView &L, const PassArgs &a,
                                              const Scal &sc, double st[kNumStats]) {
     const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const double *__restrict__ x = a.x;
+    if (HUB && t.y < 0) {
+        // a piece of a hub row: its kTileT entries from shared memory, 8 per
+        // thread in flight; the CTA's partial sums go to hub_part[ti]
+        const int2 te = tile_entries(L, t);
+        const int *__restrict__ sci = S.st[b].ci - (te.x & ~3);
+        const double *__restrict__ sw = S.st[b].w - (te.x & ~1);
+        RowAcc<OP> acc;
+        if (OP != OP_GS) acc.own = own_of<OP>(t.x, a);
+        mbar_wait(&S.bar[b], phase);
+        const int ke = te.x + te.y;
+        for (int k0 = te.x + tid; k0 < ke; k0 += 8 * kPassThreads) {
+            int c8[8];
+            double w8[8], x8[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int k = k0 + i * kPassThreads;
+                c8[i] = k < ke ? sci[k] : -1;
+                w8[i] = k < ke ? sw[k] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; i++) x8[i] = c8[i] >= 0 ? ldx<COHERENT>(x + c8[i]) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+                if (c8[i] >= 0) acc.add(w8[i], x8[i]);
+        }
+        acc.warp_sum();
+        if (lane == 0) s_red[warp] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            RowAcc<OP> tot = s_red[0];
+            for (int k = 1; k < kPassWarps; k++) tot.merge(s_red[k]);
+            a.hub_part[ti] = make_double2(tot.a, tot.b);
+        }
+        __syncthreads();   // stage b and s_red may be reused
+        return;
+    }
     const int e0 = L.rp[t.x];
     const int a4 = e0 & ~3, a2 = e0 & ~1;
     const int *__restrict__ sci = S.st[b].ci - a4;   // index with the global entry number
@@ -443,17 +535,31 @@ __device__ __forceinline__ void tile_compute(const Tile t, PassSmem &S, int b, u
     }
     if (__syncthreads_or(has_long)) {
         const int last = t.y - 1;
-        const bool cta_last = L.rp[t.y] - L.rp[last] > kTileT;
-        for (int row = t.x + warp; row < t.y; row += kPassWarps) {
-            const int kb = L.rp[row], ke = L.rp[row + 1];
-            if (ke - kb <= kShortMax || (cta_last && row == last)) continue;   // warp-uniform
-            RowAcc<OP> acc;
-            if (OP != OP_GS) acc.own = own_of<OP>(row, a);
-            acc_range<OP, COHERENT>(acc, L, x, kb + lane, ke, 32);
-            acc.warp_sum();
-            if (lane == 0) row_finish<OP>(row, acc, a, sc, st);
+        // a row longer than a tile: the whole CTA, or its piece tiles (a.hubs)
+        const int eT = L.rp[t.y];
+        const bool cta_last = eT - L.rp[last] > kTileT;
+        const int se = min(eT, e0 + kStageCap);   // end of the staged entries
+        // warp w takes the tile's rows in blocks of 32 (w, w + kPassWarps, ...):
+        // one coalesced load of their offsets, then each long row in turn, its
+        // entries from the stage when they were staged (else global memory)
+        for (int rb = t.x + warp * 32; rb < t.y; rb += kPassWarps * 32) {
+            const int row = rb + lane;
+            int kb = 0, ke = 0;
+            if (row < t.y) { kb = L.rp[row]; ke = L.rp[row + 1]; }
+            unsigned m = __ballot_sync(0xffffffffu, row < t.y && ke - kb > kShortMax && !(cta_last && row == last));
+            while (m) {
+                const int l = __ffs(m) - 1;
+                m &= m - 1;
+                const int r = rb + l, rkb = __shfl_sync(0xffffffffu, kb, l), rke = __shfl_sync(0xffffffffu, ke, l);
+                RowAcc<OP> acc;
+                if (OP != OP_GS) acc.own = own_of<OP>(r, a);
+                if (rke <= se) acc_smem<OP, COHERENT>(acc, sci, sw, x, rkb + lane, rke);
+                else acc_range<OP, COHERENT>(acc, L, x, rkb + lane, rke, 32);
+                acc.warp_sum();
+                if (lane == 0) row_finish<OP>(r, acc, a, sc, st);
+            }
         }
-        if (cta_last) {
+        if (cta_last && !HUB) {
             const int kb = L.rp[last], ke = L.rp[t.y];
             RowAcc<OP> acc;
             if (OP != OP_GS) acc.own = own_of<OP>(last, a);
@@ -493,7 +599,7 @@ __device__ __forceinline__ Scal load_scal(const PassArgs &a) {
     return sc;
 }
 
-template <int OP, int CH = 0, int SW = 0>
+template <int OP, int CH = 0, int SW = 0, bool HUB = false>
 __global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
                                                            CsrView L, PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -524,10 +630,32 @@ __global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_
             fence_proxy_async();   // generic reads of that stage (previous tile) before async writes
             issue_tile(S, L, tiles[ahead], (it + kStages - 1) % kStages, pol);
         }
-        tile_compute<OP, CH, false, SW>(tiles[ti], S, b, (unsigned)(it / kStages) & 1u, s_red, L, a, sc, st);
+        tile_compute<OP, CH, false, SW, HUB>(tiles[ti], ti, S, b, (unsigned)(it / kStages) & 1u, s_red, L, a, sc, st);
     }
-    if (OP == OP_GS && !(a.stat_mode & 4)) return;   // uniform: statistics not wanted
-    grid_reduce(st, a.partials, a.counter, [&](const double *tot) {
+    if (OP == OP_GS && !(a.stat_mode & 4) && !HUB) return;   // uniform: statistics not wanted
+    // the last CTA first completes the hub rows: partial sums of their piece
+    // tiles folded in piece order, then the row epilogue (outputs, statistics
+    // in a fixed hub -> thread map)
+    auto hub_rows = [&](double hs[kNumStats]) {
+        if (!HUB) return;
+        for (int h = threadIdx.x; h < a.nhub; h += kPassThreads) {
+            const int4 hb = a.hubs[h];
+            RowAcc<OP> acc;
+            if (OP != OP_GS) acc.own = own_of<OP>(hb.x, a);
+            for (int k0 = 0; k0 < hb.z; k0 += 8) {   // 8 partials in flight, folded in order
+                double2 pp[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    pp[i] = k0 + i < hb.z ? __ldcg(a.hub_part + hb.y + k0 + i) : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    if (k0 + i < hb.z) { acc.a += pp[i].x; acc.b += pp[i].y; }
+            }
+            row_finish<OP>(hb.x, acc, a, sc, hs);
+        }
+    };
+    grid_reduce(st, a.partials, a.counter, hub_rows, [&](const double *tot) {
+        if (OP == OP_GS && !(a.stat_mode & 4)) return;
         if (OP == OP_RQ && a.rq_raw) {
             a.result[0] = tot[0];
             a.result[1] = tot[1];
@@ -1435,7 +1563,10 @@ struct Enq {
                                 : CsrView{L.n, L.rpN.as<int>(), L.ciN.as<int>(), L.wN.as<double>()};
         // GS: the chunk of 4 suits <= 4.5 neighbours per row, 8 the denser coarse
         // levels; dense levels (>= kDenseRowDeg per row): 4 lanes per short row
-        if (OP == OP_GS && L.nnz <= 4.5 * L.n) {
+        if (a.hubs) {   // piece tiles of hub rows in the range (power-law levels)
+            if (L.nnz >= kDenseRowDeg * (double)L.n) launch_pass(k_tilepass<OP, 0, 4, true>, grid, st, tiles, nt, v, a);
+            else launch_pass(k_tilepass<OP, 0, 0, true>, grid, st, tiles, nt, v, a);
+        } else if (OP == OP_GS && L.nnz <= 4.5 * L.n) {
             grid = std::min(nt, pass_grid(3));
             launch_pass(k_tilepass<OP_GS, 4>, grid, st, tiles, nt, v, a);
         } else if (L.nnz >= kDenseRowDeg * (double)L.n) {
@@ -1445,8 +1576,15 @@ struct Enq {
         }
         launches++;
     }
+    // hp: the pass whose hub rows have piece tiles in [tb, te) (colour c, or
+    // ncolors for the natural-order pass)
     template <int OP>
-    void pass(const Level &L, int tb, int te, PassArgs a) {
+    void pass(const Level &L, int tb, int te, PassArgs a, int hp) {
+        if (!L.hoff.empty() && L.hoff[hp + 1] > L.hoff[hp]) {
+            a.hubs = L.hubs.as<int4>() + L.hoff[hp];
+            a.nhub = L.hoff[hp + 1] - L.hoff[hp];
+            a.hub_part = L.hub_part.as<double2>();
+        }
         pass_tiles<OP>(L, L.tiles.as<Tile>() + tb, te - tb, a);
     }
     // One sweep = the level's GS schedule (L.gs_runs): grid-wide tile passes for
@@ -1461,7 +1599,7 @@ struct Enq {
             a.n = L.n;
             a.out_stat = out_slot;
             a.stat_mode = mode;
-            pass<OP_GS>(L, L.ctile[cb], L.ctile[cb + 1], a);
+            pass<OP_GS>(L, L.ctile[cb], L.ctile[cb + 1], a, cb);
         } else if (FDL_GS_PIECES) {
             launch_gs_pieces(st, L, cb, ce, sweeps, x, out_slot, mode, kind == 1);
             launches++;
@@ -1521,7 +1659,7 @@ struct Enq {
         a.stat_mode = 7;
         a.n = L.n;
         a.shift = L.shift;
-        pass<OP_PI>(L, L.nat_tile_begin(), L.ntiles, a);
+        pass<OP_PI>(L, L.nat_tile_begin(), L.ntiles, a, L.ncolors);
     }
     void rq(const Level &L, const double *x, const double *in_slot, double *vnat, const double *sign) {
         PassArgs a{};
@@ -1531,7 +1669,7 @@ struct Enq {
         a.vnat = vnat;
         a.sign = sign;
         a.result = h.result.as<double>();
-        pass<OP_RQ>(L, L.nat_tile_begin(), L.ntiles, a);
+        pass<OP_RQ>(L, L.nat_tile_begin(), L.ntiles, a, L.ncolors);
     }
     void prolong(const Level &L, const int *map, const double *xc, double *y, double *out_slot,
                  double *mean_copy = nullptr) {
@@ -1595,6 +1733,12 @@ int rowpass_grid() {
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_RQ, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_RQ, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_GS, 0, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI, 0, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_RQ, 0, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 
     int b3 = 0;
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_tilepass<OP_GS, 4>, kPassThreads, smem));

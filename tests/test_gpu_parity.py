@@ -73,6 +73,8 @@ SMALL = {
     # mid-size dense level (n > 12288, average degree >= 64): the cluster colouring
     "dense16k_deg70": lambda: gg.random_connected(16000, 560000, 22),
     "hub3000_3hubs": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
+    # a row of 4999 entries: five piece tiles of the row passes (hub rows > 1024 entries)
+    "star5000": lambda: gg.star(5000),
     "clique70_tail2000": lambda: clique_with_tail(70, 2000),
     "tiny_p5": lambda: gg.path(5),
     "tiny_p3": lambda: gg.path(3),
@@ -110,7 +112,8 @@ def test_hierarchy_full_sort_fallback(fd, orc, name, monkeypatch):
     test_hierarchy_bit_exact(fd, orc, name)
 
 
-@pytest.mark.parametrize("name", ["grid32_unit(config0)", "grid3d_12_lognormal", "rmat12", "rand300"])
+@pytest.mark.parametrize("name", ["grid32_unit(config0)", "grid3d_12_lognormal", "rmat12", "rand300",
+                                  "hub3000_3hubs", "star5000"])
 def test_single_ops_vs_oracle(fd, orc, name):
     g = SMALL[name]()
     levels = orc.build_hierarchy(orc_graph(orc, g), orc.Config())
