@@ -52,9 +52,23 @@ constexpr int kPassWarps = kPassThreads / 32;
 // entries per row gathered together (x 2 rows in flight) and CTAs per SM, per
 // pass kind (tuned with tools/build_variants.py: the GS passes, with no own
 // value and a sparse colour sub-range, prefer a deeper chunk)
+#ifndef FDL_PI_CHUNK
+#define FDL_PI_CHUNK 4
+#endif
+#ifndef FDL_GS4_MINB
+#define FDL_GS4_MINB 7
+#endif
+#ifndef FDL_GS4_MAXDEG
+#define FDL_GS4_MAXDEG 8.0
+#endif
 template <int OP, int CH> struct PassTune {
-    static constexpr int chunk = CH ? CH : (OP == 0 ? 8 : 4);
-    static constexpr int min_blocks = ((chunk == 4 && OP != 2) ? 4 : 3) * FDL_PASS_MINB / 4;
+    static constexpr int chunk = CH ? CH : (OP == 0 ? 8 : FDL_PI_CHUNK);
+    // the chunk-4 GS pass (levels of <= 8 entries per row) keeps 7 CTAs per SM
+    // (72 registers): measured on the 8192^2 grid, level-0 sweep 1.23 ms with
+    // 8 CTAs, 1.15 / 1.05 / 1.01 ms with 5 / 6 / 7; levels 1-4 gain 2-10 % over
+    // the chunk-8 pass; the power step prefers 8 CTAs (tools/gpu_levels_variants.sh)
+    static constexpr int min_blocks = (OP == 0 && chunk == 4) ? FDL_GS4_MINB
+                                      : ((chunk == 4 && OP != 2) ? 4 : 3) * FDL_PASS_MINB / 4;
 };
 constexpr int kNumStats = 3;
 constexpr int kCiBuf = kStageCap + 8;   // + start alignment (<= 3) + 16-byte round-up (<= 3)
@@ -1566,7 +1580,7 @@ struct Enq {
         if (a.hubs) {   // piece tiles of hub rows in the range (power-law levels)
             if (L.nnz >= kDenseRowDeg * (double)L.n) launch_pass(k_tilepass<OP, 0, 4, true>, grid, st, tiles, nt, v, a);
             else launch_pass(k_tilepass<OP, 0, 0, true>, grid, st, tiles, nt, v, a);
-        } else if (OP == OP_GS && L.nnz <= 4.5 * L.n) {
+        } else if (OP == OP_GS && L.nnz <= FDL_GS4_MAXDEG * L.n) {
             grid = std::min(nt, pass_grid(3));
             launch_pass(k_tilepass<OP_GS, 4>, grid, st, tiles, nt, v, a);
         } else if (L.nnz >= kDenseRowDeg * (double)L.n) {
