@@ -180,6 +180,9 @@ void readback(cudaStream_t st, std::initializer_list<ReadPiece> pieces);
 void readback(cudaStream_t st, const std::vector<ReadPiece> &pieces);
 // the same wait without copies
 void host_wait(cudaStream_t st);
+// Stream-ordered copy of a small host array to the device without a stream
+// synchronisation (pinned staging, fdl_prims.cu); src may be reused on return.
+void upload(cudaStream_t st, void *dst, const void *src, size_t bytes);
 // Stable LSD radix sort of (key, value) pairs on bits [0, bits); result in keys/vals.
 void radix_sort_u32_i32(unsigned *keys, int *vals, int64_t n, int bits, cudaStream_t st);
 // stable sort of the vertices by colour (< 256 colours): perm, inv, degree in sorted order, segment starts

@@ -79,13 +79,12 @@ struct Level {
     // [ctile[c], ctile[c+1])), then the natural-order tiles [ctile[ncolors], ntiles)
     DBuf tiles;
     std::vector<int> ctile;
-    DBuf ctile_d;            // device copy of ctile
     std::vector<int> seg;    // [ncolors + 1] GS row range of every colour
     DBuf seg_d;              // device copy of seg
     int gs_tail_c0 = 0;      // colours [gs_tail_c0, ncolors) run in one single-CTA launch
     std::vector<int> gs_runs;  // GS schedule of one sweep: (c_begin, c_end, kind) triplets,
-                               // kind 0 = grid tile pass of one colour, 1 = cluster run,
-                               // 2 = single-CTA run (k_gs_pieces; FDL_GS_PIECES=0: k_gs_multi)
+                               // kind 0 = grid tile pass of one colour, 1 / 2 = k_gs_multi
+                               // cluster / single-CTA run, 3 / 4 = k_gs_pieces cluster / single-CTA run
     // hub rows (> kTileT entries): piece tiles at the end of their pass's tile
     // range; hubs of colour c at [hoff[c], hoff[c+1]), of the natural pass at
     // [hoff[ncolors], hoff[ncolors+1]) (empty hoff: no hubs)

@@ -5,6 +5,7 @@
 // CSR offset scans everywhere, the Galerkin product's long-row path (two-key
 // radix sort) and the multicolour layout (sort by colour).
 #include <algorithm>
+#include <mutex>
 #include <climits>
 #include <cstring>
 
@@ -135,60 +136,115 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const int *in, int *ou
     }
 }
 
-// ---------------------------------------------------------------- readbacks
+// ---------------------------------------------------------------- readbacks / uploads
+// Per-thread host scratch: a pinned readback buffer, a pinned upload arena and
+// the polling events.  The setup's helper thread is created per
+// fiedler_create, so the scratch objects come from a process-wide pool (no
+// cudaMallocHost / cudaFreeHost / event creation per create).
 namespace {
-struct PinnedScratch {
-    void *p = nullptr;
-    size_t cap = 0;
+struct ThreadScratch {
+    void *pin = nullptr;           // readbacks
+    size_t pincap = 0;
+    char *up = nullptr;            // uploads
+    size_t upcap = 0, upoff = 0;
+    cudaStream_t upst = nullptr;   // stream of the pending uploads
     cudaEvent_t ev[kMaxDevices] = {};
-    ~PinnedScratch() {
-        if (p) cudaFreeHost(p);
-        for (cudaEvent_t e : ev)
-            if (e) cudaEventDestroy(e);
-    }
 };
-thread_local PinnedScratch tl_pin;
+std::mutex g_scratch_mu;
+std::vector<ThreadScratch *> g_scratch_free;
 
-void poll(cudaStream_t st) {
-    cudaEvent_t &ev = tl_pin.ev[current_device()];
+void poll_on(ThreadScratch &s, cudaStream_t st) {
+    cudaEvent_t &ev = s.ev[current_device()];
     if (!ev) FDL_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     FDL_CK(cudaEventRecord(ev, st));
     cudaError_t e;
     while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
     }
     FDL_CK(e);
+    if (s.upst == st) s.upoff = 0;   // this stream's uploads are complete
 }
+
+struct ScratchHolder {
+    ThreadScratch *s = nullptr;
+    ThreadScratch &get() {
+        if (!s) {
+            std::lock_guard<std::mutex> lk(g_scratch_mu);
+            if (!g_scratch_free.empty()) {
+                s = g_scratch_free.back();
+                g_scratch_free.pop_back();
+            } else {
+                s = new ThreadScratch();
+            }
+        }
+        return *s;
+    }
+    ~ScratchHolder() {
+        if (!s) return;
+        if (s->upoff) {   // uploads still pending: let them land before the arena is reused
+            cudaStreamSynchronize(s->upst);
+            s->upoff = 0;
+        }
+        std::lock_guard<std::mutex> lk(g_scratch_mu);
+        g_scratch_free.push_back(s);
+    }
+};
+thread_local ScratchHolder tl_scratch;
 }  // namespace
 
-void host_wait(cudaStream_t st) { poll(st); }
+void host_wait(cudaStream_t st) { poll_on(tl_scratch.get(), st); }
 
 void readback(cudaStream_t st, std::initializer_list<ReadPiece> pieces) {
     readback(st, std::vector<ReadPiece>(pieces));
 }
 
 void readback(cudaStream_t st, const std::vector<ReadPiece> &pieces) {
+    ThreadScratch &S = tl_scratch.get();
     size_t total = 0;
     for (const ReadPiece &r : pieces) total += (r.bytes + 15) & ~(size_t)15;
-    if (total > tl_pin.cap) {
-        if (tl_pin.p) FDL_CK(cudaFreeHost(tl_pin.p));
-        tl_pin.p = nullptr;
-        tl_pin.cap = 0;
+    if (total > S.pincap) {
+        if (S.pin) FDL_CK(cudaFreeHost(S.pin));
+        S.pin = nullptr;
+        S.pincap = 0;
         const size_t cap = std::max<size_t>(total, 1 << 16);
-        FDL_CK(cudaMallocHost(&tl_pin.p, cap));
-        tl_pin.cap = cap;
+        FDL_CK(cudaMallocHost(&S.pin, cap));
+        S.pincap = cap;
     }
-    char *buf = static_cast<char *>(tl_pin.p);
+    char *buf = static_cast<char *>(S.pin);
     size_t off = 0;
     for (const ReadPiece &r : pieces) {
         if (r.bytes) FDL_CK(cudaMemcpyAsync(buf + off, r.src, r.bytes, cudaMemcpyDeviceToHost, st));
         off += (r.bytes + 15) & ~(size_t)15;
     }
-    poll(st);
+    poll_on(S, st);
     off = 0;
     for (const ReadPiece &r : pieces) {
         if (r.bytes) std::memcpy(r.dst, buf + off, r.bytes);
         off += (r.bytes + 15) & ~(size_t)15;
     }
+}
+
+// Host -> device copies of small host-computed arrays (tile counts, hub lists)
+// through the pinned upload arena: a copy from pageable memory synchronises the
+// stream first (a host round trip while the device drains), one from pinned
+// memory does not.  The arena is reused once its stream has been waited on.
+void upload(cudaStream_t st, void *dst, const void *src, size_t bytes) {
+    if (!bytes) return;
+    ThreadScratch &S = tl_scratch.get();
+    const size_t r = (bytes + 15) & ~(size_t)15;
+    if (S.upoff && (S.upst != st || S.upoff + r > S.upcap)) poll_on(S, S.upst);
+    S.upoff = S.upst == st ? S.upoff : 0;
+    if (r > S.upcap) {
+        if (S.up) FDL_CK(cudaFreeHost(S.up));
+        S.up = nullptr;
+        S.upcap = 0;
+        const size_t cap = std::max<size_t>(r, 1 << 20);
+        FDL_CK(cudaMallocHost(reinterpret_cast<void **>(&S.up), cap));
+        S.upcap = cap;
+    }
+    std::memcpy(S.up + S.upoff, src, bytes);
+    FDL_CK(cudaMemcpyAsync(dst, S.up + S.upoff, bytes, cudaMemcpyHostToDevice, st));
+    S.upoff += r;
+    S.upst = st;
 }
 
 void scan_exclusive(const int *in, int *out, int64_t n, int *total, cudaStream_t st) {

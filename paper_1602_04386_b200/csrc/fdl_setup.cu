@@ -2674,6 +2674,7 @@ __global__ void k_permute_rows(int n, const int *inv, const int *rp, const int *
     const int64_t nsub = (int64_t)gridDim.x * blockDim.x / W;
     const int64_t sub = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / W;
     double dm = 0.0;
+    int lm = 0;   // longest row (dmax[1]: rows longer than a tile need piece tiles)
     for (int64_t r0 = sub; r0 < n; r0 += nsub * kPermRows) {
         int b[kPermRows], e[kPermRows], iv[kPermRows], o[kPermRows], c[kPermRows];
         double x[kPermRows];
@@ -2706,6 +2707,7 @@ __global__ void k_permute_rows(int n, const int *inv, const int *rp, const int *
 #pragma unroll
             for (int l = 0; l < W; l++) d += __shfl_sync(smask, x[u], l, W);
             const int len = e[u] - b[u];
+            lm = max(lm, len);
             for (int k0 = W; k0 < len; k0 += W) {   // rows longer than W (uniform in the sub-warp)
                 const int k = k0 + lane;
                 double y = 0.0;
@@ -2721,8 +2723,14 @@ __global__ void k_permute_rows(int n, const int *inv, const int *rp, const int *
         }
     }
 #pragma unroll
-    for (int o2 = 16; o2; o2 >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o2));
-    if (lane_id() == 0) atomicMax(dmax, (unsigned long long)__double_as_longlong(dm));
+    for (int o2 = 16; o2; o2 >>= 1) {
+        dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o2));
+        lm = max(lm, __shfl_xor_sync(0xffffffffu, lm, o2));
+    }
+    if (lane_id() == 0) {
+        atomicMax(dmax, (unsigned long long)__double_as_longlong(dm));
+        atomicMax(dmax + 1, (unsigned long long)lm);
+    }
 }
 
 __global__ void k_gather_i32(int k, const int *src, const int *idx, int *out) {
@@ -2768,16 +2776,31 @@ __global__ void k_make_tiles(const int *rp, int s0, int s1, int ntiles, Tile *ou
 // the GS tiles of every colour in one launch: tile t belongs to the colour c
 // with ctile[c] <= t < ctile[c + 1] (binary search), then as k_make_tiles
 // (cwin[c]: window tiles of colour c; the slots after them hold hub piece tiles)
-__global__ void k_make_tiles_colours(const int *rp, const int *seg, const int *ctile, const int *cwin, int ncolors,
-                                     Tile *out) {
-    const int nt = ctile[ncolors];
+// tile offsets of the colours (ctile, ncolors + 1) and their window tile
+// counts (cwin): in the kernel parameters (inline in the launch, no copy) up
+// to kCtParam colours, else in device memory
+constexpr int kCtParam = 512;
+struct CtParam {
+    int ctile[kCtParam + 1];
+    int cwin[kCtParam];
+    __device__ int ct(int i) const { return ctile[i]; }
+    __device__ int cw(int i) const { return cwin[i]; }
+};
+struct CtPtr {
+    const int *ctile, *cwin;
+    __device__ int ct(int i) const { return ctile[i]; }
+    __device__ int cw(int i) const { return cwin[i]; }
+};
+template <class CT>
+__global__ void k_make_tiles_colours(const int *rp, const int *seg, const CT T, int ncolors, Tile *out) {
+    const int nt = T.ct(ncolors);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
         int lo = 0, hi = ncolors - 1;   // last c with ctile[c] <= t
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (ctile[mid] <= t) lo = mid; else hi = mid - 1;
+            if (T.ct(mid) <= t) lo = mid; else hi = mid - 1;
         }
-        const int c = lo, s0 = seg[c], s1 = seg[c + 1], tl = t - ctile[c], ntc = cwin[c];
+        const int c = lo, s0 = seg[c], s1 = seg[c + 1], tl = t - T.ct(c), ntc = T.cw(c);
         if (tl >= ntc) continue;
         const long long C0 = (long long)rp[s0] + s0;
         const int a = tl == 0 ? s0 : lower_bound_coord(rp, s0, s1, C0 + (long long)tl * kTileT);
@@ -2838,8 +2861,8 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     const size_t w_bytes = (size_t)std::max(g.nnz, 1) * 8 + kPadBytes;
     L.ci.alloc(ci_bytes, st);
     L.w.alloc(w_bytes, st);
-    DBuf dmax(8, st);
-    FDL_CK(cudaMemsetAsync(dmax.p, 0, 8, st));
+    DBuf dmax(16, st);   // {max d_i (bits of a non-negative double), longest row}
+    FDL_CK(cudaMemsetAsync(dmax.p, 0, 16, st));
     DISPATCH_W(avg, (k_permute_rows<W><<<sub_grid(n, W), 256, 0, st>>>(
                          n, L.inv.as<int>(), g.rp, g.ci, g.w, L.rp.as<int>(),
                          L.ci.as<int>(), L.w.as<double>(), dmax.as<unsigned long long>())));
@@ -2853,19 +2876,24 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     k_seg_fix<<<1, 1, 0, st>>>(ncolors, n, segstart.as<int>(), L.rp.as<int>(), sfix.as<int>(),
                                sfix.as<int>() + ncolors + 1);
     FDL_LAUNCH_CK();
-    // hub rows (> kTileT entries), found with the same round trip
-    DBuf hubd(16 + (size_t)std::min(n, kMaxHubs) * 16, st);
-    FDL_CK(cudaMemsetAsync(hubd.p, 0, 16, st));
-    k_hub_find<<<grid_for(n), 256, 0, st>>>(n, L.rp.as<int>(), L.perm.as<int>(), hubd.as<int>(),
-                                            reinterpret_cast<int4 *>(hubd.as<char>() + 16));
-    FDL_LAUNCH_CK();
     double dm = 0.0;
-    int nhub = 0;
+    unsigned long long lenmax = 0;
     readback(st, {{seg.data(), sfix.p, (size_t)(ncolors + 1) * 4},
                   {segnnz.data(), sfix.as<int>() + ncolors + 1, (size_t)(ncolors + 1) * 4},
                   {&dm, dmax.p, 8},
-                  {&nhub, hubd.p, 4}});
+                  {&lenmax, dmax.as<unsigned long long>() + 1, 8}});
+    // hub rows (> kTileT entries; power-law levels only): one more round trip
     std::vector<int4> hub;   // {GS row, natural id, length, colour}
+    int nhub = 0;
+    DBuf hubd;
+    if (lenmax > (unsigned long long)kTileT) {
+        hubd.alloc(16 + (size_t)std::min(n, kMaxHubs) * 16, st);
+        FDL_CK(cudaMemsetAsync(hubd.p, 0, 16, st));
+        k_hub_find<<<grid_for(n), 256, 0, st>>>(n, L.rp.as<int>(), L.perm.as<int>(), hubd.as<int>(),
+                                                reinterpret_cast<int4 *>(hubd.as<char>() + 16));
+        FDL_LAUNCH_CK();
+        readback(st, {{&nhub, hubd.p, 4}});
+    }
     if (nhub > 0 && nhub <= kMaxHubs) {
         hub.resize(nhub);
         readback(st, {{hub.data(), hubd.as<char>() + 16, (size_t)nhub * 16}});
@@ -2879,7 +2907,7 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     // tiles: GS colours, then the natural-order pass
     L.seg = seg;
     L.seg_d.alloc((size_t)(ncolors + 1) * 4, st);
-    FDL_CK(cudaMemcpyAsync(L.seg_d.p, L.seg.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
+    FDL_CK(cudaMemcpyAsync(L.seg_d.p, sfix.p, (size_t)(ncolors + 1) * 4, cudaMemcpyDeviceToDevice, st));
     // trailing colours small enough for the single-CTA GS kernel (<= kGsTailRows rows
     // and nonzeros small enough together); a whole small level qualifies
     {
@@ -2899,11 +2927,13 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
 #endif
         constexpr int kClusterColourRows = FDL_CLUSTER_COLOUR_ROWS;
         L.gs_runs.clear();
-#if FDL_GS_PIECES
-        // k_gs_pieces runs (fdl_solve.cu): colours of <= kClusterColourRows rows,
-        // or dense colours (>= kGdDenseDeg entries per row) of <= kGdMaxEntries
-        // entries; the trailing colours of a run with <= kGdSingleEntries entries
-        // each go to one CTA (no cluster barrier)
+        // kinds: 0 = grid tile pass of one colour; 1 / 2 = k_gs_multi on a
+        // cluster / one CTA; 3 / 4 = k_gs_pieces on a cluster / one CTA.
+        // k_gs_pieces runs (fdl_solve.cu), on dense levels (>= kGdDenseDeg
+        // entries per row, where they pay off: R-MAT's 150-500 colours per level;
+        // on sparse levels k_gs_multi measured the same and needs no setup):
+        // colours of <= kClusterColourRows rows, or of <= kGdMaxEntries entries;
+        // the trailing colours of a run of at most one piece per warp go to one CTA.
 #ifndef FDL_GD_MAX_ENTRIES
 #define FDL_GD_MAX_ENTRIES 262144
 #endif
@@ -2913,7 +2943,6 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
         constexpr long long kGdMaxEntries = FDL_GD_MAX_ENTRIES, kGdSingleEntries = FDL_GD_SINGLE_ENTRIES;
         constexpr long long kGdDenseDeg = 16;
         constexpr int kGdSinglePieces = 16;   // k_gs_pieces warps per CTA
-        (void)c0;
         // eligibility and the one-CTA choice from bounds on the piece counts
         // (no readback): pieces(c) <= rows + entries / kGdPiece + 1, and a part
         // pair (two parts per CTA of an 8-CTA cluster) holds at most an eighth
@@ -2924,46 +2953,47 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
         auto elig = [&](int c) {
             const long long rows = rows_of(c), ent = ent_of(c);
             if (rows == 0) return true;
-            if (!(rows <= kClusterColourRows || (ent <= kGdMaxEntries && ent >= kGdDenseDeg * rows)))
-                return false;
+            if (!(rows <= kClusterColourRows || ent <= kGdMaxEntries)) return false;
             return pbound(c) / 8 + ent / kGdPiece + 2 <= kGdSlotCapHost;
         };
         auto single = [&](int c) { return ent_of(c) <= kGdSingleEntries && pbound(c) <= kGdSinglePieces; };
         std::vector<char> use(ncolors, 0);
         bool any = false;
-        for (int c = 0; c < ncolors; c++) {
-            use[c] = rows_of(c) > 0 && elig(c);
-            any |= use[c] != 0;
-        }
-        if (any) build_gs_pieces(L, seg, segnnz, use, st);
-        for (int c = 0; c < ncolors;) {
-            if (!any || !elig(c)) {
-                L.gs_runs.insert(L.gs_runs.end(), {c, c + 1, 0});
-                c++;
-                continue;
+        if (FDL_GS_PIECES && avg >= (double)kGdDenseDeg)
+            for (int c = 0; c < ncolors; c++) {
+                use[c] = rows_of(c) > 0 && elig(c);
+                any |= use[c] != 0;
             }
-            int e = c;
-            while (e < ncolors && elig(e) && e - c < kGdMaxRunColours) e++;
-            int t = e;
-            while (t > c && single(t - 1)) t--;
-            if (t > c) L.gs_runs.insert(L.gs_runs.end(), {c, t, 1});
-            if (e > t) L.gs_runs.insert(L.gs_runs.end(), {t, e, 2});
-            c = e;
-        }
-#else
-        for (int c = 0; c < c0;) {
-            int e = c;
-            while (e < c0 && seg[e + 1] - seg[e] <= kClusterColourRows) e++;
-            if (e > c) {
-                L.gs_runs.insert(L.gs_runs.end(), {c, e, 1});
+        if (any) {
+            build_gs_pieces(L, seg, segnnz, use, st);
+            for (int c = 0; c < ncolors;) {
+                if (!elig(c)) {
+                    L.gs_runs.insert(L.gs_runs.end(), {c, c + 1, 0});
+                    c++;
+                    continue;
+                }
+                int e = c;
+                while (e < ncolors && elig(e) && e - c < kGdMaxRunColours) e++;
+                int t = e;
+                while (t > c && single(t - 1)) t--;
+                if (t > c) L.gs_runs.insert(L.gs_runs.end(), {c, t, 3});
+                if (e > t) L.gs_runs.insert(L.gs_runs.end(), {t, e, 4});
                 c = e;
-            } else {
-                L.gs_runs.insert(L.gs_runs.end(), {c, c + 1, 0});
-                c++;
             }
+        } else {
+            for (int c = 0; c < c0;) {
+                int e = c;
+                while (e < c0 && seg[e + 1] - seg[e] <= kClusterColourRows) e++;
+                if (e > c) {
+                    L.gs_runs.insert(L.gs_runs.end(), {c, e, 1});
+                    c = e;
+                } else {
+                    L.gs_runs.insert(L.gs_runs.end(), {c, c + 1, 0});
+                    c++;
+                }
+            }
+            if (c0 < ncolors) L.gs_runs.insert(L.gs_runs.end(), {c0, ncolors, 2});
         }
-        if (c0 < ncolors) L.gs_runs.insert(L.gs_runs.end(), {c0, ncolors, 2});
-#endif
     }
     // tiles of every pass: colour c's window tiles then its hub piece tiles,
     // the natural pass likewise (hub rows: pieces of kTileT entries, a tile each)
@@ -2986,14 +3016,21 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
     cnt[ncolors] = tiles_for((long long)g.nnz + n);
     nt += cnt[ncolors] + hpieces[ncolors];
     L.ntiles = nt;
-    L.ctile_d.alloc((size_t)(ncolors + 1) * 4, st);
-    FDL_CK(cudaMemcpyAsync(L.ctile_d.p, L.ctile.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
     L.tiles.alloc((size_t)nt * sizeof(Tile), st);
-    if (L.ctile[ncolors] > 0) {
-        DBuf cwin((size_t)ncolors * 4, st);
-        FDL_CK(cudaMemcpyAsync(cwin.p, cnt.data(), (size_t)ncolors * 4, cudaMemcpyHostToDevice, st));
-        k_make_tiles_colours<<<grid_for(L.ctile[ncolors]), 256, 0, st>>>(
-            L.rp.as<int>(), L.seg_d.as<int>(), L.ctile_d.as<int>(), cwin.as<int>(), ncolors, L.tiles.as<Tile>());
+    if (L.ctile[ncolors] > 0 && ncolors <= kCtParam) {
+        CtParam T;
+        std::copy(L.ctile.begin(), L.ctile.end(), T.ctile);
+        std::copy(cnt.begin(), cnt.begin() + ncolors, T.cwin);
+        k_make_tiles_colours<CtParam><<<grid_for(L.ctile[ncolors]), 256, 0, st>>>(
+            L.rp.as<int>(), L.seg_d.as<int>(), T, ncolors, L.tiles.as<Tile>());
+        FDL_LAUNCH_CK();
+    } else if (L.ctile[ncolors] > 0) {
+        DBuf ctd((size_t)(2 * ncolors + 1) * 4, st);
+        upload(st, ctd.p, L.ctile.data(), (size_t)(ncolors + 1) * 4);
+        upload(st, ctd.as<int>() + ncolors + 1, cnt.data(), (size_t)ncolors * 4);
+        k_make_tiles_colours<CtPtr><<<grid_for(L.ctile[ncolors]), 256, 0, st>>>(
+            L.rp.as<int>(), L.seg_d.as<int>(), CtPtr{ctd.as<int>(), ctd.as<int>() + ncolors + 1}, ncolors,
+            L.tiles.as<Tile>());
         FDL_LAUNCH_CK();
     }
     k_make_tiles<<<grid_for(cnt[ncolors]), 256, 0, st>>>(g.rp, 0, n, cnt[ncolors],
@@ -3029,14 +3066,14 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
         }
         L.hoff[ncolors + 1] = (int)all.size();
         L.hubs.alloc(all.size() * sizeof(int4), st);
-        FDL_CK(cudaMemcpyAsync(L.hubs.p, all.data(), all.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+        upload(st, L.hubs.p, all.data(), all.size() * sizeof(int4));
         L.hub_part.alloc((size_t)maxpass * 16, st);
         const int k = (int)pdst.size();
         DBuf pd((size_t)k * 4, st), pt((size_t)k * sizeof(Tile), st);
-        FDL_CK(cudaMemcpyAsync(pd.p, pdst.data(), (size_t)k * 4, cudaMemcpyHostToDevice, st));
-        FDL_CK(cudaMemcpyAsync(pt.p, ptile.data(), (size_t)k * sizeof(Tile), cudaMemcpyHostToDevice, st));
+        upload(st, pd.p, pdst.data(), (size_t)k * 4);
+        upload(st, pt.p, ptile.data(), (size_t)k * sizeof(Tile));
         k_scatter_tiles<<<grid_for(k), 256, 0, st>>>(k, pd.as<int>(), pt.as<Tile>(), L.tiles.as<Tile>());
-        FDL_LAUNCH_CK();   // (pageable sources: staged by the time the copies return)
+        FDL_LAUNCH_CK();
     }
 }
 

@@ -58,6 +58,18 @@ constexpr int kPassWarps = kPassThreads / 32;
 #ifndef FDL_GS4_MINB
 #define FDL_GS4_MINB 7
 #endif
+#ifndef FDL_PI_MINB
+#define FDL_PI_MINB 8
+#endif
+#ifndef FDL_PI_MINB_SMALL
+#define FDL_PI_MINB_SMALL 7
+#endif
+#ifndef FDL_PI_BIG_ROWS
+#define FDL_PI_BIG_ROWS (48 << 20)
+#endif
+#ifndef FDL_RQ_MINB
+#define FDL_RQ_MINB 7
+#endif
 #ifndef FDL_GS4_MAXDEG
 #define FDL_GS4_MAXDEG 8.0
 #endif
@@ -67,7 +79,11 @@ template <int OP, int CH> struct PassTune {
     // (72 registers): measured on the 8192^2 grid, level-0 sweep 1.23 ms with
     // 8 CTAs, 1.15 / 1.05 / 1.01 ms with 5 / 6 / 7; levels 1-4 gain 2-10 % over
     // the chunk-8 pass; the power step prefers 8 CTAs (tools/gpu_levels_variants.sh)
+    // the power step: 8 CTAs per SM on the largest levels, 7 below (M != 0);
+    // the Rayleigh pass 7 (measured: 0.94 -> 0.86 ms on the 8192^2 grid's level 0)
     static constexpr int min_blocks = (OP == 0 && chunk == 4) ? FDL_GS4_MINB
+                                      : (OP == 1 && chunk == 4) ? FDL_PI_MINB
+                                      : (OP == 2 && chunk == 4) ? FDL_RQ_MINB
                                       : ((chunk == 4 && OP != 2) ? 4 : 3) * FDL_PASS_MINB / 4;
 };
 constexpr int kNumStats = 3;
@@ -613,8 +629,8 @@ __device__ __forceinline__ Scal load_scal(const PassArgs &a) {
     return sc;
 }
 
-template <int OP, int CH = 0, int SW = 0, bool HUB = false>
-__global__ void __launch_bounds__(kPassThreads, PassTune<OP, CH>::min_blocks) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
+template <int OP, int CH = 0, int SW = 0, bool HUB = false, int M = 0>
+__global__ void __launch_bounds__(kPassThreads, M ? M : PassTune<OP, CH>::min_blocks) k_tilepass(const Tile *__restrict__ tiles, int ntiles,
                                                            CsrView L, PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem &S = *reinterpret_cast<PassSmem *>(smem_raw);
@@ -1124,11 +1140,12 @@ __global__ void __launch_bounds__(kGdThreads, 1) k_gs_pieces(GdArgs a) {
 
 // ---- setup side: pieces and parts of a level (called by build_layout)
 // groups of 32 consecutive rows of one colour; gstart[c] = first group of colour c
+__device__ __forceinline__ int div_up_d(int a, int b) { return (a + b - 1) / b; }
 __device__ __forceinline__ int gd_group_colour(const int *gstart, int ncolors, int g) {
     int lo = 0, hi = ncolors;   // largest c with gstart[c] <= g
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (__ldg(gstart + mid) <= g) lo = mid;
+        if (gstart[mid] <= g) lo = mid;   // (global or shared memory)
         else hi = mid;
     }
     return lo;
@@ -1147,28 +1164,31 @@ __global__ void k_gd_count(const int *rp, const int *seg, const int *gstart, int
         gcnt[g] = maxlen <= kGdShort ? 1 : cnt;
     }
 }
+// the pieces of the group of rows [r0, r1) from position p
+__device__ void gd_write_group(const int *rp, int r0, int r1, int p, int4 *pieces) {
+    int maxlen = 0;
+    for (int r = r0; r < r1; r++) maxlen = max(maxlen, rp[r + 1] - rp[r]);
+    if (maxlen <= kGdShort) {
+        pieces[p] = make_int4(r0, r1, rp[r0], rp[r1]);
+        return;
+    }
+    for (int r = r0; r < r1; r++) {
+        const int kb = rp[r], ke = rp[r + 1], len = ke - kb;
+        if (len <= kGdPiece) {
+            pieces[p++] = make_int4(r, -1, kb, ke);
+            continue;
+        }
+        const int np = (len + kGdPiece - 1) / kGdPiece;
+        for (int i = 0; i < np; i++)
+            pieces[p++] = make_int4(r, i == 0 ? -(np + 1) : -2, kb + i * kGdPiece, min(kb + (i + 1) * kGdPiece, ke));
+    }
+}
 __global__ void k_gd_write(const int *rp, const int *seg, const int *gstart, int ncolors, int ngroups,
                            const int *goff, int4 *pieces) {
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
         const int c = gd_group_colour(gstart, ncolors, g);
         const int r0 = seg[c] + (g - gstart[c]) * kGdGroup, r1 = min(r0 + kGdGroup, seg[c + 1]);
-        int p = goff[g];
-        int maxlen = 0;
-        for (int r = r0; r < r1; r++) maxlen = max(maxlen, rp[r + 1] - rp[r]);
-        if (maxlen <= kGdShort) {
-            pieces[p] = make_int4(r0, r1, rp[r0], rp[r1]);
-            continue;
-        }
-        for (int r = r0; r < r1; r++) {
-            const int kb = rp[r], ke = rp[r + 1], len = ke - kb;
-            if (len <= kGdPiece) {
-                pieces[p++] = make_int4(r, -1, kb, ke);
-                continue;
-            }
-            const int np = (len + kGdPiece - 1) / kGdPiece;
-            for (int i = 0; i < np; i++)
-                pieces[p++] = make_int4(r, i == 0 ? -(np + 1) : -2, kb + i * kGdPiece, min(kb + (i + 1) * kGdPiece, ke));
-        }
+        gd_write_group(rp, r0, r1, goff[g], pieces);
     }
 }
 // parts: kGdParts + 1 piece indices per colour, cut at the first piece of a row
@@ -1182,6 +1202,88 @@ __global__ void k_gd_parts(const int *gstart, const int *goff, const int4 *piece
     parts[t] = p;
 }
 
+// The same in ONE launch for small levels (<= kGdSmallGroups groups, <= 1024
+// colours): group starts of the used colours, counts, exclusive scans and
+// the pieces / parts, in shared memory (the small levels' setup is launch-bound)
+constexpr int kGdSmallGroups = 8192;
+struct GdUse {
+    unsigned bits[32];
+};
+// in-place exclusive scan of a[0, n) by the whole CTA (blockDim.x == 1024); returns the total
+__device__ int cta_exclusive_scan(int *a, int n) {
+    __shared__ int s_w[32];
+    const int per = (n + 1023) / 1024, t = threadIdx.x, b = t * per, e = min(b + per, n);
+    int sum = 0;
+    for (int i = b; i < e; i++) sum += a[i];
+    int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((t & 31) >= o) x += y;
+    }
+    if ((t & 31) == 31) s_w[t >> 5] = x;
+    __syncthreads();
+    if (t < 32) {
+        int w = s_w[t];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (t >= o) w += y;
+        }
+        s_w[t] = w;
+    }
+    __syncthreads();
+    int run = x - sum + ((t >> 5) ? s_w[(t >> 5) - 1] : 0);
+    const int total = s_w[31];
+    for (int i = b; i < e; i++) {
+        const int v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    __syncthreads();
+    return total;
+}
+__global__ void __launch_bounds__(1024) k_gd_small(const int *rp, const int *seg, GdUse use, int ncolors,
+                                                   int4 *pieces, int *parts) {
+    __shared__ int s_gs[1025];
+    __shared__ int s_go[kGdSmallGroups + 1];
+    const int t = threadIdx.x;
+    for (int c = t; c < ncolors; c += 1024)
+        s_gs[c] = ((use.bits[c >> 5] >> (c & 31)) & 1u) ? div_up_d(seg[c + 1] - seg[c], kGdGroup) : 0;
+    __syncthreads();
+    const int ng = cta_exclusive_scan(s_gs, ncolors);
+    if (t == 0) s_gs[ncolors] = ng;
+    __syncthreads();
+    for (int g = t; g < ng; g += 1024) {
+        const int c = gd_group_colour(s_gs, ncolors, g);
+        const int r0 = seg[c] + (g - s_gs[c]) * kGdGroup, r1 = min(r0 + kGdGroup, seg[c + 1]);
+        int cnt = 0, maxlen = 0;
+        for (int r = r0; r < r1; r++) {
+            const int len = rp[r + 1] - rp[r];
+            maxlen = max(maxlen, len);
+            cnt += len > kGdPiece ? (len + kGdPiece - 1) / kGdPiece : 1;
+        }
+        s_go[g] = maxlen <= kGdShort ? 1 : cnt;
+    }
+    __syncthreads();
+    const int np = cta_exclusive_scan(s_go, ng);
+    if (t == 0) s_go[ng] = np;
+    __syncthreads();
+    for (int g = t; g < ng; g += 1024) {
+        const int c = gd_group_colour(s_gs, ncolors, g);
+        const int r0 = seg[c] + (g - s_gs[c]) * kGdGroup, r1 = min(r0 + kGdGroup, seg[c + 1]);
+        gd_write_group(rp, r0, r1, s_go[g], pieces);
+    }
+    __syncthreads();   // the parts read the pieces' kinds (global writes of this CTA)
+    for (int i = t; i < ncolors * (kGdParts + 1); i += 1024) {
+        const int c = i / (kGdParts + 1), k = i % (kGdParts + 1);
+        const int p0 = s_go[s_gs[c]], p1 = s_go[s_gs[c + 1]];
+        int p = p0 + (int)((long long)k * (p1 - p0) / kGdParts);
+        while (p < p1 && pieces[p].y == -2) p++;
+        parts[i] = p;
+    }
+}
+
 void build_gs_pieces(Level &L, const std::vector<int> &seg, const std::vector<int> &segnnz,
                      const std::vector<char> &use, cudaStream_t st) {
     const int ncolors = L.ncolors;
@@ -1193,8 +1295,19 @@ void build_gs_pieces(Level &L, const std::vector<int> &seg, const std::vector<in
         if (use[c]) bound += rows + (segnnz[c + 1] - segnnz[c]) / kGdPiece + 1;   // >= pieces of colour c
     }
     const int ngroups = gstart[ncolors];
+    if (ngroups <= kGdSmallGroups && ncolors <= 1024) {
+        GdUse u{};
+        for (int c = 0; c < ncolors; c++)
+            if (use[c]) u.bits[c >> 5] |= 1u << (c & 31);
+        L.gd_pieces.alloc((size_t)bound * sizeof(int4), st);
+        L.gd_parts.alloc((size_t)ncolors * (kGdParts + 1) * 4, st);
+        k_gd_small<<<1, 1024, 0, st>>>(L.rp.as<int>(), L.seg_d.as<int>(), u, ncolors, L.gd_pieces.as<int4>(),
+                                       L.gd_parts.as<int>());
+        FDL_LAUNCH_CK();
+        return;
+    }
     DBuf gs_d((size_t)(ncolors + 1) * 4, st);
-    FDL_CK(cudaMemcpyAsync(gs_d.p, gstart.data(), (size_t)(ncolors + 1) * 4, cudaMemcpyHostToDevice, st));
+    upload(st, gs_d.p, gstart.data(), (size_t)(ncolors + 1) * 4);
     DBuf gcnt((size_t)(ngroups + 1) * 4, st), goff((size_t)(ngroups + 1) * 4, st);
     L.gd_pieces.alloc((size_t)bound * sizeof(int4), st);
     if (ngroups > 0) {
@@ -1523,7 +1636,7 @@ static void launch_gs_pieces(cudaStream_t st, const Level &L, int c0, int c1, in
 #define FDL_DENSE_ROW_DEG 7.0
 #endif
 constexpr double kDenseRowDeg = FDL_DENSE_ROW_DEG;   // rows per tile few enough for sub-warp rows
-static DeviceCache g_pass_grid[4] = {};   // per OP (3: the GS chunk-4 variant), per device
+static DeviceCache g_pass_grid[5] = {};   // per OP (3: the GS chunk-4 variant, 4: the power step below FDL_PI_BIG_ROWS), per device
 static int pass_grid(int op) { return g_pass_grid[op][current_device()].load(); }
 
 // A tile pass as a programmatic dependent launch (FDL_PDL): its CTAs may start
@@ -1585,6 +1698,9 @@ struct Enq {
             launch_pass(k_tilepass<OP_GS, 4>, grid, st, tiles, nt, v, a);
         } else if (L.nnz >= kDenseRowDeg * (double)L.n) {
             launch_pass(k_tilepass<OP, 0, 4>, grid, st, tiles, nt, v, a);
+        } else if (OP == OP_PI && L.n < FDL_PI_BIG_ROWS) {
+            grid = std::min(nt, pass_grid(4));
+            launch_pass(k_tilepass<OP_PI, 0, 0, false, FDL_PI_MINB_SMALL>, grid, st, tiles, nt, v, a);
         } else {
             launch_pass(k_tilepass<OP>, grid, st, tiles, nt, v, a);
         }
@@ -1614,8 +1730,8 @@ struct Enq {
             a.out_stat = out_slot;
             a.stat_mode = mode;
             pass<OP_GS>(L, L.ctile[cb], L.ctile[cb + 1], a, cb);
-        } else if (FDL_GS_PIECES) {
-            launch_gs_pieces(st, L, cb, ce, sweeps, x, out_slot, mode, kind == 1);
+        } else if (kind >= 3) {
+            launch_gs_pieces(st, L, cb, ce, sweeps, x, out_slot, mode, kind == 3);
             launches++;
         } else if (kind == 1) {
             launch_gs_cluster(st, v, L.seg_d.as<int>(), cb, ce, sweeps, x, out_slot, mode, L.n);
@@ -1754,8 +1870,12 @@ int rowpass_grid() {
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI, 0, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_RQ, 0, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 
-    int b3 = 0;
+    FDL_CK(cudaFuncSetAttribute(k_tilepass<OP_PI, 0, 0, false, FDL_PI_MINB_SMALL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int b3 = 0, b4 = 0;
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_tilepass<OP_GS, 4>, kPassThreads, smem));
+    FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_tilepass<OP_PI, 0, 0, false, FDL_PI_MINB_SMALL>,
+                                                         kPassThreads, smem));
     int b0 = 0, b1 = 0, b2 = 0;
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_tilepass<OP_GS>, kPassThreads, smem));
     FDL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_tilepass<OP_PI>, kPassThreads, smem));
@@ -1767,7 +1887,8 @@ int rowpass_grid() {
     g_pass_grid[OP_PI][cdev].store(sms * std::max(1, b1));
     g_pass_grid[OP_RQ][cdev].store(sms * std::max(1, b2));
     g_pass_grid[3][cdev].store(sms * std::max(1, b3));
-    const int all = sms * std::max(std::max(1, b3), std::max(b0, std::max(b1, b2)));
+    g_pass_grid[4][cdev].store(sms * std::max(1, b4));
+    const int all = sms * std::max(std::max(std::max(1, b3), b4), std::max(b0, std::max(b1, b2)));
     cache[cdev].store(all);
     return all;
 }
