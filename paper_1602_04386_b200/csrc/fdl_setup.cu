@@ -2664,7 +2664,10 @@ __global__ void k_inv_and_deg(int n, const int *perm, const int *rp, int *inv, i
 // inv gathers streaming; the writes form one sequential stream per colour.
 // The sub-warp handles kPermRows rows per step with all their loads in flight,
 // and also yields max_i d_i (Gershgorin shift, R5) with every d_i summed in
-// stored (= natural ascending) order, as the oracle.
+// stored (= natural ascending) order, as the oracle.  Rows longer than a tile
+// (hubs) are left to k_hub_permute: a sub-warp walking a 30000-entry row 32
+// entries at a time, with a 32-step ordered fold per chunk, took ~1 ms per hub
+// (R-MAT level 1: 9 ms of layout).
 constexpr int kPermRows = 4;
 template <int W>
 __global__ void k_permute_rows(int n, const int *inv, const int *rp, const int *ci, const double *w,
@@ -2708,6 +2711,7 @@ __global__ void k_permute_rows(int n, const int *inv, const int *rp, const int *
             for (int l = 0; l < W; l++) d += __shfl_sync(smask, x[u], l, W);
             const int len = e[u] - b[u];
             lm = max(lm, len);
+            if (len > kTileT) continue;   // a hub row: k_hub_permute (its first W entries are copied)
             for (int k0 = W; k0 < len; k0 += W) {   // rows longer than W (uniform in the sub-warp)
                 const int k = k0 + lane;
                 double y = 0.0;
@@ -2820,6 +2824,46 @@ __global__ void k_hub_find(int n, const int *rp, const int *perm, int *count, in
         }
     }
 }
+// hub rows of the GS layout (list from k_hub_find: {GS row, natural id, length}):
+// a CTA per row copies entries W.. (k_permute_rows copied the first W) with
+// renumbered columns, 4 per thread in flight; thread 0 folds d_v over the whole
+// row in stored order (the oracle's order) while the others copy
+__global__ void __launch_bounds__(256) k_hub_permute(int nh, const int4 *hubs, int W, const int *inv, const int *rp,
+                                                     const int *ci, const double *w, const int *rpp, int *cip,
+                                                     double *wp, unsigned long long *dmax) {
+    for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int4 hb = hubs[h];
+        const int b = rp[hb.y], len = hb.z, o = rpp[hb.x];
+        if (threadIdx.x == 0) {
+            double d = 0.0;
+            for (int k0 = 0; k0 < len; k0 += 8) {
+                double y[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) y[i] = k0 + i < len ? w[b + k0 + i] : 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    if (k0 + i < len) d += y[i];
+            }
+            atomicMax(dmax, (unsigned long long)__double_as_longlong(d));
+        }
+        for (int k0 = W + threadIdx.x; k0 < len; k0 += 4 * blockDim.x) {
+            int c[4];
+            double y[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int k = k0 + u * blockDim.x;
+                c[u] = k < len ? ci[b + k] : -1;
+                y[u] = k < len ? w[b + k] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (c[u] >= 0) {
+                    cip[o + k0 + u * blockDim.x] = inv[c[u]];
+                    wp[o + k0 + u * blockDim.x] = y[u];
+                }
+        }
+    }
+}
 __global__ void k_scatter_tiles(int k, const int *dst, const Tile *src, Tile *tiles) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) tiles[dst[i]] = src[i];
 }
@@ -2893,6 +2937,14 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
                                                 reinterpret_cast<int4 *>(hubd.as<char>() + 16));
         FDL_LAUNCH_CK();
         readback(st, {{&nhub, hubd.p, 4}});
+        FDL_REQUIRE(nhub <= kMaxHubs, FIEDLER_ERR_INTERNAL, "too many rows longer than a tile");
+        // the hub rows' entries past the first W and their degrees
+        const int W = avg <= 4.5 ? 4 : avg <= 9 ? 8 : avg <= 18 ? 16 : 32;   // DISPATCH_W's sub-warp
+        k_hub_permute<<<std::min(nhub, kNumSMs * 8), 256, 0, st>>>(
+            nhub, reinterpret_cast<const int4 *>(hubd.as<char>() + 16), W, L.inv.as<int>(), g.rp, g.ci, g.w,
+            L.rp.as<int>(), L.ci.as<int>(), L.w.as<double>(), dmax.as<unsigned long long>());
+        FDL_LAUNCH_CK();
+        readback(st, {{&dm, dmax.p, 8}});
     }
     if (nhub > 0 && nhub <= kMaxHubs) {
         hub.resize(nhub);
