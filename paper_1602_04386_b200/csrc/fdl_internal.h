@@ -110,8 +110,9 @@ struct Level {
 // every handle cost up to tens of milliseconds now and then (driver work).
 struct StreamSet {
     cudaStream_t stream = nullptr;    // the handle's stream
-    cudaStream_t stream2 = nullptr;   // setup: colourings beside the coarsening chain
-    cudaEvent_t ev[4] = {};           // 0: join, 1: pattern, 2: setup scratch, 3: spare (no timing)
+    cudaStream_t stream2 = nullptr;   // setup: colourings beside the coarsening chain (even levels)
+    cudaStream_t stream3 = nullptr;   // setup: colourings of the odd levels
+    cudaEvent_t ev[4] = {};           // 0: join, 1: pattern, 2: setup scratch, 3: second join (no timing)
     cudaEvent_t tev[2] = {};          // timing events of create / solve
 };
 
@@ -121,6 +122,7 @@ struct Handle {
     cudaStream_t stream = nullptr;
     bool own_stream = false;          // always true: the handle owns `stream` (fdl_api.cu)
     cudaStream_t stream2 = nullptr;   // setup: colourings overlapped with the coarsening chain
+    cudaStream_t stream3 = nullptr;   // setup: the same for the odd levels
     cudaEvent_t ev_pattern = nullptr; // host input: level-0 pattern (rp, ci) on the device
     cudaEvent_t ev_join = nullptr;    // joins a caller's stream with `stream` (fdl_api.cu StreamJoin)
     SmallArena arena;                 // small buffers of the create (fdl_common.cuh); freed last

@@ -3246,9 +3246,10 @@ struct LevelFeed {
     }
 };
 
+// levels first, first + stride, ... (one helper thread and stream per residue)
 static void colour_and_layout(Handle &h, std::vector<NatGraph> &graphs, std::vector<cudaEvent_t> &lev_ev,
-                              LevelFeed &feed, PhaseTimes &pt, cudaStream_t sb) {
-    for (int ell = 0; feed.wait_for(ell); ell++) {
+                              LevelFeed &feed, PhaseTimes &pt, cudaStream_t sb, int first, int stride) {
+    for (int ell = first; feed.wait_for(ell); ell += stride) {
         Level &L = h.levels[ell];
         NatGraph &g = graphs[ell];
         // the colouring needs the pattern (level 0 from host input: its event,
@@ -3288,20 +3289,26 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
     graphs.reserve((size_t)maxl + 1);
     std::vector<cudaEvent_t> lev_ev((size_t)maxl + 1, nullptr);
     LevelFeed feed;
-    std::exception_ptr side_err;
-    long long side_launches = 0;
-    std::thread side;
-    auto run_side = [&] {
+    // two helper threads colour and lay out the even / odd levels on the two
+    // side streams, so a level's colouring starts as soon as the level exists
+    // even while the previous level's layout still runs (serial: one pass on st)
+    constexpr int kSides = 2;
+    cudaStream_t sides[kSides] = {sb, serial ? sb : h.stream3};
+    std::exception_ptr side_err[kSides];
+    long long side_launches[kSides] = {0, 0};
+    std::thread side[kSides];
+    auto run_side = [&](int k, int first, int stride) {
         const long long l0 = g_launch_count;
         try {
             FDL_CK(cudaSetDevice(h.device));
-            colour_and_layout(h, graphs, lev_ev, feed, pt, sb);
+            colour_and_layout(h, graphs, lev_ev, feed, pt, sides[k], first, stride);
         } catch (...) {
-            side_err = std::current_exception();
+            side_err[k] = std::current_exception();
         }
-        side_launches = g_launch_count - l0;
+        side_launches[k] = g_launch_count - l0;
     };
-    if (!serial) side = std::thread(run_side);
+    if (!serial)
+        for (int k = 0; k < kSides; k++) side[k] = std::thread(run_side, k, k, kSides);
     try {
         graphs.emplace_back(std::move(g0));
         for (int ell = 0;; ell++) {
@@ -3334,26 +3341,34 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
         }
     } catch (...) {
         feed.finish();
-        if (side.joinable()) side.join();
-        cudaStreamSynchronize(sb);
+        for (int k = 0; k < kSides; k++) {
+            if (side[k].joinable()) side[k].join();
+            cudaStreamSynchronize(sides[k]);
+        }
         for (cudaEvent_t e : lev_ev)
             if (e) cudaEventDestroy(e);
         throw;
     }
     feed.finish();
-    if (serial) run_side();
-    else side.join();
-    g_launch_count += serial ? 0 : side_launches;
+    if (serial) {
+        run_side(0, 0, 1);
+    } else {
+        for (int k = 0; k < kSides; k++) side[k].join();
+        for (int k = 0; k < kSides; k++) g_launch_count += side_launches[k];
+    }
     for (cudaEvent_t e : lev_ev)
         if (e) cudaEventDestroy(e);
-    if (side_err) {
-        cudaStreamSynchronize(sb);
-        std::rethrow_exception(side_err);
-    }
+    for (int k = 0; k < kSides; k++)
+        if (side_err[k]) {
+            for (int j = 0; j < kSides; j++) cudaStreamSynchronize(sides[j]);
+            std::rethrow_exception(side_err[k]);
+        }
     // the main stream continues after the colourings and layouts
-    cudaEvent_t ev = h.set.ev[2];
-    FDL_CK(cudaEventRecord(ev, sb));
-    FDL_CK(cudaStreamWaitEvent(st, ev, 0));
+    const cudaEvent_t jev[kSides] = {h.set.ev[2], h.set.ev[3]};
+    for (int k = 0; k < kSides; k++) {
+        FDL_CK(cudaEventRecord(jev[k], sides[k]));
+        FDL_CK(cudaStreamWaitEvent(st, jev[k], 0));
+    }
     trace_mark(st, "colourings and layouts joined");
     const int J = (int)h.levels.size() - 1;
     for (int ell = 0; ell <= J; ell++) take_natural(graphs[ell], h.levels[ell], st);
