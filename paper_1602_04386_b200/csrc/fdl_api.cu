@@ -65,8 +65,10 @@ static StreamSet take_stream_set(int dev) {
         FDL_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         const int pr = FDL_STREAM2_PRIO > 0 ? hi : FDL_STREAM2_PRIO < 0 ? lo : 0;
         FDL_CK(cudaStreamCreateWithPriority(&s.stream2, cudaStreamNonBlocking, pr));
-        FDL_CK(cudaStreamCreateWithPriority(&s.stream3, cudaStreamNonBlocking, pr));
+        s.side[0] = s.stream2;
+        for (int k = 1; k < kSides; k++) FDL_CK(cudaStreamCreateWithPriority(&s.side[k], cudaStreamNonBlocking, pr));
     }
+    for (int k = 0; k < kSides; k++) FDL_CK(cudaEventCreateWithFlags(&s.sev[k], cudaEventDisableTiming));
     for (cudaEvent_t &e : s.ev) FDL_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (cudaEvent_t &e : s.tev) FDL_CK(cudaEventCreate(&e));
     return s;
@@ -83,9 +85,8 @@ Handle::~Handle() {
     // the buffers are freed stream-ordered on the streams that allocated them
     // (the setup's side streams are idle): drain the handle's work first, so no
     // buffer goes back to the pool while a solve still reads it
-    const bool ok = (!stream || cudaStreamSynchronize(stream) == cudaSuccess) &&
-                    (!stream2 || cudaStreamSynchronize(stream2) == cudaSuccess) &&
-                    (!stream3 || cudaStreamSynchronize(stream3) == cudaSuccess);
+    bool ok = !stream || cudaStreamSynchronize(stream) == cudaSuccess;
+    for (int k = 0; k < kSides; k++) ok = ok && (!set.side[k] || cudaStreamSynchronize(set.side[k]) == cudaSuccess);
     levels.clear();
     xa.release(); xb.release(); vnat.release(); scal.release();
     partials.release(); counter.release(); result.release();
@@ -267,7 +268,6 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     h->set = take_stream_set(o.device);
     h->stream = h->set.stream;
     h->stream2 = h->set.stream2;
-    h->stream3 = h->set.stream3;
     h->ev_join = h->set.ev[0];
     h->own_stream = true;
     cudaStream_t st = h->stream;

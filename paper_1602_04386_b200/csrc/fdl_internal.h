@@ -108,11 +108,19 @@ struct Level {
 // The streams and events of a handle come from a per-device pool and go back
 // to it at fiedler_destroy (fdl_api.cu): creating and destroying them for
 // every handle cost up to tens of milliseconds now and then (driver work).
+// helper threads / side streams of the setup (colourings and layouts of the
+// levels = k mod kSides on side stream k; build knob FDL_SIDES)
+#ifndef FDL_SIDES
+#define FDL_SIDES 2
+#endif
+constexpr int kMaxSides = 4;
+constexpr int kSides = FDL_SIDES < 1 ? 1 : FDL_SIDES > kMaxSides ? kMaxSides : FDL_SIDES;
 struct StreamSet {
     cudaStream_t stream = nullptr;    // the handle's stream
-    cudaStream_t stream2 = nullptr;   // setup: colourings beside the coarsening chain (even levels)
-    cudaStream_t stream3 = nullptr;   // setup: colourings of the odd levels
-    cudaEvent_t ev[4] = {};           // 0: join, 1: pattern, 2: setup scratch, 3: second join (no timing)
+    cudaStream_t stream2 = nullptr;   // setup: colourings beside the coarsening chain (levels = 0 mod kSides)
+    cudaStream_t side[kMaxSides] = {};   // setup: side[0] = stream2, side[k] the levels = k mod kSides
+    cudaEvent_t ev[4] = {};           // 0: join, 1: pattern, 2: setup scratch, 3: spare (no timing)
+    cudaEvent_t sev[kMaxSides] = {};  // joins of the side streams
     cudaEvent_t tev[2] = {};          // timing events of create / solve
 };
 
@@ -122,7 +130,6 @@ struct Handle {
     cudaStream_t stream = nullptr;
     bool own_stream = false;          // always true: the handle owns `stream` (fdl_api.cu)
     cudaStream_t stream2 = nullptr;   // setup: colourings overlapped with the coarsening chain
-    cudaStream_t stream3 = nullptr;   // setup: the same for the odd levels
     cudaEvent_t ev_pattern = nullptr; // host input: level-0 pattern (rp, ci) on the device
     cudaEvent_t ev_join = nullptr;    // joins a caller's stream with `stream` (fdl_api.cu StreamJoin)
     SmallArena arena;                 // small buffers of the create (fdl_common.cuh); freed last

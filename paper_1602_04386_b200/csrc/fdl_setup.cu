@@ -3289,13 +3289,13 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
     graphs.reserve((size_t)maxl + 1);
     std::vector<cudaEvent_t> lev_ev((size_t)maxl + 1, nullptr);
     LevelFeed feed;
-    // two helper threads colour and lay out the even / odd levels on the two
-    // side streams, so a level's colouring starts as soon as the level exists
+    // kSides helper threads colour and lay out the levels = k mod kSides on
+    // side stream k, so a level's colouring starts as soon as the level exists
     // even while the previous level's layout still runs (serial: one pass on st)
-    constexpr int kSides = 2;
-    cudaStream_t sides[kSides] = {sb, serial ? sb : h.stream3};
+    cudaStream_t sides[kSides];
+    for (int k = 0; k < kSides; k++) sides[k] = serial ? sb : h.set.side[k];
     std::exception_ptr side_err[kSides];
-    long long side_launches[kSides] = {0, 0};
+    long long side_launches[kSides] = {};
     std::thread side[kSides];
     auto run_side = [&](int k, int first, int stride) {
         const long long l0 = g_launch_count;
@@ -3364,10 +3364,9 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
             std::rethrow_exception(side_err[k]);
         }
     // the main stream continues after the colourings and layouts
-    const cudaEvent_t jev[kSides] = {h.set.ev[2], h.set.ev[3]};
     for (int k = 0; k < kSides; k++) {
-        FDL_CK(cudaEventRecord(jev[k], sides[k]));
-        FDL_CK(cudaStreamWaitEvent(st, jev[k], 0));
+        FDL_CK(cudaEventRecord(h.set.sev[k], sides[k]));
+        FDL_CK(cudaStreamWaitEvent(st, h.set.sev[k], 0));
     }
     trace_mark(st, "colourings and layouts joined");
     const int J = (int)h.levels.size() - 1;
