@@ -2528,6 +2528,15 @@ __global__ void __launch_bounds__(kSmallColourThreads, 1) k_color_cluster(int n,
 #define FDL_COLOUR_GRID_FRAC 0.3333
 #endif
 constexpr double kColourGridFrac = FDL_COLOUR_GRID_FRAC;
+// dense levels (W = 32 sub-warps: power-law graphs) take a smaller share: their
+// colouring is a long chain of rounds that slowed the concurrent Galerkin
+// product of R-MAT's level 0 from 6.7 ms (alone) to 26.6 ms at a third of the
+// grid (measured: R-MAT step 137.0 / 128.5 / 130.3 ms at 1/3, 0.2, 0.12; the
+// grids keep 1/3: config 4 72.8 / 78.2 / 85.3 ms)
+#ifndef FDL_COLOUR_GRID_FRAC_DENSE
+#define FDL_COLOUR_GRID_FRAC_DENSE 0.2
+#endif
+constexpr double kColourGridFracDense = FDL_COLOUR_GRID_FRAC_DENSE;
 
 struct ColourJob {
     DBuf la, lb, indeg, counts, mx, st8;
@@ -2624,7 +2633,8 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             // both cooperative kernels fit side by side with room for the rest
             // of the coarsening chain (a full-grid cooperative launch would wait
             // for the other one to drain)
-            DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, kColourGridFrac, (int64_t)n * W));
+            DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, W == 32 ? kColourGridFracDense : kColourGridFrac,
+                                         (int64_t)n * W));
             tr.report(job.counts.as<int>());
         }
     }
