@@ -2836,42 +2836,46 @@ __global__ void k_hub_find(int n, const int *rp, const int *perm, int *count, in
 }
 // hub rows of the GS layout (list from k_hub_find: {GS row, natural id, length}):
 // a CTA per row copies entries W.. (k_permute_rows copied the first W) with
-// renumbered columns, 4 per thread in flight; thread 0 folds d_v over the whole
-// row in stored order (the oracle's order) while the others copy
+// renumbered columns, 4 per thread in flight, and stages the weights chunk by
+// chunk in shared memory, where thread 0 folds d_v in stored order (the
+// oracle's order) without waiting on global loads
+constexpr int kHubChunk = 4096;
 __global__ void __launch_bounds__(256) k_hub_permute(int nh, const int4 *hubs, int W, const int *inv, const int *rp,
                                                      const int *ci, const double *w, const int *rpp, int *cip,
                                                      double *wp, unsigned long long *dmax) {
+    __shared__ double sw[kHubChunk];
     for (int h = blockIdx.x; h < nh; h += gridDim.x) {
         const int4 hb = hubs[h];
         const int b = rp[hb.y], len = hb.z, o = rpp[hb.x];
-        if (threadIdx.x == 0) {
-            double d = 0.0;
-            for (int k0 = 0; k0 < len; k0 += 8) {
-                double y[8];
+        double d = 0.0;
+        for (int c0 = 0; c0 < len; c0 += kHubChunk) {
+            const int cn = min(kHubChunk, len - c0);
+            for (int i0 = threadIdx.x; i0 < cn; i0 += 4 * blockDim.x) {
+                int c[4];
+                double y[4];
 #pragma unroll
-                for (int i = 0; i < 8; i++) y[i] = k0 + i < len ? w[b + k0 + i] : 0.0;
-#pragma unroll
-                for (int i = 0; i < 8; i++)
-                    if (k0 + i < len) d += y[i];
-            }
-            atomicMax(dmax, (unsigned long long)__double_as_longlong(d));
-        }
-        for (int k0 = W + threadIdx.x; k0 < len; k0 += 4 * blockDim.x) {
-            int c[4];
-            double y[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int k = k0 + u * blockDim.x;
-                c[u] = k < len ? ci[b + k] : -1;
-                y[u] = k < len ? w[b + k] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++)
-                if (c[u] >= 0) {
-                    cip[o + k0 + u * blockDim.x] = inv[c[u]];
-                    wp[o + k0 + u * blockDim.x] = y[u];
+                for (int u = 0; u < 4; u++) {
+                    const int i = i0 + u * blockDim.x;
+                    c[u] = i < cn ? ci[b + c0 + i] : -1;
+                    y[u] = i < cn ? w[b + c0 + i] : 0.0;
                 }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (c[u] >= 0) {
+                        const int i = i0 + u * blockDim.x;
+                        sw[i] = y[u];
+                        if (c0 + i >= W) {
+                            cip[o + c0 + i] = inv[c[u]];
+                            wp[o + c0 + i] = y[u];
+                        }
+                    }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int i = 0; i < cn; i++) d += sw[i];
+            __syncthreads();
         }
+        if (threadIdx.x == 0) atomicMax(dmax, (unsigned long long)__double_as_longlong(d));
     }
 }
 __global__ void k_scatter_tiles(int k, const int *dst, const Tile *src, Tile *tiles) {
