@@ -308,6 +308,86 @@ __device__ __forceinline__ int rank_row(int v, int b, int deg, const int *ci, co
     return top;
 }
 
+// Rows longer than the in-kernel ranking (kSortSlots * W entries) of dense
+// levels: without a ranking, a vertex whose target got matched rescans its
+// whole row, and on R-MAT's dense levels (30-55 handshake rounds, a few
+// matches per round, thousands of vertices pointing at each popular one) the
+// rescans were most of the matching's time.  This pass ranks every row of
+// kSortSlots * W < deg <= kRankMax entries once (a CTA per row: bitonic sort
+// of (w, hash) descending in shared memory; w > 0, so its bits order like the
+// value), so re-pointing is a cursor advance for them too.
+constexpr int kRankMax = 8192;
+#ifndef FDL_RANK_MIN_AVG
+#define FDL_RANK_MIN_AVG 450
+#endif
+// levels this dense (entries per row) rank their long rows: measured on R-MAT
+// (step 126.3 / 120.2 / 118.3 / 118.8 ms at 64 / 200 / 450 / 800; below ~450 the
+// sorts cost more than the rescans they save)
+constexpr double kRankMinAvg = FDL_RANK_MIN_AVG;
+constexpr int kRankSmall = 1024;   // rows up to this many entries: small CTAs, many per SM
+__device__ __forceinline__ void rank_row_cta(int v, int b, int deg, int P, const int *ci, const double *w,
+                                             uint64_t salt, int *nbr, unsigned long long *kw,
+                                             unsigned long long *kh, int *kj) {
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        if (i < deg) {
+            const int j = ci[b + i];
+            kw[i] = (unsigned long long)__double_as_longlong(w[b + i]);
+            kh[i] = edge_hash(salt, v, j);
+            kj[i] = j;
+        } else {
+            kw[i] = 0ull;   // padding sorts last (every weight is > 0)
+            kh[i] = 0ull;
+            kj[i] = -1;
+        }
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ jj;
+                if (ixj <= i) continue;
+                // descending overall: blocks with (i & k) == 0 descending
+                const bool gt = kw[ixj] > kw[i] || (kw[ixj] == kw[i] && kh[ixj] > kh[i]);
+                const bool lt = kw[ixj] < kw[i] || (kw[ixj] == kw[i] && kh[ixj] < kh[i]);
+                if (((i & k) == 0) ? gt : lt) {
+                    const unsigned long long tw = kw[i], th = kh[i];
+                    const int tj = kj[i];
+                    kw[i] = kw[ixj]; kh[i] = kh[ixj]; kj[i] = kj[ixj];
+                    kw[ixj] = tw; kh[ixj] = th; kj[ixj] = tj;
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < deg; i += blockDim.x) nbr[b + i] = kj[i];
+    __syncthreads();
+}
+// the rows to rank: dmin < deg <= kRankSmall into list[0..), longer ones (<= kRankMax)
+// from the top of the list downwards (cnt[0], cnt[1])
+__global__ void k_rank_list(int n, const int *rp, int dmin, int *list, int *cnt) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int deg = rp[v + 1] - rp[v];
+        if (deg <= dmin || deg > kRankMax) continue;
+        if (deg <= kRankSmall) list[atomicAdd(cnt, 1)] = v;
+        else list[n - 1 - atomicAdd(cnt + 1, 1)] = v;
+    }
+}
+template <int T, int CAP>
+__global__ void __launch_bounds__(T) k_rank_rows(int n, const int *rp, const int *ci, const double *w, uint64_t salt,
+                                                 const int *list, const int *cnt, bool big, int *nbr) {
+    extern __shared__ __align__(16) unsigned char rk_smem[];
+    unsigned long long *kw = reinterpret_cast<unsigned long long *>(rk_smem);
+    unsigned long long *kh = kw + CAP;
+    int *kj = reinterpret_cast<int *>(kh + CAP);
+    const int m = big ? cnt[1] : cnt[0];
+    for (int i = blockIdx.x; i < m; i += gridDim.x) {
+        const int v = big ? list[n - 1 - i] : list[i];
+        const int b = rp[v], deg = rp[v + 1] - b;
+        int P = 1;
+        while (P < deg) P <<= 1;
+        rank_row_cta(v, b, deg, P, ci, w, salt, nbr, kw, kh, kj);
+    }
+}
+
 // counts[r] = length of the work list of round r (zeroed by the host); the
 // lists ping-pong between la and lb.  rounds_out[0] = handshake rounds.
 // W == 1 (low-degree levels): round 0 takes two rows per thread and the first
@@ -317,7 +397,7 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
                                                              const double *w, uint64_t salt, int *m,
                                                              int *ptr, int *mate, int *nbr, int *cursor,
                                                              int *la, int *lb, int *counts,
-                                                             int *rounds_out, int *lm, int *mcount) {
+                                                             int *rounds_out, int *lm, int *mcount, int rank_avail) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
@@ -380,9 +460,13 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
         if (v >= 0) { b = rp[v]; deg = rp[v + 1] - b; }
         constexpr int kSortSlots = SortSlots<W>::value;
         const bool sortable = deg <= kSortSlots * W;
+        // rows ranked by k_rank_long_rows (dense levels, W == 32: one vertex per warp)
+        const bool presorted = W == 32 && rank_avail && v >= 0 && !sortable && deg <= kRankMax;
         int bj;
-        const bool ranked = __all_sync(0xffffffffu, v < 0 || sortable);   // warp-uniform
-        if (ranked) {
+        const bool ranked = presorted || __all_sync(0xffffffffu, v < 0 || sortable);   // warp-uniform
+        if (presorted) {
+            bj = nbr[b];
+        } else if (ranked) {
             double wv[kSortSlots];
             unsigned long long hv[kSortSlots];
             int cv[kSortSlots], rank[kSortSlots];
@@ -567,12 +651,28 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
                 const int cur = v >= 0 ? cursor[v] : -1;
                 int bj = -1;
                 const bool rescan = v >= 0 && cur < 0;
-                if (v >= 0 && cur >= 0 && lane == 0) {
+                if (v >= 0 && cur >= 0) {
+                    // cursor advance by the sub-warp: W candidates per step, the
+                    // first free one by a ballot (was one dependent pair of loads
+                    // per candidate in lane 0)
                     const int b = rp[v], deg = rp[v + 1] - b;
+                    const unsigned sub = W == 32 ? 0xffffffffu
+                                                 : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
                     int c = cur + 1;
-                    while (c < deg && mate[nbr[b + c]] >= 0) c++;
+                    for (;; c += W) {
+                        const int k = c + lane;
+                        const int j = k < deg ? nbr[b + k] : -1;
+                        const bool freej = j >= 0 && mate[j] < 0;
+                        const bool endk = k >= deg;
+                        const unsigned hit = __ballot_sync(sub, freej || endk) & sub;
+                        if (hit) {
+                            const int f = __ffs(hit >> ((threadIdx.x & 31) & ~(W - 1))) - 1;
+                            c += f;
+                            break;
+                        }
+                    }
                     bj = c < deg ? nbr[b + c] : -1;
-                    cursor[v] = c;
+                    if (lane == 0) cursor[v] = c;
                 }
                 const int bs = heaviest<W>(rescan ? v : -1, rp, ci, w, salt, lane,
                                            [&](int j) { return mate[j] >= 0; });
@@ -742,7 +842,28 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
             *pcur = cursor.as<int>(), *pa = la.as<int>(), *pb = lb.as<int>(), *pc = counts.as<int>(),
             *pr = counts.as<int>() + kMaxRounds;
         int *plm = lmv.as<int>(), *pmc = mcount.as<int>();
-        void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr, &plm, &pmc};
+        int ra = avg > kRankMinAvg ? 1 : 0;   // long rows ranked by k_rank_rows (below)
+        void *args[] = {&n, &rp, &ci, &w, &salt, &pm, &pp, &pmate, &pn, &pcur, &pa, &pb, &pc, &pr, &plm, &pmc, &ra};
+        if (avg > kRankMinAvg) {   // dense W == 32 levels: rank the long rows first
+            static DeviceCache attr{};
+            std::atomic<int> &a = attr[current_device()];
+            if (!a.load()) {
+                FDL_CK(cudaFuncSetAttribute(k_rank_rows<512, kRankMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kRankMax * 20));
+                a.store(1);
+            }
+            DBuf rl((size_t)n * 4 + 16, st);
+            int *rcnt = rl.as<int>() + n;
+            FDL_CK(cudaMemsetAsync(rcnt, 0, 8, st));
+            k_rank_list<<<grid_for(n), 256, 0, st>>>(n, rp, SortSlots<32>::value * 32, rl.as<int>(), rcnt);
+            FDL_LAUNCH_CK();
+            k_rank_rows<128, kRankSmall><<<kNumSMs * 8, 128, kRankSmall * 20, st>>>(n, rp, ci, w, salt, rl.as<int>(),
+                                                                                  rcnt, false, pn);
+            FDL_LAUNCH_CK();
+            k_rank_rows<512, kRankMax><<<kNumSMs, 512, kRankMax * 20, st>>>(n, rp, ci, w, salt, rl.as<int>(), rcnt,
+                                                                          true, pn);
+            FDL_LAUNCH_CK();
+        }
         RoundTrace tr(st, "match");
         DISPATCH_WC(avg, coop_launch(k_match_coop<W>, args, st, kMatchGridFrac, (int64_t)n * W));
         tr.report(counts.as<int>());
