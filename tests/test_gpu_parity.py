@@ -72,6 +72,9 @@ SMALL = {
     "dense1500_deg120": lambda: gg.random_connected(1500, 90000, 21),
     # mid-size dense level (n > 12288, average degree >= 64): the cluster colouring
     "dense16k_deg70": lambda: gg.random_connected(16000, 560000, 22),
+    # levels of >= 450 entries per row rank their long rows before the matching (k_rank_rows)
+    "complete500": lambda: gg.complete(500),
+    "dense3000_deg500": lambda: gg.random_connected(3000, 750000, 23),
     "hub3000_3hubs": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
     # a row of 4999 entries: five piece tiles of the row passes (hub rows > 1024 entries)
     "star5000": lambda: gg.star(5000),
