@@ -289,6 +289,19 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
         convert_row_ptr(row_ptr, n, nnz, g0.own_rp.as<int>(), st);
         g0.ci = col_idx;
         g0.w = weights;
+        // the handle's own copy of the level-0 columns / weights (the power
+        // steps' natural CSR, padded for the bulk copies), made on a side stream
+        // while the setup reads the caller's arrays: it used to be a 3 GB copy
+        // on the main stream at the end of the setup (config 4: ~1 ms)
+        if (nnz) {
+            cudaStream_t sd = h->set.side[kSides > 1 ? 1 : 0];
+            FDL_CK(cudaEventRecord(h->set.ev[3], st));
+            FDL_CK(cudaStreamWaitEvent(sd, h->set.ev[3], 0));
+            g0.own_ci.alloc(padded((size_t)nnz * 4), sd);
+            g0.own_w.alloc(padded((size_t)nnz * 8), sd);
+            FDL_CK(cudaMemcpyAsync(g0.own_ci.p, col_idx, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, sd));
+            FDL_CK(cudaMemcpyAsync(g0.own_w.p, weights, (size_t)nnz * 8, cudaMemcpyDeviceToDevice, sd));
+        }
     } else {
         DBuf rp64((size_t)(n + 1) * 8, st);
         FDL_CK(cudaMemcpyAsync(rp64.p, row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st));

@@ -3267,8 +3267,10 @@ static void build_layout(NatGraph &g, const int *color_nat, int ncolors, Level &
 // the natural CSR of a level for the PI / RQ passes: taken over from the setup
 // graph when it owns padded storage, copied otherwise (the caller's level 0)
 static void take_natural(NatGraph &g, Level &L, cudaStream_t st) {
+    // (an owned buffer always holds the level's array: the setup's own output,
+    // the staged host input, or the side-stream copy of a device input)
     auto take = [&](DBuf &own, const void *ptr, size_t bytes, DBuf &dst) {
-        if (own.p && own.p == ptr && own.bytes >= padded(bytes)) {
+        if (own.p && own.bytes >= padded(bytes)) {
             dst = std::move(own);
         } else {
             dst.alloc(padded(bytes), st);
@@ -3401,6 +3403,14 @@ static void colour_and_layout(Handle &h, std::vector<NatGraph> &graphs, std::vec
         if (ell == 0 && h.ev_pattern) FDL_CK(cudaStreamWaitEvent(sb, lev_ev[0], 0));
         pt.mark(ell, 3, 0, sb);
         build_layout(g, L.color_nat.as<int>(), cr[2] + 1, L, sb);
+        // the prolongation map into GS numbering, qg = q o perm, once the
+        // matching of this level is done (the next level exists)
+        if (feed.wait_for(ell + 1)) {
+            FDL_CK(cudaStreamWaitEvent(sb, lev_ev[ell + 1], 0));
+            L.qg.alloc((size_t)L.n * 4, sb);
+            k_compose_qg<<<grid_for(L.n), 256, 0, sb>>>(L.n, L.perm.as<int>(), L.q_nat.as<int>(), L.qg.as<int>());
+            FDL_LAUNCH_CK();
+        }
         pt.mark(ell, 3, 1, sb);
         trace_mark(sb, ell == 0 ? "L0 colour+layout (second stream)" : "Lk colour+layout (second stream)");
     }
@@ -3506,13 +3516,6 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
     trace_mark(st, "colourings and layouts joined");
     const int J = (int)h.levels.size() - 1;
     for (int ell = 0; ell <= J; ell++) take_natural(graphs[ell], h.levels[ell], st);
-    for (int ell = 0; ell < J; ell++) {
-        Level &L = h.levels[ell];
-        L.qg.alloc((size_t)L.n * 4, st);
-        k_compose_qg<<<grid_for(L.n), 256, 0, st>>>(L.n, L.perm.as<int>(), L.q_nat.as<int>(),
-                                                    L.qg.as<int>());
-        FDL_LAUNCH_CK();
-    }
     host_wait(st);
     pt.collect(h.levels);
     trace_mark(st, "compose qp");
