@@ -188,6 +188,45 @@ constexpr int kMatchUnroll = FDL_MATCH_UNROLL;
 constexpr double kMatchGridFrac = FDL_MATCH_GRID_FRAC;
 static_assert(kAppendCap >= 2 * kMatchUnroll * kCoopThreads, "append buffer too small");   // JP depth can reach thousands on dense cores
 
+// Grid-wide barrier of the cooperative kernels (all CTAs resident) with a
+// polling backoff (FDL_GRID_BACKOFF=1), instead of cg's grid sync, which spins
+// its CTA masters on an acquire load: tried in case the long chains of rounds
+// slowed the other streams' kernels with polls -- measured 0.2-2 ms slower on
+// every config (the barrier's own latency grows), so off by default.
+// bar[0] = arrivals, bar[1] = generation (zero at launch).
+#ifndef FDL_GRID_BACKOFF
+#define FDL_GRID_BACKOFF 0
+#endif
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void grid_sync_bo(cg::grid_group &grid, unsigned *bar) {
+    if (!FDL_GRID_BACKOFF) {
+        grid.sync();
+        return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire_gpu(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            unsigned ns = 32;
+            while (ld_acquire_gpu(bar + 1) == g) {
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // FIEDLER_TRACE: per-phase device timestamps of the cooperative kernels
 __device__ unsigned long long *g_round_ts = nullptr;
 __device__ __forceinline__ void round_stamp(int i) {
@@ -399,6 +438,7 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
                                                              int *la, int *lb, int *counts,
                                                              int *rounds_out, int *lm, int *mcount, int rank_avail) {
     cg::grid_group grid = cg::this_grid();
+    unsigned *gbar = reinterpret_cast<unsigned *>(counts + kMaxRounds + 4);
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
     if (threadIdx.x == 0) s_n = 0;
@@ -521,7 +561,7 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
     }
     __syncthreads();
     app.flush(la, counts);
-    grid.sync();
+    grid_sync_bo(grid, gbar);
     round_stamp(stamp++);
     int *in = la, *out = lb;
     bool implicit = W == 1;   // the first list of W == 1 is every vertex, in order
@@ -545,7 +585,7 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
                     if (p[u] >= 0 && ptr[p[u]] == v[u]) mate[v[u]] = p[u];
             }
         }
-        grid.sync();
+        grid_sync_bo(grid, gbar);
         round_stamp(stamp++);
         // (b) unmatched vertices whose target got matched re-point at their
         //     heaviest FREE neighbour (cursor advance, or a rescan for long rows)
@@ -640,7 +680,7 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
                 __syncthreads();
                 if (app.due(kAppendCap - kCoopThreads)) app.flush(out, gcount);
             }
-            grid.sync();
+            grid_sync_bo(grid, gbar);
             // (b2) a sub-warp per mover re-points it at its heaviest FREE neighbour
             //      (cursor advance, or a rescan of a long row); slot s of CTA b
             //      takes mover base + s * gridDim + b, spread over all CTAs
@@ -687,7 +727,7 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
         }
         __syncthreads();
         app.flush(out, gcount);
-        grid.sync();
+        grid_sync_bo(grid, gbar);
         round_stamp(stamp++);
         r++;
         cnt = *(volatile int *)gcount;
@@ -830,11 +870,11 @@ static int hec_parallel(const NatGraph &g, uint64_t salt, DBuf &q, DBuf &mate, i
     FDL_CK(cudaMemsetAsync(mcount.p, 0, (size_t)kMaxRounds * 4, st));
     DBuf m((size_t)n * 4, st), ptr((size_t)n * 4, st), la((size_t)n * 4, st), lb((size_t)n * 4, st),
         nbr((size_t)std::max(g.nnz, 1) * 4, st), cursor((size_t)n * 4, st),
-        counts((size_t)(kMaxRounds + 2) * 4, st);
+        counts((size_t)(kMaxRounds + 8) * 4, st);
     q.alloc((size_t)n * 4, st);
     mate.alloc((size_t)n * 4, st);
     FDL_CK(cudaMemsetAsync(mate.p, 0xff, (size_t)n * 4, st));
-    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 2) * 4, st));
+    FDL_CK(cudaMemsetAsync(counts.p, 0, (size_t)(kMaxRounds + 8) * 4, st));
     {
         const int *rp = g.rp, *ci = g.ci;
         const double *w = g.w;
@@ -2111,6 +2151,7 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks)
     k_color_byte(int n, const int *rp, const int *ci, uint64_t salt, int *color, unsigned char *st8,
                  int *la, int *lb, int *counts, int *rounds_out, int *flag) {
     cg::grid_group grid = cg::this_grid();
+    unsigned *gbar = reinterpret_cast<unsigned *>(counts + kMaxRounds + 4);
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base, s_big;
     if (threadIdx.x == 0) { s_n = 0; s_big = 0; }
@@ -2142,7 +2183,7 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks)
     __syncthreads();
     app.flush(la, counts);
     if (threadIdx.x == 0 && s_big) atomicOr(flag, 1);
-    grid.sync();
+    grid_sync_bo(grid, gbar);
     round_stamp(stamp++);
     if (*(volatile int *)flag) {   // grid-uniform: the int-state kernel takes over
         if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = 0;
@@ -2165,7 +2206,7 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks)
         }
         __syncthreads();
         app.flush(out, gcount);
-        grid.sync();
+        grid_sync_bo(grid, gbar);
         round_stamp(stamp++);
         r++;
         cnt = *(volatile int *)gcount;
@@ -2189,6 +2230,7 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
     // gated (after k_color_byte): runs only when the byte state could not be used
     if (gate && *(volatile const int *)gate == 0) return;
     cg::grid_group grid = cg::this_grid();
+    unsigned *gbar = reinterpret_cast<unsigned *>(counts + kMaxRounds + 4);
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
     __shared__ unsigned s_bm[W > 1 ? kCoopThreads / W : 1][kBmWords];   // first-fit bitmaps
@@ -2251,7 +2293,7 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
     }
     __syncthreads();
     app.flush(la, counts);
-    grid.sync();
+    grid_sync_bo(grid, gbar);
     round_stamp(stamp++);
     int *in = la, *out = lb;
     int r = 0;
@@ -2317,7 +2359,7 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
         if (W > 1) heavy_round(out, gcount);
         __syncthreads();
         app.flush(out, gcount);
-        grid.sync();
+        grid_sync_bo(grid, gbar);
         round_stamp(stamp++);
         r++;
         cnt = *(volatile int *)gcount;
@@ -2706,8 +2748,8 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
     job.la.alloc((size_t)n * 4, st);
     job.lb.alloc((size_t)n * 4, st);
     job.indeg.alloc((size_t)n * 4, st);
-    job.counts.alloc((size_t)(kMaxRounds + 4) * 4, st);
-    FDL_CK(cudaMemsetAsync(job.counts.p, 0, (size_t)(kMaxRounds + 4) * 4, st));
+    job.counts.alloc((size_t)(kMaxRounds + 8) * 4, st);
+    FDL_CK(cudaMemsetAsync(job.counts.p, 0, (size_t)(kMaxRounds + 8) * 4, st));
     {
         const int *rp = g.rp, *ci = g.ci;
         int *pcol = color.as<int>(), *pin = job.indeg.as<int>(), *pa = job.la.as<int>(), *pb = job.lb.as<int>(),
