@@ -1070,10 +1070,18 @@ __global__ void __launch_bounds__(kGdThreads, 1) k_gs_pieces(GdArgs a) {
         const int2 R = item_rng(it);
         const int P0 = R.x, P1 = R.y;
         int has_split = gd_piece<CLUSTER, XS>(cur, warp, slots, L, xg, xs, ncl, lane);
-        for (int pi = P0 + warp + kGdWarps; pi < P1; pi += kGdWarps) {
-            GdPiece q;
-            gd_load(q, a.pieces, pi, P1, L, lane);
-            has_split |= gd_piece<CLUSTER, XS>(q, pi - P0, slots, L, xg, xs, ncl, lane);
+        // the warp's further pieces (a colour's long rows), two at a time with
+        // both pieces' loads in flight together (the prefetch registers of
+        // `cur` are free until the next colour's loads are issued)
+        for (int pi = P0 + warp + kGdWarps; pi < P1; pi += 2 * kGdWarps) {
+            const int pj = pi + kGdWarps;
+            const int4 d1 = gd_desc(a.pieces, pi, P1), d2b = gd_desc(a.pieces, pj, P1);
+            const int2 o1 = gd_offs(d1, L, lane), o2b = gd_offs(d2b, L, lane);
+            GdPiece q1, q2;
+            gd_data(q1, d1, o1, L);
+            gd_data(q2, d2b, o2b, L);
+            has_split |= gd_piece<CLUSTER, XS>(q1, pi - P0, slots, L, xg, xs, ncl, lane);
+            if (pj < P1) has_split |= gd_piece<CLUSTER, XS>(q2, pj - P0, slots, L, xg, xs, ncl, lane);
         }
         if (__syncthreads_or(has_split)) {
             // rows split into pieces: the warp of the first piece folds the
