@@ -182,8 +182,11 @@ constexpr int kMaxRounds = 1 << 16;
 constexpr int kMatchUnroll = FDL_MATCH_UNROLL;
 // the matching and the colouring (second stream) are both cooperative: each
 // takes part of the co-resident grid so that they can run side by side
+// (round 2, two side streams: config 4 step 72.1 / 71.9 / 71.8 / 76.0 ms at a
+// matching share of 0.5 / 0.55 / 0.6 / 0.63 -- past ~0.6 the cooperative
+// launches no longer fit beside each other; 0.55 keeps a margin)
 #ifndef FDL_MATCH_GRID_FRAC
-#define FDL_MATCH_GRID_FRAC 0.5
+#define FDL_MATCH_GRID_FRAC 0.55
 #endif
 constexpr double kMatchGridFrac = FDL_MATCH_GRID_FRAC;
 static_assert(kAppendCap >= 2 * kMatchUnroll * kCoopThreads, "append buffer too small");   // JP depth can reach thousands on dense cores
