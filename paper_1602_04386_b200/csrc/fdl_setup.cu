@@ -2225,11 +2225,126 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks)
 // higher-priority neighbours; a vertex is coloured once all of them are, then
 // it releases its lower-priority neighbours.  Every vertex and edge is handled
 // a constant number of times (the round-based JP rescans waiting vertices).
+// The JP rounds of k_color_coop, for a group of CTAs: the whole cooperative
+// grid (GridG) or, for the deep tail of a dense level's priority DAG (hundreds
+// to thousands of rounds with a handful of ready vertices each), one thread-
+// block cluster (ClusterG, k_color_tail): a cluster barrier instead of a grid
+// barrier per round.  In the grid, the rounds stop once a list is shorter than
+// tail_list (tail_list = 0: never) and the state goes to counts[kMaxRounds + 4..7].
+struct ColourShared {
+    int *s_buf;
+    int *s_n, *s_base;
+    unsigned (*s_bm)[kBmWords];
+    int *s_heavy;
+    int *s_nh;
+    int *s_red;
+};
+struct GridG {
+    cg::grid_group &g;
+    unsigned *bar;
+    __device__ int nb() const { return gridDim.x; }
+    __device__ int rank() const { return blockIdx.x; }
+    __device__ void sync() { grid_sync_bo(g, bar); }
+};
+struct ClusterG {
+    __device__ int nb() const { return (int)cg::this_cluster().num_blocks(); }
+    __device__ int rank() const { return (int)cg::this_cluster().block_rank(); }
+    __device__ void sync() { cg::this_cluster().sync(); }
+};
+constexpr int kColourTailSlot = kMaxRounds + 6;   // counts[..]: {round, list parity, tail needed}
+template <int W, class G>
+__device__ void colour_rounds(G &grp, const ColourShared &sh, int n, const int *rp, const int *ci, uint64_t salt,
+                              int *color, int *indeg, int *la, int *lb, int *counts, int *rounds_out, int r,
+                              int parity, int tail_list, int stamp) {
+    (void)n;
+    CtaAppend app{sh.s_buf, sh.s_n, sh.s_base};
+    const int lane = threadIdx.x & (W - 1);
+    const int per_block = kCoopThreads / W;
+    int *in = parity ? lb : la, *out = parity ? la : lb;
+    int cnt = *(volatile int *)&counts[r];
+    auto heavy_round = [&](int *hout, int *hcount) {
+        const int nh = *sh.s_nh;   // read after a barrier
+        for (int i = 0; i < nh; i++) {
+            const int hv = sh.s_heavy[i];
+            cta_first_fit(hv, rp, ci, salt, color, sh.s_bm[0], sh.s_red);
+            const uint64_t pv = splitmix64(salt ^ (uint64_t)hv);
+            for (int k = rp[hv] + threadIdx.x; k < rp[hv + 1]; k += blockDim.x) {
+                const int u = ci[k];
+                if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, hv)) continue;
+                if (atomicSub(&indeg[u], 1) == 1) app.push_safe(u, hout, hcount);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) *sh.s_nh = 0;
+        __syncthreads();
+    };
+    const int NB = grp.nb(), RK = grp.rank();
+    while (cnt > 0 && r + 1 < kMaxRounds) {
+        if (tail_list > 0 && cnt < tail_list) {   // uniform: hand the rest to the cluster
+            if (RK == 0 && threadIdx.x == 0) {
+                counts[kColourTailSlot] = r;
+                counts[kColourTailSlot + 1] = in == la ? 0 : 1;
+                counts[kColourTailSlot + 2] = 1;
+            }
+            return;
+        }
+        int *gcount = counts + r + 1;
+        // W == 1: contiguous entries per CTA; W > 1: sub-warp slot s of CTA b
+        // takes entry base + s * NB + b, so a short list (the deep rounds
+        // of dense levels) is spread over all CTAs, at most one heavy vertex each
+        // (W == 1 takes two entries per thread: idx and idx + kCoopThreads)
+        for (long long base = W == 1 ? (long long)RK * 2 * kCoopThreads : 0; base < cnt;
+             base += (long long)NB * (W == 1 ? 2 * kCoopThreads : per_block)) {
+            const long long idx = W == 1 ? base + threadIdx.x
+                                         : base + (long long)(threadIdx.x / W) * NB + RK;
+            int v = idx < cnt ? in[idx] : -1;
+            if (W > 1 && v >= 0 && rp[v + 1] - rp[v] > kHeavyDeg) {   // the CTA does it below
+                if (lane == 0) sh.s_heavy[atomicAdd(sh.s_nh, 1)] = v;
+                v = -1;
+            }
+            if (W == 1) {
+                const long long idx1 = idx + kCoopThreads;   // the thread's second entry
+                const int v1 = idx1 < cnt ? in[idx1] : -1;
+                colour_pair_w1(v, v1, rp, ci, salt, IntColourState{color, indeg}, app, out, gcount, rounds_out);
+            } else {
+                // all higher-priority neighbours are coloured: first fit
+                color_first_fit<W>(v, rp, ci, salt, color, lane, sh.s_bm[threadIdx.x / W]);
+                // release the lower-priority neighbours
+                if (v >= 0) {
+                    const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+                    for (int k = rp[v] + lane; k < rp[v + 1]; k += W) {
+                        const int u = ci[k];
+                        if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
+                        if (atomicSub(&indeg[u], 1) == 1) app.push_safe(u, out, gcount);
+                    }
+                }
+            }
+            __syncthreads();
+            const int nh1 = *sh.s_nh;   // read by every thread before the next barrier
+            __syncthreads();
+            if (W > 1 && nh1 > kHeavyCap - per_block) {
+                heavy_round(out, gcount);
+                __syncthreads();
+            }
+            if (app.due(kAppendCap - 2 * kCoopThreads)) app.flush(out, gcount);
+        }
+        if (W > 1) heavy_round(out, gcount);
+        __syncthreads();
+        app.flush(out, gcount);
+        grp.sync();
+        round_stamp(stamp++);
+        r++;
+        cnt = *(volatile int *)gcount;
+        int *t = in; in = out; out = t;
+    }
+    if (RK == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
+}
+
 template <int W>
 __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int n, const int *rp, const int *ci,
                                                              uint64_t salt, int *color, int *indeg,
                                                              int *la, int *lb, int *counts,
-                                                             int *rounds_out, const int *gate) {
+                                                             int *rounds_out, const int *gate, int tail_list) {
     // gated (after k_color_byte): runs only when the byte state could not be used
     if (gate && *(volatile const int *)gate == 0) return;
     cg::grid_group grid = cg::this_grid();
@@ -2298,77 +2413,30 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
     app.flush(la, counts);
     grid_sync_bo(grid, gbar);
     round_stamp(stamp++);
-    int *in = la, *out = lb;
-    int r = 0;
-    int cnt = *(volatile int *)&counts[0];
-    // the deferred heavy vertices of this CTA: colour, then release, whole CTA
-    auto heavy_round = [&](int *hout, int *hcount) {
-        const int nh = s_nh;   // read after a barrier
-        for (int i = 0; i < nh; i++) {
-            const int hv = s_heavy[i];
-            cta_first_fit(hv, rp, ci, salt, color, s_bm[0], s_red);
-            const uint64_t pv = splitmix64(salt ^ (uint64_t)hv);
-            for (int k = rp[hv] + threadIdx.x; k < rp[hv + 1]; k += blockDim.x) {
-                const int u = ci[k];
-                if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, hv)) continue;
-                if (atomicSub(&indeg[u], 1) == 1) app.push_safe(u, hout, hcount);
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) s_nh = 0;
-        __syncthreads();
-    };
-    while (cnt > 0 && r + 1 < kMaxRounds) {
-        int *gcount = counts + r + 1;
-        // W == 1: contiguous entries per CTA; W > 1: sub-warp slot s of CTA b
-        // takes entry base + s * gridDim + b, so a short list (the deep rounds
-        // of dense levels) is spread over all CTAs, at most one heavy vertex each
-        // (W == 1 takes two entries per thread: idx and idx + kCoopThreads)
-        for (long long base = W == 1 ? (long long)blockIdx.x * 2 * kCoopThreads : 0; base < cnt;
-             base += (long long)gridDim.x * (W == 1 ? 2 * kCoopThreads : per_block)) {
-            const long long idx = W == 1 ? base + threadIdx.x
-                                         : base + (long long)(threadIdx.x / W) * gridDim.x + blockIdx.x;
-            int v = idx < cnt ? in[idx] : -1;
-            if (W > 1 && v >= 0 && rp[v + 1] - rp[v] > kHeavyDeg) {   // the CTA does it below
-                if (lane == 0) s_heavy[atomicAdd(&s_nh, 1)] = v;
-                v = -1;
-            }
-            if (W == 1) {
-                const long long idx1 = idx + kCoopThreads;   // the thread's second entry
-                const int v1 = idx1 < cnt ? in[idx1] : -1;
-                colour_pair_w1(v, v1, rp, ci, salt, IntColourState{color, indeg}, app, out, gcount, rounds_out);
-            } else {
-                // all higher-priority neighbours are coloured: first fit
-                color_first_fit<W>(v, rp, ci, salt, color, lane, s_bm[threadIdx.x / W]);
-                // release the lower-priority neighbours
-                if (v >= 0) {
-                    const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
-                    for (int k = rp[v] + lane; k < rp[v + 1]; k += W) {
-                        const int u = ci[k];
-                        if (higher_prio(splitmix64(salt ^ (uint64_t)u), u, pv, v)) continue;
-                        if (atomicSub(&indeg[u], 1) == 1) app.push_safe(u, out, gcount);
-                    }
-                }
-            }
-            __syncthreads();
-            const int nh1 = s_nh;   // read by every thread before the next barrier
-            __syncthreads();
-            if (W > 1 && nh1 > kHeavyCap - per_block) {
-                heavy_round(out, gcount);
-                __syncthreads();
-            }
-            if (app.due(kAppendCap - 2 * kCoopThreads)) app.flush(out, gcount);
-        }
-        if (W > 1) heavy_round(out, gcount);
-        __syncthreads();
-        app.flush(out, gcount);
-        grid_sync_bo(grid, gbar);
-        round_stamp(stamp++);
-        r++;
-        cnt = *(volatile int *)gcount;
-        int *t = in; in = out; out = t;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
+    GridG grp{grid, gbar};
+    const ColourShared sh{s_buf, &s_n, &s_base, s_bm, s_heavy, &s_nh, s_red};
+    colour_rounds<W>(grp, sh, n, rp, ci, salt, color, indeg, la, lb, counts, rounds_out, 0, 0, tail_list, stamp);
+}
+
+// The tail of a colouring k_color_coop handed over (counts[kColourTailSlot + 2]
+// set): the same rounds on one thread-block cluster.
+template <int W>
+__global__ void __launch_bounds__(kCoopThreads, 1) k_color_tail(int n, const int *rp, const int *ci, uint64_t salt,
+                                                                int *color, int *indeg, int *la, int *lb,
+                                                                int *counts, int *rounds_out) {
+    if (*(volatile const int *)&counts[kColourTailSlot + 2] == 0) return;
+    __shared__ int s_buf[kAppendCap];
+    __shared__ int s_n, s_base;
+    __shared__ unsigned s_bm[W > 1 ? kCoopThreads / W : 1][kBmWords];
+    __shared__ int s_heavy[W > 1 ? kHeavyCap : 1];
+    __shared__ int s_nh;
+    __shared__ int s_red[32];
+    if (threadIdx.x == 0) { s_n = 0; s_nh = 0; }
+    __syncthreads();
+    ClusterG grp;
+    const ColourShared sh{s_buf, &s_n, &s_base, s_bm, s_heavy, &s_nh, s_red};
+    colour_rounds<W>(grp, sh, n, rp, ci, salt, color, indeg, la, lb, counts, rounds_out,
+                     counts[kColourTailSlot], counts[kColourTailSlot + 1], 0, 1 << 20);
 }
 
 // Small dense levels (n <= kSmallColourN, average degree >= 64: the coarse levels of power-law
@@ -2743,6 +2811,60 @@ static bool cluster_colour_ok() {
     return slot.load() == 2;
 }
 
+#ifndef FDL_COLOUR_TAIL_LIST
+#define FDL_COLOUR_TAIL_LIST 4096
+#endif
+constexpr int kColourTailList = FDL_COLOUR_TAIL_LIST;
+#ifndef FDL_COLOUR_TAIL_CL
+#define FDL_COLOUR_TAIL_CL 16
+#endif
+// k_color_tail<32> on a 16-CTA cluster where the device allows (else 8, else one CTA)
+static void launch_colour_tail(int n, const int *rp, const int *ci, uint64_t salt, int *pcol, int *pin, int *pa,
+                               int *pb, int *pc, int *pr, cudaStream_t st) {
+    static DeviceCache cache{};
+    std::atomic<int> &slot = cache[current_device()];
+    int cl = slot.load();
+    if (!cl) {
+        cl = 1;
+        for (int c : {FDL_COLOUR_TAIL_CL, 8}) {
+            if (c <= 1) break;
+            if (c > 8 && cudaFuncSetAttribute(k_color_tail<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                             cudaSuccess)
+                continue;
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(c);
+            q.blockDim = dim3(kCoopThreads);
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = c;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, k_color_tail<32>, &q) == cudaSuccess && nc > 0) {
+                cl = c;
+                break;
+            }
+        }
+        (void)cudaGetLastError();
+        slot.store(cl);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(kCoopThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FDL_CK(cudaLaunchKernelEx(&cfg, k_color_tail<32>, n, rp, ci, salt, pcol, pin, pa, pb, pc, pr));
+    FDL_LAUNCH_CK();
+}
+
 static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJob &job, cudaStream_t st) {
     int n = g.n;
     const double avg = n ? (double)g.nnz / n : 0.0;
@@ -2751,14 +2873,17 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
     job.la.alloc((size_t)n * 4, st);
     job.lb.alloc((size_t)n * 4, st);
     job.indeg.alloc((size_t)n * 4, st);
-    job.counts.alloc((size_t)(kMaxRounds + 8) * 4, st);
-    FDL_CK(cudaMemsetAsync(job.counts.p, 0, (size_t)(kMaxRounds + 8) * 4, st));
+    job.counts.alloc((size_t)(kMaxRounds + 12) * 4, st);
+    FDL_CK(cudaMemsetAsync(job.counts.p, 0, (size_t)(kMaxRounds + 12) * 4, st));
     {
         const int *rp = g.rp, *ci = g.ci;
         int *pcol = color.as<int>(), *pin = job.indeg.as<int>(), *pa = job.la.as<int>(), *pb = job.lb.as<int>(),
             *pc = job.counts.as<int>(), *pr = job.counts.as<int>() + kMaxRounds;
         const int *gate = nullptr;
-        void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr, &gate};
+        // dense levels hand the deep tail of the DAG (lists shorter than this)
+        // to one cluster (k_color_tail)
+        int tail = avg > 18 ? kColourTailList : 0;
+        void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr, &gate, &tail};
         if (n <= kSmallColourN && avg >= kSmallColourMinDeg) {
             static DeviceCache attr{};
             std::atomic<int> &attr_slot = attr[current_device()];
@@ -2801,6 +2926,7 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             // for the other one to drain)
             DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, W == 32 ? kColourGridFracDense : kColourGridFrac,
                                          (int64_t)n * W));
+            if (tail) launch_colour_tail(n, rp, ci, salt, pcol, pin, pa, pb, pc, pr, st);
             tr.report(job.counts.as<int>());
         }
     }
