@@ -318,6 +318,9 @@ __device__ __forceinline__ bool edge_greater(double wa, unsigned long long ha, d
 // strict edge order (nbr[rp[v] + rank] = neighbour): re-pointing to the
 // heaviest FREE neighbour is then a cursor advance.  Longer rows are rescanned.
 template <int W> struct SortSlots { static constexpr int value = W == 1 ? 8 : 4; };
+// movers whose rescan is longer than this go to the whole CTA (k_match_coop, W > 1)
+constexpr int kMatchHeavyDeg = 2048;
+constexpr int kMatchHeavyCap = 64;
 
 // One thread ranks the <= S entries of row v in the strict edge order
 // (nbr[b + rank] = neighbour); returns the heaviest neighbour (-1: none).
@@ -444,7 +447,11 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
     unsigned *gbar = reinterpret_cast<unsigned *>(counts + kMaxRounds + 4);
     __shared__ int s_buf[kAppendCap];
     __shared__ int s_n, s_base;
-    if (threadIdx.x == 0) s_n = 0;
+    __shared__ int s_hm[kMatchHeavyCap], s_nhm;   // heavy movers of this CTA (W > 1)
+    __shared__ double s_aw[kCoopThreads / 32];
+    __shared__ unsigned long long s_ah[kCoopThreads / 32];
+    __shared__ int s_aj[kCoopThreads / 32];
+    if (threadIdx.x == 0) { s_n = 0; s_nhm = 0; }
     __syncthreads();
     CtaAppend app{s_buf, &s_n, &s_base};
     int stamp = 0;
@@ -717,16 +724,75 @@ __global__ void __launch_bounds__(kCoopThreads, kMatchMinBlocks) k_match_coop(in
                     bj = c < deg ? nbr[b + c] : -1;
                     if (lane == 0) cursor[v] = c;
                 }
-                const int bs = heaviest<W>(rescan ? v : -1, rp, ci, w, salt, lane,
+                // a rescan of a row longer than kMatchHeavyDeg: deferred to the
+                // whole CTA (below) -- a sub-warp walking a 10000-entry row took
+                // ~0.4 ms, and on dense levels a hub re-points in most rounds
+                int hslot = -1;
+                if (W > 1 && rescan && lane == 0 && rp[v + 1] - rp[v] > kMatchHeavyDeg) {
+                    hslot = atomicAdd(&s_nhm, 1);
+                    if (hslot < kMatchHeavyCap) s_hm[hslot] = v;
+                }
+                hslot = __shfl_sync(0xffffffffu, hslot, (threadIdx.x & 31) & ~(W - 1));
+                const bool deferred = hslot >= 0 && hslot < kMatchHeavyCap;
+                const int bs = heaviest<W>(rescan && !deferred ? v : -1, rp, ci, w, salt, lane,
                                            [&](int j) { return mate[j] >= 0; });
                 if (rescan) bj = bs;
-                if (v >= 0 && lane == 0) {
+                if (v >= 0 && lane == 0 && !deferred) {
                     ptr[v] = bj;
                     if (bj >= 0) app.push(v);
                 }
                 __syncthreads();
                 if (app.due(kAppendCap - kCoopThreads)) app.flush(out, gcount);
             }
+            // the deferred heavy rescans: the CTA's threads over the row, 4
+            // entries each in flight, then a CTA argmax in the strict order
+            const int nhm = min(s_nhm, kMatchHeavyCap);   // read after the loop's barrier
+            for (int i = 0; i < nhm; i++) {
+                const int hv = s_hm[i];
+                double bw = 0.0;
+                unsigned long long bh = 0;
+                int bj = -1;
+                const int kb = rp[hv], ke = rp[hv + 1];
+                for (int k0 = kb + threadIdx.x; k0 < ke; k0 += 4 * kCoopThreads) {
+                    int jj[4], mm[4];
+                    double ww[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int k = k0 + u * kCoopThreads;
+                        jj[u] = k < ke ? ci[k] : -1;
+                        ww[u] = k < ke ? w[k] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) mm[u] = jj[u] >= 0 ? mate[jj[u]] : 0;
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (jj[u] < 0 || mm[u] >= 0) continue;
+                        const unsigned long long h = edge_hash(salt, hv, jj[u]);
+                        if (bj < 0 || ww[u] > bw || (ww[u] == bw && h > bh)) { bw = ww[u]; bh = h; bj = jj[u]; }
+                    }
+                }
+                argmax_reduce<32>(bw, bh, bj);
+                if (lane_id() == 0) {
+                    s_aw[threadIdx.x >> 5] = bw;
+                    s_ah[threadIdx.x >> 5] = bh;
+                    s_aj[threadIdx.x >> 5] = bj;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    for (int q = 1; q < kCoopThreads / 32; q++)
+                        if (s_aj[q] >= 0 &&
+                            (bj < 0 || s_aw[q] > bw || (s_aw[q] == bw && s_ah[q] > bh))) {
+                            bw = s_aw[q];
+                            bh = s_ah[q];
+                            bj = s_aj[q];
+                        }
+                    ptr[hv] = bj;
+                    if (bj >= 0) app.push_safe(hv, out, gcount);
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) s_nhm = 0;
+            __syncthreads();
         }
         __syncthreads();
         app.flush(out, gcount);
@@ -2227,10 +2293,9 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks)
 // a constant number of times (the round-based JP rescans waiting vertices).
 // The JP rounds of k_color_coop, for a group of CTAs: the whole cooperative
 // grid (GridG) or, for the deep tail of a dense level's priority DAG (hundreds
-// to thousands of rounds with a handful of ready vertices each), one thread-
-// block cluster (ClusterG, k_color_tail): a cluster barrier instead of a grid
-// barrier per round.  In the grid, the rounds stop once a list is shorter than
-// tail_list (tail_list = 0: never) and the state goes to counts[kMaxRounds + 4..7].
+// to thousands of rounds with a handful of ready vertices each), its first
+// kColourTailCtas CTAs (SubG) with a barrier of their own.  In the grid, the
+// rounds stop once a list is shorter than tail_list (tail_list = 0: never).
 struct ColourShared {
     int *s_buf;
     int *s_n, *s_base;
@@ -2246,14 +2311,41 @@ struct GridG {
     __device__ int rank() const { return blockIdx.x; }
     __device__ void sync() { grid_sync_bo(g, bar); }
 };
-struct ClusterG {
-    __device__ int nb() const { return (int)cg::this_cluster().num_blocks(); }
-    __device__ int rank() const { return (int)cg::this_cluster().block_rank(); }
-    __device__ void sync() { cg::this_cluster().sync(); }
+// the first K CTAs of the cooperative grid (the others have exited), with a
+// barrier of their own in global memory: bar[0] arrivals, bar[1] generation
+struct SubG {
+    int K;
+    unsigned *bar;
+    __device__ int nb() const { return K; }
+    __device__ int rank() const { return blockIdx.x; }
+    __device__ void sync() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned g = ld_acquire_gpu(bar + 1);
+            __threadfence();
+            if (atomicAdd(bar, 1u) == (unsigned)K - 1) {
+                atomicExch(bar, 0u);
+                __threadfence();
+                atomicAdd(bar + 1, 1u);
+            } else {
+                while (ld_acquire_gpu(bar + 1) == g) {
+                }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
 };
-constexpr int kColourTailSlot = kMaxRounds + 6;   // counts[..]: {round, list parity, tail needed}
+#ifndef FDL_COLOUR_TAIL_CTAS
+#define FDL_COLOUR_TAIL_CTAS 48
+#endif
+// (R-MAT step 131.6 / 113.3 / 104.6 / 101.4 / 102.2 / 105.2 ms with 8 / 16 / 32 /
+// 48 / 64 / 96 tail CTAs; a 16-CTA cluster kernel instead measured 112.1)
+constexpr int kColourTailCtas = FDL_COLOUR_TAIL_CTAS;
+// returns {round, list parity} when it hands over (a list shorter than
+// tail_list), {-1, 0} when the colouring is complete
 template <int W, class G>
-__device__ void colour_rounds(G &grp, const ColourShared &sh, int n, const int *rp, const int *ci, uint64_t salt,
+__device__ int2 colour_rounds(G &grp, const ColourShared &sh, int n, const int *rp, const int *ci, uint64_t salt,
                               int *color, int *indeg, int *la, int *lb, int *counts, int *rounds_out, int r,
                               int parity, int tail_list, int stamp) {
     (void)n;
@@ -2280,14 +2372,7 @@ __device__ void colour_rounds(G &grp, const ColourShared &sh, int n, const int *
     };
     const int NB = grp.nb(), RK = grp.rank();
     while (cnt > 0 && r + 1 < kMaxRounds) {
-        if (tail_list > 0 && cnt < tail_list) {   // uniform: hand the rest to the cluster
-            if (RK == 0 && threadIdx.x == 0) {
-                counts[kColourTailSlot] = r;
-                counts[kColourTailSlot + 1] = in == la ? 0 : 1;
-                counts[kColourTailSlot + 2] = 1;
-            }
-            return;
-        }
+        if (tail_list > 0 && cnt < tail_list) return make_int2(r, in == la ? 0 : 1);   // uniform
         int *gcount = counts + r + 1;
         // W == 1: contiguous entries per CTA; W > 1: sub-warp slot s of CTA b
         // takes entry base + s * NB + b, so a short list (the deep rounds
@@ -2338,6 +2423,7 @@ __device__ void colour_rounds(G &grp, const ColourShared &sh, int n, const int *
         int *t = in; in = out; out = t;
     }
     if (RK == 0 && threadIdx.x == 0) rounds_out[0] = cnt == 0 ? r : -1;
+    return make_int2(-1, 0);
 }
 
 template <int W>
@@ -2415,29 +2501,20 @@ __global__ void __launch_bounds__(kCoopThreads, kCoopMinBlocks) k_color_coop(int
     round_stamp(stamp++);
     GridG grp{grid, gbar};
     const ColourShared sh{s_buf, &s_n, &s_base, s_bm, s_heavy, &s_nh, s_red};
-    colour_rounds<W>(grp, sh, n, rp, ci, salt, color, indeg, la, lb, counts, rounds_out, 0, 0, tail_list, stamp);
+    const int2 hand = colour_rounds<W>(grp, sh, n, rp, ci, salt, color, indeg, la, lb, counts, rounds_out, 0, 0,
+                                       tail_list, stamp);
+    if (hand.x < 0) return;
+    // the deep tail of the DAG (short lists, hundreds of rounds): the first
+    // kColourTailCtas CTAs alone, with a barrier of their own (a grid barrier
+    // over every CTA cost ~10 us a round); the others leave the SMs to the
+    // other streams' kernels
+    const int K = min((int)gridDim.x, kColourTailCtas);
+    if ((int)blockIdx.x >= K) return;
+    SubG sub{K, reinterpret_cast<unsigned *>(counts + kMaxRounds + 8)};
+    colour_rounds<W>(sub, sh, n, rp, ci, salt, color, indeg, la, lb, counts, rounds_out, hand.x, hand.y, 0,
+                     stamp + hand.x);
 }
 
-// The tail of a colouring k_color_coop handed over (counts[kColourTailSlot + 2]
-// set): the same rounds on one thread-block cluster.
-template <int W>
-__global__ void __launch_bounds__(kCoopThreads, 1) k_color_tail(int n, const int *rp, const int *ci, uint64_t salt,
-                                                                int *color, int *indeg, int *la, int *lb,
-                                                                int *counts, int *rounds_out) {
-    if (*(volatile const int *)&counts[kColourTailSlot + 2] == 0) return;
-    __shared__ int s_buf[kAppendCap];
-    __shared__ int s_n, s_base;
-    __shared__ unsigned s_bm[W > 1 ? kCoopThreads / W : 1][kBmWords];
-    __shared__ int s_heavy[W > 1 ? kHeavyCap : 1];
-    __shared__ int s_nh;
-    __shared__ int s_red[32];
-    if (threadIdx.x == 0) { s_n = 0; s_nh = 0; }
-    __syncthreads();
-    ClusterG grp;
-    const ColourShared sh{s_buf, &s_n, &s_base, s_bm, s_heavy, &s_nh, s_red};
-    colour_rounds<W>(grp, sh, n, rp, ci, salt, color, indeg, la, lb, counts, rounds_out,
-                     counts[kColourTailSlot], counts[kColourTailSlot + 1], 0, 1 << 20);
-}
 
 // Small dense levels (n <= kSmallColourN, average degree >= 64: the coarse levels of power-law
 // graphs: hundreds of colours, priority DAGs ~n deep): the same topological JP
@@ -2815,55 +2892,6 @@ static bool cluster_colour_ok() {
 #define FDL_COLOUR_TAIL_LIST 4096
 #endif
 constexpr int kColourTailList = FDL_COLOUR_TAIL_LIST;
-#ifndef FDL_COLOUR_TAIL_CL
-#define FDL_COLOUR_TAIL_CL 16
-#endif
-// k_color_tail<32> on a 16-CTA cluster where the device allows (else 8, else one CTA)
-static void launch_colour_tail(int n, const int *rp, const int *ci, uint64_t salt, int *pcol, int *pin, int *pa,
-                               int *pb, int *pc, int *pr, cudaStream_t st) {
-    static DeviceCache cache{};
-    std::atomic<int> &slot = cache[current_device()];
-    int cl = slot.load();
-    if (!cl) {
-        cl = 1;
-        for (int c : {FDL_COLOUR_TAIL_CL, 8}) {
-            if (c <= 1) break;
-            if (c > 8 && cudaFuncSetAttribute(k_color_tail<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                             cudaSuccess)
-                continue;
-            cudaLaunchConfig_t q = {};
-            q.gridDim = dim3(c);
-            q.blockDim = dim3(kCoopThreads);
-            cudaLaunchAttribute qa[1];
-            qa[0].id = cudaLaunchAttributeClusterDimension;
-            qa[0].val.clusterDim.x = c;
-            qa[0].val.clusterDim.y = 1;
-            qa[0].val.clusterDim.z = 1;
-            q.attrs = qa;
-            q.numAttrs = 1;
-            int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, k_color_tail<32>, &q) == cudaSuccess && nc > 0) {
-                cl = c;
-                break;
-            }
-        }
-        (void)cudaGetLastError();
-        slot.store(cl);
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cl);
-    cfg.blockDim = dim3(kCoopThreads);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    FDL_CK(cudaLaunchKernelEx(&cfg, k_color_tail<32>, n, rp, ci, salt, pcol, pin, pa, pb, pc, pr));
-    FDL_LAUNCH_CK();
-}
 
 static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJob &job, cudaStream_t st) {
     int n = g.n;
@@ -2881,7 +2909,7 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             *pc = job.counts.as<int>(), *pr = job.counts.as<int>() + kMaxRounds;
         const int *gate = nullptr;
         // dense levels hand the deep tail of the DAG (lists shorter than this)
-        // to one cluster (k_color_tail)
+        // to the first kColourTailCtas CTAs of the grid
         int tail = avg > 18 ? kColourTailList : 0;
         void *args[] = {&n, &rp, &ci, &salt, &pcol, &pin, &pa, &pb, &pc, &pr, &gate, &tail};
         if (n <= kSmallColourN && avg >= kSmallColourMinDeg) {
@@ -2926,7 +2954,6 @@ static void color_launch(const NatGraph &g, uint64_t salt, DBuf &color, ColourJo
             // for the other one to drain)
             DISPATCH_WC(avg, coop_launch(k_color_coop<W>, args, st, W == 32 ? kColourGridFracDense : kColourGridFrac,
                                          (int64_t)n * W));
-            if (tail) launch_colour_tail(n, rp, ci, salt, pcol, pin, pa, pb, pc, pr, st);
             tr.report(job.counts.as<int>());
         }
     }
