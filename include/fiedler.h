@@ -283,6 +283,141 @@ FIEDLER_API int fiedler_dist_op(fiedler_handle h, int32_t level, int32_t op, int
                                 const double *x, double *y, double *stat, const double *stat_in,
                                 const double *sign_slot, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Row-partitioned SETUP of the fine levels (Algorithm 3 Step 1, PAPER.md:117-125;
+ * DESIGN.md section 9).  Handle-free operations on one level's whole CSR
+ * (device arrays, the conventions of fiedler_create: int64 row_ptr, int32
+ * ascending columns, float64 weights; every rank holds the whole level), each
+ * run on the caller's OWN rows [r0, r1) only.  The driver
+ * (paper_1602_04386_b200/dist.py, PartitionedSetup) exchanges the state of the
+ * boundary rows between the calls with its collectives library:
+ *   matching   rounds of POINT, halo(ptr), RESOLVE, halo(mate) until no own
+ *              free row has a free neighbour anywhere (all-reduce);
+ *   aggregates LEADERS (count), exclusive scan of the counts over ranks,
+ *              IDS, halo(q), MATES, halo(q), JOIN, all-gather of q;
+ *   Galerkin   the coarse rows [a0, a1) of the caller's leaders (contiguous:
+ *              aggregates are numbered by increasing leader), all-gathered;
+ *   colouring  Jones-Plassmann rounds with halo(colour) until no row is left.
+ * The results are those of fiedler_create, bit for bit, for any partition
+ * (R2-R4: every rule is a strict order independent of the schedule).
+ * State arrays (mate, ptr, q, colour) are device int32 [n]; only own rows are
+ * written, ghost rows are read.  `stream` = cudaStream_t (NULL = legacy default
+ * stream).  Calls that return a count synchronise `stream`; the others only
+ * enqueue.  Errors: ARG (sizes, ranges, NULL pointers), CUDA, NOMEM.
+ * ------------------------------------------------------------------------- */
+
+/* Row partition of a level for `nranks` ranks: bounds[k] = the first row r with
+ * row_ptr[r] + r >= floor(k (nnz + n) / nranks) (rows + nonzeros balanced; the
+ * rule of fiedler_dist_plan), bounds[0] = 0, bounds[nranks] = n.  row_ptr:
+ * device; bounds: host [nranks + 1].  Synchronises. */
+FIEDLER_API int fiedler_pset_bounds(int64_t n, const int64_t *row_ptr, int32_t nranks, int64_t *bounds,
+                                    void *stream);
+
+/* Halo send lists of rank `rank`: for every peer p != rank (peer-major), the own
+ * rows that have a neighbour in p's rows, ascending.  By symmetry of the graph
+ * they are p's ghost rows of this rank, i.e. p's receive list from `rank`.
+ * bounds: host [nranks + 1] (fiedler_pset_bounds).  send_count: host [nranks]
+ * (0 for p == rank).  send_idx: device [sum send_count] of natural row ids, or
+ * NULL to get the counts only.  Synchronises. */
+FIEDLER_API int fiedler_pset_halo(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, int32_t nranks,
+                                  int32_t rank, const int64_t *bounds, int32_t *send_idx, int64_t *send_count,
+                                  void *stream);
+
+/* Halo pack / unpack of int32 state: out[k] = x[idx[k]] (gather) and
+ * x[idx[k]] = in[k] (scatter), k < count.  Device arrays; enqueue only. */
+FIEDLER_API int fiedler_pset_gather(const int32_t *x, const int32_t *idx, int64_t count, int32_t *out,
+                                    void *stream);
+/* x[idx[k]] = in[k], k < count (the unpack of fiedler_pset_gather's buffers). */
+FIEDLER_API int fiedler_pset_scatter(const int32_t *in, const int32_t *idx, int64_t count, int32_t *x,
+                                     void *stream);
+
+#define FIEDLER_PSET_POINT 0     /* matching: ptr[v] = the heaviest free neighbour of own free v        */
+#define FIEDLER_PSET_RESOLVE 1   /* matching: mate[v] = ptr[v] where ptr[ptr[v]] == v                   */
+
+/* One half-round of the parallel heavy-edge matching (Algorithm 1, PAPER.md:49-74,
+ * in the parallel order of R2) on own rows.  Edge order: (w, h) decreasing,
+ * h({u,v}) = splitmix64(salt ^ (min << 32 | max)), salt = splitmix64(seed ^
+ * (TAG_MATCH + level)).  mate[v] = -1 while v is free.  POINT: for own free v,
+ * ptr[v] = the first neighbour u in that order with mate[u] == -1 (-1 if none);
+ * *active (host) = the number of own rows with ptr[v] >= 0 (synchronises).
+ * RESOLVE: own free v with u = ptr[v] >= 0 and ptr[u] == v gets mate[v] = u
+ * (the handshake: the edge is the heaviest free edge at both ends, so the
+ * greedy heaviest-first matching of R2 takes it).  The caller initialises mate
+ * and ptr to -1 and exchanges ptr (after POINT) and mate (after RESOLVE) of the
+ * boundary rows; when the all-reduced *active is 0 the matching is maximal
+ * and equals R2's greedy matching. */
+FIEDLER_API int fiedler_pset_match(int32_t phase, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                   const double *weights, int64_t r0, int64_t r1, uint64_t seed, int32_t level,
+                                   int32_t *mate, int32_t *ptr, int64_t *active, void *stream);
+
+#define FIEDLER_PSET_LEADERS 0   /* *count = own leaders (synchronises)                                   */
+#define FIEDLER_PSET_IDS 1       /* q[v] = offset + rank of v among own leaders; -1 on other own rows     */
+#define FIEDLER_PSET_MATES 2     /* own matched non-leader v: q[v] = q[mate[v]]                           */
+#define FIEDLER_PSET_JOIN 3      /* own unmatched v with neighbours: q[v] = q[m(v)], m(v) heaviest nbr    */
+
+/* Aggregate numbering of R2 on own rows, given the maximal
+ * matching `mate`.  The leader of an aggregate is min(u, mate(u)) for a matched
+ * pair, the vertex itself if it has no neighbour; an unmatched vertex joins the
+ * aggregate of its heaviest neighbour m(v) (edge order of fiedler_pset_match),
+ * which is matched.  Aggregates are numbered by increasing leader: rank r's
+ * leaders get the contiguous ids [offset, offset + count_r), offset = the sum of
+ * the counts of the lower ranks.  Between IDS / MATES / JOIN the caller
+ * exchanges q of the boundary rows. */
+FIEDLER_API int fiedler_pset_aggregate(int32_t phase, int64_t n, const int64_t *row_ptr,
+                                       const int32_t *col_idx, const double *weights, int64_t r0, int64_t r1,
+                                       uint64_t seed, int32_t level, const int32_t *mate, int32_t *q,
+                                       int64_t offset, int64_t *count, void *stream);
+
+/* Galerkin product I L I^T (R3) for the coarse rows [a0, a1) given
+ * the WHOLE aggregate map q (device int32 [n]).  Phase 0: *count = the number of
+ * crossing contributions of those rows (an upper bound of their coarse
+ * nonzeros; synchronises).  Phase 1 (cap >= that bound): the coarse adjacency
+ * rows in CSR with LOCAL offsets: crp (device int64 [a1 - a0 + 1], crp[0] = 0),
+ * ascending columns cci (device int32), weights cw (device float64): W_c(A, B) =
+ * the left fold of the fine weights w_ij over the fine edges {i < j} with
+ * {q(i), q(j)} = {A, B} in (i, j) lexicographic order; *count = crp[a1 - a0]
+ * (synchronises). */
+FIEDLER_API int fiedler_pset_galerkin(int32_t phase, int64_t n, const int64_t *row_ptr,
+                                      const int32_t *col_idx, const double *weights, const int32_t *q,
+                                      int64_t a0, int64_t a1, int64_t cap, int64_t *crp, int32_t *cci,
+                                      double *cw, int64_t *count, void *stream);
+
+/* One Jones-Plassmann round of the colouring of R4 on own rows: an own
+ * uncoloured v (colour[v] == -1) all of whose neighbours u of higher priority
+ * (pi(u), u) > (pi(v), v), pi(x) = splitmix64(salt ^ x), salt =
+ * splitmix64(seed ^ (TAG_COLOR + level)), are coloured takes the smallest
+ * colour none of its coloured neighbours has -- the greedy first-fit colouring
+ * in decreasing priority, independent of the schedule.  out (host int64 [2]):
+ * {own rows still uncoloured, largest own colour (-1 if none)}; synchronises. */
+FIEDLER_API int fiedler_pset_colour(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, int64_t r0,
+                                    int64_t r1, uint64_t seed, int32_t level, int32_t *colour, int64_t *out,
+                                    void *stream);
+
+/* One level of a hierarchy built outside fiedler_create (fiedler_pset_*): the
+ * level's aggregate map, matching and colouring (device int32 [n_l]) and the
+ * next level's adjacency (device CSR, fiedler_create's conventions). */
+typedef struct fiedler_preset_level {
+    const int32_t *agg, *mate, *color;
+    int32_t ncolors, match_rounds, colour_rounds, reserved;
+    int64_t n_next, nnz_next;
+    const int64_t *rp_next;
+    const int32_t *ci_next;
+    const double *w_next;
+} fiedler_preset_level;
+
+/* fiedler_create whose levels 0..npreset-1 are given: their matching, aggregate
+ * map, colouring and next level are copied from `preset` instead of being
+ * computed (the preset levels must be levels fiedler_create would coarsen:
+ * n_l > coarsest_size, l + 1 < max_levels, not stalled by R9); the coarser
+ * levels, every layout and the solve state are built as by fiedler_create.
+ * The preset arrays are copied before the call returns (caller keeps
+ * ownership).  npreset = 0 is fiedler_create.  Errors: those of fiedler_create,
+ * ARG (npreset outside [0, max_levels - 1], NULL preset arrays, sizes). */
+FIEDLER_API int fiedler_create_preset(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                                      const double *weights, int32_t mem, const fiedler_opts *opts,
+                                      int32_t npreset, const fiedler_preset_level *preset,
+                                      fiedler_handle *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,7 +53,16 @@ FIEDLER_DOP_HALO_UNPACK = 12
 EXPORTED = ("fiedler_default_opts", "fiedler_create", "fiedler_solve", "fiedler_destroy",
             "fiedler_last_error", "fiedler_num_levels", "fiedler_level_size",
             "fiedler_level_export", "fiedler_level_apply", "fiedler_level_time",
-            "fiedler_dist_plan", "fiedler_dist_op")
+            "fiedler_dist_plan", "fiedler_dist_op", "fiedler_pset_bounds", "fiedler_pset_halo",
+            "fiedler_pset_gather", "fiedler_pset_scatter", "fiedler_pset_match", "fiedler_pset_aggregate",
+            "fiedler_pset_galerkin", "fiedler_pset_colour", "fiedler_create_preset")
+
+FIEDLER_PSET_POINT = 0
+FIEDLER_PSET_RESOLVE = 1
+FIEDLER_PSET_LEADERS = 0
+FIEDLER_PSET_IDS = 1
+FIEDLER_PSET_MATES = 2
+FIEDLER_PSET_JOIN = 3
 
 
 class fiedler_opts(ctypes.Structure):
@@ -95,6 +104,14 @@ class fiedler_dist_plan_info(ctypes.Structure):
                 ("send_count", ctypes.c_int64 * FIEDLER_MAX_RANKS),
                 ("recv_count", ctypes.c_int64 * FIEDLER_MAX_RANKS),
                 ("send_total", ctypes.c_int64), ("recv_total", ctypes.c_int64)]
+
+
+class fiedler_preset_level(ctypes.Structure):
+    _fields_ = [("agg", ctypes.c_void_p), ("mate", ctypes.c_void_p), ("color", ctypes.c_void_p),
+                ("ncolors", ctypes.c_int32), ("match_rounds", ctypes.c_int32),
+                ("colour_rounds", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("n_next", ctypes.c_int64), ("nnz_next", ctypes.c_int64),
+                ("rp_next", ctypes.c_void_p), ("ci_next", ctypes.c_void_p), ("w_next", ctypes.c_void_p)]
 
 
 class FiedlerError(RuntimeError):
@@ -142,6 +159,22 @@ def _load():
         lib.fiedler_dist_plan.argtypes = [P, i32, i32, i32, ctypes.POINTER(fiedler_dist_plan_info)]
         lib.fiedler_dist_op.restype = ctypes.c_int
         lib.fiedler_dist_op.argtypes = [P, i32, i32, i64, P, P, P, P, P, P]
+        u64 = ctypes.c_uint64
+        i64p = ctypes.POINTER(i64)
+        lib.fiedler_pset_bounds.argtypes = [i64, P, i32, i64p, P]
+        lib.fiedler_pset_halo.argtypes = [i64, P, P, i32, i32, i64p, P, i64p, P]
+        lib.fiedler_pset_gather.argtypes = [P, P, i64, P, P]
+        lib.fiedler_pset_scatter.argtypes = [P, P, i64, P, P]
+        lib.fiedler_pset_match.argtypes = [i32, i64, P, P, P, i64, i64, u64, i32, P, P, i64p, P]
+        lib.fiedler_pset_aggregate.argtypes = [i32, i64, P, P, P, i64, i64, u64, i32, P, P, i64, i64p, P]
+        lib.fiedler_pset_galerkin.argtypes = [i32, i64, P, P, P, P, i64, i64, i64, P, P, P, i64p, P]
+        lib.fiedler_pset_colour.argtypes = [i64, P, P, i64, i64, u64, i32, P, i64p, P]
+        lib.fiedler_create_preset.argtypes = [i64, i64, P, P, P, i32, ctypes.POINTER(fiedler_opts), i32,
+                                              ctypes.POINTER(fiedler_preset_level), ctypes.POINTER(P)]
+        for f in ("fiedler_pset_bounds", "fiedler_pset_halo", "fiedler_pset_gather", "fiedler_pset_scatter",
+                  "fiedler_pset_match", "fiedler_pset_aggregate", "fiedler_pset_galerkin",
+                  "fiedler_pset_colour", "fiedler_create_preset"):
+            getattr(lib, f).restype = ctypes.c_int
         lib.fiedler_level_apply.restype = ctypes.c_int
         lib.fiedler_level_apply.argtypes = [P, i32, i32, i32, P, P, i32, ctypes.POINTER(ctypes.c_double)]
         _lib = lib
@@ -279,6 +312,90 @@ def fiedler_dist_op(handle, level, op, arg=0, x=None, y=None, stat=None, stat_in
         return t.data_ptr()
     _check(_load().fiedler_dist_op(handle, level, op, int(arg), ptr(x), ptr(y), ptr(stat), ptr(stat_in),
                                    ptr(sign_slot), stream))
+
+
+# ---------------------------------------------------------------- partitioned setup
+def _dptr(t, itemsize=None):
+    """Device pointer of a contiguous CUDA tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous() or (itemsize and t.dtype.itemsize != itemsize):
+        raise TypeError("expected a contiguous CUDA tensor of %s-byte items" % itemsize)
+    return t.data_ptr()
+
+
+def fiedler_pset_bounds(n, row_ptr, nranks, stream=None):
+    """Row bounds [nranks + 1] of the rows + nonzeros balanced partition (list of int)."""
+    b = (ctypes.c_int64 * (nranks + 1))()
+    _check(_load().fiedler_pset_bounds(int(n), _dptr(row_ptr, 8), int(nranks), b, stream))
+    return list(b)
+
+
+def fiedler_pset_halo(n, row_ptr, col_idx, nranks, rank, bounds, send_idx=None, stream=None):
+    """Send counts per peer (list); fills send_idx (CUDA int32) when given."""
+    b = (ctypes.c_int64 * (nranks + 1))(*bounds)
+    c = (ctypes.c_int64 * nranks)()
+    _check(_load().fiedler_pset_halo(int(n), _dptr(row_ptr, 8), _dptr(col_idx, 4), int(nranks), int(rank), b,
+                                     _dptr(send_idx, 4), c, stream))
+    return list(c)
+
+
+def fiedler_pset_gather(x, idx, count, out, stream=None):
+    _check(_load().fiedler_pset_gather(_dptr(x, 4), _dptr(idx, 4), int(count), _dptr(out, 4), stream))
+
+
+def fiedler_pset_scatter(inp, idx, count, x, stream=None):
+    _check(_load().fiedler_pset_scatter(_dptr(inp, 4), _dptr(idx, 4), int(count), _dptr(x, 4), stream))
+
+
+def fiedler_pset_match(phase, n, rp, ci, w, r0, r1, seed, level, mate, ptr, stream=None):
+    """One matching half-round; returns the active count for POINT (else 0)."""
+    a = ctypes.c_int64(0)
+    _check(_load().fiedler_pset_match(int(phase), int(n), _dptr(rp, 8), _dptr(ci, 4), _dptr(w, 8), int(r0),
+                                      int(r1), int(seed) & (2**64 - 1), int(level), _dptr(mate, 4), _dptr(ptr, 4),
+                                      ctypes.byref(a), stream))
+    return a.value
+
+
+def fiedler_pset_aggregate(phase, n, rp, ci, w, r0, r1, seed, level, mate, q, offset=0, stream=None):
+    """One aggregate-numbering phase; returns the own leader count for LEADERS / IDS."""
+    c = ctypes.c_int64(0)
+    _check(_load().fiedler_pset_aggregate(int(phase), int(n), _dptr(rp, 8), _dptr(ci, 4), _dptr(w, 8), int(r0),
+                                          int(r1), int(seed) & (2**64 - 1), int(level), _dptr(mate, 4),
+                                          _dptr(q, 4), int(offset), ctypes.byref(c), stream))
+    return c.value
+
+
+def fiedler_pset_galerkin(phase, n, rp, ci, w, q, a0, a1, cap=0, crp=None, cci=None, cw=None, stream=None):
+    """Phase 0: contribution count; phase 1: coarse rows [a0, a1) into crp / cci / cw, returns their nnz."""
+    c = ctypes.c_int64(0)
+    _check(_load().fiedler_pset_galerkin(int(phase), int(n), _dptr(rp, 8), _dptr(ci, 4), _dptr(w, 8), _dptr(q, 4),
+                                         int(a0), int(a1), int(cap), _dptr(crp, 8), _dptr(cci, 4), _dptr(cw, 8),
+                                         ctypes.byref(c), stream))
+    return c.value
+
+
+def fiedler_pset_colour(n, rp, ci, r0, r1, seed, level, colour, stream=None):
+    """One Jones-Plassmann round; returns (own rows left uncoloured, largest own colour)."""
+    out = (ctypes.c_int64 * 2)()
+    _check(_load().fiedler_pset_colour(int(n), _dptr(rp, 8), _dptr(ci, 4), int(r0), int(r1),
+                                       int(seed) & (2**64 - 1), int(level), _dptr(colour, 4), out, stream))
+    return out[0], out[1]
+
+
+def fiedler_create_preset(n, nnz, row_ptr, col_idx, weights, opts, presets):
+    """fiedler_create with levels 0..len(presets)-1 given (fiedler_preset_level list)."""
+    prp, m0 = _ptr(row_ptr, np.int64)
+    pci, m1 = _ptr(col_idx, np.int32)
+    pw, m2 = _ptr(weights, np.float64)
+    if len({m0, m1, m2}) != 1:
+        raise ValueError("row_ptr, col_idx and weights must live in the same memory")
+    arr = (fiedler_preset_level * max(len(presets), 1))(*presets)
+    h = ctypes.c_void_p()
+    _check(_load().fiedler_create_preset(int(n), int(nnz), prp, pci, pw, m0,
+                                         ctypes.byref(opts) if opts is not None else None, len(presets),
+                                         arr if presets else None, ctypes.byref(h)))
+    return h.value
 
 
 class FiedlerSolver:

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfiedler.so")
-SOURCES = ["fdl_prims.cu", "fdl_setup.cu", "fdl_solve.cu", "fdl_api.cu"]
+SOURCES = ["fdl_prims.cu", "fdl_setup.cu", "fdl_solve.cu", "fdl_api.cu", "fdl_pset.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",

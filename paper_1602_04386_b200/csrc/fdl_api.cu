@@ -202,22 +202,6 @@ int prepare_solve(Handle &h, const SolveCfg &cfg);
 
 using namespace fdl;
 
-#define API_BEGIN try {
-#define API_END                                                  \
-    }                                                            \
-    catch (const fdl::Error &e) {                                \
-        fdl::set_error(e.what());                                \
-        return e.code;                                           \
-    }                                                            \
-    catch (const std::bad_alloc &) {                             \
-        fdl::set_error("host allocation failed");                \
-        return FIEDLER_ERR_NOMEM;                                \
-    }                                                            \
-    catch (const std::exception &e) {                            \
-        fdl::set_error(e.what());                                \
-        return FIEDLER_ERR_INTERNAL;                             \
-    }
-
 extern "C" {
 
 void fiedler_default_opts(fiedler_opts *o) {
@@ -240,6 +224,12 @@ const char *fiedler_last_error(void) { return fdl::g_last_error.c_str(); }
 int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
                    const double *weights, int32_t mem, const fiedler_opts *opts,
                    fiedler_handle *out) {
+    return fiedler_create_preset(n, nnz, row_ptr, col_idx, weights, mem, opts, 0, nullptr, out);
+}
+
+int fiedler_create_preset(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                          const double *weights, int32_t mem, const fiedler_opts *opts, int32_t npreset,
+                          const fiedler_preset_level *preset, fiedler_handle *out) {
     API_BEGIN
     fdl::set_error("");
     FDL_REQUIRE(out != nullptr, FIEDLER_ERR_ARG, "out is NULL");
@@ -255,6 +245,17 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     FDL_REQUIRE(o.coarsest_size >= 2 && o.max_levels >= 1 && o.max_levels <= FIEDLER_MAX_LEVELS &&
                     o.gs_sweeps >= 0 && o.power_iters >= 0,
                 FIEDLER_ERR_ARG, "invalid options");
+    FDL_REQUIRE(npreset >= 0 && npreset < o.max_levels && (npreset == 0 || preset), FIEDLER_ERR_ARG,
+                "npreset outside [0, max_levels - 1] or NULL preset");
+    for (int l = 0; l < npreset; l++) {
+        const fiedler_preset_level &P = preset[l];
+        const int64_t nl = l == 0 ? n : preset[l - 1].n_next;
+        FDL_REQUIRE(P.agg && P.mate && P.color && P.rp_next && (P.nnz_next == 0 || (P.ci_next && P.w_next)),
+                    FIEDLER_ERR_ARG, "NULL preset array");
+        FDL_REQUIRE(P.n_next >= 2 && P.n_next < nl && P.nnz_next >= 0 && P.nnz_next < (int64_t(1) << 31) - 1 &&
+                        P.ncolors >= 1 && P.ncolors <= nl,
+                    FIEDLER_ERR_ARG, "preset level sizes out of range");
+    }
     trace_mark(nullptr, "create: enter");
     check_device(o.device);
     trace_mark(nullptr, "create: check_device");
@@ -262,6 +263,7 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     std::unique_ptr<Handle> h(new Handle());
     h->device = o.device;
     h->opts = o;
+    h->preset.assign(preset, preset + npreset);
     // The handle always works on a stream of its own: every device buffer it
     // allocates is freed on that stream, which lives until fiedler_destroy.  A
     // caller's stream (opts->stream) is joined with events (StreamJoin).
@@ -327,6 +329,7 @@ int fiedler_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t
     trace_mark(st, "create: input staging");
     const long long l0 = g_launch_count;
     build_hierarchy(*h, std::move(g0));
+    h->preset.clear();   // copied (build_hierarchy synchronises the stream)
     prepare_solve(*h, cfg_of(o));
     trace_mark(st, "create: prepare_solve");
     if (trace_enabled()) {

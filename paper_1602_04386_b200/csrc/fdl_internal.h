@@ -135,6 +135,9 @@ struct Handle {
     SmallArena arena;                 // small buffers of the create (fdl_common.cuh); freed last
     fiedler_opts opts{};
     std::vector<Level> levels;
+    // fiedler_create_preset: levels 0..preset.size()-1 copied from these
+    // (matching, aggregates, colouring, next level) instead of computed
+    std::vector<fiedler_preset_level> preset;
     int n0 = 0;
     // solve state
     DBuf xa, xb;             // level vectors (sized n0)
@@ -193,4 +196,23 @@ void dist_op(Handle &h, int level, int op, int64_t arg, const double *x, double 
 // fiedler_level_time: CUDA-event timing of `reps` back-to-back row passes
 void time_level_op(Handle &h, int level, int op, int reps, double *ms_per_rep, double *bytes_per_rep);
 
+
+// error translation of the extern "C" entry points (fdl_api.cu, fdl_pset.cu)
+void set_error(const std::string &m);
 }  // namespace fdl
+
+#define API_BEGIN try {
+#define API_END                                                  \
+    }                                                            \
+    catch (const fdl::Error &e) {                                \
+        fdl::set_error(e.what());                                \
+        return e.code;                                           \
+    }                                                            \
+    catch (const std::bad_alloc &) {                             \
+        fdl::set_error("host allocation failed");                \
+        return FIEDLER_ERR_NOMEM;                                \
+    }                                                            \
+    catch (const std::exception &e) {                            \
+        fdl::set_error(e.what());                                \
+        return FIEDLER_ERR_INTERNAL;                             \
+    }

@@ -3582,6 +3582,35 @@ struct LevelFeed {
 };
 
 // levels first, first + stride, ... (one helper thread and stream per residue)
+// fiedler_create_preset: a level's matching / aggregates and the next level
+// given by the caller (fiedler_pset_*), copied into the handle's buffers
+static int take_preset_match(const fiedler_preset_level &P, int n, Level &L, cudaStream_t st) {
+    L.q_nat.alloc((size_t)n * 4, st);
+    L.mate_nat.alloc((size_t)n * 4, st);
+    FDL_CK(cudaMemcpyAsync(L.q_nat.p, P.agg, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    FDL_CK(cudaMemcpyAsync(L.mate_nat.p, P.mate, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    L.match_rounds = P.match_rounds;
+    return (int)P.n_next;
+}
+
+static NatGraph take_preset_graph(const fiedler_preset_level &P, cudaStream_t st) {
+    NatGraph out;
+    out.n = (int)P.n_next;
+    out.nnz = (int)P.nnz_next;
+    out.own_rp.alloc(padded((size_t)(out.n + 1) * 4), st);
+    convert_row_ptr(P.rp_next, out.n, out.nnz, out.own_rp.as<int>(), st);
+    out.own_ci.alloc(padded((size_t)std::max(out.nnz, 1) * 4), st);
+    out.own_w.alloc(padded((size_t)std::max(out.nnz, 1) * 8), st);
+    if (out.nnz) {
+        FDL_CK(cudaMemcpyAsync(out.own_ci.p, P.ci_next, (size_t)out.nnz * 4, cudaMemcpyDeviceToDevice, st));
+        FDL_CK(cudaMemcpyAsync(out.own_w.p, P.w_next, (size_t)out.nnz * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    out.rp = out.own_rp.as<int>();
+    out.ci = out.own_ci.as<int>();
+    out.w = out.own_w.as<double>();
+    return out;
+}
+
 static void colour_and_layout(Handle &h, std::vector<NatGraph> &graphs, std::vector<cudaEvent_t> &lev_ev,
                               LevelFeed &feed, PhaseTimes &pt, cudaStream_t sb, int first, int stride) {
     for (int ell = first; feed.wait_for(ell); ell += stride) {
@@ -3592,10 +3621,20 @@ static void colour_and_layout(Handle &h, std::vector<NatGraph> &graphs, std::vec
         FDL_CK(cudaStreamWaitEvent(sb, ell == 0 && h.ev_pattern ? h.ev_pattern : lev_ev[ell], 0));
         ColourJob job;
         pt.mark(ell, 2, 0, sb);
-        color_launch(g, salt_color(h.opts.seed, ell), L.color_nat, job, sb);
-        pt.mark(ell, 2, 1, sb);
         int cr[3];
-        readback(sb, {{cr, job.counts.as<int>() + kMaxRounds, 8}, {cr + 2, job.mx.p, 4}});
+        if (ell < (int)h.preset.size()) {   // fiedler_create_preset: the colouring is given
+            const fiedler_preset_level &P = h.preset[ell];
+            L.color_nat.alloc((size_t)g.n * 4, sb);
+            FDL_CK(cudaMemcpyAsync(L.color_nat.p, P.color, (size_t)g.n * 4, cudaMemcpyDeviceToDevice, sb));
+            cr[0] = P.colour_rounds;
+            cr[1] = 0;
+            cr[2] = P.ncolors - 1;
+            pt.mark(ell, 2, 1, sb);
+        } else {
+            color_launch(g, salt_color(h.opts.seed, ell), L.color_nat, job, sb);
+            pt.mark(ell, 2, 1, sb);
+            readback(sb, {{cr, job.counts.as<int>() + kMaxRounds, 8}, {cr + 2, job.mx.p, 4}});
+        }
         FDL_REQUIRE(cr[0] >= 0 && cr[1] == 0, FIEDLER_ERR_INTERNAL, "colouring did not terminate");
         L.color_rounds = cr[0];
         if (ell == 0 && h.ev_pattern) FDL_CK(cudaStreamWaitEvent(sb, lev_ev[0], 0));
@@ -3662,19 +3701,25 @@ void build_hierarchy(Handle &h, NatGraph &&g0) {
             FDL_CK(cudaEventRecord(lev_ev[ell], st));
             feed.publish(ell + 1);
             bool coarsen = cur.n > o.coarsest_size && ell + 1 < maxl;
+            const bool pre = ell < (int)h.preset.size();
+            FDL_REQUIRE(!pre || coarsen, FIEDLER_ERR_ARG,
+                        "a preset level must be one fiedler_create coarsens (n > coarsest_size, below max_levels)");
             if (coarsen) {
                 pt.mark(ell, 0, 0, st);
-                int c = hec_parallel(cur, salt_match(o.seed, ell), L.q_nat, L.mate_nat, L.match_rounds, st);
+                int c = pre ? take_preset_match(h.preset[ell], cur.n, L, st)
+                            : hec_parallel(cur, salt_match(o.seed, ell), L.q_nat, L.mate_nat, L.match_rounds, st);
                 pt.mark(ell, 0, 1, st);
                 trace_mark(st, ell == 0 ? "L0 matching" : "Lk matching");
                 // stall guard (R9): stop when HEC no longer shrinks the graph
                 if ((double)c > 0.95 * (double)cur.n || c < 2) {
+                    FDL_REQUIRE(!pre, FIEDLER_ERR_ARG, "a preset level stalls the coarsening (R9)");
                     coarsen = false;
                     L.q_nat.release();
                     L.mate_nat.release();
                 } else {
                     pt.mark(ell, 1, 0, st);
-                    NatGraph next = galerkin(cur, L.q_nat.as<int>(), c, st);
+                    NatGraph next = pre ? take_preset_graph(h.preset[ell], st)
+                                        : galerkin(cur, L.q_nat.as<int>(), c, st);
                     pt.mark(ell, 1, 1, st);
                     trace_mark(st, ell == 0 ? "L0 galerkin" : "Lk galerkin");
                     graphs.emplace_back(std::move(next));

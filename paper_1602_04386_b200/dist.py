@@ -70,6 +70,12 @@ class Comm:
     def all_to_all(self, out, inp, out_splits, in_splits):  # pragma: no cover - interface
         raise NotImplementedError
 
+    def allgatherv(self, out, inp, sizes):
+        """out = concatenation over ranks of every rank's `inp` (rank k's has
+        sizes[k] items).  Default: one all-to-all with the input repeated."""
+        rep = inp.unsqueeze(0).expand(self.nranks, inp.numel()).reshape(-1) if inp.numel() else inp
+        self.all_to_all(out, rep.contiguous(), list(sizes), [inp.numel()] * self.nranks)
+
 
 class TorchComm(Comm):
     """torch.distributed process group (NCCL for CUDA tensors, gloo for CPU)."""
@@ -91,6 +97,18 @@ class TorchComm(Comm):
         self.dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits),
                                     input_split_sizes=list(in_splits), group=self.group)
 
+    def allgatherv(self, out, inp, sizes):
+        # equal-size all-gather of the inputs padded to the largest, then compaction
+        m = max(sizes)
+        pad = torch.zeros(max(m, 1), dtype=inp.dtype, device=inp.device)
+        pad[:inp.numel()] = inp
+        parts = [torch.empty_like(pad) for _ in range(self.nranks)]
+        self.dist.all_gather(parts, pad, group=self.group)
+        o = 0
+        for k, sz in enumerate(sizes):
+            out[o:o + sz] = parts[k][:sz]
+            o += sz
+
 
 class LocalComm(Comm):
     """Single rank: every collective is the identity."""
@@ -103,6 +121,9 @@ class LocalComm(Comm):
 
     def all_to_all(self, out, inp, out_splits, in_splits):
         out.copy_(inp)
+
+    def allgatherv(self, out, inp, sizes):
+        out[:inp.numel()] = inp
 
 
 class LibOps:
@@ -290,3 +311,273 @@ class PartitionedSolver:
         v = self._allgather(0, vnat)
         res = rq.cpu()
         return v[:ops.sizes[0]].clone(), float(res[0]), float(res[1])
+
+
+# =========================================================================
+# Row-partitioned setup of the fine levels (Algorithm 3 Step 1)
+# =========================================================================
+@dataclass
+class SetupGraph:
+    """One level's whole adjacency (every rank holds it): int64 row offsets,
+    int32 columns, float64 weights (the conventions of fiedler_create)."""
+    n: int
+    nnz: int
+    rp: object
+    ci: object
+    w: object
+
+
+@dataclass
+class PresetLevel:
+    """A partitioned level's setup results, gathered on every rank: the aggregate
+    map q, the matching, the colouring (whole arrays) and the next level."""
+    level: int
+    q: object
+    mate: object
+    colour: object
+    ncolors: int
+    match_rounds: int
+    colour_rounds: int
+    nxt: SetupGraph
+    row_bounds: List[int]
+
+
+class LibSetupOps:
+    """Setup operations backed by libfiedler's fiedler_pset_* kernels on one GPU;
+    every call is issued on one stream shared with torch's tensor work."""
+
+    def __init__(self, device, stream=None):
+        self.device = device
+        self.torch_stream = torch.cuda.Stream(device) if stream is None else torch.cuda.ExternalStream(stream)
+        self.stream = self.torch_stream.cuda_stream
+
+    def stream_ctx(self):
+        return torch.cuda.stream(self.torch_stream)
+
+    def full(self, n, value, dtype):
+        return torch.full((max(n, 1),), value, dtype=dtype, device=self.device)
+
+    def bounds(self, g, nranks):
+        from . import fiedler_pset_bounds
+        return fiedler_pset_bounds(g.n, g.rp, nranks, self.stream)
+
+    def halo(self, g, nranks, rank, bounds):
+        from . import fiedler_pset_halo
+        counts = fiedler_pset_halo(g.n, g.rp, g.ci, nranks, rank, bounds, None, self.stream)
+        idx = self.full(sum(counts), 0, torch.int32)
+        if sum(counts):
+            fiedler_pset_halo(g.n, g.rp, g.ci, nranks, rank, bounds, idx, self.stream)
+        return idx, counts
+
+    def gather(self, x, idx, count, out):
+        from . import fiedler_pset_gather
+        fiedler_pset_gather(x, idx, count, out, self.stream)
+
+    def scatter(self, inp, idx, count, x):
+        from . import fiedler_pset_scatter
+        fiedler_pset_scatter(inp, idx, count, x, self.stream)
+
+    def match(self, phase, g, r0, r1, seed, level, mate, ptr):
+        from . import fiedler_pset_match
+        return fiedler_pset_match(phase, g.n, g.rp, g.ci, g.w, r0, r1, seed, level, mate, ptr, self.stream)
+
+    def aggregate(self, phase, g, r0, r1, seed, level, mate, q, offset=0):
+        from . import fiedler_pset_aggregate
+        return fiedler_pset_aggregate(phase, g.n, g.rp, g.ci, g.w, r0, r1, seed, level, mate, q, offset,
+                                      self.stream)
+
+    def galerkin(self, phase, g, q, a0, a1, cap=0, crp=None, cci=None, cw=None):
+        from . import fiedler_pset_galerkin
+        return fiedler_pset_galerkin(phase, g.n, g.rp, g.ci, g.w, q, a0, a1, cap, crp, cci, cw, self.stream)
+
+    def colour(self, g, r0, r1, seed, level, colour):
+        from . import fiedler_pset_colour
+        return fiedler_pset_colour(g.n, g.rp, g.ci, r0, r1, seed, level, colour, self.stream)
+
+
+class PartitionedSetup:
+    """Algorithm 3 Step 1 with row-partitioned fine levels.
+
+    Every rank holds the current level's whole CSR and owns the rows
+    [bounds[r], bounds[r+1]) (rows + nonzeros balanced).  Per level:
+
+      * heavy-edge matching (Algorithm 1, parallel order R2):
+        handshake rounds POINT / RESOLVE on own rows with the boundary rows'
+        ptr and mate exchanged after each half-round (one all-to-all each),
+        until the all-reduced count of own free rows with a free neighbour is 0;
+      * aggregate numbering: own leader counts, their exclusive
+        scan over ranks (an all-reduce of the count vector) gives each rank a
+        contiguous id range; IDS, MATES and JOIN with q exchanged in between;
+        q and the matching are all-gathered;
+      * Galerkin product (R3) of the rank's own coarse rows (the
+        aggregates of its leaders), all-gathered into the next level;
+      * colouring (R4): Jones-Plassmann rounds with the boundary colours
+        exchanged after every round, all-gathered.
+
+    Levels with fewer than `min_rows` vertices are left to fiedler_create on
+    every rank (fiedler_create_preset takes the partitioned levels as given).
+    The result equals fiedler_create's hierarchy bit for bit (every rule is a
+    strict order, independent of partition and schedule)."""
+
+    def __init__(self, ops, comm: Comm, min_rows: int = 1 << 20, coarsest_size: int = 25,
+                 max_levels: int = 50, seed: int = 0, stall_ratio: float = 0.95):
+        self.ops = ops
+        self.comm = comm
+        self.min_rows = min_rows
+        self.coarsest_size = coarsest_size
+        self.max_levels = max_levels
+        self.seed = seed
+        self.stall_ratio = stall_ratio
+        self.bytes_sent = 0          # halo + all-gather bytes this rank sent in the last run
+        self.rounds = []             # (match rounds, colour rounds) per partitioned level
+
+    # ---------------------------------------------------------------- helpers
+    def _scalar_sum(self, v):
+        t = torch.tensor([int(v)], dtype=torch.int64, device=self._dev)
+        self.comm.allreduce_sum(t)
+        return int(t.item())
+
+    def _per_rank(self, v):
+        """[value of every rank] (an all-reduce of a one-hot vector)."""
+        t = torch.zeros(self.comm.nranks, dtype=torch.int64, device=self._dev)
+        t[self.comm.rank] = int(v)
+        self.comm.allreduce_sum(t)
+        return [int(x) for x in t.tolist()]
+
+    def _exchange(self, x):
+        """Own boundary rows of x -> the other ranks' ghost rows (int32 state)."""
+        if self.comm.nranks == 1:
+            return
+        ops = self.ops
+        ops.gather(x, self._send_idx, self._ns, self._sbuf)
+        self.comm.all_to_all(self._rbuf[:self._nr], self._sbuf[:self._ns], self._recv_counts, self._send_counts)
+        ops.scatter(self._rbuf, self._recv_idx, self._nr, x)
+        self.bytes_sent += 4 * self._ns
+
+    def _allgather(self, own, sizes, dtype):
+        out = self.ops.full(sum(sizes), 0, dtype)
+        self.comm.allgatherv(out[:sum(sizes)], own, sizes)
+        self.bytes_sent += own.element_size() * own.numel() * max(self.comm.nranks - 1, 0)
+        return out
+
+    # ---------------------------------------------------------------- run
+    def run(self, g: SetupGraph) -> List[PresetLevel]:
+        ctx = getattr(self.ops, "stream_ctx", None)
+        if ctx is None:
+            return self._run(g)
+        with ctx():
+            return self._run(g)
+
+    def _run(self, g):
+        self._dev = g.rp.device
+        self.bytes_sent = 0
+        self.rounds = []
+        out = []
+        ell = 0
+        while g.n > self.coarsest_size and ell + 1 < self.max_levels and g.n >= self.min_rows:
+            lev = self._level(g, ell)
+            if lev is None:      # the matching stalls (R9): fiedler_create decides this level
+                break
+            out.append(lev)
+            g = lev.nxt
+            ell += 1
+        return out
+
+    def _level(self, g, ell):
+        from . import (FIEDLER_PSET_IDS, FIEDLER_PSET_JOIN, FIEDLER_PSET_LEADERS, FIEDLER_PSET_MATES,
+                       FIEDLER_PSET_POINT, FIEDLER_PSET_RESOLVE)
+        ops, comm = self.ops, self.comm
+        N, rk = comm.nranks, comm.rank
+        i32 = torch.int32
+        bounds = ops.bounds(g, N)
+        r0, r1 = bounds[rk], bounds[rk + 1]
+        # halo plan: send lists by the library, receive lists = the peers' send lists to us
+        self._send_idx, self._send_counts = ops.halo(g, N, rk, bounds)
+        sc = torch.tensor(self._send_counts, dtype=torch.int64, device=self._dev)
+        rc = torch.zeros_like(sc)
+        comm.all_to_all(rc, sc, [1] * N, [1] * N)
+        self._recv_counts = [int(x) for x in rc.tolist()]
+        self._ns, self._nr = sum(self._send_counts), sum(self._recv_counts)
+        self._recv_idx = ops.full(self._nr, 0, i32)
+        comm.all_to_all(self._recv_idx[:self._nr], self._send_idx[:self._ns], self._recv_counts, self._send_counts)
+        self._sbuf = ops.full(self._ns, 0, i32)
+        self._rbuf = ops.full(self._nr, 0, i32)
+
+        # heavy-edge matching: handshake rounds
+        mate = ops.full(g.n, -1, i32)
+        ptr = ops.full(g.n, -1, i32)
+        mrounds = 0
+        while True:
+            act = ops.match(FIEDLER_PSET_POINT, g, r0, r1, self.seed, ell, mate, ptr)
+            if self._scalar_sum(act) == 0:
+                break
+            self._exchange(ptr)
+            ops.match(FIEDLER_PSET_RESOLVE, g, r0, r1, self.seed, ell, mate, ptr)
+            self._exchange(mate)
+            mrounds += 1
+        # aggregates numbered by increasing leader: contiguous id range per rank
+        own_leaders = ops.aggregate(FIEDLER_PSET_LEADERS, g, r0, r1, self.seed, ell, mate, ptr)
+        counts = self._per_rank(own_leaders)
+        c = sum(counts)
+        if c > self.stall_ratio * g.n or c < 2:
+            return None
+        a0 = sum(counts[:rk])
+        a1 = a0 + counts[rk]
+        q = ops.full(g.n, -1, i32)
+        ops.aggregate(FIEDLER_PSET_IDS, g, r0, r1, self.seed, ell, mate, q, a0)
+        self._exchange(q)
+        ops.aggregate(FIEDLER_PSET_MATES, g, r0, r1, self.seed, ell, mate, q)
+        self._exchange(q)
+        ops.aggregate(FIEDLER_PSET_JOIN, g, r0, r1, self.seed, ell, mate, q)
+        rows = [bounds[k + 1] - bounds[k] for k in range(N)]
+        q_full = self._allgather(q[r0:r1], rows, i32)
+        mate_full = self._allgather(mate[r0:r1], rows, i32)
+
+        # Galerkin product of the own coarse rows [a0, a1), gathered
+        cap = ops.galerkin(0, g, q_full, a0, a1)
+        crp = ops.full(a1 - a0 + 1, 0, torch.int64)
+        cci = ops.full(cap, 0, i32)
+        cw = ops.full(cap, 0.0, torch.float64)
+        own_nnz = ops.galerkin(1, g, q_full, a0, a1, cap, crp, cci, cw)
+        nnzs = self._per_rank(own_nnz)
+        nnz_c = sum(nnzs)
+        ci_next = self._allgather(cci[:own_nnz], nnzs, i32)
+        w_next = self._allgather(cw[:own_nnz], nnzs, torch.float64)
+        rp_own = crp[:a1 - a0] + sum(nnzs[:rk])
+        rp_next = self._allgather(rp_own, counts, torch.int64)
+        rp_full = ops.full(c + 1, 0, torch.int64)
+        rp_full[:c] = rp_next[:c]
+        rp_full[c] = nnz_c
+        nxt = SetupGraph(n=c, nnz=nnz_c, rp=rp_full[:c + 1], ci=ci_next[:max(nnz_c, 1)], w=w_next[:max(nnz_c, 1)])
+
+        # colouring: Jones-Plassmann rounds
+        colour = ops.full(g.n, -1, i32)
+        crounds = 0
+        maxc = -1
+        while True:
+            left, mc = ops.colour(g, r0, r1, self.seed, ell, colour)
+            maxc = max(maxc, mc)
+            crounds += 1
+            self._exchange(colour)
+            if self._scalar_sum(left) == 0:
+                break
+        ncolors = max(self._per_rank(maxc + 1))
+        colour_full = self._allgather(colour[r0:r1], rows, i32)
+        self.rounds.append((mrounds, crounds))
+        return PresetLevel(level=ell, q=q_full[:g.n], mate=mate_full[:g.n], colour=colour_full[:g.n],
+                           ncolors=ncolors, match_rounds=mrounds, colour_rounds=crounds, nxt=nxt,
+                           row_bounds=bounds)
+
+
+def create_from_presets(g: SetupGraph, presets: List[PresetLevel], opts=None):
+    """fiedler_create_preset on the partitioned levels (device arrays)."""
+    from . import fiedler_create_preset, fiedler_default_opts, fiedler_preset_level
+    pl = []
+    for p in presets:
+        s = fiedler_preset_level()
+        s.agg, s.mate, s.color = p.q.data_ptr(), p.mate.data_ptr(), p.colour.data_ptr()
+        s.ncolors, s.match_rounds, s.colour_rounds = p.ncolors, p.match_rounds, p.colour_rounds
+        s.n_next, s.nnz_next = p.nxt.n, p.nxt.nnz
+        s.rp_next, s.ci_next, s.w_next = p.nxt.rp.data_ptr(), p.nxt.ci.data_ptr(), p.nxt.w.data_ptr()
+        pl.append(s)
+    return fiedler_create_preset(g.n, g.nnz, g.rp, g.ci, g.w, opts or fiedler_default_opts(), pl)

@@ -218,3 +218,161 @@ def run_threads(nranks, fn):
     if errs:
         raise errs[0]
     return res
+
+
+# ---------------------------------------------------------------------------
+# Partitioned setup (paper_1602_04386_b200/dist.py PartitionedSetup): a plain
+# numpy implementation of the fiedler_pset_* operations, written from their
+# definitions in include/fiedler.h, on CPU tensors.  Lets the driver run on
+# gloo ranks; the result is compared with the oracle's hierarchy.
+# ---------------------------------------------------------------------------
+class RefSetupOps:
+    def __init__(self):
+        import oracle
+        self.o = oracle
+
+    def full(self, n, value, dtype):
+        return torch.full((max(n, 1),), value, dtype=dtype)
+
+    @staticmethod
+    def _np(g):
+        return g.rp.numpy(), g.ci.numpy(), g.w.numpy()
+
+    def bounds(self, g, nranks):
+        rp = g.rp.numpy()
+        coord = rp[:-1] + np.arange(g.n)
+        total = int(rp[-1]) + g.n
+        return [0] + [int(np.searchsorted(coord, total * k // nranks, side="left"))
+                      for k in range(1, nranks)] + [g.n]
+
+    def halo(self, g, nranks, rank, bounds):
+        rp, ci, _ = self._np(g)
+        r0, r1 = bounds[rank], bounds[rank + 1]
+        owner = np.searchsorted(np.asarray(bounds[1:-1]), np.arange(g.n), side="right")
+        send = [[] for _ in range(nranks)]
+        for v in range(r0, r1):
+            for p in sorted({int(owner[j]) for j in ci[rp[v]:rp[v + 1]] if j < r0 or j >= r1}):
+                send[p].append(v)
+        idx = [v for p in range(nranks) for v in send[p]]
+        t = self.full(len(idx), 0, torch.int32)
+        t[:len(idx)] = torch.tensor(idx, dtype=torch.int32)
+        return t, [len(s) for s in send]
+
+    def gather(self, x, idx, count, out):
+        out[:count] = x[idx[:count].long()]
+
+    def scatter(self, inp, idx, count, x):
+        x[idx[:count].long()] = inp[:count]
+
+    def _edge_key(self, salt, v, u, w):
+        lo, hi = min(v, u), max(v, u)
+        return (w, self.o.splitmix64((salt ^ ((lo << 32) | hi)) & self.o.MASK64))
+
+    def match(self, phase, g, r0, r1, seed, level, mate, ptr):
+        rp, ci, w = self._np(g)
+        salt = self.o.salt_match(seed, level)
+        if phase == 0:
+            act = 0
+            for v in range(r0, r1):
+                if mate[v] >= 0:
+                    continue
+                best, bk = -1, None
+                for k in range(rp[v], rp[v + 1]):
+                    u = int(ci[k])
+                    if mate[u] >= 0:
+                        continue
+                    key = self._edge_key(salt, v, u, w[k])
+                    if best < 0 or key > bk:
+                        best, bk = u, key
+                ptr[v] = best
+                act += best >= 0
+            return act
+        new = mate.clone()
+        for v in range(r0, r1):
+            u = int(ptr[v])
+            if mate[v] < 0 and u >= 0 and int(ptr[u]) == v:
+                new[v] = u
+        mate.copy_(new)
+        return 0
+
+    def _heaviest(self, g, salt, v):
+        rp, ci, w = self._np(g)
+        best, bk = -1, None
+        for k in range(rp[v], rp[v + 1]):
+            key = self._edge_key(salt, v, int(ci[k]), w[k])
+            if best < 0 or key > bk:
+                best, bk = int(ci[k]), key
+        return best
+
+    def aggregate(self, phase, g, r0, r1, seed, level, mate, q, offset=0):
+        rp = g.rp.numpy()
+        if phase in (0, 1):
+            lead = [v for v in range(r0, r1)
+                    if (mate[v] >= 0 and v < mate[v]) or (mate[v] < 0 and rp[v + 1] == rp[v])]
+            if phase == 1:
+                q[r0:r1] = -1
+                for i, v in enumerate(lead):
+                    q[v] = offset + i
+            return len(lead)
+        if phase == 2:
+            for v in range(r0, r1):
+                if 0 <= mate[v] < v:
+                    q[v] = q[int(mate[v])]
+            return 0
+        salt = self.o.salt_match(seed, level)
+        for v in range(r0, r1):
+            if mate[v] < 0 and rp[v + 1] > rp[v]:
+                m = self._heaviest(g, salt, v)
+                assert mate[m] >= 0 and q[m] >= 0
+                q[v] = q[m]
+        return 0
+
+    def galerkin(self, phase, g, q, a0, a1, cap=0, crp=None, cci=None, cw=None):
+        rp, ci, w = self._np(g)
+        qn = q.numpy()
+        contrib = []
+        for i in range(g.n):
+            a = int(qn[i])
+            if not a0 <= a < a1:
+                continue
+            for k in range(rp[i], rp[i + 1]):
+                j = int(ci[k])
+                b = int(qn[j])
+                if b != a:
+                    contrib.append((a, b, min(i, j), max(i, j), w[k]))
+        if phase == 0:
+            return len(contrib)
+        contrib.sort(key=lambda t: t[:4])
+        rows = {}
+        for a, b, _, _, wk in contrib:        # left fold in (lo, hi) order per (A, B)
+            d = rows.setdefault(a, {})
+            d[b] = wk if b not in d else d[b] + wk
+        nnz = 0
+        for a in range(a0, a1):
+            crp[a - a0] = nnz
+            for b in sorted(rows.get(a, {})):
+                cci[nnz] = b
+                cw[nnz] = rows[a][b]
+                nnz += 1
+        crp[a1 - a0] = nnz
+        return nnz
+
+    def colour(self, g, r0, r1, seed, level, colour):
+        rp, ci, _ = self._np(g)
+        salt = self.o.salt_color(seed, level)
+        pi = lambda x: (self.o.splitmix64((salt ^ x) & self.o.MASK64), x)   # noqa: E731
+        start = colour.clone()            # a round reads the state at its start
+        left, mx = 0, -1
+        for v in range(r0, r1):
+            if start[v] < 0:
+                nb = [int(u) for u in ci[rp[v]:rp[v + 1]]]
+                if all(start[u] >= 0 for u in nb if pi(u) > pi(v)):
+                    used = {int(start[u]) for u in nb if start[u] >= 0}
+                    c = 0
+                    while c in used:
+                        c += 1
+                    colour[v] = c
+                else:
+                    left += 1
+            mx = max(mx, int(colour[v]))
+        return left, mx

@@ -113,6 +113,17 @@ def test_argument_errors_before_any_device_work():
     assert lib.fiedler_solve(None, None, None, 0, None, None) == p.FIEDLER_ERR_ARG
     assert lib.fiedler_dist_plan(None, 0, 1, 0, None) == p.FIEDLER_ERR_ARG
     assert "handle" in p.fiedler_last_error().lower()
+    # partitioned setup: argument errors are reported before any device work
+    b = (ctypes.c_int64 * 3)()
+    assert lib.fiedler_pset_bounds(4, None, 2, b, None) == p.FIEDLER_ERR_ARG
+    assert lib.fiedler_pset_bounds(4, rp.ctypes.data, 0, b, None) == p.FIEDLER_ERR_ARG
+    assert lib.fiedler_pset_match(0, 2, rp.ctypes.data, ci.ctypes.data, w.ctypes.data, 0, 3, 0, 0, None,
+                                  None, None, None) == p.FIEDLER_ERR_ARG
+    assert lib.fiedler_pset_galerkin(0, 2, None, None, None, None, 0, 1, 0, None, None, None, None,
+                                     None) == p.FIEDLER_ERR_ARG
+    assert lib.fiedler_create_preset(2, 2, rp.ctypes.data, ci.ctypes.data, w.ctypes.data, 0, None, -1, None,
+                                     ctypes.byref(h)) == p.FIEDLER_ERR_ARG
+    assert "preset" in p.fiedler_last_error().lower()
 
 
 def test_header_documents_every_entry_point():

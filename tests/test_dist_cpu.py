@@ -105,3 +105,53 @@ def test_local_comm_single_rank(orc):
     v, lam, _ = PartitionedSolver(RefOps(orc.build_hierarchy(og, orc.Config())), LocalComm()).solve()
     assert abs(lam - ref.lambda2) / ref.lambda2 <= 1e-10
     assert np.allclose(v.numpy(), ref.vector, rtol=0, atol=1e-9)
+
+
+# ------------------------------------------------------------------ partitioned setup
+def _setup_worker(rank, world, port, name, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from dist_ref import RefSetupOps
+        from paper_1602_04386_b200.dist import PartitionedSetup, SetupGraph, TorchComm
+        g = _graph(name)
+        sg = SetupGraph(g.n, g.nnz, torch.from_numpy(g.rp), torch.from_numpy(g.ci), torch.from_numpy(g.w))
+        ps = PartitionedSetup(RefSetupOps(), TorchComm(), min_rows=1)
+        pres = ps.run(sg)
+        q.put((rank, [(p.q[:p.q.numel()].numpy().copy(), p.mate.numpy().copy(), p.colour.numpy().copy(),
+                       p.ncolors, p.nxt.rp.numpy().copy(), p.nxt.ci[:p.nxt.nnz].numpy().copy(),
+                       p.nxt.w[:p.nxt.nnz].numpy().copy(), p.row_bounds) for p in pres], ps.bytes_sent))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name", [(2, "grid"), (3, "rand"), (2, "hub")])
+def test_partitioned_setup_matches_oracle_hierarchy(orc, world, name):
+    """Every partitioned level's matching, aggregates, colouring and coarse
+    level equal the oracle's hierarchy bit for bit, on every rank."""
+    import torch.multiprocessing as mp
+    g = _graph(name)
+    levels = orc.build_hierarchy(orc.Graph.from_csr(g.n, g.rp, g.ci, g.w), orc.Config())
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_setup_worker, args=(r, world, port, name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get() for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    for rank, pres, sent in out:
+        assert len(pres) == len(levels) - 1, "every coarsened level is partitioned (min_rows=1)"
+        assert sent > 0
+        for ell, (qv, mate, col, ncol, rp, ci, w, bounds) in enumerate(pres):
+            L, Ln = levels[ell], levels[ell + 1]
+            assert len(set(bounds)) > 2 or L.g.n < world, "rows split across ranks"
+            assert np.array_equal(qv, L.q) and np.array_equal(mate, L.mate)
+            assert np.array_equal(col, L.color) and ncol == L.ncolors
+            assert np.array_equal(rp, Ln.g.rp) and np.array_equal(ci, Ln.g.ci)
+            assert np.array_equal(w, Ln.g.w)     # bit for bit (R3 summation order)

@@ -119,3 +119,105 @@ def test_multi_rank_threads_match_oracle(fd, orc, name, world):
         cos = abs(float(v @ ref.vector)) / (np.linalg.norm(v) * np.linalg.norm(ref.vector))
         assert 1 - cos <= 1e-10
         assert np.allclose(v, ref.vector, rtol=0, atol=1e-9)
+
+
+# ------------------------------------------------------------------ partitioned setup
+def _setup_graph(g):
+    import torch
+    from paper_1602_04386_b200.dist import SetupGraph
+    return SetupGraph(g.n, g.nnz, torch.from_numpy(g.rp).cuda(), torch.from_numpy(g.ci).cuda(),
+                      torch.from_numpy(g.w).cuda())
+
+
+def _check_presets(pres, levels, n_expected):
+    assert len(pres) == n_expected
+    for ell, p in enumerate(pres):
+        L, Ln = levels[ell], levels[ell + 1]
+        assert np.array_equal(p.q.cpu().numpy(), L.q), ell
+        assert np.array_equal(p.mate.cpu().numpy(), L.mate), ell
+        assert np.array_equal(p.colour.cpu().numpy(), L.color), ell
+        assert p.ncolors == L.ncolors
+        assert p.nxt.n == Ln.g.n and p.nxt.nnz == Ln.g.nnz
+        assert np.array_equal(p.nxt.rp.cpu().numpy(), Ln.g.rp)
+        assert np.array_equal(p.nxt.ci[:p.nxt.nnz].cpu().numpy(), Ln.g.ci)
+        assert np.array_equal(p.nxt.w[:p.nxt.nnz].cpu().numpy(), Ln.g.w)
+
+
+@pytest.mark.parametrize("name,world", [("grid64x45", 2), ("rmat12", 3), ("hub", 2), ("grid3d_14", 4)])
+def test_partitioned_setup_and_solve_threads_match_oracle(fd, orc, name, world):
+    """Ranks as threads on one GPU: the partitioned setup (fiedler_pset_*) gives
+    the oracle's hierarchy bit for bit on every rank; fiedler_create_preset on it
+    exports the oracle's levels; the partitioned solve on that handle matches
+    the oracle's Fiedler vector."""
+    import torch
+    from dist_ref import ThreadComm, run_threads
+    from paper_1602_04386_b200.dist import (LibOps, LibSetupOps, PartitionedSetup, PartitionedSolver,
+                                            create_from_presets)
+    g = GRAPHS[name]()
+    og = orc.Graph.from_csr(g.n, g.rp, g.ci, g.w)
+    levels = orc.build_hierarchy(og, orc.Config())
+    ref = orc.solve(og, orc.Config(), levels=levels)
+
+    def rank_fn(rank, shared):
+        comm = ThreadComm(shared, rank, world, sync_cuda=True)
+        ops = LibSetupOps(torch.device("cuda"))
+        sg = _setup_graph(g)
+        torch.cuda.synchronize()
+        ps = PartitionedSetup(ops, comm, min_rows=1)
+        pres = ps.run(sg)
+        torch.cuda.synchronize()
+        _check_presets(pres, levels, len(levels) - 1)
+        opts = fd.fiedler_default_opts(stream=ops.stream)
+        h = create_from_presets(sg, pres, opts)
+        try:
+            for ell in range(len(levels)):
+                ex = fd.fiedler_level_export(h, ell)
+                L = levels[ell]
+                assert np.array_equal(ex["rp"], L.g.rp) and np.array_equal(ex["ci"], L.g.ci)
+                assert np.array_equal(ex["w"], L.g.w) and np.array_equal(ex["color"], L.color)
+                if L.q is not None:
+                    assert np.array_equal(ex["agg"], L.q) and np.array_equal(ex["mate"], L.mate)
+            solver = PartitionedSolver(LibOps(h, torch.device("cuda")), comm, min_rows=1)
+            v, lam, _ = solver.solve()
+            torch.cuda.synchronize()
+            return v.cpu().numpy(), lam, ps.bytes_sent
+        finally:
+            fd.fiedler_destroy(h)
+
+    for v, lam, sent in run_threads(world, rank_fn):
+        assert sent > 0
+        assert abs(lam - ref.lambda2) / ref.lambda2 <= 1e-10
+        cos = abs(float(v @ ref.vector)) / (np.linalg.norm(v) * np.linalg.norm(ref.vector))
+        assert 1 - cos <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["grid64x45", "rmat12", "hub"])
+def test_single_rank_setup_equals_fiedler_create(fd, orc, name):
+    """World size 1 (LocalComm): the pset kernels alone rebuild fiedler_create's
+    hierarchy; min_rows cuts the partitioned prefix at a middle level."""
+    import torch
+    from paper_1602_04386_b200.dist import LibSetupOps, LocalComm, PartitionedSetup, create_from_presets
+    g = GRAPHS[name]()
+    levels = orc.build_hierarchy(orc.Graph.from_csr(g.n, g.rp, g.ci, g.w), orc.Config())
+    ops = LibSetupOps(torch.device("cuda"))
+    sg = _setup_graph(g)
+    torch.cuda.synchronize()
+    cut = levels[min(2, len(levels) - 1)].g.n
+    pres = PartitionedSetup(ops, LocalComm(), min_rows=cut).run(sg)
+    torch.cuda.synchronize()
+    _check_presets(pres, levels, sum(1 for L in levels[:-1] if L.g.n >= cut))
+    h = create_from_presets(sg, pres, fd.fiedler_default_opts(stream=ops.stream))
+    h2 = _handle(fd, g)
+    try:
+        assert fd.fiedler_num_levels(h) == fd.fiedler_num_levels(h2) == len(levels)
+        for ell in range(len(levels)):
+            a, b = fd.fiedler_level_export(h, ell), fd.fiedler_level_export(h2, ell)
+            for k in ("rp", "ci", "w", "color"):
+                assert np.array_equal(a[k], b[k]), (ell, k)
+        v1 = torch.empty(g.n, dtype=torch.float64, device="cuda")
+        v2 = torch.empty(g.n, dtype=torch.float64, device="cuda")
+        l1, l2 = fd.fiedler_solve(h, v1), fd.fiedler_solve(h2, v2)
+        assert l1 == l2 and torch.equal(v1, v2)
+    finally:
+        fd.fiedler_destroy(h)
+        fd.fiedler_destroy(h2)
