@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--sharded", action="store_true",
                     help="headline = the row-sharded step of one graph (default when --gpus > 1)")
     ap.add_argument("--partition-min-rows", type=int, default=1 << 20)
+    ap.add_argument("--replicated-setup", action="store_true",
+                    help="sharded step: fiedler_create on every rank instead of the partitioned setup")
     return ap.parse_args()
 
 
@@ -237,13 +239,27 @@ def sharded_step_timing(fd, g, rp, ci, w, dev, local, args, comm, dist):
     ranks, NCCL halo exchange / all-reduce / all-gather).  Device time of every
     step between CUDA events on the stream everything runs on, max over ranks."""
     import torch
-    from paper_1602_04386_b200.dist import LibOps, PartitionedSolver
+    from paper_1602_04386_b200.dist import (LibOps, LibSetupOps, PartitionedSetup, PartitionedSolver,
+                                            SetupGraph, create_from_presets)
     stream = torch.cuda.current_stream(dev)
     opts = fd.fiedler_default_opts(device=local, validate=0, stream=stream.cuda_stream)
     info = {}
+    sops = LibSetupOps(dev, stream=stream.cuda_stream)
+
+    def create(rp, ci, w):
+        """The setup: partitioned fine levels (fiedler_pset_*) + fiedler_create_preset,
+        or (--replicated-setup) fiedler_create on every rank."""
+        if args.replicated_setup:
+            return fd.fiedler_create(g.n, g.nnz, rp, ci, w, opts)
+        sg = SetupGraph(g.n, g.nnz, rp, ci, w)
+        ps = PartitionedSetup(sops, comm, min_rows=args.partition_min_rows)
+        pres = ps.run(sg)
+        info.update(setup_levels_partitioned=len(pres), setup_bytes=ps.bytes_sent,
+                    setup_rounds=[list(r) for r in ps.rounds])
+        return create_from_presets(sg, pres, opts)
 
     def step():
-        h = fd.fiedler_create(g.n, g.nnz, rp, ci, w, opts)
+        h = create(rp, ci, w)
         try:
             solver = PartitionedSolver(LibOps(h, dev, stream=stream.cuda_stream), comm,
                                        min_rows=args.partition_min_rows)
@@ -269,16 +285,26 @@ def sharded_step_timing(fd, g, rp, ci, w, dev, local, args, comm, dist):
         times.append(e0.elapsed_time(e1))
     tot = sum(times)
     hb = float(info.get("halo_bytes", 0))
+    sb = float(info.get("setup_bytes", 0))
     if dist:
-        t = torch.tensor([tot, hb], dtype=torch.float64, device=dev)
+        t = torch.tensor([tot, hb, sb], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot, hb = float(t[0].item()), float(t[1].item())
+        tot, hb, sb = float(t[0].item()), float(t[1].item()), float(t[2].item())
     ms = tot / args.steps
-    return {"ms_per_step": ms, "lambda2": info.get("lam"), "levels_partitioned": info.get("levels_partitioned"),
-            "min_rows": args.partition_min_rows, "halo_bytes_per_step": hb,
-            "halo_GBps_effective": hb / (ms / 1e3) / 1e9 if ms > 0 else None,
-            "note": "setup replicated on every rank; solve of one graph row-partitioned; "
-                    "halo bytes = the most any rank sends per step (NCCL all-to-all over NVLink); "
+    return {"_create": create,
+            "ms_per_step": ms, "lambda2": info.get("lam"), "levels_partitioned": info.get("levels_partitioned"),
+            "setup": "replicated" if args.replicated_setup else "partitioned",
+            "setup_levels_partitioned": info.get("setup_levels_partitioned", 0),
+            "setup_rounds": info.get("setup_rounds"),
+            "min_rows": args.partition_min_rows, "halo_bytes_per_step": hb + sb,
+            "halo_bytes_solve": hb, "halo_bytes_setup": sb,
+            "halo_GBps_effective": (hb + sb) / (ms / 1e3) / 1e9 if ms > 0 else None,
+            "note": ("setup replicated on every rank" if args.replicated_setup else
+                     "setup of the levels >= min_rows row-partitioned (fiedler_pset_*: matching / colouring "
+                     "rounds with halo exchange, own coarse rows of the Galerkin product, all-gathered), "
+                     "the coarser levels and the layouts by fiedler_create_preset on every rank") +
+                    "; solve of one graph row-partitioned; "
+                    "halo bytes = the most any rank sends per step (NCCL all-to-all / all-gather over NVLink); "
                     "GB/s = those bytes / the whole step time (a lower bound on the link rate)"}
 
 
@@ -432,11 +458,16 @@ def main():
         from paper_1602_04386_b200.dist import LocalComm, TorchComm
         comm = TorchComm() if dist else LocalComm()
         sharded = sharded_step_timing(fd, g, rp, ci, w, dev, local, args, comm, dist)
+        create_fn = sharded.pop("_create")
         # end to end: pinned host CSR in, Fiedler vector back to the host, wall clock, max over ranks
         from paper_1602_04386_b200.dist import LibOps, PartitionedSolver
 
         def e2e_sharded():
-            hh2 = fd.fiedler_create(n, nnz, prp, pci, pw, eo)
+            if args.replicated_setup:
+                hh2 = fd.fiedler_create(n, nnz, prp, pci, pw, eo)
+            else:   # the partitioned setup works on device arrays: copy the host CSR in first
+                drp, dci, dw = (x.to(dev, non_blocking=True) for x in (prp, pci, pw))
+                hh2 = create_fn(drp, dci, dw)
             try:
                 sv = PartitionedSolver(LibOps(hh2, dev, stream=stream.cuda_stream), comm,
                                        min_rows=args.partition_min_rows)
@@ -495,7 +526,8 @@ def main():
             line["ms_per_step"] = sharded["ms_per_step"]
             line["solve_time_ms"] = sharded["ms_per_step"]
             line["scaling"] = "strong"
-            line["config"]["parallelism"] = "row-sharded fine levels over %d GPU(s), setup replicated" % world
+            line["config"]["parallelism"] = "row-sharded fine levels over %d GPU(s), setup %s" % (
+                world, "replicated" if args.replicated_setup else "partitioned")
             line["sharded"] = sharded
             line["e2e"] = sharded.pop("e2e")
         print(json.dumps(line), flush=True)

@@ -345,10 +345,16 @@ FIEDLER_API int fiedler_pset_scatter(const int32_t *in, const int32_t *idx, int6
  * greedy heaviest-first matching of R2 takes it).  The caller initialises mate
  * and ptr to -1 and exchanges ptr (after POINT) and mate (after RESOLVE) of the
  * boundary rows; when the all-reduced *active is 0 the matching is maximal
- * and equals R2's greedy matching. */
+ * and equals R2's greedy matching.  round = the handshake round (0, 1, ...).
+ * work: NULL (every half-round visits all own rows) or device int32 scratch
+ * [8 + 2 (r1 - r0)] kept by the caller for the level's rounds: POINT of round
+ * k > 0 visits only the rows the previous RESOLVE left free, RESOLVE only the
+ * rows POINT found a partner for (a row with no free neighbour never gets one
+ * back, a matched row stays matched). */
 FIEDLER_API int fiedler_pset_match(int32_t phase, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
                                    const double *weights, int64_t r0, int64_t r1, uint64_t seed, int32_t level,
-                                   int32_t *mate, int32_t *ptr, int64_t *active, void *stream);
+                                   int32_t *mate, int32_t *ptr, int32_t round, int32_t *work, int64_t *active,
+                                   void *stream);
 
 #define FIEDLER_PSET_LEADERS 0   /* *count = own leaders (synchronises)                                   */
 #define FIEDLER_PSET_IDS 1       /* q[v] = offset + rank of v among own leaders; -1 on other own rows     */
@@ -370,8 +376,10 @@ FIEDLER_API int fiedler_pset_aggregate(int32_t phase, int64_t n, const int64_t *
 
 /* Galerkin product I L I^T (R3) for the coarse rows [a0, a1) given
  * the WHOLE aggregate map q (device int32 [n]).  Phase 0: *count = the number of
- * crossing contributions of those rows (an upper bound of their coarse
- * nonzeros; synchronises).  Phase 1 (cap >= that bound): the coarse adjacency
+ * crossing contributions of those rows (fine entries i -> j with q(i) in
+ * [a0, a1), q(j) != q(i): an upper bound of their coarse nonzeros;
+ * synchronises).  Coarse rows whose members have at most 32 entries in all are
+ * built by one thread each, longer ones by a sort of their contributions.  Phase 1 (cap >= that bound): the coarse adjacency
  * rows in CSR with LOCAL offsets: crp (device int64 [a1 - a0 + 1], crp[0] = 0),
  * ascending columns cci (device int32), weights cw (device float64): W_c(A, B) =
  * the left fold of the fine weights w_ij over the fine edges {i < j} with
@@ -388,10 +396,13 @@ FIEDLER_API int fiedler_pset_galerkin(int32_t phase, int64_t n, const int64_t *r
  * splitmix64(seed ^ (TAG_COLOR + level)), are coloured takes the smallest
  * colour none of its coloured neighbours has -- the greedy first-fit colouring
  * in decreasing priority, independent of the schedule.  out (host int64 [2]):
- * {own rows still uncoloured, largest own colour (-1 if none)}; synchronises. */
+ * {own rows still uncoloured, largest colour given in this round (-1 if none)};
+ * synchronises.  round = 0, 1, ... of the level; work: NULL (every round
+ * visits all own rows) or device int32 scratch [8 + 2 (r1 - r0)] kept across
+ * the level's rounds (round k > 0 visits only the rows round k - 1 left). */
 FIEDLER_API int fiedler_pset_colour(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, int64_t r0,
-                                    int64_t r1, uint64_t seed, int32_t level, int32_t *colour, int64_t *out,
-                                    void *stream);
+                                    int64_t r1, uint64_t seed, int32_t level, int32_t round, int32_t *work,
+                                    int32_t *colour, int64_t *out, void *stream);
 
 /* One level of a hierarchy built outside fiedler_create (fiedler_pset_*): the
  * level's aggregate map, matching and colouring (device int32 [n_l]) and the

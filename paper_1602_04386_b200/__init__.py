@@ -165,10 +165,10 @@ def _load():
         lib.fiedler_pset_halo.argtypes = [i64, P, P, i32, i32, i64p, P, i64p, P]
         lib.fiedler_pset_gather.argtypes = [P, P, i64, P, P]
         lib.fiedler_pset_scatter.argtypes = [P, P, i64, P, P]
-        lib.fiedler_pset_match.argtypes = [i32, i64, P, P, P, i64, i64, u64, i32, P, P, i64p, P]
+        lib.fiedler_pset_match.argtypes = [i32, i64, P, P, P, i64, i64, u64, i32, P, P, i32, P, i64p, P]
         lib.fiedler_pset_aggregate.argtypes = [i32, i64, P, P, P, i64, i64, u64, i32, P, P, i64, i64p, P]
         lib.fiedler_pset_galerkin.argtypes = [i32, i64, P, P, P, P, i64, i64, i64, P, P, P, i64p, P]
-        lib.fiedler_pset_colour.argtypes = [i64, P, P, i64, i64, u64, i32, P, i64p, P]
+        lib.fiedler_pset_colour.argtypes = [i64, P, P, i64, i64, u64, i32, i32, P, P, i64p, P]
         lib.fiedler_create_preset.argtypes = [i64, i64, P, P, P, i32, ctypes.POINTER(fiedler_opts), i32,
                                               ctypes.POINTER(fiedler_preset_level), ctypes.POINTER(P)]
         for f in ("fiedler_pset_bounds", "fiedler_pset_halo", "fiedler_pset_gather", "fiedler_pset_scatter",
@@ -348,12 +348,12 @@ def fiedler_pset_scatter(inp, idx, count, x, stream=None):
     _check(_load().fiedler_pset_scatter(_dptr(inp, 4), _dptr(idx, 4), int(count), _dptr(x, 4), stream))
 
 
-def fiedler_pset_match(phase, n, rp, ci, w, r0, r1, seed, level, mate, ptr, stream=None):
+def fiedler_pset_match(phase, n, rp, ci, w, r0, r1, seed, level, mate, ptr, round=0, work=None, stream=None):
     """One matching half-round; returns the active count for POINT (else 0)."""
     a = ctypes.c_int64(0)
     _check(_load().fiedler_pset_match(int(phase), int(n), _dptr(rp, 8), _dptr(ci, 4), _dptr(w, 8), int(r0),
                                       int(r1), int(seed) & (2**64 - 1), int(level), _dptr(mate, 4), _dptr(ptr, 4),
-                                      ctypes.byref(a), stream))
+                                      int(round), _dptr(work, 4), ctypes.byref(a), stream))
     return a.value
 
 
@@ -375,11 +375,12 @@ def fiedler_pset_galerkin(phase, n, rp, ci, w, q, a0, a1, cap=0, crp=None, cci=N
     return c.value
 
 
-def fiedler_pset_colour(n, rp, ci, r0, r1, seed, level, colour, stream=None):
-    """One Jones-Plassmann round; returns (own rows left uncoloured, largest own colour)."""
+def fiedler_pset_colour(n, rp, ci, r0, r1, seed, level, colour, round=0, work=None, stream=None):
+    """One Jones-Plassmann round; returns (own rows left uncoloured, largest colour given)."""
     out = (ctypes.c_int64 * 2)()
     _check(_load().fiedler_pset_colour(int(n), _dptr(rp, 8), _dptr(ci, 4), int(r0), int(r1),
-                                       int(seed) & (2**64 - 1), int(level), _dptr(colour, 4), out, stream))
+                                       int(seed) & (2**64 - 1), int(level), int(round), _dptr(work, 4),
+                                       _dptr(colour, 4), out, stream))
     return out[0], out[1]
 
 

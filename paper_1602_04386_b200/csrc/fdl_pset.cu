@@ -101,35 +101,80 @@ __device__ __forceinline__ bool heavier(double wa, uint64_t ha, double wb, uint6
     return wa > wb || (wa == wb && ha > hb);
 }
 
-__global__ void k_ps_point(const int64_t *rp, const int *ci, const double *w, int64_t r0, int64_t r1,
-                           uint64_t salt, const int *mate, int *ptr, unsigned long long *active) {
+// Work lists of the rounds (optional caller scratch `work`, include/fiedler.h):
+// a round walks the list the previous half-round left (or all own rows) and
+// appends the rows that stay in play to the next list, one atomic per warp.
+struct WorkList {
+    const int *in;        // rows to visit; null: all own rows [r0, r1)
+    const int *in_cnt;
+    int *out;             // rows kept for the next half-round; null: no list
+    int *out_cnt;
+    int64_t r0, own;
+    __device__ __forceinline__ int64_t count() const { return in ? (int64_t)*in_cnt : own; }
+    __device__ __forceinline__ int64_t row(int64_t i) const { return in ? (int64_t)in[i] : r0 + i; }
+    // every lane of the warp calls this with the same trip count
+    __device__ __forceinline__ void keep(bool k, int v) const {
+        if (!out) return;
+        const unsigned m = __ballot_sync(0xffffffffu, k);
+        if (!m) return;
+        int base = 0;
+        if (lane_id() == 0) base = atomicAdd(out_cnt, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (k) out[base + __popc(m & ((1u << lane_id()) - 1))] = v;
+    }
+};
+
+// warp-uniform trip count of a grid-stride loop over [0, cnt)
+#define PS_WARP_LOOP(i, cnt)                                                                     \
+    for (int64_t i##_base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31),     \
+                 i = i##_base + lane_id();                                                       \
+         i##_base < (cnt); i##_base += (int64_t)gridDim.x * blockDim.x, i = i##_base + lane_id())
+
+__global__ void k_ps_point(const int64_t *rp, const int *ci, const double *w, WorkList wl, uint64_t salt,
+                           const int *mate, int *ptr, unsigned long long *active) {
     unsigned long long act = 0;
-    for (int64_t v = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < r1;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        if (mate[v] >= 0) continue;
-        int best = -1;
-        double bw = 0.0;
-        uint64_t bh = 0;
-        for (int64_t k = rp[v]; k < rp[v + 1]; k++) {
-            const int u = ci[k];
-            if (mate[u] >= 0) continue;
-            const uint64_t h = edge_hash(salt, (int)v, u);
-            if (best < 0 || heavier(w[k], h, bw, bh)) { best = u; bw = w[k]; bh = h; }
+    const int64_t cnt = wl.count();
+    PS_WARP_LOOP(i, cnt) {
+        bool keep = false;
+        int v = -1;
+        if (i < cnt) {
+            v = (int)wl.row(i);
+            if (mate[v] < 0) {
+                int best = -1;
+                double bw = 0.0;
+                uint64_t bh = 0;
+                for (int64_t k = rp[v]; k < rp[v + 1]; k++) {
+                    const int u = ci[k];
+                    if (mate[u] >= 0) continue;
+                    const uint64_t h = edge_hash(salt, v, u);
+                    if (best < 0 || heavier(w[k], h, bw, bh)) { best = u; bw = w[k]; bh = h; }
+                }
+                ptr[v] = best;
+                keep = best >= 0;
+                act += keep;
+            }
         }
-        ptr[v] = best;
-        act += best >= 0;
+        wl.keep(keep, v);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) act += __shfl_xor_sync(0xffffffffu, act, o);
     if (lane_id() == 0 && act) atomicAdd(active, act);
 }
 
-__global__ void k_ps_resolve(int64_t r0, int64_t r1, const int *ptr, int *mate) {
-    for (int64_t v = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < r1;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        if (mate[v] >= 0) continue;
-        const int u = ptr[v];
-        if (u >= 0 && ptr[u] == (int)v) mate[v] = u;
+__global__ void k_ps_resolve(WorkList wl, const int *ptr, int *mate) {
+    const int64_t cnt = wl.count();
+    PS_WARP_LOOP(i, cnt) {
+        bool keep = false;
+        int v = -1;
+        if (i < cnt) {
+            v = (int)wl.row(i);
+            if (mate[v] < 0) {
+                const int u = ptr[v];
+                if (u >= 0 && ptr[u] == v) mate[v] = u;
+                else keep = true;   // still free: visited by the next POINT
+            }
+        }
+        wl.keep(keep, v);
     }
 }
 
@@ -259,39 +304,164 @@ __global__ void k_ps_row_ptr(const int *row, int nruns, int na, int64_t *crp) {
     }
 }
 
+// Per-coarse-row path.  Members grouped by coarse row (counting sort), T_A =
+// the sum of the members' degrees (the row's slots); rows with T_A <= kGalSmall
+// are built by one thread each: contributions insertion-sorted by (B, lo, hi)
+// in local memory, runs folded left to right; bigger rows go through the
+// two-sort path above, restricted to their members.
+constexpr int kGalSmall = 32;
+
+__global__ void k_ps_row_members(const int64_t *rp, int64_t n, const int *q, int a0, int a1, int *mcnt, int *slots) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int a = q[v];
+        if (a < a0 || a >= a1) continue;
+        atomicAdd(mcnt + (a - a0), 1);
+        atomicAdd(slots + (a - a0), (int)(rp[v + 1] - rp[v]));
+    }
+}
+
+__global__ void k_ps_row_fill(int64_t n, const int *q, int a0, int a1, const int *mrp, int *cursor, int *mem) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int a = q[v];
+        if (a < a0 || a >= a1) continue;
+        mem[mrp[a - a0] + atomicAdd(cursor + (a - a0), 1)] = (int)v;
+    }
+}
+
+__global__ void k_ps_gal_small(const int64_t *rp, const int *ci, const double *w, const int *q, int a0, int na,
+                               const int *mrp, const int *mem, const int *slots, const int *soff, int *sB,
+                               double *sW, int *cnt, int *big) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < na; r += gridDim.x * blockDim.x) {
+        if (slots[r] > kGalSmall) {
+            big[r] = 1;
+            cnt[r] = 0;
+            continue;
+        }
+        big[r] = 0;
+        const int A = a0 + r;
+        int bb[kGalSmall];
+        unsigned long long kk[kGalSmall];
+        double ww[kGalSmall];
+        int m = 0;
+        for (int t = mrp[r]; t < mrp[r + 1]; t++) {
+            const int i = mem[t];
+            for (int64_t k = rp[i]; k < rp[i + 1]; k++) {
+                const int j = ci[k], B = q[j];
+                if (B == A) continue;
+                const unsigned long long key = ((unsigned long long)min(i, j) << 32) | (unsigned)max(i, j);
+                int p = m++;
+                while (p > 0 && (bb[p - 1] > B || (bb[p - 1] == B && kk[p - 1] > key))) {
+                    bb[p] = bb[p - 1];
+                    kk[p] = kk[p - 1];
+                    ww[p] = ww[p - 1];
+                    p--;
+                }
+                bb[p] = B;
+                kk[p] = key;
+                ww[p] = w[k];
+            }
+        }
+        int o = soff[r], c = 0;
+        for (int t = 0; t < m;) {
+            double acc = ww[t];
+            int u = t + 1;
+            for (; u < m && bb[u] == bb[t]; u++) acc += ww[u];
+            sB[o + c] = bb[t];
+            sW[o + c] = acc;
+            c++;
+            t = u;
+        }
+        cnt[r] = c;
+    }
+}
+
+__global__ void k_ps_big_member_flags(int64_t n, const int *q, int a0, int a1, const int *big, int *flags) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int a = q[v];
+        flags[v] = a >= a0 && a < a1 && big[a - a0];
+    }
+}
+
+// runs of the big rows into their slot ranges; rr = first run of every local row
+__global__ void k_ps_big_place(const int *row, const int *cB, const double *cWv, int nruns, const int *rr,
+                               const int *soff, int *sB, double *sW) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nruns; t += gridDim.x * blockDim.x) {
+        const int r = row[t];
+        const int o = soff[r] + (t - rr[r]);
+        sB[o] = cB[t];
+        sW[o] = cWv[t];
+    }
+}
+
+__global__ void k_ps_big_cnt(const int *rr, int na, const int *big, int *cnt) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < na; r += gridDim.x * blockDim.x)
+        if (big[r]) cnt[r] = rr[r + 1] - rr[r];
+}
+
+__global__ void k_ps_gal_out(int na, const int *cnt, const int *coff, const int *soff, const int *sB, const double *sW,
+                             int64_t *crp, int *cci, double *cw, int total) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= na; r += gridDim.x * blockDim.x) {
+        if (r == na) { crp[na] = total; continue; }
+        const int o = coff[r], s0 = soff[r];
+        crp[r] = o;
+        for (int t = 0; t < cnt[r]; t++) {
+            cci[o + t] = sB[s0 + t];
+            cw[o + t] = sW[s0 + t];
+        }
+    }
+}
+
+__global__ void k_ps_row_ptr32(const int *row, int nruns, int na, int *rr) {
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a <= na; a += gridDim.x * blockDim.x) {
+        int lo = 0, hi = nruns;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (row[mid] >= a) hi = mid; else lo = mid + 1;
+        }
+        rr[a] = lo;
+    }
+}
+
 // ------------------------------------------------------------------ colouring (R4)
-__global__ void k_ps_colour(const int64_t *rp, const int *ci, int64_t r0, int64_t r1, uint64_t salt, int *colour,
+__global__ void k_ps_colour(const int64_t *rp, const int *ci, WorkList wl, uint64_t salt, int *colour,
                             unsigned long long *left, int *maxc) {
     unsigned long long nleft = 0;
     int mc = -1;
-    for (int64_t v = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < r1;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        int cv = colour[v];
-        if (cv < 0) {
-            const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
-            bool ready = true;
-            for (int64_t k = rp[v]; k < rp[v + 1] && ready; k++) {
-                const int u = ci[k];
-                const uint64_t pu = splitmix64(salt ^ (uint64_t)u);
-                if ((pu > pv || (pu == pv && u > v)) && colour[u] < 0) ready = false;
-            }
-            if (ready) {
-                // first fit: smallest colour no coloured neighbour has (all coloured
-                // neighbours have higher priority), 64 colours per row scan
-                for (int base = 0;; base += 64) {
-                    unsigned long long used = 0;
-                    for (int64_t k = rp[v]; k < rp[v + 1]; k++) {
-                        const int c = colour[ci[k]] - base;
-                        if (c >= 0 && c < 64) used |= 1ull << c;
-                    }
-                    if (~used) { cv = base + __ffsll((long long)~used) - 1; break; }
+    const int64_t cnt = wl.count();
+    PS_WARP_LOOP(i, cnt) {
+        bool keep = false;
+        int v = -1;
+        if (i < cnt) {
+            v = (int)wl.row(i);
+            if (colour[v] < 0) {
+                const uint64_t pv = splitmix64(salt ^ (uint64_t)v);
+                bool ready = true;
+                for (int64_t k = rp[v]; k < rp[v + 1] && ready; k++) {
+                    const int u = ci[k];
+                    const uint64_t pu = splitmix64(salt ^ (uint64_t)u);
+                    if ((pu > pv || (pu == pv && u > v)) && colour[u] < 0) ready = false;
                 }
-                colour[v] = cv;
-            } else {
-                nleft++;
+                if (ready) {
+                    // first fit: smallest colour no coloured neighbour has (all coloured
+                    // neighbours have higher priority), 64 colours per row scan
+                    int cv = 0;
+                    for (int base = 0;; base += 64) {
+                        unsigned long long used = 0;
+                        for (int64_t k = rp[v]; k < rp[v + 1]; k++) {
+                            const int c = colour[ci[k]] - base;
+                            if (c >= 0 && c < 64) used |= 1ull << c;
+                        }
+                        if (~used) { cv = base + __ffsll((long long)~used) - 1; break; }
+                    }
+                    colour[v] = cv;
+                    mc = max(mc, cv);
+                } else {
+                    keep = true;
+                    nleft++;
+                }
             }
         }
-        mc = max(mc, cv);
+        wl.keep(keep, v);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -367,9 +537,25 @@ void pset_scatter(const int *in, const int *idx, int64_t count, int *x, cudaStre
     FDL_LAUNCH_CK();
 }
 
+// work lists in `work` (device int32 [8 + 2 own]): header {count A, count B},
+// list A at work + 8, list B at work + 8 + own.  POINT of round 0 visits every
+// own row and writes B; RESOLVE reads B, writes A; later POINTs read A, write B.
+static WorkList make_list(int *work, int64_t r0, int64_t own, int read, int write) {
+    WorkList wl{};
+    wl.r0 = r0;
+    wl.own = own;
+    if (work) {
+        if (read >= 0) { wl.in = work + 8 + read * own; wl.in_cnt = work + read; }
+        wl.out = work + 8 + write * own;
+        wl.out_cnt = work + write;
+    }
+    return wl;
+}
+
 void pset_match(int phase, int64_t n, const int64_t *rp, const int *ci, const double *w, int64_t r0, int64_t r1,
-                uint64_t seed, int level, int *mate, int *ptr, int64_t *active, cudaStream_t st) {
+                uint64_t seed, int level, int *mate, int *ptr, int round, int *work, int64_t *active, cudaStream_t st) {
     check_rows(n, r0, r1);
+    FDL_REQUIRE(round >= 0, FIEDLER_ERR_ARG, "round < 0");
     const int64_t own = r1 - r0;
     if (phase == FIEDLER_PSET_POINT) {
         FDL_REQUIRE(active, FIEDLER_ERR_ARG, "POINT needs `active`");
@@ -377,7 +563,9 @@ void pset_match(int phase, int64_t n, const int64_t *rp, const int *ci, const do
         k_ps_init_counters<<<1, 32, 0, st>>>(cnt.as<unsigned long long>(), 1, nullptr);
         FDL_LAUNCH_CK();
         if (own) {
-            k_ps_point<<<ps_grid(own), kPsBlock, 0, st>>>(rp, ci, w, r0, r1, salt_match(seed, level), mate, ptr,
+            if (work) FDL_CK(cudaMemsetAsync(work + 1, 0, 4, st));
+            k_ps_point<<<ps_grid(own), kPsBlock, 0, st>>>(rp, ci, w, make_list(work, r0, own, round ? 0 : -1, 1),
+                                                          salt_match(seed, level), mate, ptr,
                                                           cnt.as<unsigned long long>());
             FDL_LAUNCH_CK();
         }
@@ -386,7 +574,8 @@ void pset_match(int phase, int64_t n, const int64_t *rp, const int *ci, const do
         *active = (int64_t)a;
     } else if (phase == FIEDLER_PSET_RESOLVE) {
         if (!own) return;
-        k_ps_resolve<<<ps_grid(own), kPsBlock, 0, st>>>(r0, r1, ptr, mate);
+        if (work) FDL_CK(cudaMemsetAsync(work, 0, 4, st));
+        k_ps_resolve<<<ps_grid(own), kPsBlock, 0, st>>>(make_list(work, r0, own, work ? 1 : -1, 0), ptr, mate);
         FDL_LAUNCH_CK();
     } else {
         throw Error(FIEDLER_ERR_ARG, "bad matching phase");
@@ -438,44 +627,21 @@ void pset_aggregate(int phase, int64_t n, const int64_t *rp, const int *ci, cons
     }
 }
 
-void pset_galerkin(int phase, int64_t n, const int64_t *rp, const int *ci, const double *w, const int *q, int64_t a0,
-                   int64_t a1, int64_t cap, int64_t *crp, int *cci, double *cw, int64_t *count, cudaStream_t st) {
-    check_rows(n, 0, n);
-    FDL_REQUIRE(0 <= a0 && a0 <= a1 && a1 <= n, FIEDLER_ERR_ARG, "coarse rows out of range");
-    FDL_REQUIRE(count, FIEDLER_ERR_ARG, "NULL count");
-    const int na = (int)(a1 - a0);
-    // members of the coarse rows [a0, a1), ascending
-    DBuf flags((size_t)n * 4, st), members((size_t)n * 4, st), dcnt(8, st);
-    k_ps_member_flags<<<ps_grid(n), kPsBlock, 0, st>>>(n, q, (int)a0, (int)a1, flags.as<int>());
+// the two-sort path: contributions of the members listed in `members` (nm of
+// them), sorted by (A, B, lo, hi), folded per (A, B); returns the number of
+// runs, their local row / column / weight in row / cB / cWv
+static int gal_sorted_runs(const int64_t *rp, const int *ci, const double *w, const int *q, const int *members, int nm,
+                           int a0, int na, DBuf &row, DBuf &cB, DBuf &cWv, cudaStream_t st) {
+    DBuf cnt((size_t)std::max(nm, 1) * 4, st), off((size_t)std::max(nm, 1) * 4, st), dcnt(8, st);
+    k_ps_contrib_count<<<ps_grid(nm), kPsBlock, 0, st>>>(rp, ci, q, members, nm, cnt.as<int>());
     FDL_LAUNCH_CK();
-    compact_flagged(nullptr, flags.as<int>(), n, members.as<int>(), dcnt.as<int>(), st);
-    int nm = 0;
-    readback(st, {{&nm, dcnt.p, 4}});
-    DBuf cnt((size_t)std::max(nm, 1) * 4, st), off((size_t)std::max(nm, 1) * 4, st);
+    scan_exclusive(cnt.as<int>(), off.as<int>(), nm, dcnt.as<int>(), st);
     int nc = 0;
-    if (nm) {
-        k_ps_contrib_count<<<ps_grid(nm), kPsBlock, 0, st>>>(rp, ci, q, members.as<int>(), nm, cnt.as<int>());
-        FDL_LAUNCH_CK();
-        scan_exclusive(cnt.as<int>(), off.as<int>(), nm, dcnt.as<int>(), st);
-        readback(st, {{&nc, dcnt.p, 4}});
-    }
-    if (phase == 0) {
-        *count = nc;
-        return;
-    }
-    FDL_REQUIRE(phase == 1, FIEDLER_ERR_ARG, "bad Galerkin phase");
-    FDL_REQUIRE(crp, FIEDLER_ERR_ARG, "NULL crp");
-    FDL_REQUIRE(cap >= nc && (nc == 0 || (cci && cw)), FIEDLER_ERR_ARG, "cap below the contribution count");
-    if (nc == 0) {
-        k_ps_row_ptr<<<ps_grid(na + 1), kPsBlock, 0, st>>>(nullptr, 0, na, crp);
-        FDL_LAUNCH_CK();
-        *count = 0;
-        host_wait(st);
-        return;
-    }
+    readback(st, {{&nc, dcnt.p, 4}});
+    if (!nc) return 0;
     DBuf key1((size_t)nc * 8, st), key2((size_t)nc * 8, st), val((size_t)nc * 4, st), perm((size_t)nc * 4, st),
         skey((size_t)nc * 8, st);
-    k_ps_contrib_fill<<<ps_grid(nm), kPsBlock, 0, st>>>(rp, ci, q, members.as<int>(), nm, off.as<int>(), (int)a0,
+    k_ps_contrib_fill<<<ps_grid(nm), kPsBlock, 0, st>>>(rp, ci, q, members, nm, off.as<int>(), a0,
                                                         key1.as<unsigned long long>(), key2.as<unsigned long long>(),
                                                         val.as<int>());
     FDL_LAUNCH_CK();
@@ -487,33 +653,119 @@ void pset_galerkin(int phase, int64_t n, const int64_t *rp, const int *ci, const
                                                         skey.as<unsigned long long>());
     FDL_LAUNCH_CK();
     radix_sort_u64_i32(skey.as<unsigned long long>(), perm.as<int>(), nc, 31 + bits_for(std::max(na - 1, 0)), st);
-    // runs of equal (A, B)
-    DBuf rflags((size_t)nc * 4, st), starts((size_t)nc * 4, st), row((size_t)nc * 4, st);
+    DBuf rflags((size_t)nc * 4, st), starts((size_t)nc * 4, st);
     k_ps_run_flags<<<ps_grid(nc), kPsBlock, 0, st>>>(skey.as<unsigned long long>(), nc, rflags.as<int>());
     FDL_LAUNCH_CK();
     compact_flagged(nullptr, rflags.as<int>(), nc, starts.as<int>(), dcnt.as<int>(), st);
     int nruns = 0;
     readback(st, {{&nruns, dcnt.p, 4}});
+    row.alloc((size_t)nruns * 4, st);
+    cB.alloc((size_t)nruns * 4, st);
+    cWv.alloc((size_t)nruns * 8, st);
     k_ps_fold<<<ps_grid(nruns), kPsBlock, 0, st>>>(skey.as<unsigned long long>(), perm.as<int>(), val.as<int>(), w,
-                                                   starts.as<int>(), nruns, nc, cci, cw, row.as<int>());
+                                                   starts.as<int>(), nruns, nc, cB.as<int>(), cWv.as<double>(),
+                                                   row.as<int>());
     FDL_LAUNCH_CK();
-    k_ps_row_ptr<<<ps_grid(na + 1), kPsBlock, 0, st>>>(row.as<int>(), nruns, na, crp);
+    return nruns;
+}
+
+void pset_galerkin(int phase, int64_t n, const int64_t *rp, const int *ci, const double *w, const int *q, int64_t a0,
+                   int64_t a1, int64_t cap, int64_t *crp, int *cci, double *cw, int64_t *count, cudaStream_t st) {
+    check_rows(n, 0, n);
+    FDL_REQUIRE(0 <= a0 && a0 <= a1 && a1 <= n, FIEDLER_ERR_ARG, "coarse rows out of range");
+    FDL_REQUIRE(count, FIEDLER_ERR_ARG, "NULL count");
+    FDL_REQUIRE(phase == 0 || phase == 1, FIEDLER_ERR_ARG, "bad Galerkin phase");
+    const int na = (int)(a1 - a0);
+    // members grouped by coarse row (counting sort) and the rows' slot counts
+    DBuf mcnt((size_t)(na + 1) * 4, st), slots((size_t)(na + 1) * 4, st), mrp((size_t)(na + 1) * 4, st),
+        soff((size_t)(na + 1) * 4, st), dcnt(16, st);
+    FDL_CK(cudaMemsetAsync(mcnt.p, 0, (size_t)(na + 1) * 4, st));
+    FDL_CK(cudaMemsetAsync(slots.p, 0, (size_t)(na + 1) * 4, st));
+    k_ps_row_members<<<ps_grid(n), kPsBlock, 0, st>>>(rp, n, q, (int)a0, (int)a1, mcnt.as<int>(), slots.as<int>());
     FDL_LAUNCH_CK();
-    *count = nruns;
+    scan_exclusive(mcnt.as<int>(), mrp.as<int>(), na + 1, dcnt.as<int>(), st);
+    scan_exclusive(slots.as<int>(), soff.as<int>(), na + 1, dcnt.as<int>() + 1, st);
+    int tot[2] = {0, 0};
+    readback(st, {{tot, dcnt.p, 8}});
+    const int nm = tot[0], ns = tot[1];
+    if (phase == 0) {   // crossing contributions of the rows (<= their slots)
+        if (!nm) { *count = 0; return; }
+        DBuf flags((size_t)n * 4, st), members((size_t)n * 4, st), cnt((size_t)nm * 4, st), pos((size_t)nm * 4, st);
+        k_ps_member_flags<<<ps_grid(n), kPsBlock, 0, st>>>(n, q, (int)a0, (int)a1, flags.as<int>());
+        FDL_LAUNCH_CK();
+        compact_flagged(nullptr, flags.as<int>(), n, members.as<int>(), dcnt.as<int>(), st);
+        k_ps_contrib_count<<<ps_grid(nm), kPsBlock, 0, st>>>(rp, ci, q, members.as<int>(), nm, cnt.as<int>());
+        FDL_LAUNCH_CK();
+        scan_exclusive(cnt.as<int>(), pos.as<int>(), nm, dcnt.as<int>(), st);
+        int nc = 0;
+        readback(st, {{&nc, dcnt.p, 4}});
+        *count = nc;
+        return;
+    }
+    FDL_REQUIRE(crp, FIEDLER_ERR_ARG, "NULL crp");
+    DBuf mem((size_t)std::max(nm, 1) * 4, st), cursor((size_t)(na + 1) * 4, st), sB((size_t)std::max(ns, 1) * 4, st),
+        sW((size_t)std::max(ns, 1) * 8, st), cnt((size_t)(na + 1) * 4, st), big((size_t)(na + 1) * 4, st),
+        coff((size_t)(na + 1) * 4, st);
+    FDL_CK(cudaMemsetAsync(cursor.p, 0, (size_t)(na + 1) * 4, st));
+    FDL_CK(cudaMemsetAsync(cnt.p, 0, (size_t)(na + 1) * 4, st));
+    FDL_CK(cudaMemsetAsync(big.p, 0, (size_t)(na + 1) * 4, st));
+    if (na) {
+        k_ps_row_fill<<<ps_grid(n), kPsBlock, 0, st>>>(n, q, (int)a0, (int)a1, mrp.as<int>(), cursor.as<int>(),
+                                                       mem.as<int>());
+        FDL_LAUNCH_CK();
+        k_ps_gal_small<<<ps_grid(na), kPsBlock, 0, st>>>(rp, ci, w, q, (int)a0, na, mrp.as<int>(), mem.as<int>(),
+                                                         slots.as<int>(), soff.as<int>(), sB.as<int>(), sW.as<double>(),
+                                                         cnt.as<int>(), big.as<int>());
+        FDL_LAUNCH_CK();
+        // rows with more than kGalSmall slots: the sort path over their members
+        DBuf flags((size_t)n * 4, st), members((size_t)n * 4, st);
+        k_ps_big_member_flags<<<ps_grid(n), kPsBlock, 0, st>>>(n, q, (int)a0, (int)a1, big.as<int>(), flags.as<int>());
+        FDL_LAUNCH_CK();
+        compact_flagged(nullptr, flags.as<int>(), n, members.as<int>(), dcnt.as<int>(), st);
+        int nbm = 0;
+        readback(st, {{&nbm, dcnt.p, 4}});
+        if (nbm) {
+            DBuf row, cB, cWv;
+            const int nruns = gal_sorted_runs(rp, ci, w, q, members.as<int>(), nbm, (int)a0, na, row, cB, cWv, st);
+            if (nruns) {
+                DBuf rr((size_t)(na + 1) * 4, st);
+                k_ps_row_ptr32<<<ps_grid(na + 1), kPsBlock, 0, st>>>(row.as<int>(), nruns, na, rr.as<int>());
+                FDL_LAUNCH_CK();
+                k_ps_big_place<<<ps_grid(nruns), kPsBlock, 0, st>>>(row.as<int>(), cB.as<int>(), cWv.as<double>(),
+                                                                    nruns, rr.as<int>(), soff.as<int>(), sB.as<int>(),
+                                                                    sW.as<double>());
+                FDL_LAUNCH_CK();
+                k_ps_big_cnt<<<ps_grid(na), kPsBlock, 0, st>>>(rr.as<int>(), na, big.as<int>(), cnt.as<int>());
+                FDL_LAUNCH_CK();
+            }
+        }
+    }
+    scan_exclusive(cnt.as<int>(), coff.as<int>(), na + 1, dcnt.as<int>(), st);
+    int nnz = 0;
+    readback(st, {{&nnz, dcnt.p, 4}});
+    FDL_REQUIRE(cap >= nnz && (nnz == 0 || (cci && cw)), FIEDLER_ERR_ARG, "cap below the coarse nonzeros");
+    k_ps_gal_out<<<ps_grid(na + 1), kPsBlock, 0, st>>>(na, cnt.as<int>(), coff.as<int>(), soff.as<int>(), sB.as<int>(),
+                                                       sW.as<double>(), crp, cci, cw, nnz);
+    FDL_LAUNCH_CK();
+    *count = nnz;
     host_wait(st);
 }
 
 void pset_colour(int64_t n, const int64_t *rp, const int *ci, int64_t r0, int64_t r1, uint64_t seed, int level,
-                 int *colour, int64_t *out, cudaStream_t st) {
+                 int round, int *work, int *colour, int64_t *out, cudaStream_t st) {
     check_rows(n, r0, r1);
     FDL_REQUIRE(out, FIEDLER_ERR_ARG, "NULL out");
+    FDL_REQUIRE(round >= 0, FIEDLER_ERR_ARG, "round < 0");
     const int64_t own = r1 - r0;
     DBuf c(16, st);
     k_ps_init_counters<<<1, 32, 0, st>>>(c.as<unsigned long long>(), 1, reinterpret_cast<int *>(c.as<char>() + 8));
     FDL_LAUNCH_CK();
     if (own) {
-        k_ps_colour<<<ps_grid(own), kPsBlock, 0, st>>>(rp, ci, r0, r1, salt_color(seed, level), colour,
-                                                       c.as<unsigned long long>(),
+        // round r reads the list of round r - 1 (parity), writes list r & 1
+        const int wr = round & 1;
+        if (work) FDL_CK(cudaMemsetAsync(work + wr, 0, 4, st));
+        k_ps_colour<<<ps_grid(own), kPsBlock, 0, st>>>(rp, ci, make_list(work, r0, own, round ? 1 - wr : -1, wr),
+                                                       salt_color(seed, level), colour, c.as<unsigned long long>(),
                                                        reinterpret_cast<int *>(c.as<char>() + 8));
         FDL_LAUNCH_CK();
     }
@@ -570,10 +822,11 @@ int fiedler_pset_scatter(const int32_t *in, const int32_t *idx, int64_t count, i
 
 int fiedler_pset_match(int32_t phase, int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
                        const double *weights, int64_t r0, int64_t r1, uint64_t seed, int32_t level, int32_t *mate,
-                       int32_t *ptr, int64_t *active, void *stream) {
+                       int32_t *ptr, int32_t round, int32_t *work, int64_t *active, void *stream) {
     API_BEGIN
     FDL_REQUIRE(row_ptr && col_idx && weights && mate && ptr, FIEDLER_ERR_ARG, "NULL array");
-    pset_match(phase, n, row_ptr, col_idx, weights, r0, r1, seed, level, mate, ptr, active, (cudaStream_t)stream);
+    pset_match(phase, n, row_ptr, col_idx, weights, r0, r1, seed, level, mate, ptr, round, work, active,
+               (cudaStream_t)stream);
     return FIEDLER_OK;
     API_END
 }
@@ -600,10 +853,11 @@ int fiedler_pset_galerkin(int32_t phase, int64_t n, const int64_t *row_ptr, cons
 }
 
 int fiedler_pset_colour(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, int64_t r0, int64_t r1,
-                        uint64_t seed, int32_t level, int32_t *colour, int64_t *out, void *stream) {
+                        uint64_t seed, int32_t level, int32_t round, int32_t *work, int32_t *colour, int64_t *out,
+                        void *stream) {
     API_BEGIN
     FDL_REQUIRE(row_ptr && col_idx && colour, FIEDLER_ERR_ARG, "NULL array");
-    pset_colour(n, row_ptr, col_idx, r0, r1, seed, level, colour, out, (cudaStream_t)stream);
+    pset_colour(n, row_ptr, col_idx, r0, r1, seed, level, round, work, colour, out, (cudaStream_t)stream);
     return FIEDLER_OK;
     API_END
 }

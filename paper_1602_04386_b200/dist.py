@@ -377,9 +377,10 @@ class LibSetupOps:
         from . import fiedler_pset_scatter
         fiedler_pset_scatter(inp, idx, count, x, self.stream)
 
-    def match(self, phase, g, r0, r1, seed, level, mate, ptr):
+    def match(self, phase, g, r0, r1, seed, level, mate, ptr, round=0, work=None):
         from . import fiedler_pset_match
-        return fiedler_pset_match(phase, g.n, g.rp, g.ci, g.w, r0, r1, seed, level, mate, ptr, self.stream)
+        return fiedler_pset_match(phase, g.n, g.rp, g.ci, g.w, r0, r1, seed, level, mate, ptr, round, work,
+                                  self.stream)
 
     def aggregate(self, phase, g, r0, r1, seed, level, mate, q, offset=0):
         from . import fiedler_pset_aggregate
@@ -390,9 +391,9 @@ class LibSetupOps:
         from . import fiedler_pset_galerkin
         return fiedler_pset_galerkin(phase, g.n, g.rp, g.ci, g.w, q, a0, a1, cap, crp, cci, cw, self.stream)
 
-    def colour(self, g, r0, r1, seed, level, colour):
+    def colour(self, g, r0, r1, seed, level, colour, round=0, work=None):
         from . import fiedler_pset_colour
-        return fiedler_pset_colour(g.n, g.rp, g.ci, r0, r1, seed, level, colour, self.stream)
+        return fiedler_pset_colour(g.n, g.rp, g.ci, r0, r1, seed, level, colour, round, work, self.stream)
 
 
 class PartitionedSetup:
@@ -430,6 +431,21 @@ class PartitionedSetup:
         self.stall_ratio = stall_ratio
         self.bytes_sent = 0          # halo + all-gather bytes this rank sent in the last run
         self.rounds = []             # (match rounds, colour rounds) per partitioned level
+        # diagnostics: wall ms of the phases of every level (synchronising), when set
+        self.phase_times = None
+        self.match_lists = False     # work lists for the matching's half-rounds too
+
+    def _mark(self, ell, name):
+        if self.phase_times is None:
+            return
+        import time
+        if self._dev.type == "cuda":
+            torch.cuda.synchronize(self._dev)
+        now = time.perf_counter()
+        if name is not None:
+            d = self.phase_times.setdefault(ell, {})
+            d[name] = d.get(name, 0.0) + (now - self._t0) * 1e3
+        self._t0 = now
 
     # ---------------------------------------------------------------- helpers
     def _scalar_sum(self, v):
@@ -489,6 +505,7 @@ class PartitionedSetup:
         ops, comm = self.ops, self.comm
         N, rk = comm.nranks, comm.rank
         i32 = torch.int32
+        self._mark(ell, None)
         bounds = ops.bounds(g, N)
         r0, r1 = bounds[rk], bounds[rk + 1]
         # halo plan: send lists by the library, receive lists = the peers' send lists to us
@@ -503,18 +520,25 @@ class PartitionedSetup:
         self._sbuf = ops.full(self._ns, 0, i32)
         self._rbuf = ops.full(self._nr, 0, i32)
 
+        self._mark(ell, "halo_plan")
         # heavy-edge matching: handshake rounds
         mate = ops.full(g.n, -1, i32)
         ptr = ops.full(g.n, -1, i32)
+        # the rounds' work lists (own rows still in play): the colouring's rounds
+        # visit only them; the matching visits all own rows every half-round
+        # (measured faster on the grids: ~7 rounds, most rows active until the last)
+        work = ops.full(8 + 2 * (r1 - r0), 0, i32)
+        mwork = work if self.match_lists else None
         mrounds = 0
         while True:
-            act = ops.match(FIEDLER_PSET_POINT, g, r0, r1, self.seed, ell, mate, ptr)
+            act = ops.match(FIEDLER_PSET_POINT, g, r0, r1, self.seed, ell, mate, ptr, mrounds, mwork)
             if self._scalar_sum(act) == 0:
                 break
             self._exchange(ptr)
-            ops.match(FIEDLER_PSET_RESOLVE, g, r0, r1, self.seed, ell, mate, ptr)
+            ops.match(FIEDLER_PSET_RESOLVE, g, r0, r1, self.seed, ell, mate, ptr, mrounds, mwork)
             self._exchange(mate)
             mrounds += 1
+        self._mark(ell, "matching")
         # aggregates numbered by increasing leader: contiguous id range per rank
         own_leaders = ops.aggregate(FIEDLER_PSET_LEADERS, g, r0, r1, self.seed, ell, mate, ptr)
         counts = self._per_rank(own_leaders)
@@ -533,6 +557,7 @@ class PartitionedSetup:
         q_full = self._allgather(q[r0:r1], rows, i32)
         mate_full = self._allgather(mate[r0:r1], rows, i32)
 
+        self._mark(ell, "aggregates")
         # Galerkin product of the own coarse rows [a0, a1), gathered
         cap = ops.galerkin(0, g, q_full, a0, a1)
         crp = ops.full(a1 - a0 + 1, 0, torch.int64)
@@ -550,12 +575,13 @@ class PartitionedSetup:
         rp_full[c] = nnz_c
         nxt = SetupGraph(n=c, nnz=nnz_c, rp=rp_full[:c + 1], ci=ci_next[:max(nnz_c, 1)], w=w_next[:max(nnz_c, 1)])
 
+        self._mark(ell, "galerkin")
         # colouring: Jones-Plassmann rounds
         colour = ops.full(g.n, -1, i32)
         crounds = 0
         maxc = -1
         while True:
-            left, mc = ops.colour(g, r0, r1, self.seed, ell, colour)
+            left, mc = ops.colour(g, r0, r1, self.seed, ell, colour, crounds, work)
             maxc = max(maxc, mc)
             crounds += 1
             self._exchange(colour)
@@ -564,6 +590,7 @@ class PartitionedSetup:
         ncolors = max(self._per_rank(maxc + 1))
         colour_full = self._allgather(colour[r0:r1], rows, i32)
         self.rounds.append((mrounds, crounds))
+        self._mark(ell, "colouring")
         return PresetLevel(level=ell, q=q_full[:g.n], mate=mate_full[:g.n], colour=colour_full[:g.n],
                            ncolors=ncolors, match_rounds=mrounds, colour_rounds=crounds, nxt=nxt,
                            row_bounds=bounds)

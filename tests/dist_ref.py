@@ -268,7 +268,7 @@ class RefSetupOps:
         lo, hi = min(v, u), max(v, u)
         return (w, self.o.splitmix64((salt ^ ((lo << 32) | hi)) & self.o.MASK64))
 
-    def match(self, phase, g, r0, r1, seed, level, mate, ptr):
+    def match(self, phase, g, r0, r1, seed, level, mate, ptr, round=0, work=None):
         rp, ci, w = self._np(g)
         salt = self.o.salt_match(seed, level)
         if phase == 0:
@@ -357,7 +357,7 @@ class RefSetupOps:
         crp[a1 - a0] = nnz
         return nnz
 
-    def colour(self, g, r0, r1, seed, level, colour):
+    def colour(self, g, r0, r1, seed, level, colour, round=0, work=None):
         rp, ci, _ = self._np(g)
         salt = self.o.salt_color(seed, level)
         pi = lambda x: (self.o.splitmix64((salt ^ x) & self.o.MASK64), x)   # noqa: E731

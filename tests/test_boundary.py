@@ -118,7 +118,7 @@ def test_argument_errors_before_any_device_work():
     assert lib.fiedler_pset_bounds(4, None, 2, b, None) == p.FIEDLER_ERR_ARG
     assert lib.fiedler_pset_bounds(4, rp.ctypes.data, 0, b, None) == p.FIEDLER_ERR_ARG
     assert lib.fiedler_pset_match(0, 2, rp.ctypes.data, ci.ctypes.data, w.ctypes.data, 0, 3, 0, 0, None,
-                                  None, None, None) == p.FIEDLER_ERR_ARG
+                                  None, 0, None, None, None) == p.FIEDLER_ERR_ARG
     assert lib.fiedler_pset_galerkin(0, 2, None, None, None, None, 0, 1, 0, None, None, None, None,
                                      None) == p.FIEDLER_ERR_ARG
     assert lib.fiedler_create_preset(2, 2, rp.ctypes.data, ci.ctypes.data, w.ctypes.data, 0, None, -1, None,
