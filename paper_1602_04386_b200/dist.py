@@ -126,6 +126,38 @@ class LocalComm(Comm):
         out[:inp.numel()] = inp
 
 
+def _own_stream(device, stream):
+    """The torch stream the library calls of an Ops object are issued on.  A
+    NULL / default stream (0) is not passed to the library: its C ABI reads
+    NULL as "the handle's own stream" (fiedler_dist_op) or "no caller stream
+    to join" (fiedler_create), which would not be ordered with torch's work on
+    the legacy default stream; such callers get a stream of their own, joined
+    with theirs by _Joined."""
+    if stream is None or stream == 0:
+        return torch.cuda.Stream(device)
+    return torch.cuda.ExternalStream(stream)
+
+
+class _Joined:
+    """Enter: the Ops stream waits for the caller's current stream and becomes
+    current.  Exit: the caller's stream waits for the Ops stream."""
+
+    def __init__(self, s):
+        self.s = s
+
+    def __enter__(self):
+        self.caller = torch.cuda.current_stream(self.s.device)
+        self.s.wait_stream(self.caller)
+        self.ctx = torch.cuda.stream(self.s)
+        self.ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        self.ctx.__exit__(*exc)
+        self.caller.wait_stream(self.s)
+        return False
+
+
 class LibOps:
     """Ops backed by libfiedler (fiedler_dist_plan / fiedler_dist_op) on one GPU."""
 
@@ -136,13 +168,13 @@ class LibOps:
         # library kernels and torch's tensor work (allocation, zero-fill, slicing,
         # collectives) are ordered by running both on one (non-default) stream:
         # the driver enters stream_ctx() around the solve
-        self.torch_stream = torch.cuda.Stream(device) if stream is None else torch.cuda.ExternalStream(stream)
+        self.torch_stream = _own_stream(device, stream)
         self.stream = self.torch_stream.cuda_stream
         self.num_levels = fiedler_num_levels(handle)
         self.sizes = [fiedler_level_size(handle, l)[0] for l in range(self.num_levels)]
 
     def stream_ctx(self):
-        return torch.cuda.stream(self.torch_stream)
+        return _Joined(self.torch_stream)
 
     def plan(self, level, nranks, rank) -> Plan:
         from . import fiedler_dist_plan
@@ -347,12 +379,28 @@ class LibSetupOps:
     every call is issued on one stream shared with torch's tensor work."""
 
     def __init__(self, device, stream=None):
+        import os
         self.device = device
-        self.torch_stream = torch.cuda.Stream(device) if stream is None else torch.cuda.ExternalStream(stream)
+        self.torch_stream = _own_stream(device, stream)
         self.stream = self.torch_stream.cuda_stream
+        # FIEDLER_PSET_SYNC=1 (diagnostics): synchronise after every operation
+        # so that a device fault is reported by the operation that caused it
+        if os.environ.get("FIEDLER_PSET_SYNC") == "1":
+            for name in ("bounds", "halo", "gather", "scatter", "match", "aggregate", "galerkin", "colour"):
+                setattr(self, name, self._synced(name, getattr(self, name)))
+
+    def _synced(self, name, fn):
+        def call(*a, **k):
+            r = fn(*a, **k)
+            try:
+                torch.cuda.synchronize(self.device)
+            except Exception as e:   # pragma: no cover - diagnostics
+                raise RuntimeError("device fault after LibSetupOps.%s: %s" % (name, e))
+            return r
+        return call
 
     def stream_ctx(self):
-        return torch.cuda.stream(self.torch_stream)
+        return _Joined(self.torch_stream)
 
     def full(self, n, value, dtype):
         return torch.full((max(n, 1),), value, dtype=dtype, device=self.device)
@@ -597,8 +645,13 @@ class PartitionedSetup:
 
 
 def create_from_presets(g: SetupGraph, presets: List[PresetLevel], opts=None):
-    """fiedler_create_preset on the partitioned levels (device arrays)."""
+    """fiedler_create_preset on the partitioned levels (device arrays).  The
+    library joins opts.stream before it reads the arrays; with no stream given
+    (NULL: nothing to join) torch's current stream is drained first."""
     from . import fiedler_create_preset, fiedler_default_opts, fiedler_preset_level
+    opts = opts or fiedler_default_opts()
+    if not opts.stream:
+        torch.cuda.current_stream(g.rp.device).synchronize()
     pl = []
     for p in presets:
         s = fiedler_preset_level()
@@ -607,4 +660,4 @@ def create_from_presets(g: SetupGraph, presets: List[PresetLevel], opts=None):
         s.n_next, s.nnz_next = p.nxt.n, p.nxt.nnz
         s.rp_next, s.ci_next, s.w_next = p.nxt.rp.data_ptr(), p.nxt.ci.data_ptr(), p.nxt.w.data_ptr()
         pl.append(s)
-    return fiedler_create_preset(g.n, g.nnz, g.rp, g.ci, g.w, opts or fiedler_default_opts(), pl)
+    return fiedler_create_preset(g.n, g.nnz, g.rp, g.ci, g.w, opts, pl)
