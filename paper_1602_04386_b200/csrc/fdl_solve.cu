@@ -2085,17 +2085,21 @@ __global__ void k_dist_bounds(const int *rp, int n, int nranks, int *bounds) {
 
 // own GS rows of colour c: [lower_bound(perm_c, r0), lower_bound(perm_c, r1)) inside the
 // colour's segment (natural ids ascend within a colour)
-__global__ void k_dist_colour_ranges(const int *perm, const int *seg, int ncol, int r0, int r1, int *ab) {
-    const int c = threadIdx.x;
-    if (c >= ncol) return;
-    for (int side = 0; side < 2; side++) {
-        int lo = seg[c], hi = seg[c + 1];
-        const int target = side ? r1 : r0;
-        while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (perm[mid] < target) lo = mid + 1; else hi = mid;
+// own GS row range [a, b) of every colour (rows of a colour are sorted by
+// natural id) and the row offsets at its ends: ab[4c..4c+3] = {a, b, rp[a], rp[b]}
+__global__ void k_dist_colour_ranges(const int *perm, const int *seg, const int *rp, int ncol, int r0, int r1,
+                                     int *ab) {
+    for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
+        for (int side = 0; side < 2; side++) {
+            int lo = seg[c], hi = seg[c + 1];
+            const int target = side ? r1 : r0;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (perm[mid] < target) lo = mid + 1; else hi = mid;
+            }
+            ab[4 * c + side] = lo;
+            ab[4 * c + 2 + side] = rp[lo];
         }
-        ab[2 * c + side] = lo;
     }
 }
 
@@ -2190,25 +2194,22 @@ void dist_plan(Handle &h, int level, int nranks, int rank, fiedler_dist_plan_inf
     }
     // own GS tiles per colour
     const int nc = L.ncolors;
-    DBuf dseg((size_t)(nc + 1) * 4, st), dab((size_t)2 * nc * 4, st);
+    DBuf dseg((size_t)(nc + 1) * 4, st), dab((size_t)4 * nc * 4, st);
     FDL_CK(cudaMemcpyAsync(dseg.p, L.seg.data(), (size_t)(nc + 1) * 4, cudaMemcpyHostToDevice, st));
-    k_dist_colour_ranges<<<1, 128, 0, st>>>(L.perm.as<int>(), dseg.as<int>(), nc, P.r0, P.r1, dab.as<int>());
+    k_dist_colour_ranges<<<1, 256, 0, st>>>(L.perm.as<int>(), dseg.as<int>(), L.rp.as<int>(), nc, P.r0, P.r1,
+                                            dab.as<int>());
     FDL_LAUNCH_CK();
-    std::vector<int> ab(2 * nc);
-    FDL_CK(cudaMemcpyAsync(ab.data(), dab.p, (size_t)2 * nc * 4, cudaMemcpyDeviceToHost, st));
+    std::vector<int> ab(4 * nc);
+    FDL_CK(cudaMemcpyAsync(ab.data(), dab.p, (size_t)4 * nc * 4, cudaMemcpyDeviceToHost, st));
     FDL_CK(cudaStreamSynchronize(st));
     std::vector<int> cnt(nc, 0);
     P.ctile.assign(nc + 1, 0);
     int nt = 0;
     for (int c = 0; c < nc; c++) {
         P.ctile[c] = nt;
-        const int a0 = ab[2 * c], a1 = ab[2 * c + 1];
+        const int a0 = ab[4 * c], a1 = ab[4 * c + 1];
         if (a1 > a0) {
-            int q[2];
-            FDL_CK(cudaMemcpyAsync(&q[0], L.rp.as<int>() + a0, 4, cudaMemcpyDeviceToHost, st));
-            FDL_CK(cudaMemcpyAsync(&q[1], L.rp.as<int>() + a1, 4, cudaMemcpyDeviceToHost, st));
-            FDL_CK(cudaStreamSynchronize(st));
-            const long long span = (long long)(q[1] + a1) - (q[0] + a0);
+            const long long span = (long long)(ab[4 * c + 3] + a1) - (ab[4 * c + 2] + a0);
             cnt[c] = (int)((span + kTileT - 1) / kTileT);
             if (cnt[c] < 1) cnt[c] = 1;
         }
@@ -2218,7 +2219,7 @@ void dist_plan(Handle &h, int level, int nranks, int rank, fiedler_dist_plan_inf
     P.tilesGS.alloc((size_t)std::max(nt, 1) * sizeof(Tile), st);
     for (int c = 0; c < nc; c++)
         if (cnt[c]) {
-            k_make_tiles_d<<<grid_for(cnt[c]), 256, 0, st>>>(L.rp.as<int>(), ab[2 * c], ab[2 * c + 1], cnt[c],
+            k_make_tiles_d<<<grid_for(cnt[c]), 256, 0, st>>>(L.rp.as<int>(), ab[4 * c], ab[4 * c + 1], cnt[c],
                                                              P.tilesGS.as<Tile>() + P.ctile[c]);
             FDL_LAUNCH_CK();
         }

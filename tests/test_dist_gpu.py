@@ -25,7 +25,15 @@ GRAPHS = {
     "rmat12": lambda: gg.rmat(12, 16.0, seed=5),
     "hub": lambda: gg.hub_graph(3000, 4000, hubs=3, seed=4),
     "grid3d_14": lambda: gg.grid3d(14, "lognormal", seed=2),
+    "wcomplete300": lambda: _wcomplete(300, seed=7),   # 300 colours on level 0 (> 128)
 }
+
+
+def _wcomplete(n, seed):
+    """Complete graph with random weights: every level needs as many colours as vertices."""
+    rng = np.random.default_rng(seed)
+    u, v = np.triu_indices(n, 1)
+    return gg.csr_from_edges(n, u, v, rng.uniform(0.5, 1.5, u.size), "wcomplete%d" % n)
 
 
 def _handle(fd, g):
@@ -143,7 +151,8 @@ def _check_presets(pres, levels, n_expected):
         assert np.array_equal(p.nxt.w[:p.nxt.nnz].cpu().numpy(), Ln.g.w)
 
 
-@pytest.mark.parametrize("name,world", [("grid64x45", 2), ("rmat12", 3), ("hub", 2), ("grid3d_14", 4)])
+@pytest.mark.parametrize("name,world", [("grid64x45", 2), ("rmat12", 3), ("hub", 2), ("grid3d_14", 4),
+                                        ("wcomplete300", 3)])
 def test_partitioned_setup_and_solve_threads_match_oracle(fd, orc, name, world):
     """Ranks as threads on one GPU: the partitioned setup (fiedler_pset_*) gives
     the oracle's hierarchy bit for bit on every rank; fiedler_create_preset on it

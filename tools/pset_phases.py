@@ -21,7 +21,7 @@ dev = torch.device("cuda")
 sg = SetupGraph(g.n, g.nnz, torch.from_numpy(g.rp).to(dev), torch.from_numpy(g.ci).to(dev),
                 torch.from_numpy(g.w).to(dev))
 ops = LibSetupOps(dev)
-for rep in range(3):
+for rep in range(int(sys.argv[3]) if len(sys.argv) > 3 else 3):
     torch.cuda.synchronize()
     ps = PartitionedSetup(ops, LocalComm(), min_rows=min_rows)
     ps.phase_times = {}
