@@ -24,7 +24,8 @@ def _free_port():
 def _graph(name):
     return {"grid": lambda: gg.grid2d(24, "uniform", seed=3, mx=17),
             "rand": lambda: gg.random_connected(300, 700, 5),
-            "hub": lambda: gg.hub_graph(400, 500, hubs=2, seed=1)}[name]()
+            "hub": lambda: gg.hub_graph(400, 500, hubs=2, seed=1),
+            "unitgrid": lambda: gg.grid2d(20, "unit", seed=0, mx=13)}[name]()   # all weights tie (R2 hash order)
 
 
 def _worker(rank, world, port, name, gs, q):
@@ -128,7 +129,7 @@ def _setup_worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,name", [(2, "grid"), (3, "rand"), (2, "hub")])
+@pytest.mark.parametrize("world,name", [(2, "grid"), (3, "rand"), (2, "hub"), (3, "unitgrid")])
 def test_partitioned_setup_matches_oracle_hierarchy(orc, world, name):
     """Every partitioned level's matching, aggregates, colouring and coarse
     level equal the oracle's hierarchy bit for bit, on every rank."""
