@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <chrono>
 #include <initializer_list>
 #include <stdexcept>
 #include <string>
@@ -73,6 +74,8 @@ struct SmallArena {
         return p;
     }
 };
+extern std::atomic<long long> g_alloc_ns, g_alloc_calls, g_free_ns, g_free_calls;   // FIEDLER_ALLOC_STATS
+bool alloc_stats_enabled();
 extern thread_local SmallArena *tl_arena;   // set by fiedler_create for its duration
 
 // Stream-ordered device buffer (cudaMallocAsync pool; capture-safe frees are
@@ -105,10 +108,26 @@ struct DBuf {
             in_arena = true;
             return;
         }
+        if (alloc_stats_enabled()) {
+            const auto t0 = std::chrono::steady_clock::now();
+            FDL_CK(cudaMallocAsync(&p, b, st));
+            g_alloc_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+            g_alloc_calls++;
+            return;
+        }
         FDL_CK(cudaMallocAsync(&p, b, st));
     }
     void release() noexcept {
-        if (p && !in_arena) cudaFreeAsync(p, s);
+        if (p && !in_arena) {
+            if (alloc_stats_enabled()) {
+                const auto t0 = std::chrono::steady_clock::now();
+                cudaFreeAsync(p, s);
+                g_free_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+                g_free_calls++;
+            } else {
+                cudaFreeAsync(p, s);
+            }
+        }
         p = nullptr;
         bytes = 0;
         in_arena = false;
