@@ -272,6 +272,7 @@ def sharded_step_timing(fd, g, rp, ci, w, dev, local, args, comm, dist):
     for _ in range(args.warmup):
         step()
     times = []
+    ms0 = torch.cuda.memory_stats(dev)
     for _ in range(args.steps):
         if dist:
             dist.barrier()
@@ -284,6 +285,10 @@ def sharded_step_timing(fd, g, rp, ci, w, dev, local, args, comm, dist):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
     tot = sum(times)
+    ms1 = torch.cuda.memory_stats(dev)
+    info["torch_allocator"] = {k: int(ms1.get(k, 0) - ms0.get(k, 0)) for k in
+                               ("num_device_alloc", "num_device_free", "num_alloc_retries",
+                                "reserved_bytes.all.current")}
     hb = float(info.get("halo_bytes", 0))
     sb = float(info.get("setup_bytes", 0))
     if dist:
@@ -292,7 +297,8 @@ def sharded_step_timing(fd, g, rp, ci, w, dev, local, args, comm, dist):
         tot, hb, sb = float(t[0].item()), float(t[1].item()), float(t[2].item())
     ms = tot / args.steps
     return {"_create": create,
-            "ms_per_step": ms, "lambda2": info.get("lam"), "levels_partitioned": info.get("levels_partitioned"),
+            "ms_per_step": ms, "step_ms": [round(t, 2) for t in times],
+            "torch_allocator_in_timed_region": info.get("torch_allocator"), "lambda2": info.get("lam"), "levels_partitioned": info.get("levels_partitioned"),
             "setup": "replicated" if args.replicated_setup else "partitioned",
             "setup_levels_partitioned": info.get("setup_levels_partitioned", 0),
             "setup_rounds": info.get("setup_rounds"),
