@@ -231,3 +231,22 @@ def test_single_rank_setup_equals_fiedler_create(fd, orc, name):
     finally:
         fd.fiedler_destroy(h)
         fd.fiedler_destroy(h2)
+
+
+def test_own_stream_reused_per_thread(fd):
+    """The Ops objects' stream for a NULL caller stream is one per device and
+    host thread: torch's caching allocator pools freed blocks per stream, so a
+    fresh stream per solve would reuse none of the previous solve's buffers."""
+    import threading
+    import torch
+    from paper_1602_04386_b200.dist import _own_stream
+    dev = torch.device("cuda", 0)
+    a, b = _own_stream(dev, 0), _own_stream(dev, None)
+    assert a is b and a.cuda_stream != 0
+    other = []
+    t = threading.Thread(target=lambda: other.append(_own_stream(dev, 0)))
+    t.start()
+    t.join()
+    assert other[0] is not a
+    ext = _own_stream(dev, a.cuda_stream)   # a caller's real stream is used as it is
+    assert ext.cuda_stream == a.cuda_stream
